@@ -1,0 +1,110 @@
+/*
+ * admm_b200.h -- C ABI of the B200-native ADMM-LP decoder (sm_100a).
+ *
+ * This is the drop-in boundary for the reference's decoder path
+ * (polylp, /root/reference/pkg/src/polylp).  The reference is pure Python and
+ * has no FFI of its own; each entry point below replaces the Python function
+ * named beside it, and the Python shim in paper_1204_0556_b200/ binds them
+ * with ctypes (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *   - Every function returns 0 on success or a negative ADMM_E_* code; the
+ *     thread-local message is available from admm_last_error().  No C++
+ *     exception crosses this boundary.
+ *   - All array arguments of admm_decode_batch / admm_project_batch are
+ *     DEVICE pointers on the graph's device; the caller owns them.  Optional
+ *     outputs may be NULL.  Work is enqueued on `stream` (a cudaStream_t, NULL
+ *     = legacy default stream) and the call returns without synchronising.
+ *   - A graph handle is immutable after creation (like ParityCheckMatrix,
+ *     codes.py:28-32) and may be shared by host threads and streams.
+ *   - dtype: ADMM_F32 (throughput mode) or ADMM_F64 (parity mode).
+ */
+#ifndef ADMM_B200_H
+#define ADMM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADMM_B200_VERSION 1
+
+enum admm_dtype { ADMM_F32 = 0, ADMM_F64 = 1 };
+
+enum admm_status {
+  ADMM_OK = 0,
+  ADMM_E_ARG = -1,         /* invalid argument (shape, range, null pointer)   */
+  ADMM_E_UNSUPPORTED = -2, /* graph shape outside the compiled kernel buckets  */
+  ADMM_E_CUDA = -3,        /* CUDA runtime error (message has the CUDA string) */
+  ADMM_E_WORKSPACE = -4    /* workspace too small                              */
+};
+
+/* Per-frame flag bits written to flags_out. */
+#define ADMM_FLAG_CONVERGED 1u /* status == "Converged" (admm_decoder.py:23)     */
+#define ADMM_FLAG_INTEGRAL 2u  /* all |x - round(x)| <= 1e-5 (admm_decoder.py:96) */
+#define ADMM_FLAG_CODEWORD 4u  /* hard decision satisfies every check           */
+
+typedef struct admm_graph admm_graph;
+
+typedef struct admm_graph_info {
+  int32_t n_vars, n_checks, n_edges;
+  int32_t max_check_degree, max_var_degree;
+  int32_t engine;           /* 1 = resident (on-chip persistent) */
+  int32_t degree_bucket;    /* D: compiled check-degree bucket   */
+  int32_t checks_per_thread;
+  int32_t threads_per_cta;
+  int32_t ctas_per_sm_f32, ctas_per_sm_f64;
+  int32_t smem_bytes_f32, smem_bytes_f64;
+  int32_t regs_f32, regs_f64;
+  int32_t num_sms;
+} admm_graph_info;
+
+/* Build the device-resident Tanner graph.  Replaces the edge-array views of
+ * ParityCheckMatrix (codes.py:79-115): check_ptr[n_checks+1] / edge_var[E]
+ * are the reference's CSR-by-check arrays (host pointers, any variable order
+ * inside a check; edges are re-sorted as codes.py:42 does). */
+int admm_graph_create(int device, int32_t n_vars, int32_t n_checks, const int32_t* check_ptr,
+                      const int32_t* edge_var, admm_graph** out);
+int admm_graph_destroy(admm_graph* g);
+int admm_graph_get_info(const admm_graph* g, admm_graph_info* info);
+
+/* Bytes of device workspace admm_decode_batch needs for `batch` frames. */
+size_t admm_workspace_bytes(const admm_graph* g, int dtype, int64_t batch);
+
+/* Decode `batch` independent frames.  Replaces decode(gamma, code, config)
+ * (admm_decoder.py:152-182) applied frame by frame, and make_output
+ * (:92-105) for the per-frame results.
+ *   gamma      [batch][ld_gamma] channel costs (LLRs), dtype
+ *   mu, epsilon, t_max, rho: AdmmConfig (admm_decoder.py:27-44), validated here
+ *   x_out      [batch][ld_x]   final x (the iterate of the last iteration)
+ *   hard_out   [batch][ld_hard] uint8 hard decision x > 0.5
+ *   iters_out  [batch] int32 iterations run
+ *   flags_out  [batch] uint8 ADMM_FLAG_* bits
+ *   weight_out [batch] int32 Hamming weight of the hard decision
+ *   z_in/lam_in [batch][ld_edge] optional initial replicas / duals in the
+ *              reference edge order (NULL = zeros, AdmmState.initial)
+ *   z_out/lam_out [batch][ld_edge] optional final replicas / duals
+ *   workspace  device scratch of admm_workspace_bytes() bytes             */
+int admm_decode_batch(const admm_graph* g, int dtype, int64_t batch, const void* gamma,
+                      int64_t ld_gamma, double mu, double epsilon, int32_t t_max, double rho,
+                      void* x_out, int64_t ld_x, uint8_t* hard_out, int64_t ld_hard,
+                      int32_t* iters_out, uint8_t* flags_out, int32_t* weight_out,
+                      const void* z_in, const void* lam_in, void* z_out, void* lam_out,
+                      int64_t ld_edge, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Row-wise projection onto the parity polytope.  Replaces project_batch
+ * (parity_polytope.py:352-421): values and out are [m][d] row-major device
+ * arrays, 1 <= d <= 32. */
+int admm_project_batch(int dtype, int64_t m, int32_t d, const void* values, void* out,
+                       void* stream);
+
+const char* admm_last_error(void);
+int admm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ADMM_B200_H */

@@ -1,0 +1,46 @@
+"""B200-native ADMM-LP decoder for binary LDPC codes (arXiv 1204.0556).
+
+Drop-in for the decoder path of the reference package ``polylp``
+(/root/reference/pkg/src/polylp/__init__.py:8-97): the decoder names
+``AdmmConfig``, ``DecodeOutput``, ``STATUS_*``, ``decode``,
+``ParityCheckMatrix``, ``is_codeword`` and ``project_batch`` are exported
+with the reference's signatures; the arithmetic runs in hand-written sm_100a
+CUDA kernels behind the C ABI of ``include/admm_b200.h``.
+"""
+
+from .admm_decoder import (
+    INTEGRALITY_TOL,
+    STATUS_CONVERGED,
+    STATUS_MAX_ITERS,
+    AdmmConfig,
+    BatchResult,
+    DecodeOutput,
+    decode,
+    decode_batch,
+    device_graph,
+    run_iterations,
+)
+from .channels import Awgn, Bsc, llr, transmit, trial_gamma, trial_gammas
+from .codes import (
+    AlistParseError,
+    CodeGenerationError,
+    ParityCheckMatrix,
+    baseline_code,
+    emit_alist,
+    gen_regular_ldpc,
+    is_codeword,
+    make_ldpc,
+    parse_alist,
+)
+from .parity_polytope import PARITY_TOL, project_batch
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "AdmmConfig", "BatchResult", "DecodeOutput", "INTEGRALITY_TOL", "STATUS_CONVERGED",
+    "STATUS_MAX_ITERS", "decode", "decode_batch", "device_graph", "run_iterations",
+    "Awgn", "Bsc", "llr", "transmit", "trial_gamma", "trial_gammas",
+    "AlistParseError", "CodeGenerationError", "ParityCheckMatrix", "baseline_code", "emit_alist",
+    "gen_regular_ldpc", "is_codeword", "make_ldpc", "parse_alist",
+    "PARITY_TOL", "project_batch",
+]

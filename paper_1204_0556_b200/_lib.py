@@ -1,0 +1,94 @@
+"""ctypes binding of the C ABI in ``include/admm_b200.h``.
+
+The shared library ``libadmm_b200.so`` is built in-tree (``make`` or
+``__graft_entry__.build()``).  There is no fallback: if the library is
+missing, every entry point raises ``RuntimeError`` -- the decoder never
+silently runs anywhere but the CUDA kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libadmm_b200.so"
+
+ADMM_F32 = 0
+ADMM_F64 = 1
+ADMM_FLAG_CONVERGED = 1
+ADMM_FLAG_INTEGRAL = 2
+ADMM_FLAG_CODEWORD = 4
+
+#: Every symbol the public header declares (checked by the CPU test-suite).
+EXPORTED = (
+    "admm_version",
+    "admm_last_error",
+    "admm_graph_create",
+    "admm_graph_destroy",
+    "admm_graph_get_info",
+    "admm_workspace_bytes",
+    "admm_decode_batch",
+    "admm_project_batch",
+)
+
+
+class GraphInfo(ctypes.Structure):
+    _fields_ = [
+        ("n_vars", ctypes.c_int32), ("n_checks", ctypes.c_int32), ("n_edges", ctypes.c_int32),
+        ("max_check_degree", ctypes.c_int32), ("max_var_degree", ctypes.c_int32),
+        ("engine", ctypes.c_int32), ("degree_bucket", ctypes.c_int32),
+        ("checks_per_thread", ctypes.c_int32), ("threads_per_cta", ctypes.c_int32),
+        ("ctas_per_sm_f32", ctypes.c_int32), ("ctas_per_sm_f64", ctypes.c_int32),
+        ("smem_bytes_f32", ctypes.c_int32), ("smem_bytes_f64", ctypes.c_int32),
+        ("regs_f32", ctypes.c_int32), ("regs_f64", ctypes.c_int32),
+        ("num_sms", ctypes.c_int32),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load (once) and return the library; raise if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = os.environ.get("ADMM_B200_LIB", str(LIB_PATH))
+    if not Path(path).exists():
+        raise RuntimeError(
+            f"CUDA extension {path} is not built; run `make` (or __graft_entry__.build()). "
+            "The decoder has no CPU fallback.")
+    lib = ctypes.CDLL(path)
+    P, I32, I64, SZ, D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t, ctypes.c_double
+    lib.admm_version.restype = ctypes.c_int
+    lib.admm_last_error.restype = ctypes.c_char_p
+    lib.admm_graph_create.argtypes = [ctypes.c_int, I32, I32, P, P, ctypes.POINTER(P)]
+    lib.admm_graph_create.restype = ctypes.c_int
+    lib.admm_graph_destroy.argtypes = [P]
+    lib.admm_graph_destroy.restype = ctypes.c_int
+    lib.admm_graph_get_info.argtypes = [P, ctypes.POINTER(GraphInfo)]
+    lib.admm_graph_get_info.restype = ctypes.c_int
+    lib.admm_workspace_bytes.argtypes = [P, ctypes.c_int, I64]
+    lib.admm_workspace_bytes.restype = SZ
+    lib.admm_decode_batch.argtypes = [
+        P, ctypes.c_int, I64, P, I64, D, D, I32, D,
+        P, I64, P, I64, P, P, P,
+        P, P, P, P, I64, P, SZ, P,
+    ]
+    lib.admm_decode_batch.restype = ctypes.c_int
+    lib.admm_project_batch.argtypes = [ctypes.c_int, I64, I32, P, P, P]
+    lib.admm_project_batch.restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = load().admm_last_error().decode(errors="replace")
+        if rc == -1:
+            raise ValueError(msg)
+        raise RuntimeError(f"admm_b200 error {rc}: {msg}")

@@ -1,0 +1,292 @@
+"""ADMM-LP decoder: the reference-compatible API over the sm_100a kernels.
+
+Mirror of ``polylp.admm_decoder`` (/root/reference/pkg/src/polylp/admm_decoder.py):
+
+* :class:`AdmmConfig` -- same fields, defaults and validation (:27-44);
+* :class:`DecodeOutput` and the ``STATUS_*`` strings (:23-24, :74-89);
+* :func:`decode` ``(gamma, code, config) -> DecodeOutput`` -- same
+  arguments, errors and output convention (:152-182), computed in fp64 on the
+  GPU (the parity mode);
+
+and the B200 batch entry point :func:`decode_batch`, which decodes a
+``[B, N]`` block of frames in one launch (fp32 throughput mode or fp64
+parity mode) and returns per-frame results as device tensors.
+
+There is no CPU fallback: a missing extension raises ``RuntimeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+from numpy.typing import ArrayLike, NDArray
+
+from . import _lib
+from .codes import ParityCheckMatrix, as_code
+
+INTEGRALITY_TOL = 1e-5
+STATUS_CONVERGED = "Converged"
+STATUS_MAX_ITERS = "MaxIters"
+
+
+@dataclass(frozen=True)
+class AdmmConfig:
+    """Penalty, stopping tolerance, iteration cap and over-relaxation
+    (admm_decoder.py:27-44)."""
+
+    mu: float = 3.0
+    epsilon: float = 1e-5
+    t_max: int = 1000
+    rho: float = 1.9
+
+    def __post_init__(self) -> None:
+        if self.mu <= 0:
+            raise ValueError("mu must be positive")
+        if self.epsilon <= 0:
+            raise ValueError("epsilon must be positive")
+        if self.t_max < 1:
+            raise ValueError("t_max must be at least 1")
+        if not (1.0 <= self.rho < 2.0):
+            raise ValueError("rho must be in [1, 2)")
+
+
+@dataclass(frozen=True)
+class DecodeOutput:
+    """Result of one decode (admm_decoder.py:74-89)."""
+
+    x: NDArray[np.float64]
+    status: str
+    integral: bool
+    iterations: int
+    hard_decision: NDArray[np.uint8]
+    ml_certificate: bool
+
+
+# ---------------------------------------------------------------------------
+# Device graph
+# ---------------------------------------------------------------------------
+class DeviceGraph:
+    """Owner of an ``admm_graph`` handle (immutable, one per code and device)."""
+
+    def __init__(self, code: ParityCheckMatrix, device: int):
+        lib = _lib.load()
+        self.code = code
+        self.device = int(device)
+        ptr = np.ascontiguousarray(code.check_ptr, dtype=np.int32)
+        ev = np.ascontiguousarray(code.edge_var, dtype=np.int32)
+        h = ctypes.c_void_p()
+        _lib.check(lib.admm_graph_create(self.device, code.n_vars, code.n_checks,
+                                         ptr.ctypes.data, ev.ctypes.data, ctypes.byref(h)))
+        self._h = h
+        info = _lib.GraphInfo()
+        _lib.check(lib.admm_graph_get_info(self._h, ctypes.byref(info)))
+        self.info = info.as_dict()
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    def workspace_bytes(self, dtype_code: int, batch: int) -> int:
+        return int(_lib.load().admm_workspace_bytes(self._h, dtype_code, batch))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.load().admm_graph_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+
+def device_graph(code, device=None) -> DeviceGraph:
+    code = as_code(code)
+    dev = torch.device(device if device is not None else "cuda")
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    g = code._device_graphs.get(idx)
+    if g is None:
+        g = DeviceGraph(code, idx)
+        code._device_graphs[idx] = g
+    return g
+
+
+def _dtype_code(dtype) -> int:
+    if dtype in (torch.float32, "f32", "float32", np.float32):
+        return _lib.ADMM_F32
+    if dtype in (torch.float64, "f64", "float64", np.float64, float):
+        return _lib.ADMM_F64
+    raise ValueError(f"unsupported dtype {dtype!r}; use float32 or float64")
+
+
+# ---------------------------------------------------------------------------
+# Batch decode
+# ---------------------------------------------------------------------------
+@dataclass
+class BatchResult:
+    """Per-frame results of :func:`decode_batch` (device tensors)."""
+
+    iterations: torch.Tensor          # [B] int32
+    flags: torch.Tensor               # [B] uint8, ADMM_FLAG_* bits
+    weight: torch.Tensor              # [B] int32, Hamming weight of the hard decision
+    x: torch.Tensor | None = None     # [B, N] final x
+    hard: torch.Tensor | None = None  # [B, N] uint8
+    z: torch.Tensor | None = None     # [B, E] final replicas (reference edge order)
+    lam: torch.Tensor | None = None   # [B, E] final duals
+    info: dict = field(default_factory=dict)
+
+    @property
+    def converged(self) -> torch.Tensor:
+        return (self.flags & _lib.ADMM_FLAG_CONVERGED) != 0
+
+    @property
+    def integral(self) -> torch.Tensor:
+        return (self.flags & _lib.ADMM_FLAG_INTEGRAL) != 0
+
+    @property
+    def codeword(self) -> torch.Tensor:
+        return (self.flags & _lib.ADMM_FLAG_CODEWORD) != 0
+
+    @property
+    def ml_certificate(self) -> torch.Tensor:
+        return self.integral & self.codeword
+
+    def output(self, k: int) -> DecodeOutput:
+        """Frame k as a reference :class:`DecodeOutput` (host arrays)."""
+        if self.x is None:
+            raise ValueError("decode_batch was called with want_x=False")
+        x = self.x[k].detach().double().cpu().numpy()
+        hard = (x > 0.5).astype(np.uint8)
+        flags = int(self.flags[k])
+        integral = bool(flags & _lib.ADMM_FLAG_INTEGRAL)
+        return DecodeOutput(
+            x=x,
+            status=STATUS_CONVERGED if flags & _lib.ADMM_FLAG_CONVERGED else STATUS_MAX_ITERS,
+            integral=integral,
+            iterations=int(self.iterations[k]),
+            hard_decision=hard,
+            ml_certificate=integral and bool(flags & _lib.ADMM_FLAG_CODEWORD),
+        )
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def launch(dg: DeviceGraph, code_dt: int, g: torch.Tensor, config: AdmmConfig, iters, flags, weight, *,
+           x=None, hard=None, z0=None, lam0=None, z_out=None, lam_out=None, workspace, stream) -> None:
+    """Enqueue one ``admm_decode_batch`` on caller-owned device buffers (no
+    allocation, no validation beyond the C ABI's)."""
+    N, E = dg.code.n_vars, dg.code.n_edges
+    _lib.check(_lib.load().admm_decode_batch(
+        dg.handle, code_dt, g.shape[0], g.data_ptr(), g.stride(0),
+        float(config.mu), float(config.epsilon), int(config.t_max), float(config.rho),
+        _ptr(x), N if x is None else x.stride(0), _ptr(hard), N if hard is None else hard.stride(0),
+        iters.data_ptr(), flags.data_ptr(), weight.data_ptr(),
+        _ptr(z0), _ptr(lam0), _ptr(z_out), _ptr(lam_out), E,
+        workspace.data_ptr(), workspace.numel(), stream.cuda_stream))
+
+
+def decode_batch(
+    gammas,
+    code,
+    config: AdmmConfig = AdmmConfig(),
+    *,
+    dtype=torch.float64,
+    device=None,
+    want_x: bool = True,
+    want_hard: bool = False,
+    z0=None,
+    lam0=None,
+    want_state: bool = False,
+    validate: bool = True,
+    stream: torch.cuda.Stream | None = None,
+) -> BatchResult:
+    """Decode ``gammas`` ([B, N], one frame per row) on the GPU.
+
+    Frames are independent; the result for a frame does not depend on the
+    batch it was decoded in.  ``dtype`` selects the arithmetic: float64 is
+    the parity mode, float32 the throughput mode.  ``z0``/``lam0`` ([B, E],
+    reference edge order) replace the zero initial state; ``want_state``
+    returns the final replicas and duals.  Work is enqueued on ``stream``
+    (default: the current stream) and the call does not synchronise.
+    """
+    code = as_code(code)
+    tdt = torch.float64 if _dtype_code(dtype) == _lib.ADMM_F64 else torch.float32
+    dev = torch.device(device) if device is not None else (
+        gammas.device if isinstance(gammas, torch.Tensor) and gammas.is_cuda else torch.device("cuda"))
+    g = torch.as_tensor(gammas)
+    if g.ndim == 1:
+        g = g.unsqueeze(0)
+    if g.ndim != 2 or g.shape[1] != code.n_vars:
+        raise ValueError(f"expected a [B, {code.n_vars}] block of LLR vectors")
+    g = g.to(device=dev, dtype=tdt, non_blocking=True)
+    if not g.is_contiguous():
+        g = g.contiguous()
+    if validate and not bool(torch.isfinite(g).all()):
+        raise ValueError("LLR vector must be finite")
+    B, N, E = g.shape[0], code.n_vars, code.n_edges
+    dg = device_graph(code, dev)
+    code_dt = _dtype_code(tdt)
+    iters = torch.empty(B, dtype=torch.int32, device=dev)
+    flags = torch.empty(B, dtype=torch.uint8, device=dev)
+    weight = torch.empty(B, dtype=torch.int32, device=dev)
+    x = torch.empty((B, N), dtype=tdt, device=dev) if want_x else None
+    hard = torch.empty((B, N), dtype=torch.uint8, device=dev) if want_hard else None
+    zi = li = None
+    if z0 is not None or lam0 is not None:
+        if z0 is None or lam0 is None:
+            raise ValueError("z0 and lam0 go together")
+        zi = torch.as_tensor(z0).to(device=dev, dtype=tdt).reshape(B, E).contiguous()
+        li = torch.as_tensor(lam0).to(device=dev, dtype=tdt).reshape(B, E).contiguous()
+    zo = torch.empty((B, E), dtype=tdt, device=dev) if want_state else None
+    lo = torch.empty((B, E), dtype=tdt, device=dev) if want_state else None
+    ws_bytes = dg.workspace_bytes(code_dt, B)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    launch(dg, code_dt, g, config, iters, flags, weight, x=x, hard=hard, z0=zi, lam0=li, z_out=zo,
+           lam_out=lo, workspace=ws, stream=st)
+    # keep inputs alive until the kernel has consumed them
+    res = BatchResult(iterations=iters, flags=flags, weight=weight, x=x, hard=hard, z=zo, lam=lo,
+                      info=dg.info)
+    res._keepalive = (g, zi, li, ws)  # type: ignore[attr-defined]
+    return res
+
+
+# ---------------------------------------------------------------------------
+# Reference-compatible single-frame entry point
+# ---------------------------------------------------------------------------
+def decode(gamma: ArrayLike, code, config: AdmmConfig = AdmmConfig()) -> DecodeOutput:
+    """Solve the decoding LP for one LLR vector (admm_decoder.py:152-182).
+
+    Drop-in for ``polylp.decode``: same arguments, ``ValueError`` on a wrong
+    shape or non-finite input, fp64 arithmetic, fresh output arrays.
+    """
+    code = as_code(code)
+    gamma = np.asarray(gamma, dtype=float)
+    if gamma.shape != (code.n_vars,):
+        raise ValueError(f"expected a length-{code.n_vars} LLR vector")
+    if not np.all(np.isfinite(gamma)):
+        raise ValueError("LLR vector must be finite")
+    res = decode_batch(gamma[None, :], code, config, dtype=torch.float64, validate=False)
+    torch.cuda.current_stream().synchronize()
+    return res.output(0)
+
+
+def run_iterations(gamma, code, config: AdmmConfig, iterations: int, z0=None, lam0=None):
+    """Run exactly ``iterations`` ADMM iterations (x-, z-, lambda-update, as
+    admm_decoder.py:171-177) from the given replicas/duals (zeros by
+    default) and return ``(x, z, lam)`` as fp64 host arrays.  The GPU
+    analogue of driving ``x_update``/``z_update``/``lambda_update`` by hand
+    (tests/test_admm.py:151-160 of the reference)."""
+    code = as_code(code)
+    cfg = AdmmConfig(mu=config.mu, epsilon=1e-300, t_max=int(iterations), rho=config.rho)
+    g = np.asarray(gamma, dtype=float).reshape(1, -1)
+    E = code.n_edges
+    z0 = np.zeros(E) if z0 is None else np.asarray(z0, dtype=float)
+    lam0 = np.zeros(E) if lam0 is None else np.asarray(lam0, dtype=float)
+    res = decode_batch(g, code, cfg, dtype=torch.float64, z0=z0[None], lam0=lam0[None], want_state=True)
+    torch.cuda.current_stream().synchronize()
+    return (res.x[0].cpu().numpy(), res.z[0].cpu().numpy(), res.lam[0].cpu().numpy())

@@ -1,0 +1,286 @@
+// C ABI of the ADMM-LP decoder: graph construction, kernel selection and
+// launch.  See include/admm_b200.h for the contract.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/admm_b200.h"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(ADMM_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define ADMM_CUDA(call)                                  \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);  \
+  } while (0)
+
+}  // namespace
+
+struct admm_graph {
+  int device = 0;
+  int n_vars = 0, n_checks = 0, n_edges = 0;
+  int dmax = 0, dvmax_actual = 0;
+  int D = 0, DVMAX = 0, CPT = 0, NT = 0, m_pad = 0;
+  int num_sms = 0;
+  // device arrays
+  int* chk_var = nullptr;
+  uint16_t* var_pos = nullptr;
+  uint8_t* var_deg = nullptr;
+  int* edge_base = nullptr;
+  // per-dtype launch data
+  admm::ResidentLaunch launch[2];
+};
+
+namespace {
+
+const int kBuckets[] = {4, 6, 8, 13, 16, 32};
+
+int pick_bucket(int d) {
+  for (int b : kBuckets)
+    if (d <= b) return b;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int admm_version(void) { return ADMM_B200_VERSION; }
+
+const char* admm_last_error(void) { return g_last_error.c_str(); }
+
+int admm_graph_create(int device, int32_t n_vars, int32_t n_checks, const int32_t* check_ptr,
+                      const int32_t* edge_var, admm_graph** out) {
+  if (!out || !check_ptr || !edge_var) return fail(ADMM_E_ARG, "null pointer argument");
+  *out = nullptr;
+  if (n_vars <= 0 || n_checks <= 0) return fail(ADMM_E_ARG, "n_vars and n_checks must be positive");
+  if (check_ptr[0] != 0) return fail(ADMM_E_ARG, "check_ptr[0] must be 0");
+  const int E = check_ptr[n_checks];
+  std::vector<std::vector<int>> rows(n_checks);
+  std::vector<int> vdeg(n_vars, 0);
+  int dmax = 0;
+  for (int c = 0; c < n_checks; ++c) {
+    const int a = check_ptr[c], b = check_ptr[c + 1];
+    if (b <= a) return fail(ADMM_E_ARG, "check " + std::to_string(c) + " has no variables");
+    for (int e = a; e < b; ++e) {
+      const int v = edge_var[e];
+      if (v < 0 || v >= n_vars)
+        return fail(ADMM_E_ARG, "check " + std::to_string(c) + " has a variable index out of range");
+      rows[c].push_back(v);
+    }
+    std::sort(rows[c].begin(), rows[c].end());
+    for (size_t k = 1; k < rows[c].size(); ++k)
+      if (rows[c][k] == rows[c][k - 1])
+        return fail(ADMM_E_ARG, "check " + std::to_string(c) + " has a parallel edge");
+    for (int v : rows[c]) vdeg[v]++;
+    dmax = std::max<int>(dmax, rows[c].size());
+  }
+  const int dvmax = *std::max_element(vdeg.begin(), vdeg.end());
+
+  auto* g = new admm_graph();
+  g->device = device;
+  g->n_vars = n_vars;
+  g->n_checks = n_checks;
+  g->n_edges = E;
+  g->dmax = dmax;
+  g->dvmax_actual = dvmax;
+  g->D = pick_bucket(dmax);
+  g->DVMAX = dvmax <= 4 ? 4 : (dvmax <= 8 ? 8 : 0);
+  if (!g->D || !g->DVMAX) {
+    delete g;
+    return fail(ADMM_E_UNSUPPORTED, "check degree > 32 or variable degree > 8 is not supported");
+  }
+  cudaError_t ce = cudaSetDevice(device);
+  if (ce != cudaSuccess) {
+    delete g;
+    return cuda_fail(ce, "cudaSetDevice");
+  }
+  cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device);
+  int smem_optin = 0;
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+
+  // Kernel shape: smallest checks-per-thread whose CTA fits 512 threads, the
+  // 16-bit message positions, the register file and shared memory.
+  bool placed = false;
+  for (int cpt : {1, 2, 4}) {
+    const int nt = ((n_checks + cpt - 1) / cpt + 31) / 32 * 32;
+    if (nt > 512) continue;
+    const int m_pad = nt * cpt;
+    if ((long long)g->D * m_pad >= 65535) continue;
+    bool ok = true;
+    for (int dt = 0; dt < 2 && ok; ++dt) {
+      admm::ResidentLaunch L{};
+      if (!admm::resident_lookup(dt, g->D, cpt, g->DVMAX, &L)) { ok = false; break; }
+      const admm::ResidentSmem S(dt ? 8 : 4, n_vars, g->D * m_pad, g->DVMAX);
+      if (S.total > smem_optin) { ok = false; break; }
+      cudaFuncAttributes fa{};
+      if (cudaFuncGetAttributes(&fa, L.fn) != cudaSuccess) { ok = false; break; }
+      if (fa.numRegs * nt > 65536 || nt > fa.maxThreadsPerBlock) { ok = false; break; }
+      cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, S.total);
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L.fn, nt, S.total);
+      if (occ < 1) { ok = false; break; }
+      L.smem = S.total;
+      L.occupancy = occ;
+      L.regs = fa.numRegs;
+      g->launch[dt] = L;
+    }
+    if (!ok) continue;
+    g->CPT = cpt;
+    g->NT = nt;
+    g->m_pad = m_pad;
+    placed = true;
+    break;
+  }
+  cudaGetLastError();
+  if (!placed) {
+    delete g;
+    return fail(ADMM_E_UNSUPPORTED, "graph does not fit the resident engine (too many checks or edges)");
+  }
+
+  // Device layout.
+  const int D = g->D, MP = g->m_pad;
+  std::vector<int> chk_var((size_t)D * MP, -1);
+  std::vector<int> edge_base(n_checks);
+  std::vector<std::vector<int>> var_slots(n_vars);
+  for (int c = 0; c < n_checks; ++c) {
+    edge_base[c] = check_ptr[c];
+    for (size_t k = 0; k < rows[c].size(); ++k) {
+      chk_var[k * MP + c] = rows[c][k];
+      var_slots[rows[c][k]].push_back((int)k * MP + c);  // appended in increasing check order
+    }
+  }
+  std::vector<uint16_t> var_pos((size_t)n_vars * g->DVMAX, 0);
+  std::vector<uint8_t> var_deg(n_vars);
+  for (int v = 0; v < n_vars; ++v) {
+    var_deg[v] = (uint8_t)var_slots[v].size();
+    for (size_t j = 0; j < var_slots[v].size(); ++j) var_pos[(size_t)v * g->DVMAX + j] = (uint16_t)var_slots[v][j];
+  }
+  auto up = [&](void** dst, const void* src, size_t bytes) -> cudaError_t {
+    cudaError_t e = cudaMalloc(dst, bytes);
+    if (e != cudaSuccess) return e;
+    return cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+  };
+  cudaError_t e1 = up((void**)&g->chk_var, chk_var.data(), chk_var.size() * sizeof(int));
+  cudaError_t e2 = up((void**)&g->var_pos, var_pos.data(), var_pos.size() * sizeof(uint16_t));
+  cudaError_t e3 = up((void**)&g->var_deg, var_deg.data(), var_deg.size());
+  cudaError_t e4 = up((void**)&g->edge_base, edge_base.data(), edge_base.size() * sizeof(int));
+  for (cudaError_t e : {e1, e2, e3, e4}) {
+    if (e != cudaSuccess) {
+      admm_graph_destroy(g);
+      return cuda_fail(e, "graph upload");
+    }
+  }
+  *out = g;
+  return ADMM_OK;
+}
+
+int admm_graph_destroy(admm_graph* g) {
+  if (!g) return ADMM_OK;
+  cudaSetDevice(g->device);
+  cudaFree(g->chk_var);
+  cudaFree(g->var_pos);
+  cudaFree(g->var_deg);
+  cudaFree(g->edge_base);
+  delete g;
+  return ADMM_OK;
+}
+
+int admm_graph_get_info(const admm_graph* g, admm_graph_info* info) {
+  if (!g || !info) return fail(ADMM_E_ARG, "null pointer argument");
+  std::memset(info, 0, sizeof(*info));
+  info->n_vars = g->n_vars;
+  info->n_checks = g->n_checks;
+  info->n_edges = g->n_edges;
+  info->max_check_degree = g->dmax;
+  info->max_var_degree = g->dvmax_actual;
+  info->engine = 1;
+  info->degree_bucket = g->D;
+  info->checks_per_thread = g->CPT;
+  info->threads_per_cta = g->NT;
+  info->ctas_per_sm_f32 = g->launch[0].occupancy;
+  info->ctas_per_sm_f64 = g->launch[1].occupancy;
+  info->smem_bytes_f32 = g->launch[0].smem;
+  info->smem_bytes_f64 = g->launch[1].smem;
+  info->regs_f32 = g->launch[0].regs;
+  info->regs_f64 = g->launch[1].regs;
+  info->num_sms = g->num_sms;
+  return ADMM_OK;
+}
+
+size_t admm_workspace_bytes(const admm_graph* g, int dtype, int64_t batch) {
+  (void)g;
+  (void)dtype;
+  (void)batch;
+  return 256;  // the frame queue counter (padded)
+}
+
+int admm_decode_batch(const admm_graph* g, int dtype, int64_t batch, const void* gamma,
+                      int64_t ld_gamma, double mu, double epsilon, int32_t t_max, double rho,
+                      void* x_out, int64_t ld_x, uint8_t* hard_out, int64_t ld_hard,
+                      int32_t* iters_out, uint8_t* flags_out, int32_t* weight_out,
+                      const void* z_in, const void* lam_in, void* z_out, void* lam_out,
+                      int64_t ld_edge, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!g) return fail(ADMM_E_ARG, "null graph");
+  if (dtype != ADMM_F32 && dtype != ADMM_F64) return fail(ADMM_E_ARG, "dtype must be ADMM_F32 or ADMM_F64");
+  if (batch < 0) return fail(ADMM_E_ARG, "batch must be non-negative");
+  if (batch == 0) return ADMM_OK;
+  if (!gamma) return fail(ADMM_E_ARG, "gamma is null");
+  if (ld_gamma < g->n_vars) return fail(ADMM_E_ARG, "ld_gamma < n_vars");
+  if (x_out && ld_x < g->n_vars) return fail(ADMM_E_ARG, "ld_x < n_vars");
+  if (hard_out && ld_hard < g->n_vars) return fail(ADMM_E_ARG, "ld_hard < n_vars");
+  if (!(mu > 0)) return fail(ADMM_E_ARG, "mu must be positive");
+  if (!(epsilon > 0)) return fail(ADMM_E_ARG, "epsilon must be positive");
+  if (t_max < 1) return fail(ADMM_E_ARG, "t_max must be at least 1");
+  if (!(rho >= 1.0 && rho < 2.0)) return fail(ADMM_E_ARG, "rho must be in [1, 2)");
+  if ((z_in == nullptr) != (lam_in == nullptr)) return fail(ADMM_E_ARG, "z_in and lam_in go together");
+  if ((z_out == nullptr) != (lam_out == nullptr)) return fail(ADMM_E_ARG, "z_out and lam_out go together");
+  if ((z_in || z_out) && ld_edge < g->n_edges) return fail(ADMM_E_ARG, "ld_edge < n_edges");
+  if (!workspace || workspace_bytes < admm_workspace_bytes(g, dtype, batch))
+    return fail(ADMM_E_WORKSPACE, "workspace too small");
+  if (batch > (1ll << 31) - 1024) return fail(ADMM_E_ARG, "batch too large for one call");
+
+  ADMM_CUDA(cudaSetDevice(g->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  ADMM_CUDA(cudaMemsetAsync(workspace, 0, sizeof(int), st));
+  const admm::ResidentLaunch& L = g->launch[dtype];
+  const long long grid = std::min<long long>(batch, (long long)L.occupancy * g->num_sms);
+  const double thr = epsilon * epsilon * (double)g->n_edges;  // admm_decoder.py:169
+
+  admm::ResidentGraphArgs ga{g->n_vars, g->n_checks, g->m_pad, g->chk_var, g->var_pos, g->var_deg, g->edge_base};
+  admm::ResidentFrameArgs fa{batch, gamma, ld_gamma, mu, rho, thr, t_max, z_in, lam_in, ld_edge,
+                             x_out, ld_x, hard_out, ld_hard, iters_out, flags_out, weight_out,
+                             z_out, lam_out, reinterpret_cast<int*>(workspace)};
+  L.launch(ga, fa, (int)grid, g->NT, L.smem, st);
+  ADMM_CUDA(cudaGetLastError());
+  return ADMM_OK;
+}
+
+int admm_project_batch(int dtype, int64_t m, int32_t d, const void* values, void* out, void* stream) {
+  if (dtype != ADMM_F32 && dtype != ADMM_F64) return fail(ADMM_E_ARG, "dtype must be ADMM_F32 or ADMM_F64");
+  if (m < 0 || d < 1) return fail(ADMM_E_ARG, "project_batch expects an (m, d) array with d >= 1");
+  if (d > 32) return fail(ADMM_E_UNSUPPORTED, "project_batch supports d <= 32");
+  if (m == 0) return ADMM_OK;
+  if (!values || !out) return fail(ADMM_E_ARG, "null pointer argument");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (!admm::launch_project(dtype, pick_bucket(d), m, d, values, out, st))
+    return fail(ADMM_E_UNSUPPORTED, "no projection kernel for this degree");
+  ADMM_CUDA(cudaGetLastError());
+  return ADMM_OK;
+}
+
+}  // extern "C"

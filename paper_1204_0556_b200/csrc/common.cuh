@@ -1,0 +1,66 @@
+// Shared device helpers for the ADMM-LP decoder kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+namespace admm {
+
+// Per-precision constants.  kTol is the facet-test tolerance: the reference's
+// PARITY_TOL = 1e-9 (parity_polytope.py:19) in fp64; in fp32 the value is
+// scaled to single-precision rounding (1e-9 is below one ulp of r >= 1).  The
+// tolerance only decides whether a point within kTol of the facet is left
+// on the cube clip, so the choice is output-continuous.
+template <typename T> struct Num;
+template <> struct Num<float> {
+  static constexpr float kTol = 1e-6f;
+  __device__ __forceinline__ static float inf() { return CUDART_INF_F; }
+};
+template <> struct Num<double> {
+  static constexpr double kTol = 1e-9;
+  __device__ __forceinline__ static double inf() { return CUDART_INF; }
+};
+
+__device__ __forceinline__ float clip01(float v) { return fminf(fmaxf(v, 0.0f), 1.0f); }
+__device__ __forceinline__ double clip01(double v) { return fmin(fmax(v, 0.0), 1.0); }
+__device__ __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ float vmin(float a, float b) { return fminf(a, b); }
+__device__ __forceinline__ double vmax(double a, double b) { return fmax(a, b); }
+__device__ __forceinline__ double vmin(double a, double b) { return fmin(a, b); }
+
+// Compare-exchange primitives used by the generated sorting networks.
+template <typename T> __device__ __forceinline__ void ce_desc(T& a, T& b) {
+  const T hi = vmax(a, b), lo = vmin(a, b);
+  a = hi;
+  b = lo;
+}
+template <typename T> __device__ __forceinline__ void ce_asc(T& a, T& b) {
+  const T lo = vmin(a, b), hi = vmax(a, b);
+  a = lo;
+  b = hi;
+}
+
+// Rounded arithmetic.  fp64 is the parity mode: products and sums are kept
+// separate (no FMA contraction) so every update reproduces the reference's
+// numpy expression tree operation by operation.  fp32 is the throughput mode
+// and lets the compiler contract to FFMA.
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return a * b; }
+__device__ __forceinline__ float add_rn(float a, float b) { return a + b; }
+__device__ __forceinline__ float sub_rn(float a, float b) { return a - b; }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdividef(a, b); }
+
+// Butterfly all-reduce inside a warp.  IEEE addition is commutative, so every
+// lane ends with a bitwise identical sum (lane i adds a_i + a_j, lane j adds
+// a_j + a_i at each level): the convergence decision is uniform.
+template <typename T> __device__ __forceinline__ T warp_allsum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace admm

@@ -1,0 +1,96 @@
+// Host-visible kernel registry: type-erased launchers for every compiled
+// (dtype, degree bucket, checks-per-thread, variable-degree bucket) variant.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "resident.cuh"
+
+namespace admm {
+
+struct ResidentGraphArgs {
+  int n_vars, n_checks, m_pad;
+  const int* chk_var;
+  const uint16_t* var_pos;
+  const uint8_t* var_deg;
+  const int* edge_base;
+};
+
+struct ResidentFrameArgs {
+  long long batch;
+  const void* gamma;
+  long long ld_gamma;
+  double mu, rho, thr;
+  int t_max;
+  const void* z_in;
+  const void* lam_in;
+  long long ld_edge;
+  void* x_out;
+  long long ld_x;
+  uint8_t* hard_out;
+  long long ld_hard;
+  int* iters_out;
+  uint8_t* flags_out;
+  int* weight_out;
+  void* z_out;
+  void* lam_out;
+  int* queue;
+};
+
+using ResidentLaunchFn = void (*)(const ResidentGraphArgs&, const ResidentFrameArgs&, int grid, int nt,
+                                  int smem, cudaStream_t st);
+
+struct ResidentLaunch {
+  const void* fn;
+  ResidentLaunchFn launch;
+  int smem, occupancy, regs;
+};
+
+template <typename T, int D, int CPT, int DVMAX>
+void launch_resident(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int grid, int nt, int smem,
+                     cudaStream_t st) {
+  ResidentParams<T> p;
+  p.n_vars = g.n_vars;
+  p.n_checks = g.n_checks;
+  p.m_pad = g.m_pad;
+  p.chk_var = g.chk_var;
+  p.var_pos = g.var_pos;
+  p.var_deg = g.var_deg;
+  p.edge_base = g.edge_base;
+  p.batch = a.batch;
+  p.gamma = static_cast<const T*>(a.gamma);
+  p.ld_gamma = a.ld_gamma;
+  p.mu = T(a.mu);
+  p.inv_mu = T(1.0 / a.mu);
+  p.rho = T(a.rho);
+  p.one_minus_rho = T(1.0 - a.rho);
+  p.thr = T(a.thr);
+  p.t_max = a.t_max;
+  p.z_in = static_cast<const T*>(a.z_in);
+  p.lam_in = static_cast<const T*>(a.lam_in);
+  p.ld_edge = a.ld_edge;
+  p.x_out = static_cast<T*>(a.x_out);
+  p.ld_x = a.ld_x;
+  p.hard_out = a.hard_out;
+  p.ld_hard = a.ld_hard;
+  p.iters_out = a.iters_out;
+  p.flags_out = a.flags_out;
+  p.weight_out = a.weight_out;
+  p.z_out = static_cast<T*>(a.z_out);
+  p.lam_out = static_cast<T*>(a.lam_out);
+  p.queue = a.queue;
+  resident_decode_kernel<T, D, CPT, DVMAX><<<grid, nt, smem, st>>>(p);
+}
+
+// Defined in resident_f32.cu / resident_f64.cu.
+bool resident_lookup_f32(int D, int CPT, int DVMAX, ResidentLaunch* out);
+bool resident_lookup_f64(int D, int CPT, int DVMAX, ResidentLaunch* out);
+inline bool resident_lookup(int dtype, int D, int CPT, int DVMAX, ResidentLaunch* out) {
+  return dtype ? resident_lookup_f64(D, CPT, DVMAX, out) : resident_lookup_f32(D, CPT, DVMAX, out);
+}
+
+// Defined in project.cu.
+bool launch_project(int dtype, int D, long long m, int d, const void* in, void* out, cudaStream_t st);
+
+}  // namespace admm

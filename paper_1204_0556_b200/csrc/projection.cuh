@@ -1,0 +1,131 @@
+// Exact Euclidean projection onto the parity polytope PP_d, in registers.
+//
+// Contract: the reference's project_batch (parity_polytope.py:352-421).
+//   v  = u sorted descending (stable)                      :366-367
+//   c  = clip(v, 0, 1); r = 2 floor(sum c / 2), r <= d       :368-372
+//   f  = +1 on the top r+1 coordinates, -1 elsewhere          :374
+//   fz = 2 * sum_{k<=r} c_k - sum c                           :375-376
+//   beta_max = (v_r - v_{r+1}) / 2, or v_r when r = d-1       :378-380
+//   inside (return c) when r >= d, fz <= r + TOL, beta_max<=0 :382
+//   otherwise z = clip(v - beta f, 0, 1) with beta the root of
+//   g(beta) = f . clip(v - beta f, 0, 1) = r on [0, beta_max], capped at
+//   beta_max when g stays above r                             :385-414
+//
+// B200 formulation (no grid, no permutation).  Writing s_k for the shift at
+// which coordinate k enters the open band (0,1) -- s_k = u_k - 1 on the +1
+// block and s_k = -u_k on the -1 block -- every coordinate is active on
+// exactly (s_k, s_k + 1), so g(beta) = (r + 1) - sum_k clip(beta - s_k, 0, 1)
+// and g(beta) = r  <=>  sum_k max(beta - s_k, 0) = 1 below the root.  That is
+// water-filling: with s sorted ascending and P_j = 1 + s_(1) + ... + s_(j),
+// every partial line (P_j)/j over-estimates the root and the active prefix
+// attains it, so
+//          beta* = min(beta_max, min_j P_j / j).
+// Two value-only sorting networks (no index payload: f is recovered as
+// u_k >= v_r, exact whenever the row is projected because v_r > v_{r+1}
+// then) and one prefix scan replace the reference's O(d^2) grid evaluation.
+// The result agrees with project_batch to rounding (tests/test_projection*).
+//
+// Degree handling: arrays are sized D (a compile-time bucket); the active
+// degree d <= D is a runtime value and padded slots must hold -inf in u.
+#pragma once
+
+#include "common.cuh"
+#include "sortnet.cuh"
+
+namespace admm {
+
+// Sum of c[0..d) in numpy's pairwise_sum order for short rows: sequential
+// below 8 elements, eight interleaved partial sums combined as a tree and a
+// sequential tail otherwise.  Zeros in padded slots leave the sequential sum
+// unchanged.  Only matters at rounding level (it fixes r = even floor of the
+// l1 norm bit-exactly in fp64 where the norm sits on an even integer).
+template <typename T, int D>
+__device__ __forceinline__ T numpy_rowsum(const T (&c)[D], int d) {
+  T seq = c[0];
+#pragma unroll
+  for (int k = 1; k < D; ++k) seq = add_rn(seq, c[k]);
+  if constexpr (D < 8) {
+    return seq;
+  } else {
+    T acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = c[j];
+    // Full blocks of eight beyond the first (numpy adds block i into lane j).
+    constexpr int kBlocks = D / 8;
+#pragma unroll
+    for (int b = 1; b < kBlocks; ++b) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const bool in = (b * 8 + 8) <= d;  // block fully inside the active row
+        if (in) acc[j] = add_rn(acc[j], c[b * 8 + j]);
+      }
+    }
+    T res = add_rn(add_rn(add_rn(acc[0], acc[1]), add_rn(acc[2], acc[3])),
+                   add_rn(add_rn(acc[4], acc[5]), add_rn(acc[6], acc[7])));
+    const int tail0 = (d / 8) * 8;
+#pragma unroll
+    for (int k = 8; k < D; ++k)
+      if (k >= tail0) res = add_rn(res, c[k]);
+    return d < 8 ? seq : res;
+  }
+}
+
+// Project u (degree d <= D; u[k] = -inf for k >= d) onto PP_d.  z[k] for
+// k >= d is left as 0.  Returns true when the facet test sent the row through
+// the water-filling search (diagnostics only).
+template <typename T, int D>
+__device__ __forceinline__ bool project_pp(const T (&u)[D], T (&z)[D], int d) {
+  T v[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) v[k] = u[k];
+  SortNet<D>::desc(v);
+
+  T c[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) c[k] = clip01(v[k]);
+  const T total = numpy_rowsum<T, D>(c, d);
+  int r = 2 * static_cast<int>(floor(total * T(0.5)));
+  r = r < d ? r : d;
+  const int top = r < d - 1 ? r : d - 1;
+  const int nxt = (r + 1) < (d - 1) ? (r + 1) : (d - 1);
+
+  // Order statistics v_top, v_nxt and the head sum sum_{k<=top} c_k, read
+  // out of the sorted registers with compile-time indices.
+  T v_top = v[0], v_nxt = v[0], head = c[0], run = c[0];
+#pragma unroll
+  for (int k = 1; k < D; ++k) {
+    run = add_rn(run, c[k]);
+    if (k == top) { v_top = v[k]; head = run; }
+    if (k == nxt) v_nxt = v[k];
+  }
+  const T fz = sub_rn(mul_rn(T(2), head), total);
+  const T beta_max = (r <= d - 2) ? mul_rn(T(0.5), sub_rn(v_top, v_nxt)) : v_top;
+  const bool inside = (r >= d) || (fz <= T(r) + Num<T>::kTol) || (beta_max <= T(0));
+
+  if (inside) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) z[k] = (k < d) ? clip01(u[k]) : T(0);
+    return false;
+  }
+
+  // Water-filling for the shift beta (see header comment).
+  T s[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) s[k] = (u[k] >= v_top) ? sub_rn(u[k], T(1)) : -u[k];  // pads: +inf
+  SortNet<D>::asc(s);
+  T beta = beta_max;
+  T p = T(1);
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    p = add_rn(p, s[j]);
+    beta = vmin(beta, mul_rn(p, T(1) / T(j + 1)));
+  }
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const T t = (u[k] >= v_top) ? sub_rn(u[k], beta) : add_rn(u[k], beta);
+    z[k] = (k < d) ? clip01(t) : T(0);
+  }
+  return true;
+}
+
+}  // namespace admm

@@ -1,0 +1,43 @@
+// Instantiation table for one dtype (included by resident_f32.cu / _f64.cu).
+#pragma once
+#include "kernels.cuh"
+
+namespace admm {
+
+template <typename T, int D, int CPT, int DVMAX>
+ResidentLaunch make_entry() {
+  return ResidentLaunch{reinterpret_cast<const void*>(&resident_decode_kernel<T, D, CPT, DVMAX>),
+                        &launch_resident<T, D, CPT, DVMAX>, 0, 0, 0};
+}
+
+template <typename T, int D, int DVMAX>
+bool lookup_cpt(int CPT, ResidentLaunch* out) {
+  switch (CPT) {
+    case 1: *out = make_entry<T, D, 1, DVMAX>(); return true;
+    case 2: *out = make_entry<T, D, 2, DVMAX>(); return true;
+    case 4: *out = make_entry<T, D, 4, DVMAX>(); return true;
+  }
+  return false;
+}
+
+template <typename T, int D>
+bool lookup_dv(int CPT, int DVMAX, ResidentLaunch* out) {
+  if (DVMAX == 4) return lookup_cpt<T, D, 4>(CPT, out);
+  if (DVMAX == 8) return lookup_cpt<T, D, 8>(CPT, out);
+  return false;
+}
+
+template <typename T>
+bool resident_lookup_t(int D, int CPT, int DVMAX, ResidentLaunch* out) {
+  switch (D) {
+    case 4: return lookup_dv<T, 4>(CPT, DVMAX, out);
+    case 6: return lookup_dv<T, 6>(CPT, DVMAX, out);
+    case 8: return lookup_dv<T, 8>(CPT, DVMAX, out);
+    case 13: return lookup_dv<T, 13>(CPT, DVMAX, out);
+    case 16: return lookup_dv<T, 16>(CPT, DVMAX, out);
+    case 32: return CPT == 1 ? lookup_dv<T, 32>(1, DVMAX, out) : false;
+  }
+  return false;
+}
+
+}  // namespace admm

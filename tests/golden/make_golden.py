@@ -1,0 +1,155 @@
+"""Generate the golden fixtures in tests/golden/ from the REFERENCE package.
+
+Run in the build container (the only place /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+Everything stored here is an output of the read-only reference
+``polylp`` (/root/reference/pkg/src/polylp) on seeded inputs; the oracle
+(oracle/admm_oracle.py) and the CUDA path are both checked against these
+files, and neither the GPU tests nor bench.py read /root/reference.
+
+Fixtures
+--------
+projection.npz     project_batch on adversarial rows for d = 1..13 plus the
+                   reference's KAT rows (test_parity_polytope.py:139-157).
+decode_cfg1.npz    BASELINE config 1: (3,6) n=96 from make_ldpc(seed 0,
+                   parallel edges repaired), AWGN 3.0 dB, frames
+                   trial_gamma(seed=1, point=0, trial=t) for t < 1000,
+                   AdmmConfig(mu=5.0): iterations, status, hard decisions,
+                   integral, certificate for all 1000 frames, full x for the
+                   first 200.
+fixed_cfg1.npz     config-1 frames 0..15 decoded for a FIXED number of
+                   iterations (epsilon=1e-300 so eps^2 == 0) T = 1, 50, 1000.
+decode_cfg2.npz    config-2 code (n=1008, girth 6) at 2.0 dB, 24 frames.
+decode_cfg4.npz    config-4 code ((3,13), n=1040, girth 6) at 4.0 dB, 24 frames.
+steps.npz          single-iteration state dumps (x, z, lam) after 1, 2, 3
+                   iterations for one config-1 frame (x_update / z_update /
+                   lambda_update driven directly, as test_admm.py:151-160).
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import polylp  # noqa: E402  (the reference, read-only)
+from polylp import AdmmConfig, decode, project_batch  # noqa: E402
+from polylp.admm_decoder import AdmmState, lambda_update, x_update, z_update  # noqa: E402
+
+from paper_1204_0556_b200.codes import baseline_code  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+
+def ref_code(code):
+    return polylp.ParityCheckMatrix(code.n_vars, [np.asarray(c) for c in code.check_neighborhoods])
+
+
+def pack_checks(code):
+    return code.check_ptr.astype(np.int64), code.edge_var.astype(np.int64)
+
+
+def awgn_frames(code, snr_db, seed, point, trials):
+    ch = polylp.Awgn(snr_db, code.design_rate)
+    out = []
+    for t in trials:
+        rng = np.random.default_rng(np.random.SeedSequence(entropy=seed, spawn_key=(point, t)))
+        y = polylp.transmit(np.zeros(code.n_vars, dtype=np.uint8), ch, rng)
+        out.append(polylp.llr(y, ch))
+    return np.array(out)
+
+
+def projection_fixture():
+    rng = np.random.default_rng(20241020)
+    rec = {}
+    for d in range(1, 14):
+        rows = np.concatenate([
+            rng.uniform(-2.0, 3.0, size=(160, d)),
+            rng.integers(-1, 3, size=(40, d)).astype(float),       # exact ties at 0 / 1
+            np.round(rng.uniform(-1.0, 2.0, size=(40, d)) * 4) / 4,  # quarter grid
+            rng.normal(0.5, 0.6, size=(80, d)),
+        ])
+        rec[f"in_d{d}"] = rows
+        rec[f"out_d{d}"] = project_batch(rows)
+    kat_in = [[1, 1, 0, 0], [1, 0, 0], [1, -0.2], [0, 0, 1], [0.7], [-3.0]]
+    for k, u in enumerate(kat_in):
+        u = np.array([u], dtype=float)
+        rec[f"kat_in_{k}"] = u
+        rec[f"kat_out_{k}"] = project_batch(u)
+    np.savez_compressed(OUT / "projection.npz", **rec)
+
+
+def decode_fixture(name, code, snr_db, n_frames, n_x, cfg):
+    rc = ref_code(code)
+    gam = awgn_frames(code, snr_db, seed=1, point=0, trials=range(n_frames))
+    iters = np.zeros(n_frames, np.int32)
+    status = np.zeros(n_frames, np.uint8)
+    integral = np.zeros(n_frames, np.uint8)
+    cert = np.zeros(n_frames, np.uint8)
+    hard = np.zeros((n_frames, code.n_vars), np.uint8)
+    xs = np.zeros((n_x, code.n_vars))
+    for t in range(n_frames):
+        out = decode(gam[t], rc, cfg)
+        iters[t] = out.iterations
+        status[t] = out.status == polylp.STATUS_CONVERGED
+        integral[t] = out.integral
+        cert[t] = out.ml_certificate
+        hard[t] = out.hard_decision
+        if t < n_x:
+            xs[t] = out.x
+    ptr, ev = pack_checks(code)
+    np.savez_compressed(
+        OUT / name, n_vars=code.n_vars, check_ptr=ptr, edge_var=ev, snr_db=snr_db,
+        mu=cfg.mu, epsilon=cfg.epsilon, t_max=cfg.t_max, rho=cfg.rho,
+        gamma_head=gam[:n_x], iterations=iters, converged=status, integral=integral,
+        certificate=cert, hard=np.packbits(hard, axis=1), x=xs)
+    print(name, "mean iters", iters.mean(), "word errors", int((hard.sum(1) > 0).sum()))
+
+
+def fixed_fixture(code):
+    rc = ref_code(code)
+    gam = awgn_frames(code, 3.0, seed=1, point=0, trials=range(16))
+    rec = {"gamma": gam}
+    for T in (1, 50, 1000):
+        cfg = AdmmConfig(mu=5.0, epsilon=1e-300, t_max=T)
+        rec[f"x_T{T}"] = np.array([decode(g, rc, cfg).x for g in gam])
+    ptr, ev = pack_checks(code)
+    np.savez_compressed(OUT / "fixed_cfg1.npz", n_vars=code.n_vars, check_ptr=ptr, edge_var=ev, **rec)
+
+
+def steps_fixture(code):
+    rc = ref_code(code)
+    gam = awgn_frames(code, 3.0, seed=1, point=0, trials=[7])[0]
+    cfg = AdmmConfig(mu=5.0)
+    st = AdmmState.initial(rc)
+    rec = {"gamma": gam}
+    for t in range(1, 4):
+        x_update(st, rc, gam, cfg)
+        z_update(st, rc, cfg)
+        lambda_update(st, rc, cfg)
+        rec[f"x{t}"] = st.x.copy()
+        rec[f"z{t}"] = st.z.copy()
+        rec[f"lam{t}"] = st.lam.copy()
+    ptr, ev = pack_checks(code)
+    np.savez_compressed(OUT / "steps.npz", n_vars=code.n_vars, check_ptr=ptr, edge_var=ev, **rec)
+
+
+def main():
+    projection_fixture()
+    c1 = baseline_code("cfg1_n96")
+    decode_fixture("decode_cfg1.npz", c1, 3.0, 1000, 200, AdmmConfig(mu=5.0))
+    fixed_fixture(c1)
+    steps_fixture(c1)
+    decode_fixture("decode_cfg2.npz", baseline_code("cfg2_n1008"), 2.0, 24, 24, AdmmConfig(mu=5.0))
+    decode_fixture("decode_cfg4.npz", baseline_code("cfg4_n1040"), 4.0, 24, 24, AdmmConfig(mu=5.0))
+
+
+if __name__ == "__main__":
+    main()

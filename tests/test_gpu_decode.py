@@ -1,0 +1,175 @@
+"""Decoder parity on the GPU against the reference's outputs (golden
+fixtures) and the oracle, through the C ABI."""
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_code, load_golden
+from oracle import admm_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _frames(f, code, n):
+    rate = 1.0 - code.n_checks / code.n_vars
+    return np.array([O.trial_gamma_awgn(code.n_vars, float(f["snr_db"]), rate, 1, 0, t) for t in range(n)])
+
+
+def _cfg(f):
+    from paper_1204_0556_b200 import AdmmConfig
+
+    return AdmmConfig(mu=float(f["mu"]), epsilon=float(f["epsilon"]), t_max=int(f["t_max"]), rho=float(f["rho"]))
+
+
+@pytest.mark.parametrize("name", ["decode_cfg1.npz", "decode_cfg2.npz", "decode_cfg4.npz"])
+def test_f64_decode_matches_reference_golden(cuda_ok, name):
+    """fp64 mode: identical iteration counts, status, hard decisions,
+    integrality and certificates; x within 1e-9 (BASELINE north_star)."""
+    from paper_1204_0556_b200 import decode_batch
+
+    f = load_golden(name)
+    code = golden_code(f)
+    B = len(f["iterations"])
+    gam = _frames(f, code, B)
+    res = decode_batch(gam, code, _cfg(f), dtype=torch.float64, want_hard=True)
+    it = res.iterations.cpu().numpy()
+    fl = res.flags.cpu().numpy()
+    hard = res.hard.cpu().numpy()
+    want_hard = np.unpackbits(f["hard"], axis=1)[:, : code.n_vars]
+    assert np.array_equal(it, f["iterations"])
+    assert np.array_equal((fl & 1) != 0, f["converged"] != 0)
+    assert np.array_equal((fl & 2) != 0, f["integral"] != 0)
+    assert np.array_equal(((fl & 2) != 0) & ((fl & 4) != 0), f["certificate"] != 0)
+    assert np.array_equal(hard, want_hard)
+    nx = len(f["x"])
+    assert np.abs(res.x[:nx].cpu().numpy() - f["x"]).max() <= 1e-9
+    assert np.array_equal(res.weight.cpu().numpy(), want_hard.sum(1))
+
+
+@pytest.mark.parametrize("T", [1, 50, 1000])
+def test_f64_fixed_iterations_match_reference_golden(cuda_ok, T):
+    from paper_1204_0556_b200 import AdmmConfig, decode_batch
+
+    f = load_golden("fixed_cfg1.npz")
+    code = golden_code(f)
+    res = decode_batch(f["gamma"], code, AdmmConfig(mu=5.0, epsilon=1e-300, t_max=T), dtype=torch.float64)
+    assert (res.iterations.cpu().numpy() == T).all()
+    assert np.abs(res.x.cpu().numpy() - f[f"x_T{T}"]).max() <= 1e-9
+
+
+def test_f64_iteration_state_matches_reference_golden(cuda_ok):
+    """x, z, lambda after 1, 2, 3 iterations (AdmmState dumps)."""
+    from paper_1204_0556_b200 import AdmmConfig, run_iterations
+
+    f = load_golden("steps.npz")
+    code = golden_code(f)
+    for t in (1, 2, 3):
+        x, z, lam = run_iterations(f["gamma"], code, AdmmConfig(mu=5.0), t)
+        assert np.abs(x - f[f"x{t}"]).max() <= 1e-12
+        assert np.abs(z - f[f"z{t}"]).max() <= 1e-12
+        assert np.abs(lam - f[f"lam{t}"]).max() <= 1e-12
+
+
+def test_message_passing_single_iteration_from_random_state(cuda_ok):
+    """test_admm.py:208-240: one iteration from arbitrary (z, lambda) equals
+    the oracle's x-/z-/lambda-update."""
+    from paper_1204_0556_b200 import AdmmConfig, make_ldpc, run_iterations
+
+    code = make_ldpc(18, 3, 6, seed=8, girth6=False)
+    rng = np.random.default_rng(9)
+    gamma = rng.normal(0.0, 1.0, 18)
+    z0 = rng.uniform(0, 1, code.n_edges)
+    lam0 = rng.normal(0, 1, code.n_edges)
+    cfg = AdmmConfig(rho=1.0, mu=2.5)
+    x, z, lam = run_iterations(gamma, code, cfg, 1, z0, lam0)
+    g = O.Graph.of(code)
+    p = O.Params(rho=1.0, mu=2.5)
+    xo = O.x_step(z0, lam0, gamma, g, p)
+    zo, w = O.z_step(xo, z0, lam0, g, p)
+    lo = O.lam_step(lam0, w, zo, p)
+    assert np.abs(x - xo).max() <= 1e-12
+    assert np.abs(z - zo).max() <= 1e-9
+    assert np.abs(lam - lo).max() <= 1e-9
+
+
+def test_f32_hard_decisions_match(cuda_ok):
+    """fp32 mode on config 1: >= 99.9% identical hard decisions and
+    frame-error counts within 2 standard errors."""
+    from paper_1204_0556_b200 import decode_batch
+
+    f = load_golden("decode_cfg1.npz")
+    code = golden_code(f)
+    gam = _frames(f, code, 1000)
+    res = decode_batch(gam, code, _cfg(f), dtype=torch.float32, want_hard=True)
+    hard = res.hard.cpu().numpy()
+    want = np.unpackbits(f["hard"], axis=1)[:, : code.n_vars]
+    same = (hard == want).all(axis=1).mean()
+    assert same >= 0.999
+    fe32, fe64 = int((hard.sum(1) > 0).sum()), int((want.sum(1) > 0).sum())
+    w = fe64 / 1000
+    assert abs(fe32 - fe64) / 1000 <= 2 * np.sqrt(2 * w * (1 - w) / 1000) + 1e-3
+
+
+def test_decode_drop_in_api(cuda_ok):
+    from paper_1204_0556_b200 import STATUS_CONVERGED, AdmmConfig, ParityCheckMatrix, decode, make_ldpc
+
+    single = ParityCheckMatrix.from_dense([[1, 1, 1, 1]])
+    out = decode(np.array([2.2, 2.2, -1.0, 2.2]), single)          # test_admm.py:94-102
+    assert out.status == STATUS_CONVERGED and out.integral and out.ml_certificate
+    assert np.allclose(out.x, 0.0, atol=1e-4) and out.hard_decision.tolist() == [0, 0, 0, 0]
+    code = make_ldpc(30, 3, 6, seed=1, girth6=False)
+    out = decode(np.ones(30), code)                                  # test_admm.py:104-110
+    assert out.status == STATUS_CONVERGED and out.integral and out.iterations <= 5
+    with pytest.raises(ValueError):
+        decode(np.ones(3), single)
+    with pytest.raises(ValueError):
+        decode(np.array([1.0, np.inf, 0.0, 0.0]), single)
+    with pytest.raises(ValueError):
+        AdmmConfig(mu=0.0)
+
+
+def test_irregular_and_degree_zero_codes_match_oracle(cuda_ok):
+    from paper_1204_0556_b200 import AdmmConfig, ParityCheckMatrix, decode_batch
+
+    codes = [
+        ParityCheckMatrix.from_dense([[1, 1, 0, 1, 1, 0, 0], [1, 0, 1, 1, 0, 1, 0], [0, 1, 1, 1, 0, 0, 1]]),
+        ParityCheckMatrix.from_dense([[1, 1], [1, 1], [1, 1]]),
+        ParityCheckMatrix(6, [[0, 1, 2], [1, 2, 3, 4]]),          # variable 5 has degree 0
+        ParityCheckMatrix(20, [list(range(0, 9)), list(range(5, 20)), [0, 7, 19]]),
+    ]
+    rng = np.random.default_rng(3)
+    for code in codes:
+        gam = rng.normal(0.5, 1.2, (40, code.n_vars))
+        cfg = AdmmConfig(mu=3.0, t_max=300)
+        res = decode_batch(gam, code, cfg, dtype=torch.float64)
+        g = O.Graph.of(code)
+        for t in range(len(gam)):
+            r = O.decode(gam[t], g, O.Params(mu=3.0, t_max=300))
+            assert int(res.iterations[t]) == r.iterations
+            assert np.abs(res.x[t].cpu().numpy() - r.x).max() <= 1e-9
+
+
+def test_determinism_and_batch_invariance(cuda_ok):
+    from paper_1204_0556_b200 import AdmmConfig, baseline_code, decode_batch
+
+    code = baseline_code("cfg2_n1008")
+    g = torch.randn(300, code.n_vars, device="cuda", generator=torch.Generator("cuda").manual_seed(0)) * 2.4 + 3.0
+    cfg = AdmmConfig(mu=5.0)
+    for dt in (torch.float32, torch.float64):
+        a = decode_batch(g, code, cfg, dtype=dt)
+        b = decode_batch(g, code, cfg, dtype=dt)
+        c = decode_batch(g[100:140], code, cfg, dtype=dt)
+        assert torch.equal(a.x, b.x) and torch.equal(a.iterations, b.iterations)
+        assert torch.equal(a.x[100:140], c.x) and torch.equal(a.iterations[100:140], c.iterations)
+
+
+def test_empty_batch_and_shape_errors(cuda_ok):
+    from paper_1204_0556_b200 import baseline_code, decode_batch
+
+    code = baseline_code("cfg1_n96")
+    res = decode_batch(np.zeros((0, 96)), code)
+    assert res.iterations.numel() == 0
+    with pytest.raises(ValueError):
+        decode_batch(np.zeros((3, 95)), code)
+    with pytest.raises(ValueError):
+        decode_batch(np.full((2, 96), np.nan), code)
