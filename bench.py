@@ -148,7 +148,7 @@ def run_reference(args):
 
     code = baseline_code("cfg2_n1008")
     workers = os.cpu_count() or 1
-    fpp = args.cpu_frames or max(8, 4 * math.ceil(workers / 7))
+    fpp = args.cpu_frames or 16 * workers
     times, frames, eus = [], 0, 0
     for s in range(args.warmup + args.steps):
         dt, nf, eu = cpu_sample(code, fpp, workers, seed_base=s * fpp)
@@ -306,7 +306,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         workers = os.cpu_count() or 1
-        fpp = args.cpu_frames or max(8, 4 * math.ceil(workers / 7))
+        fpp = args.cpu_frames or 16 * workers
         dt, nf, eu = cpu_sample(code, fpp, workers)
         cpu = {"value": nf / dt, "unit": "frames/s", "cores": workers, "kind": "port",
                "edge_updates_per_s": eu / dt,

@@ -51,7 +51,7 @@ typedef struct admm_graph admm_graph;
 typedef struct admm_graph_info {
   int32_t n_vars, n_checks, n_edges;
   int32_t max_check_degree, max_var_degree;
-  int32_t engine;           /* 1 = resident (on-chip persistent) */
+  int32_t engine;           /* 1 = resident generic, 2 = resident regular-code fast path */
   int32_t degree_bucket;    /* D: compiled check-degree bucket   */
   int32_t checks_per_thread;
   int32_t threads_per_cta;

@@ -180,8 +180,13 @@ def launch(dg: DeviceGraph, code_dt: int, g: torch.Tensor, config: AdmmConfig, i
     """Enqueue one ``admm_decode_batch`` on caller-owned device buffers (no
     allocation, no validation beyond the C ABI's)."""
     N, E = dg.code.n_vars, dg.code.n_edges
+    if g.shape[0] == 0:
+        return
+    if g.stride(1) != 1:
+        raise ValueError("LLR rows must be contiguous")
+    ld = g.stride(0) if g.shape[0] > 1 else N  # a single row may carry any stride(0)
     _lib.check(_lib.load().admm_decode_batch(
-        dg.handle, code_dt, g.shape[0], g.data_ptr(), g.stride(0),
+        dg.handle, code_dt, g.shape[0], g.data_ptr(), ld,
         float(config.mu), float(config.epsilon), int(config.t_max), float(config.rho),
         _ptr(x), N if x is None else x.stride(0), _ptr(hard), N if hard is None else hard.stride(0),
         iters.data_ptr(), flags.data_ptr(), weight.data_ptr(),
@@ -223,7 +228,7 @@ def decode_batch(
     if g.ndim != 2 or g.shape[1] != code.n_vars:
         raise ValueError(f"expected a [B, {code.n_vars}] block of LLR vectors")
     g = g.to(device=dev, dtype=tdt, non_blocking=True)
-    if not g.is_contiguous():
+    if not g.is_contiguous() or (g.shape[0] > 1 and g.stride(0) != g.shape[1]):
         g = g.contiguous()
     if validate and not bool(torch.isfinite(g).all()):
         raise ValueError("LLR vector must be finite")

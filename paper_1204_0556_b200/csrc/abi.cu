@@ -34,13 +34,15 @@ struct admm_graph {
   int device = 0;
   int n_vars = 0, n_checks = 0, n_edges = 0;
   int dmax = 0, dvmax_actual = 0;
-  int D = 0, DVMAX = 0, CPT = 0, NT = 0, m_pad = 0;
+  int D = 0, DVMAX = 0, CPT = 0, NT = 0, m_pad = 0, VPT = 0;
+  int kind = 0;  // 1 = generic resident, 2 = regular resident
   int num_sms = 0;
   // device arrays
   int* chk_var = nullptr;
   uint16_t* var_pos = nullptr;
   uint8_t* var_deg = nullptr;
   int* edge_base = nullptr;
+  int* var_edge = nullptr;
   // per-dtype launch data
   admm::ResidentLaunch launch[2];
 };
@@ -113,38 +115,62 @@ int admm_graph_create(int device, int32_t n_vars, int32_t n_checks, const int32_
   int smem_optin = 0;
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
 
-  // Kernel shape: smallest checks-per-thread whose CTA fits 512 threads, the
-  // 16-bit message positions, the register file and shared memory.
-  bool placed = false;
-  for (int cpt : {1, 2, 4}) {
-    const int nt = ((n_checks + cpt - 1) / cpt + 31) / 32 * 32;
-    if (nt > 512) continue;
+  bool regular = true;
+  for (int c = 0; c < n_checks && regular; ++c) regular = (int)rows[c].size() == dmax;
+  for (int v = 0; v < n_vars && regular; ++v) regular = vdeg[v] == dvmax;
+
+  // Validate one candidate launch shape for both dtypes and record it.
+  auto try_shape = [&](bool reg, int cpt, int nt, int* vpt_out) -> bool {
     const int m_pad = nt * cpt;
-    if ((long long)g->D * m_pad >= 65535) continue;
-    bool ok = true;
-    for (int dt = 0; dt < 2 && ok; ++dt) {
+    admm::ResidentLaunch Ls[2];
+    int vpt = 0;
+    for (int dt = 0; dt < 2; ++dt) {
       admm::ResidentLaunch L{};
-      if (!admm::resident_lookup(dt, g->D, cpt, g->DVMAX, &L)) { ok = false; break; }
-      const admm::ResidentSmem S(dt ? 8 : 4, n_vars, g->D * m_pad, g->DVMAX);
-      if (S.total > smem_optin) { ok = false; break; }
+      int smem = 0;
+      if (reg) {
+        const int need = (n_vars + nt - 1) / nt;
+        if (!admm::regular_lookup(dt, dmax, dvmax, cpt, need, &vpt, &L)) return false;
+        smem = admm::regular_smem_bytes(dt ? 8 : 4, dmax, n_vars, m_pad);
+      } else {
+        if ((long long)g->D * m_pad >= 65535) return false;
+        if (!admm::resident_lookup(dt, g->D, cpt, g->DVMAX, &L)) return false;
+        smem = admm::ResidentSmem(dt ? 8 : 4, n_vars, g->D * m_pad, g->DVMAX).total;
+      }
+      if (smem > smem_optin) return false;
       cudaFuncAttributes fa{};
-      if (cudaFuncGetAttributes(&fa, L.fn) != cudaSuccess) { ok = false; break; }
-      if (fa.numRegs * nt > 65536 || nt > fa.maxThreadsPerBlock) { ok = false; break; }
-      cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, S.total);
+      if (cudaFuncGetAttributes(&fa, L.fn) != cudaSuccess) return false;
+      if (fa.numRegs * nt > 65536 || nt > fa.maxThreadsPerBlock) return false;
+      if (cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
       int occ = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L.fn, nt, S.total);
-      if (occ < 1) { ok = false; break; }
-      L.smem = S.total;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L.fn, nt, smem);
+      if (occ < 1) return false;
+      L.smem = smem;
       L.occupancy = occ;
       L.regs = fa.numRegs;
-      g->launch[dt] = L;
+      Ls[dt] = L;
     }
-    if (!ok) continue;
-    g->CPT = cpt;
-    g->NT = nt;
-    g->m_pad = m_pad;
-    placed = true;
-    break;
+    g->launch[0] = Ls[0];
+    g->launch[1] = Ls[1];
+    *vpt_out = vpt;
+    return true;
+  };
+
+  bool placed = false;
+  for (int pass = regular ? 0 : 1; pass < 2 && !placed; ++pass) {
+    const bool reg = pass == 0;
+    for (int cpt : {1, 2, 3, 4}) {
+      const int nt = ((n_checks + cpt - 1) / cpt + 31) / 32 * 32;
+      if (nt > 512) continue;
+      int vpt = 0;
+      if (!try_shape(reg, cpt, nt, &vpt)) continue;
+      g->kind = reg ? 2 : 1;
+      g->CPT = cpt;
+      g->NT = nt;
+      g->m_pad = nt * cpt;
+      g->VPT = vpt;
+      placed = true;
+      break;
+    }
   }
   cudaGetLastError();
   if (!placed) {
@@ -164,6 +190,15 @@ int admm_graph_create(int device, int32_t n_vars, int32_t n_checks, const int32_
       var_slots[rows[c][k]].push_back((int)k * MP + c);  // appended in increasing check order
     }
   }
+  std::vector<int> var_edge((size_t)n_vars * dvmax, -1);
+  {
+    std::vector<int> fill(n_vars, 0);
+    for (int c = 0; c < n_checks; ++c)
+      for (size_t k = 0; k < rows[c].size(); ++k) {
+        const int v = rows[c][k];
+        var_edge[(size_t)v * dvmax + fill[v]++] = check_ptr[c] + (int)k;  // increasing edge id
+      }
+  }
   std::vector<uint16_t> var_pos((size_t)n_vars * g->DVMAX, 0);
   std::vector<uint8_t> var_deg(n_vars);
   for (int v = 0; v < n_vars; ++v) {
@@ -179,7 +214,8 @@ int admm_graph_create(int device, int32_t n_vars, int32_t n_checks, const int32_
   cudaError_t e2 = up((void**)&g->var_pos, var_pos.data(), var_pos.size() * sizeof(uint16_t));
   cudaError_t e3 = up((void**)&g->var_deg, var_deg.data(), var_deg.size());
   cudaError_t e4 = up((void**)&g->edge_base, edge_base.data(), edge_base.size() * sizeof(int));
-  for (cudaError_t e : {e1, e2, e3, e4}) {
+  cudaError_t e5 = up((void**)&g->var_edge, var_edge.data(), var_edge.size() * sizeof(int));
+  for (cudaError_t e : {e1, e2, e3, e4, e5}) {
     if (e != cudaSuccess) {
       admm_graph_destroy(g);
       return cuda_fail(e, "graph upload");
@@ -196,6 +232,7 @@ int admm_graph_destroy(admm_graph* g) {
   cudaFree(g->var_pos);
   cudaFree(g->var_deg);
   cudaFree(g->edge_base);
+  cudaFree(g->var_edge);
   delete g;
   return ADMM_OK;
 }
@@ -208,7 +245,7 @@ int admm_graph_get_info(const admm_graph* g, admm_graph_info* info) {
   info->n_edges = g->n_edges;
   info->max_check_degree = g->dmax;
   info->max_var_degree = g->dvmax_actual;
-  info->engine = 1;
+  info->engine = g->kind;
   info->degree_bucket = g->D;
   info->checks_per_thread = g->CPT;
   info->threads_per_cta = g->NT;
@@ -261,7 +298,8 @@ int admm_decode_batch(const admm_graph* g, int dtype, int64_t batch, const void*
   const long long grid = std::min<long long>(batch, (long long)L.occupancy * g->num_sms);
   const double thr = epsilon * epsilon * (double)g->n_edges;  // admm_decoder.py:169
 
-  admm::ResidentGraphArgs ga{g->n_vars, g->n_checks, g->m_pad, g->chk_var, g->var_pos, g->var_deg, g->edge_base};
+  admm::ResidentGraphArgs ga{g->n_vars, g->n_checks, g->m_pad, g->chk_var, g->var_pos, g->var_deg,
+                             g->edge_base, g->var_edge};
   admm::ResidentFrameArgs fa{batch, gamma, ld_gamma, mu, rho, thr, t_max, z_in, lam_in, ld_edge,
                              x_out, ld_x, hard_out, ld_hard, iters_out, flags_out, weight_out,
                              z_out, lam_out, reinterpret_cast<int*>(workspace)};

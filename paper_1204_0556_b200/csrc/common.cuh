@@ -22,7 +22,7 @@ template <> struct Num<double> {
   __device__ __forceinline__ static double inf() { return CUDART_INF; }
 };
 
-__device__ __forceinline__ float clip01(float v) { return fminf(fmaxf(v, 0.0f), 1.0f); }
+__device__ __forceinline__ float clip01(float v) { return __saturatef(v); }  // [0,1]; -inf -> 0
 __device__ __forceinline__ double clip01(double v) { return fmin(fmax(v, 0.0), 1.0); }
 __device__ __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
 __device__ __forceinline__ float vmin(float a, float b) { return fminf(a, b); }
@@ -61,6 +61,30 @@ template <typename T> __device__ __forceinline__ T warp_allsum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// 32-bit shared-memory addressing.  Addresses are computed once (per CTA or
+// per frame) and kept in registers, so the hot loops issue bare LDS/STS with
+// no generic-to-shared conversion.  The "memory" clobber keeps the compiler
+// from moving them across __syncthreads().
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ float lds(uint32_t a, float) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ double lds(uint32_t a, double) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void sts(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
 
 }  // namespace admm

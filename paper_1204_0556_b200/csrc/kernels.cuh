@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include "resident.cuh"
+#include "resident_regular.cuh"
 
 namespace admm {
 
@@ -15,6 +16,7 @@ struct ResidentGraphArgs {
   const uint16_t* var_pos;
   const uint8_t* var_deg;
   const int* edge_base;
+  const int* var_edge;  // [n_vars][DV] reference edge ids (regular kernels)
 };
 
 struct ResidentFrameArgs {
@@ -47,9 +49,8 @@ struct ResidentLaunch {
   int smem, occupancy, regs;
 };
 
-template <typename T, int D, int CPT, int DVMAX>
-void launch_resident(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int grid, int nt, int smem,
-                     cudaStream_t st) {
+template <typename T>
+ResidentParams<T> make_params(const ResidentGraphArgs& g, const ResidentFrameArgs& a) {
   ResidentParams<T> p;
   p.n_vars = g.n_vars;
   p.n_checks = g.n_checks;
@@ -80,7 +81,26 @@ void launch_resident(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int
   p.z_out = static_cast<T*>(a.z_out);
   p.lam_out = static_cast<T*>(a.lam_out);
   p.queue = a.queue;
-  resident_decode_kernel<T, D, CPT, DVMAX><<<grid, nt, smem, st>>>(p);
+  return p;
+}
+
+template <typename T, int D, int CPT, int DVMAX>
+void launch_resident(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int grid, int nt, int smem,
+                     cudaStream_t st) {
+  resident_decode_kernel<T, D, CPT, DVMAX><<<grid, nt, smem, st>>>(make_params<T>(g, a));
+}
+
+template <typename T, int D, int DV, int CPT, int VPT, int MINB>
+void launch_regular(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int grid, int nt, int smem,
+                    cudaStream_t st) {
+  resident_regular_kernel<T, D, DV, CPT, VPT, MINB><<<grid, nt, smem, st>>>(make_params<T>(g, a), g.var_edge);
+}
+
+// Regular-code variants: (D, DV, CPT, VPT).  Returns false when none fits.
+bool regular_lookup_f32(int D, int DV, int CPT, int VPT_min, int* VPT, ResidentLaunch* out);
+bool regular_lookup_f64(int D, int DV, int CPT, int VPT_min, int* VPT, ResidentLaunch* out);
+inline bool regular_lookup(int dtype, int D, int DV, int CPT, int VPT_min, int* VPT, ResidentLaunch* out) {
+  return dtype ? regular_lookup_f64(D, DV, CPT, VPT_min, VPT, out) : regular_lookup_f32(D, DV, CPT, VPT_min, VPT, out);
 }
 
 // Defined in resident_f32.cu / resident_f64.cu.

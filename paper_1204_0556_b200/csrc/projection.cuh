@@ -128,4 +128,53 @@ __device__ __forceinline__ bool project_pp(const T (&u)[D], T (&z)[D], int d) {
   return true;
 }
 
+// Fixed-degree variant used by the regular-code kernels: d == D at compile
+// time, no padding, and branch-free -- a row that passes the facet test gets
+// beta = 0, and clip(u - 0 * f) is exactly the cube clip the reference
+// returns for it (:418).  Same contract as project_pp.
+template <typename T, int D>
+__device__ __forceinline__ void project_pp_fixed(const T (&u)[D], T (&z)[D]) {
+  T v[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) v[k] = u[k];
+  SortNet<D>::desc(v);
+  T c[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) c[k] = clip01(v[k]);
+  const T total = numpy_rowsum<T, D>(c, D);
+  const int r = 2 * static_cast<int>(floor(total * T(0.5)));
+  // Projected rows have r even and r <= D - 1, so r indexes an even slot.
+  T v_top = v[0], v_nxt = v[D > 1 ? 1 : 0], head = c[0], run = c[0];
+#pragma unroll
+  for (int k = 1; k < D; ++k) {
+    run = add_rn(run, c[k]);
+    if ((k & 1) == 0 && k == r) {
+      v_top = v[k];
+      v_nxt = v[k + 1 < D ? k + 1 : k];
+      head = run;
+    }
+  }
+  const T fz = sub_rn(mul_rn(T(2), head), total);
+  const T beta_max = (r <= D - 2) ? mul_rn(T(0.5), sub_rn(v_top, v_nxt)) : v_top;
+  const bool inside = (r >= D) || (fz <= T(r) + Num<T>::kTol) || (beta_max <= T(0));
+
+  bool up[D];
+  T s[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    up[k] = u[k] >= v_top;
+    s[k] = up[k] ? sub_rn(u[k], T(1)) : -u[k];
+  }
+  SortNet<D>::asc(s);
+  T beta = beta_max, p = T(1);
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    p = add_rn(p, s[j]);
+    beta = vmin(beta, mul_rn(p, T(1) / T(j + 1)));
+  }
+  beta = inside ? T(0) : beta;
+#pragma unroll
+  for (int k = 0; k < D; ++k) z[k] = clip01(up[k] ? sub_rn(u[k], beta) : add_rn(u[k], beta));
+}
+
 }  // namespace admm

@@ -40,4 +40,32 @@ bool resident_lookup_t(int D, int CPT, int DVMAX, ResidentLaunch* out) {
   return false;
 }
 
+template <typename T, int D, int DV, int CPT, int VPT>
+ResidentLaunch make_regular() {
+  constexpr int MINB = (sizeof(T) == 4 && CPT == 1 && D <= 8) ? 2 : 1;
+  return ResidentLaunch{reinterpret_cast<const void*>(&resident_regular_kernel<T, D, DV, CPT, VPT, MINB>),
+                        &launch_regular<T, D, DV, CPT, VPT, MINB>, 0, 0, 0};
+}
+
+// The compiled regular shapes.  VPT is the smallest compiled value >= the
+// variables-per-thread the graph needs.
+template <typename T>
+bool regular_lookup_t(int D, int DV, int CPT, int VPT_min, int* VPT, ResidentLaunch* out) {
+#define ADMM_REG(d, dv, cpt, vpt)                                         \
+  if (D == d && DV == dv && CPT == cpt && VPT_min <= vpt) {               \
+    *VPT = vpt;                                                           \
+    *out = make_regular<T, d, dv, cpt, vpt>();                            \
+    return true;                                                          \
+  }
+  ADMM_REG(6, 3, 1, 2)
+  ADMM_REG(6, 3, 2, 4)
+  ADMM_REG(6, 3, 3, 6)
+  ADMM_REG(6, 3, 4, 8)
+  ADMM_REG(13, 3, 1, 5)
+  ADMM_REG(4, 2, 1, 2)
+  ADMM_REG(4, 3, 1, 2)
+#undef ADMM_REG
+  return false;
+}
+
 }  // namespace admm

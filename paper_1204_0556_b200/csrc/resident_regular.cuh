@@ -1,0 +1,232 @@
+// Resident engine, regular-code fast path: every check has degree D and
+// every variable degree DV (the (3,6) and (3,13) BASELINE codes).
+//
+// Same algorithm and frame scheduling as resident_decode_kernel
+// (resident.cuh); what changes is how the work maps onto the SM:
+//   * all degrees are compile-time, so the projection is branch-free
+//     (project_pp_fixed) and no per-edge degree tests exist;
+//   * every shared-memory address a thread touches in the hot loop -- the D
+//     x-gather addresses of its checks, the DV message addresses of its
+//     variables, its own message row and x slots -- is computed once per CTA
+//     and kept in registers as a 32-bit shared address (bare LDS/STS);
+//   * the messages are stored check-major with an odd row stride
+//     (msg[c * DS + k], DS = D or D+1) so a warp's stores hit 32 distinct
+//     banks and the row offset is an instruction immediate;
+//   * each thread owns VPT variables whose LLR/mu stays in registers;
+//   * the stop rule runs as one barrier-reduction (__syncthreads_or): if any
+//     thread's own partial residual sum already reaches eps^2 * E the frame
+//     cannot have converged (sums of non-negative terms are monotone under
+//     round-to-nearest), and the exact full sum is only formed when every
+//     partial is below the threshold.
+#pragma once
+
+#include "resident.cuh"
+
+namespace admm {
+
+template <int D>
+struct MsgStride {
+  static constexpr int value = (D % 2 == 0) ? D + 1 : D;
+};
+
+template <typename T, int D, int DV, int CPT, int VPT, int MINB>
+__global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const ResidentParams<T> p,
+                                                                     const int* __restrict__ var_edge) {
+  constexpr int DS = MsgStride<D>::value;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int N = p.n_vars, M = p.n_checks;
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = NT >> 5;
+  const int MP = NT * CPT;
+  T* msg = reinterpret_cast<T*>(smem_raw);
+  T* xs = msg + MP * DS;
+  T* red = xs + ((N + 1) & ~1);
+  int* s_int = reinterpret_cast<int*>(red + 64);  // [0] frame, [1] weight
+  const uint32_t msg_a = smem_u32(msg), xs_a = smem_u32(xs);
+  constexpr uint32_t ES = sizeof(T);
+
+  // ---- per-thread graph registers (once per CTA) ----
+  uint32_t xaddr[CPT][D];
+  uint32_t mrow[CPT];
+  bool cact[CPT];
+#pragma unroll
+  for (int q = 0; q < CPT; ++q) {
+    const int c = tid + q * NT;
+    cact[q] = c < M;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const int v = cact[q] ? __ldg(p.chk_var + k * p.m_pad + c) : 0;
+      xaddr[q][k] = xs_a + ES * v;
+    }
+    mrow[q] = msg_a + ES * (c * DS);
+  }
+  uint32_t vaddr[VPT][DV];
+  uint32_t xst[VPT];
+  bool vact[VPT];
+#pragma unroll
+  for (int q = 0; q < VPT; ++q) {
+    const int i = tid + q * NT;
+    vact[q] = i < N;
+#pragma unroll
+    for (int j = 0; j < DV; ++j) {
+      const int e = vact[q] ? __ldg(var_edge + i * DV + j) : 0;  // reference edge id = c * D + k
+      vaddr[q][j] = msg_a + ES * ((e / D) * DS + (e % D));
+    }
+    xst[q] = xs_a + ES * i;
+  }
+
+  const T inv_mu = p.inv_mu;
+  constexpr bool kF64 = sizeof(T) == 8;
+  T z[CPT][D], lam[CPT][D];
+  T gm[VPT];
+
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) {
+      s_int[0] = atomicAdd(p.queue, 1);
+      s_int[1] = 0;
+    }
+    __syncthreads();
+    const long long f = s_int[0];
+    if (f >= p.batch) break;
+
+    // ---- frame setup ----
+    const T* g = p.gamma + f * p.ld_gamma;
+#pragma unroll
+    for (int q = 0; q < VPT; ++q) gm[q] = vact[q] ? div_rn(g[tid + q * NT], p.mu) : T(0);
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) {
+      const int c = tid + q * NT;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        T z0 = T(0), l0 = T(0);
+        if (p.z_in != nullptr && cact[q]) {
+          const long long e = f * p.ld_edge + (long long)c * D + k;
+          z0 = p.z_in[e];
+          l0 = p.lam_in[e];
+        }
+        z[q][k] = z0;
+        lam[q][k] = l0;
+        if (cact[q]) sts(mrow[q] + ES * k, sub_rn(z0, kF64 ? div_rn(l0, p.mu) : mul_rn(l0, inv_mu)));
+      }
+    }
+    __syncthreads();
+
+    int t = 0;
+    bool converged = false;
+    while (t < p.t_max) {
+      ++t;
+      // ---- x-update (admm_decoder.py:108-124): edges summed in edge order ----
+#pragma unroll
+      for (int q = 0; q < VPT; ++q) {
+        if (vact[q]) {
+          T acc = lds(vaddr[q][0], T());
+#pragma unroll
+          for (int j = 1; j < DV; ++j) acc = add_rn(acc, lds(vaddr[q][j], T()));
+          const T num = sub_rn(acc, gm[q]);
+          const T xv = clip01(kF64 ? div_rn(num, T(DV)) : mul_rn(num, T(1) / T(DV)));
+          sts(xst[q], xv);
+        }
+      }
+      __syncthreads();
+
+      // ---- fused z-update, projection, residuals, lambda-update ----
+      T primal = T(0), moved = T(0);
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) {
+        if (cact[q]) {
+          T gx[D], w[D], u[D], zn[D];
+#pragma unroll
+          for (int k = 0; k < D; ++k) gx[k] = lds(xaddr[q][k], T());
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            w[k] = add_rn(mul_rn(p.rho, gx[k]), mul_rn(p.one_minus_rho, z[q][k]));
+            u[k] = add_rn(w[k], kF64 ? div_rn(lam[q][k], p.mu) : mul_rn(lam[q][k], inv_mu));
+          }
+          project_pp_fixed<T, D>(u, zn);
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            const T r1 = sub_rn(gx[k], zn[k]);
+            const T r2 = sub_rn(zn[k], z[q][k]);
+            primal = add_rn(primal, mul_rn(r1, r1));
+            moved = add_rn(moved, mul_rn(r2, r2));
+            lam[q][k] = add_rn(lam[q][k], mul_rn(p.mu, sub_rn(w[k], zn[k])));
+            z[q][k] = zn[k];
+            sts(mrow[q] + ES * k, sub_rn(zn[k], kF64 ? div_rn(lam[q][k], p.mu) : mul_rn(lam[q][k], inv_mu)));
+          }
+        }
+      }
+      // ---- stop rule (admm_decoder.py:169,174-181) ----
+      if (__syncthreads_or(primal >= p.thr || moved >= p.thr)) continue;
+      primal = warp_allsum(primal);
+      moved = warp_allsum(moved);
+      if (lane == 0) {
+        red[2 * warp] = primal;
+        red[2 * warp + 1] = moved;
+      }
+      __syncthreads();
+      T a = lane < nwarps ? red[2 * lane] : T(0);
+      T b = lane < nwarps ? red[2 * lane + 1] : T(0);
+      a = warp_allsum(a);
+      b = warp_allsum(b);
+      if (a < p.thr && b < p.thr) {
+        converged = true;
+        break;
+      }
+    }
+
+    // ---- outputs (make_output, admm_decoder.py:92-105; is_codeword, codes.py:145-154) ----
+    bool integral = true;
+    int ones = 0;
+#pragma unroll
+    for (int q = 0; q < VPT; ++q) {
+      if (vact[q]) {
+        const int i = tid + q * NT;
+        const T xv = lds(xst[q], T());
+        const bool h = xv > T(0.5);
+        ones += h;
+        integral &= vmin(fabs(xv), fabs(T(1) - xv)) <= T(1e-5);
+        if (p.x_out) p.x_out[f * p.ld_x + i] = xv;
+        if (p.hard_out) p.hard_out[f * p.ld_hard + i] = h;
+      }
+    }
+    bool odd = false;
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) {
+      if (cact[q]) {
+        const int c = tid + q * NT;
+        int par = 0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) par ^= (lds(xaddr[q][k], T()) > T(0.5));
+        odd |= par;
+        if (p.z_out) {
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            const long long e = f * p.ld_edge + (long long)c * D + k;
+            p.z_out[e] = z[q][k];
+            p.lam_out[e] = lam[q][k];
+          }
+        }
+      }
+    }
+    ones = __reduce_add_sync(0xffffffffu, ones);
+    if (lane == 0 && ones) atomicAdd(s_int + 1, ones);
+    const int all_integral = __syncthreads_and(integral);
+    const int any_odd = __syncthreads_or(odd);
+    if (tid == 0) {
+      if (p.iters_out) p.iters_out[f] = t;
+      if (p.flags_out)
+        p.flags_out[f] = (converged ? kFlagConverged : 0) | (all_integral ? kFlagIntegral : 0) |
+                         (any_odd ? 0 : kFlagCodeword);
+      if (p.weight_out) p.weight_out[f] = s_int[1];
+    }
+  }
+}
+
+// Shared memory of the regular kernel (bytes).
+inline int regular_smem_bytes(int elem, int D, int n_vars, int m_pad) {
+  const int ds = (D % 2 == 0) ? D + 1 : D;
+  return elem * (m_pad * ds + ((n_vars + 1) & ~1) + 64) + 16;
+}
+
+}  // namespace admm
