@@ -245,18 +245,15 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
 
-    # statistics of the last step, merged with ONE all-reduce of int64 counters
-    cnt = torch.zeros(6, dtype=torch.int64, device=dev)
-    for o in outs:
-        w = o.weight.to(torch.int64)
-        err = w > 0
-        it = o.iterations.to(torch.int64)
-        cnt += torch.stack([torch.tensor(o.iterations.numel(), device=dev), err.sum(), w.sum(),
-                            torch.where(err, 0, it).sum(), torch.where(err, it, 0).sum(),
-                            o.converged.sum()])
-    if world > 1:
-        dist.all_reduce(cnt)
-    cnt = cnt.cpu().tolist()
+    # statistics of one step, merged with ONE all-reduce of int64 counters
+    from paper_1204_0556_b200.distributed import allreduce_counters, counters_as_dict, counters_from_results
+
+    cnt = torch.zeros(8, dtype=torch.int64, device=dev)
+    for k in range(len(POINTS_DB)):
+        o = decode_batch(gam[k], code, cfg, dtype=tdt, want_x=False, want_hard=True, validate=False)
+        cost = (gam[k].to(torch.float64) * o.hard.to(torch.float64)).sum(dim=1)
+        cnt += counters_from_results(o.iterations, o.weight, o.converged, o.codeword, cost, code.n_edges)
+    cnt = counters_as_dict(allreduce_counters(cnt))
 
     frames_per_step = F * len(POINTS_DB)
     value = world * frames_per_step * args.steps / elapsed
@@ -274,7 +271,8 @@ def run_ours(args):
     tpath = ROOT / "profiles" / "traffic.json"
     if tpath.exists():
         try:
-            traffic = json.loads(tpath.read_text()).get(f"bytes_per_launch_{args.dtype}")
+            bpf = json.loads(tpath.read_text()).get(f"bytes_per_frame_{args.dtype}")
+            traffic = None if bpf is None else bpf * F  # ncu DRAM bytes per frame x frames per launch
         except Exception:
             traffic = None
 
@@ -326,13 +324,16 @@ def run_ours(args):
                        "engine": info},
             "edge_updates_per_s": eu_total,
             "mean_iterations": iters_sum / frames_per_step,
-            "stats_last_step": dict(zip(["trials", "word_errors", "bit_errors", "iter_sum_correct",
-                                         "iter_sum_erroneous", "converged"], cnt)),
+            "stats_one_step_all_ranks": cnt,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "bytes_model": f"{bpe} B per edge-update (two-kernel HBM schedule, SURVEY 8d) x "
                                         f"{edge_updates // len(POINTS_DB)} edge-updates per launch",
-                         "kernel": "resident_decode_kernel", "avg_launch_ms": launch_s * 1e3},
+                         "kernel": f"resident engine {info.get('engine')} (1 generic, 2 regular)",
+                         "avg_launch_ms": launch_s * 1e3,
+                         "note": "fused on-chip design: the HBM-model bytes are never moved (edge state stays in "
+                                 "registers/SMEM); `traffic` is the ncu DRAM bytes per launch; the real bound is SM "
+                                 "instruction issue (DESIGN.md 3.4)"},
             "gpu_launches": args.steps * len(POINTS_DB),
             "clocks": clk,
             "e2e": e2e,
