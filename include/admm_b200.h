@@ -46,12 +46,19 @@ enum admm_status {
 #define ADMM_FLAG_INTEGRAL 2u  /* all |x - round(x)| <= 1e-5 (admm_decoder.py:96) */
 #define ADMM_FLAG_CODEWORD 4u  /* hard decision satisfies every check           */
 
+/* Engine selection for admm_graph_create_ex. */
+enum admm_engine {
+  ADMM_ENGINE_AUTO = 0,      /* resident if the code fits one SM, else streaming */
+  ADMM_ENGINE_RESIDENT = 1,  /* one CTA per frame, state on chip (fails if it does not fit) */
+  ADMM_ENGINE_STREAMING = 3  /* batch-interleaved L2-resident state, cooperative kernel */
+};
+
 typedef struct admm_graph admm_graph;
 
 typedef struct admm_graph_info {
   int32_t n_vars, n_checks, n_edges;
   int32_t max_check_degree, max_var_degree;
-  int32_t engine;           /* 1 = resident generic, 2 = resident regular-code fast path */
+  int32_t engine;           /* 1 resident generic, 2 resident regular fast path, 3 streaming */
   int32_t degree_bucket;    /* D: compiled check-degree bucket   */
   int32_t checks_per_thread;
   int32_t threads_per_cta;
@@ -67,6 +74,9 @@ typedef struct admm_graph_info {
  * inside a check; edges are re-sorted as codes.py:42 does). */
 int admm_graph_create(int device, int32_t n_vars, int32_t n_checks, const int32_t* check_ptr,
                       const int32_t* edge_var, admm_graph** out);
+/* Same, with an explicit engine (enum admm_engine). */
+int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int32_t* check_ptr,
+                         const int32_t* edge_var, int engine, admm_graph** out);
 int admm_graph_destroy(admm_graph* g);
 int admm_graph_get_info(const admm_graph* g, admm_graph_info* info);
 
@@ -93,6 +103,31 @@ int admm_decode_batch(const admm_graph* g, int dtype, int64_t batch, const void*
                       int32_t* iters_out, uint8_t* flags_out, int32_t* weight_out,
                       const void* z_in, const void* lam_in, void* z_out, void* lam_out,
                       int64_t ld_edge, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Channel of the fused frame synthesis (channels.py:19-61); the codeword is
+ * all-zero (the reference harness's default, simulator.py:252-256). */
+enum admm_channel_kind { ADMM_CHANNEL_BSC = 1, ADMM_CHANNEL_AWGN = 2 };
+typedef struct admm_channel {
+  int32_t kind;  /* admm_channel_kind */
+  double p;      /* BSC crossover probability, (0, 0.5] */
+  double snr_db; /* AWGN Eb/N0 in dB */
+  double rate;   /* AWGN code rate in (0, 1] (noise variance 1/(2 R 10^(snr/10))) */
+} admm_channel;
+
+/* Decode frames trial0 .. trial0+batch-1 of channel point `point` whose LLRs
+ * are SYNTHESISED on the GPU from (seed, point, trial) with Philox4x32-10 --
+ * the counter-based analogue of the reference harness's per-trial seeding
+ * (simulator.py:169-173): a trial's LLRs never depend on the batch, engine or
+ * GPU that decodes it.  Outputs as admm_decode_batch; no LLR input traffic. */
+int admm_decode_synth(const admm_graph* g, int dtype, int64_t batch, const admm_channel* channel,
+                      uint64_t seed, uint32_t point, int64_t trial0, double mu, double epsilon,
+                      int32_t t_max, double rho, void* x_out, int64_t ld_x, uint8_t* hard_out,
+                      int64_t ld_hard, int32_t* iters_out, uint8_t* flags_out, int32_t* weight_out,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* The same synthesised LLRs written to memory ([batch][ld] device array). */
+int admm_synth_llr(int dtype, int64_t batch, int32_t n_vars, const admm_channel* channel, uint64_t seed,
+                   uint32_t point, int64_t trial0, void* out, int64_t ld, void* stream);
 
 /* Row-wise projection onto the parity polytope.  Replaces project_batch
  * (parity_polytope.py:352-421): values and out are [m][d] row-major device

@@ -17,7 +17,9 @@ from .admm_decoder import (
     DecodeOutput,
     decode,
     decode_batch,
+    decode_synth,
     device_graph,
+    synth_llr,
     run_iterations,
 )
 from .channels import Awgn, Bsc, llr, transmit, trial_gamma, trial_gammas
@@ -38,7 +40,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "AdmmConfig", "BatchResult", "DecodeOutput", "INTEGRALITY_TOL", "STATUS_CONVERGED",
-    "STATUS_MAX_ITERS", "decode", "decode_batch", "device_graph", "run_iterations",
+    "STATUS_MAX_ITERS", "decode", "decode_batch", "decode_synth", "device_graph", "synth_llr", "run_iterations",
     "Awgn", "Bsc", "llr", "transmit", "trial_gamma", "trial_gammas",
     "AlistParseError", "CodeGenerationError", "ParityCheckMatrix", "baseline_code", "emit_alist",
     "gen_regular_ldpc", "is_codeword", "make_ldpc", "parse_alist",

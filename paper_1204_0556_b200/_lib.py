@@ -19,18 +19,29 @@ ADMM_F64 = 1
 ADMM_FLAG_CONVERGED = 1
 ADMM_FLAG_INTEGRAL = 2
 ADMM_FLAG_CODEWORD = 4
+ENGINES = {"auto": 0, "resident": 1, "streaming": 3}
 
 #: Every symbol the public header declares (checked by the CPU test-suite).
 EXPORTED = (
     "admm_version",
     "admm_last_error",
     "admm_graph_create",
+    "admm_graph_create_ex",
     "admm_graph_destroy",
     "admm_graph_get_info",
     "admm_workspace_bytes",
     "admm_decode_batch",
+    "admm_decode_synth",
+    "admm_synth_llr",
     "admm_project_batch",
 )
+
+
+class Channel(ctypes.Structure):
+    """struct admm_channel (include/admm_b200.h)."""
+
+    _fields_ = [("kind", ctypes.c_int32), ("p", ctypes.c_double), ("snr_db", ctypes.c_double),
+                ("rate", ctypes.c_double)]
 
 
 class GraphInfo(ctypes.Structure):
@@ -68,6 +79,8 @@ def load() -> ctypes.CDLL:
     lib.admm_last_error.restype = ctypes.c_char_p
     lib.admm_graph_create.argtypes = [ctypes.c_int, I32, I32, P, P, ctypes.POINTER(P)]
     lib.admm_graph_create.restype = ctypes.c_int
+    lib.admm_graph_create_ex.argtypes = [ctypes.c_int, I32, I32, P, P, ctypes.c_int, ctypes.POINTER(P)]
+    lib.admm_graph_create_ex.restype = ctypes.c_int
     lib.admm_graph_destroy.argtypes = [P]
     lib.admm_graph_destroy.restype = ctypes.c_int
     lib.admm_graph_get_info.argtypes = [P, ctypes.POINTER(GraphInfo)]
@@ -80,6 +93,14 @@ def load() -> ctypes.CDLL:
         P, P, P, P, I64, P, SZ, P,
     ]
     lib.admm_decode_batch.restype = ctypes.c_int
+    lib.admm_decode_synth.argtypes = [
+        P, ctypes.c_int, I64, ctypes.POINTER(Channel), ctypes.c_uint64, ctypes.c_uint32, I64, D, D, I32, D,
+        P, I64, P, I64, P, P, P, P, SZ, P,
+    ]
+    lib.admm_decode_synth.restype = ctypes.c_int
+    lib.admm_synth_llr.argtypes = [ctypes.c_int, I64, I32, ctypes.POINTER(Channel), ctypes.c_uint64,
+                                   ctypes.c_uint32, I64, P, I64, P]
+    lib.admm_synth_llr.restype = ctypes.c_int
     lib.admm_project_batch.argtypes = [ctypes.c_int, I64, I32, P, P, P]
     lib.admm_project_batch.restype = ctypes.c_int
     _lib = lib

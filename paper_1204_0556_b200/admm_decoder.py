@@ -71,15 +71,18 @@ class DecodeOutput:
 class DeviceGraph:
     """Owner of an ``admm_graph`` handle (immutable, one per code and device)."""
 
-    def __init__(self, code: ParityCheckMatrix, device: int):
+    def __init__(self, code: ParityCheckMatrix, device: int, engine: str = "auto"):
         lib = _lib.load()
         self.code = code
         self.device = int(device)
+        self.engine = engine
         ptr = np.ascontiguousarray(code.check_ptr, dtype=np.int32)
         ev = np.ascontiguousarray(code.edge_var, dtype=np.int32)
         h = ctypes.c_void_p()
-        _lib.check(lib.admm_graph_create(self.device, code.n_vars, code.n_checks,
-                                         ptr.ctypes.data, ev.ctypes.data, ctypes.byref(h)))
+        if engine not in _lib.ENGINES:
+            raise ValueError(f"unknown engine {engine!r}; use one of {sorted(_lib.ENGINES)}")
+        _lib.check(lib.admm_graph_create_ex(self.device, code.n_vars, code.n_checks, ptr.ctypes.data,
+                                            ev.ctypes.data, _lib.ENGINES[engine], ctypes.byref(h)))
         self._h = h
         info = _lib.GraphInfo()
         _lib.check(lib.admm_graph_get_info(self._h, ctypes.byref(info)))
@@ -102,14 +105,19 @@ class DeviceGraph:
             self._h = None
 
 
-def device_graph(code, device=None) -> DeviceGraph:
+def device_graph(code, device=None, engine: str = "auto") -> DeviceGraph:
+    """The (cached) device-resident graph of ``code`` on ``device``.
+
+    ``engine``: "auto" (resident when the code fits one SM, else streaming),
+    "resident" or "streaming" (csrc/streaming.cuh)."""
     code = as_code(code)
     dev = torch.device(device if device is not None else "cuda")
     idx = dev.index if dev.index is not None else torch.cuda.current_device()
-    g = code._device_graphs.get(idx)
+    key = (idx, engine)
+    g = code._device_graphs.get(key)
     if g is None:
-        g = DeviceGraph(code, idx)
-        code._device_graphs[idx] = g
+        g = DeviceGraph(code, idx, engine)
+        code._device_graphs[key] = g
     return g
 
 
@@ -208,6 +216,7 @@ def decode_batch(
     want_state: bool = False,
     validate: bool = True,
     stream: torch.cuda.Stream | None = None,
+    engine: str = "auto",
 ) -> BatchResult:
     """Decode ``gammas`` ([B, N], one frame per row) on the GPU.
 
@@ -233,7 +242,7 @@ def decode_batch(
     if validate and not bool(torch.isfinite(g).all()):
         raise ValueError("LLR vector must be finite")
     B, N, E = g.shape[0], code.n_vars, code.n_edges
-    dg = device_graph(code, dev)
+    dg = device_graph(code, dev, engine)
     code_dt = _dtype_code(tdt)
     iters = torch.empty(B, dtype=torch.int32, device=dev)
     flags = torch.empty(B, dtype=torch.uint8, device=dev)
@@ -295,3 +304,64 @@ def run_iterations(gamma, code, config: AdmmConfig, iterations: int, z0=None, la
     res = decode_batch(g, code, cfg, dtype=torch.float64, z0=z0[None], lam0=lam0[None], want_state=True)
     torch.cuda.current_stream().synchronize()
     return (res.x[0].cpu().numpy(), res.z[0].cpu().numpy(), res.lam[0].cpu().numpy())
+
+
+# ---------------------------------------------------------------------------
+# Fused on-GPU frame synthesis (csrc/synth.cuh)
+# ---------------------------------------------------------------------------
+def _channel_struct(channel) -> "_lib.Channel":
+    from .channels import Awgn, Bsc
+
+    if isinstance(channel, Bsc):
+        return _lib.Channel(1, float(channel.p), 0.0, 0.0)
+    if isinstance(channel, Awgn):
+        return _lib.Channel(2, 0.0, float(channel.snr_db), float(channel.rate))
+    raise TypeError("channel must be a Bsc or Awgn")
+
+
+def synth_llr(n_vars: int, channel, *, seed: int, point: int, trial0: int, batch: int,
+              dtype=torch.float64, device=None, stream=None) -> torch.Tensor:
+    """LLRs of trials trial0 .. trial0+batch-1 at channel point ``point``,
+    generated on the GPU from (seed, point, trial) -- exactly the frames
+    :func:`decode_synth` decodes.  All-zero codeword."""
+    dev = torch.device(device if device is not None else "cuda")
+    tdt = torch.float64 if _dtype_code(dtype) == _lib.ADMM_F64 else torch.float32
+    out = torch.empty((batch, n_vars), dtype=tdt, device=dev)
+    ch = _channel_struct(channel)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    _lib.check(_lib.load().admm_synth_llr(_dtype_code(tdt), batch, n_vars, ctypes.byref(ch), int(seed) & (2**64 - 1),
+                                          int(point), int(trial0), out.data_ptr(), n_vars, st.cuda_stream))
+    return out
+
+
+def decode_synth(code, channel, config: AdmmConfig = AdmmConfig(), *, seed: int, point: int = 0,
+                 trial0: int = 0, batch: int, dtype=torch.float32, device=None, want_x: bool = False,
+                 want_hard: bool = False, engine: str = "auto", stream=None) -> BatchResult:
+    """Decode trials trial0 .. trial0+batch-1 with LLRs synthesised inside
+    the decode kernel (no LLR traffic).  A trial's frame depends only on
+    (seed, point, trial), so results are independent of batching, engine and
+    GPU count."""
+    code = as_code(code)
+    dev = torch.device(device if device is not None else "cuda")
+    tdt = torch.float64 if _dtype_code(dtype) == _lib.ADMM_F64 else torch.float32
+    dg = device_graph(code, dev, engine)
+    code_dt = _dtype_code(tdt)
+    B, N = int(batch), code.n_vars
+    iters = torch.empty(B, dtype=torch.int32, device=dev)
+    flags = torch.empty(B, dtype=torch.uint8, device=dev)
+    weight = torch.empty(B, dtype=torch.int32, device=dev)
+    x = torch.empty((B, N), dtype=tdt, device=dev) if want_x else None
+    hard = torch.empty((B, N), dtype=torch.uint8, device=dev) if want_hard else None
+    ws_bytes = dg.workspace_bytes(code_dt, B)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    ch = _channel_struct(channel)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    if B > 0:
+        _lib.check(_lib.load().admm_decode_synth(
+            dg.handle, code_dt, B, ctypes.byref(ch), int(seed) & (2**64 - 1), int(point), int(trial0),
+            float(config.mu), float(config.epsilon), int(config.t_max), float(config.rho),
+            _ptr(x), N, _ptr(hard), N, iters.data_ptr(), flags.data_ptr(), weight.data_ptr(),
+            ws.data_ptr(), ws_bytes, st.cuda_stream))
+    res = BatchResult(iterations=iters, flags=flags, weight=weight, x=x, hard=hard, info=dg.info)
+    res._keepalive = (ws,)  # type: ignore[attr-defined]
+    return res

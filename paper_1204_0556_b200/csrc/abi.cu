@@ -1,6 +1,7 @@
 // C ABI of the ADMM-LP decoder: graph construction, kernel selection and
 // launch.  See include/admm_b200.h for the contract.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -35,7 +36,9 @@ struct admm_graph {
   int n_vars = 0, n_checks = 0, n_edges = 0;
   int dmax = 0, dvmax_actual = 0;
   int D = 0, DVMAX = 0, CPT = 0, NT = 0, m_pad = 0, VPT = 0;
-  int kind = 0;  // 1 = generic resident, 2 = regular resident
+  int kind = 0;  // 1 = generic resident, 2 = regular resident, 3 = streaming
+  int l2_bytes = 0;
+  admm::StreamLaunch slaunch[2];
   int num_sms = 0;
   // device arrays
   int* chk_var = nullptr;
@@ -67,7 +70,14 @@ const char* admm_last_error(void) { return g_last_error.c_str(); }
 
 int admm_graph_create(int device, int32_t n_vars, int32_t n_checks, const int32_t* check_ptr,
                       const int32_t* edge_var, admm_graph** out) {
+  return admm_graph_create_ex(device, n_vars, n_checks, check_ptr, edge_var, ADMM_ENGINE_AUTO, out);
+}
+
+int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int32_t* check_ptr,
+                         const int32_t* edge_var, int engine, admm_graph** out) {
   if (!out || !check_ptr || !edge_var) return fail(ADMM_E_ARG, "null pointer argument");
+  if (engine != ADMM_ENGINE_AUTO && engine != ADMM_ENGINE_RESIDENT && engine != ADMM_ENGINE_STREAMING)
+    return fail(ADMM_E_ARG, "unknown engine");
   *out = nullptr;
   if (n_vars <= 0 || n_checks <= 0) return fail(ADMM_E_ARG, "n_vars and n_checks must be positive");
   if (check_ptr[0] != 0) return fail(ADMM_E_ARG, "check_ptr[0] must be 0");
@@ -114,6 +124,7 @@ int admm_graph_create(int device, int32_t n_vars, int32_t n_checks, const int32_
   cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device);
   int smem_optin = 0;
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  cudaDeviceGetAttribute(&g->l2_bytes, cudaDevAttrL2CacheSize, device);
 
   bool regular = true;
   for (int c = 0; c < n_checks && regular; ++c) regular = (int)rows[c].size() == dmax;
@@ -156,7 +167,7 @@ int admm_graph_create(int device, int32_t n_vars, int32_t n_checks, const int32_
   };
 
   bool placed = false;
-  for (int pass = regular ? 0 : 1; pass < 2 && !placed; ++pass) {
+  for (int pass = regular ? 0 : 1; pass < 2 && !placed && engine != ADMM_ENGINE_STREAMING; ++pass) {
     const bool reg = pass == 0;
     for (int cpt : {1, 2, 3, 4}) {
       const int nt = ((n_checks + cpt - 1) / cpt + 31) / 32 * 32;
@@ -172,10 +183,33 @@ int admm_graph_create(int device, int32_t n_vars, int32_t n_checks, const int32_
       break;
     }
   }
+  if (!placed && engine != ADMM_ENGINE_RESIDENT) {
+    // Streaming engine: batch-interleaved state in global memory (L2-resident).
+    bool ok = true;
+    for (int dt = 0; dt < 2 && ok; ++dt) {
+      admm::StreamLaunch L{};
+      if (!admm::stream_lookup(dt, g->D, &L)) { ok = false; break; }
+      cudaFuncAttributes fa{};
+      if (cudaFuncGetAttributes(&fa, L.fn) != cudaSuccess) { ok = false; break; }
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L.fn, admm::kStreamThreads, 0);
+      if (occ < 1) { ok = false; break; }
+      L.occupancy = occ;
+      L.regs = fa.numRegs;
+      g->slaunch[dt] = L;
+    }
+    if (ok) {
+      g->kind = 3;
+      g->CPT = 1;
+      g->NT = admm::kStreamThreads;
+      g->m_pad = (n_checks + admm::kStreamCK - 1) / admm::kStreamCK * admm::kStreamCK;
+      placed = true;
+    }
+  }
   cudaGetLastError();
   if (!placed) {
     delete g;
-    return fail(ADMM_E_UNSUPPORTED, "graph does not fit the resident engine (too many checks or edges)");
+    return fail(ADMM_E_UNSUPPORTED, "no engine fits this graph");
   }
 
   // Device layout.
@@ -249,35 +283,88 @@ int admm_graph_get_info(const admm_graph* g, admm_graph_info* info) {
   info->degree_bucket = g->D;
   info->checks_per_thread = g->CPT;
   info->threads_per_cta = g->NT;
-  info->ctas_per_sm_f32 = g->launch[0].occupancy;
-  info->ctas_per_sm_f64 = g->launch[1].occupancy;
-  info->smem_bytes_f32 = g->launch[0].smem;
-  info->smem_bytes_f64 = g->launch[1].smem;
-  info->regs_f32 = g->launch[0].regs;
-  info->regs_f64 = g->launch[1].regs;
+  const bool st = g->kind == 3;
+  info->ctas_per_sm_f32 = st ? g->slaunch[0].occupancy : g->launch[0].occupancy;
+  info->ctas_per_sm_f64 = st ? g->slaunch[1].occupancy : g->launch[1].occupancy;
+  info->smem_bytes_f32 = st ? 0 : g->launch[0].smem;
+  info->smem_bytes_f64 = st ? 0 : g->launch[1].smem;
+  info->regs_f32 = st ? g->slaunch[0].regs : g->launch[0].regs;
+  info->regs_f64 = st ? g->slaunch[1].regs : g->launch[1].regs;
   info->num_sms = g->num_sms;
   return ADMM_OK;
 }
 
+namespace {
+
+// Frame slots of the streaming engine: as many as keep the whole state in
+// ~55 % of L2, a multiple of 32, and no more than the batch needs.
+int stream_slots(const admm_graph* g, int dtype, int64_t batch) {
+  const size_t elem = dtype ? 8 : 4;
+  const long long ncblk = (g->n_checks + admm::kStreamCK - 1) / admm::kStreamCK;
+  const size_t per = admm::StreamLayout(elem, g->n_edges, g->n_vars, ncblk, 32).total / 32 + 1;
+  long long s = (long long)(0.55 * (double)g->l2_bytes) / (long long)per;
+  s = std::max<long long>(32, s / 32 * 32);
+  s = std::min<long long>(s, 4096);
+  const long long need = std::max<long long>(32, (batch + 31) / 32 * 32);
+  return (int)std::min(s, need);
+}
+
+}  // namespace
+
 size_t admm_workspace_bytes(const admm_graph* g, int dtype, int64_t batch) {
-  (void)g;
-  (void)dtype;
-  (void)batch;
+  if (!g) return 0;
+  if (g->kind == 3) {
+    const int S = stream_slots(g, dtype, batch);
+    const long long ncblk = (g->n_checks + admm::kStreamCK - 1) / admm::kStreamCK;
+    return admm::StreamLayout(dtype ? 8 : 4, g->n_edges, g->n_vars, ncblk, S).total;
+  }
   return 256;  // the frame queue counter (padded)
 }
 
-int admm_decode_batch(const admm_graph* g, int dtype, int64_t batch, const void* gamma,
-                      int64_t ld_gamma, double mu, double epsilon, int32_t t_max, double rho,
-                      void* x_out, int64_t ld_x, uint8_t* hard_out, int64_t ld_hard,
-                      int32_t* iters_out, uint8_t* flags_out, int32_t* weight_out,
-                      const void* z_in, const void* lam_in, void* z_out, void* lam_out,
-                      int64_t ld_edge, void* workspace, size_t workspace_bytes, void* stream) {
+}  // extern "C"
+
+namespace {
+
+int make_synth(const admm_channel* ch, uint64_t seed, uint32_t point, int64_t trial0, admm::SynthParams* s) {
+  *s = admm::SynthParams{};
+  if (!ch) return fail(ADMM_E_ARG, "null channel");
+  s->seed_lo = static_cast<uint32_t>(seed);
+  s->seed_hi = static_cast<uint32_t>(seed >> 32);
+  s->point = point;
+  s->trial0 = trial0;
+  if (trial0 < 0) return fail(ADMM_E_ARG, "trial0 must be non-negative");
+  if (ch->kind == ADMM_CHANNEL_BSC) {
+    if (!(ch->p > 0.0 && ch->p <= 0.5)) return fail(ADMM_E_ARG, "BSC crossover probability must be in (0, 0.5]");
+    s->kind = 1;
+    s->bsc_p = ch->p;
+    s->bsc_llr = std::log((1.0 - ch->p) / ch->p);
+    return ADMM_OK;
+  }
+  if (ch->kind == ADMM_CHANNEL_AWGN) {
+    if (!(ch->rate > 0.0 && ch->rate <= 1.0)) return fail(ADMM_E_ARG, "code rate must be in (0, 1]");
+    if (!std::isfinite(ch->snr_db)) return fail(ADMM_E_ARG, "snr_db must be finite");
+    const double var = 1.0 / (2.0 * ch->rate * std::pow(10.0, ch->snr_db / 10.0));  // channels.py:59-61
+    s->kind = 2;
+    s->sigma = std::sqrt(var);
+    s->two_over_var = 2.0 / var;
+    return ADMM_OK;
+  }
+  return fail(ADMM_E_ARG, "unknown channel kind");
+}
+
+int decode_impl(const admm_graph* g, int dtype, int64_t batch, const void* gamma, int64_t ld_gamma,
+                const admm::SynthParams& synth, double mu, double epsilon, int32_t t_max, double rho,
+                void* x_out, int64_t ld_x, uint8_t* hard_out, int64_t ld_hard, int32_t* iters_out,
+                uint8_t* flags_out, int32_t* weight_out, const void* z_in, const void* lam_in, void* z_out,
+                void* lam_out, int64_t ld_edge, void* workspace, size_t workspace_bytes, void* stream) {
   if (!g) return fail(ADMM_E_ARG, "null graph");
   if (dtype != ADMM_F32 && dtype != ADMM_F64) return fail(ADMM_E_ARG, "dtype must be ADMM_F32 or ADMM_F64");
   if (batch < 0) return fail(ADMM_E_ARG, "batch must be non-negative");
   if (batch == 0) return ADMM_OK;
-  if (!gamma) return fail(ADMM_E_ARG, "gamma is null");
-  if (ld_gamma < g->n_vars) return fail(ADMM_E_ARG, "ld_gamma < n_vars");
+  if (synth.kind == 0) {
+    if (!gamma) return fail(ADMM_E_ARG, "gamma is null");
+    if (ld_gamma < g->n_vars) return fail(ADMM_E_ARG, "ld_gamma < n_vars");
+  }
   if (x_out && ld_x < g->n_vars) return fail(ADMM_E_ARG, "ld_x < n_vars");
   if (hard_out && ld_hard < g->n_vars) return fail(ADMM_E_ARG, "ld_hard < n_vars");
   if (!(mu > 0)) return fail(ADMM_E_ARG, "mu must be positive");
@@ -293,6 +380,22 @@ int admm_decode_batch(const admm_graph* g, int dtype, int64_t batch, const void*
 
   ADMM_CUDA(cudaSetDevice(g->device));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (g->kind == 3) {
+    if (z_in || z_out) return fail(ADMM_E_UNSUPPORTED, "state input/output is not supported by the streaming engine");
+    const double thr = epsilon * epsilon * (double)g->n_edges;  // admm_decoder.py:169
+    const int S = stream_slots(g, dtype, batch);
+    const admm::StreamLaunch& L = g->slaunch[dtype];
+    const int grid = L.occupancy * g->num_sms;
+    admm::StreamGraphArgs sg{g->n_vars, g->n_checks, g->n_edges, g->m_pad, g->dvmax_actual,
+                             g->chk_var, g->edge_base, g->var_edge};
+    admm::ResidentFrameArgs fa{batch, gamma, ld_gamma, mu, rho, thr, t_max, nullptr, nullptr, 0,
+                               x_out, ld_x, hard_out, ld_hard, iters_out, flags_out, weight_out,
+                               nullptr, nullptr, nullptr, synth};
+    const int rc = L.launch(sg, fa, S, workspace, grid, st);
+    if (rc != 0) return cuda_fail((cudaError_t)rc, "cudaLaunchCooperativeKernel");
+    ADMM_CUDA(cudaGetLastError());
+    return ADMM_OK;
+  }
   ADMM_CUDA(cudaMemsetAsync(workspace, 0, sizeof(int), st));
   const admm::ResidentLaunch& L = g->launch[dtype];
   const long long grid = std::min<long long>(batch, (long long)L.occupancy * g->num_sms);
@@ -302,8 +405,51 @@ int admm_decode_batch(const admm_graph* g, int dtype, int64_t batch, const void*
                              g->edge_base, g->var_edge};
   admm::ResidentFrameArgs fa{batch, gamma, ld_gamma, mu, rho, thr, t_max, z_in, lam_in, ld_edge,
                              x_out, ld_x, hard_out, ld_hard, iters_out, flags_out, weight_out,
-                             z_out, lam_out, reinterpret_cast<int*>(workspace)};
+                             z_out, lam_out, reinterpret_cast<int*>(workspace), synth};
   L.launch(ga, fa, (int)grid, g->NT, L.smem, st);
+  ADMM_CUDA(cudaGetLastError());
+  return ADMM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int admm_decode_batch(const admm_graph* g, int dtype, int64_t batch, const void* gamma,
+                      int64_t ld_gamma, double mu, double epsilon, int32_t t_max, double rho,
+                      void* x_out, int64_t ld_x, uint8_t* hard_out, int64_t ld_hard,
+                      int32_t* iters_out, uint8_t* flags_out, int32_t* weight_out,
+                      const void* z_in, const void* lam_in, void* z_out, void* lam_out,
+                      int64_t ld_edge, void* workspace, size_t workspace_bytes, void* stream) {
+  return decode_impl(g, dtype, batch, gamma, ld_gamma, admm::SynthParams{}, mu, epsilon, t_max, rho, x_out,
+                     ld_x, hard_out, ld_hard, iters_out, flags_out, weight_out, z_in, lam_in, z_out, lam_out,
+                     ld_edge, workspace, workspace_bytes, stream);
+}
+
+int admm_decode_synth(const admm_graph* g, int dtype, int64_t batch, const admm_channel* channel,
+                      uint64_t seed, uint32_t point, int64_t trial0, double mu, double epsilon,
+                      int32_t t_max, double rho, void* x_out, int64_t ld_x, uint8_t* hard_out,
+                      int64_t ld_hard, int32_t* iters_out, uint8_t* flags_out, int32_t* weight_out,
+                      void* workspace, size_t workspace_bytes, void* stream) {
+  admm::SynthParams sp;
+  const int rc = make_synth(channel, seed, point, trial0, &sp);
+  if (rc) return rc;
+  return decode_impl(g, dtype, batch, nullptr, 0, sp, mu, epsilon, t_max, rho, x_out, ld_x, hard_out, ld_hard,
+                     iters_out, flags_out, weight_out, nullptr, nullptr, nullptr, nullptr, 0, workspace,
+                     workspace_bytes, stream);
+}
+
+int admm_synth_llr(int dtype, int64_t batch, int32_t n_vars, const admm_channel* channel, uint64_t seed,
+                   uint32_t point, int64_t trial0, void* out, int64_t ld, void* stream) {
+  if (dtype != ADMM_F32 && dtype != ADMM_F64) return fail(ADMM_E_ARG, "dtype must be ADMM_F32 or ADMM_F64");
+  if (batch < 0 || n_vars <= 0) return fail(ADMM_E_ARG, "bad shape");
+  if (ld < n_vars) return fail(ADMM_E_ARG, "ld < n_vars");
+  admm::SynthParams sp;
+  const int rc = make_synth(channel, seed, point, trial0, &sp);
+  if (rc) return rc;
+  if (batch == 0) return ADMM_OK;
+  if (!out) return fail(ADMM_E_ARG, "null output");
+  admm::launch_synth(dtype, batch, n_vars, sp, out, ld, reinterpret_cast<cudaStream_t>(stream));
   ADMM_CUDA(cudaGetLastError());
   return ADMM_OK;
 }

@@ -7,6 +7,7 @@
 
 #include "resident.cuh"
 #include "resident_regular.cuh"
+#include "streaming.cuh"
 
 namespace admm {
 
@@ -38,6 +39,7 @@ struct ResidentFrameArgs {
   void* z_out;
   void* lam_out;
   int* queue;
+  SynthParams synth;
 };
 
 using ResidentLaunchFn = void (*)(const ResidentGraphArgs&, const ResidentFrameArgs&, int grid, int nt,
@@ -81,6 +83,7 @@ ResidentParams<T> make_params(const ResidentGraphArgs& g, const ResidentFrameArg
   p.z_out = static_cast<T*>(a.z_out);
   p.lam_out = static_cast<T*>(a.lam_out);
   p.queue = a.queue;
+  p.synth = a.synth;
   return p;
 }
 
@@ -110,7 +113,77 @@ inline bool resident_lookup(int dtype, int D, int CPT, int DVMAX, ResidentLaunch
   return dtype ? resident_lookup_f64(D, CPT, DVMAX, out) : resident_lookup_f32(D, CPT, DVMAX, out);
 }
 
+// ---- streaming engine ----
+struct StreamGraphArgs {
+  int n_vars, n_checks, n_edges, m_pad, dvmax;
+  const int* chk_var;
+  const int* edge_base;
+  const int* var_edge;
+};
+
+struct StreamLaunch {
+  const void* fn;
+  int (*launch)(const StreamGraphArgs&, const ResidentFrameArgs&, int S, void* ws, int grid, cudaStream_t st);
+  int occupancy, regs;
+};
+
+template <typename T, int D>
+int launch_streaming(const StreamGraphArgs& g, const ResidentFrameArgs& a, int S, void* ws, int grid,
+                     cudaStream_t st) {
+  StreamParams<T> p{};
+  p.n_vars = g.n_vars;
+  p.n_checks = g.n_checks;
+  p.n_edges = g.n_edges;
+  p.m_pad = g.m_pad;
+  p.chk_var = g.chk_var;
+  p.edge_base = g.edge_base;
+  p.var_edge = g.var_edge;
+  p.dvmax = g.dvmax;
+  p.batch = a.batch;
+  p.gamma = static_cast<const T*>(a.gamma);
+  p.ld_gamma = a.ld_gamma;
+  p.mu = T(a.mu);
+  p.inv_mu = T(1.0 / a.mu);
+  p.rho = T(a.rho);
+  p.one_minus_rho = T(1.0 - a.rho);
+  p.thr = T(a.thr);
+  p.t_max = a.t_max;
+  p.x_out = static_cast<T*>(a.x_out);
+  p.ld_x = a.ld_x;
+  p.hard_out = a.hard_out;
+  p.ld_hard = a.ld_hard;
+  p.iters_out = a.iters_out;
+  p.flags_out = a.flags_out;
+  p.weight_out = a.weight_out;
+  p.S = S;
+  p.synth = a.synth;
+  const long long ncblk = (g.n_checks + kStreamCK - 1) / kStreamCK;
+  const StreamLayout L(sizeof(T), g.n_edges, g.n_vars, ncblk, S);
+  char* base = static_cast<char*>(ws);
+  p.zl = reinterpret_cast<T*>(base + L.zl);
+  p.msg = reinterpret_cast<T*>(base + L.msg);
+  p.x = reinterpret_cast<T*>(base + L.x);
+  p.gm = reinterpret_cast<T*>(base + L.gm);
+  p.part = reinterpret_cast<T*>(base + L.part);
+  p.frame = reinterpret_cast<long long*>(base + L.ints);
+  int* ib = reinterpret_cast<int*>(base + L.ints + StreamLayout::al(sizeof(long long) * S));
+  p.notconv = ib;
+  p.st = ib + S;
+  p.tcount = ib + 2 * S;
+  p.conv = ib + 3 * S;
+  p.weight = ib + 4 * S;
+  p.nonint = ib + 5 * S;
+  p.odd = ib + 6 * S;
+  p.ctr = ib + 7 * S;
+  void* args[] = {&p};
+  return (int)cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&streaming_decode_kernel<T, D>), grid,
+                                          kStreamThreads, args, 0, st);
+}
+
+bool stream_lookup(int dtype, int D, StreamLaunch* out);
+
 // Defined in project.cu.
 bool launch_project(int dtype, int D, long long m, int d, const void* in, void* out, cudaStream_t st);
+void launch_synth(int dtype, long long batch, int n, const SynthParams& s, void* out, long long ld, cudaStream_t st);
 
 }  // namespace admm

@@ -35,6 +35,25 @@ bool launch_project_t(int D, long long m, int d, const void* in, void* out, cuda
   return false;
 }
 
+template <typename T>
+__global__ void synth_kernel(long long batch, int n, SynthParams s, T* out, long long ld) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= batch * n) return;
+  const long long f = idx / n;
+  const int i = static_cast<int>(idx - f * n);
+  out[f * ld + i] = static_cast<T>(synth_llr(s, s.trial0 + f, i));
+}
+
+void launch_synth(int dtype, long long batch, int n, const SynthParams& s, void* out, long long ld, cudaStream_t st) {
+  const long long total = batch * n;
+  const int nt = 256;
+  const long long grid = (total + nt - 1) / nt;
+  if (dtype)
+    synth_kernel<double><<<grid, nt, 0, st>>>(batch, n, s, static_cast<double*>(out), ld);
+  else
+    synth_kernel<float><<<grid, nt, 0, st>>>(batch, n, s, static_cast<float*>(out), ld);
+}
+
 bool launch_project(int dtype, int D, long long m, int d, const void* in, void* out, cudaStream_t st) {
   return dtype ? launch_project_t<double>(D, m, d, in, out, st) : launch_project_t<float>(D, m, d, in, out, st);
 }

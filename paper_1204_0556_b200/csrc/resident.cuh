@@ -24,6 +24,7 @@
 
 #include "common.cuh"
 #include "projection.cuh"
+#include "synth.cuh"
 
 namespace admm {
 
@@ -61,7 +62,17 @@ struct ResidentParams {
   T* lam_out;
   // work queue
   int* queue;
+  // fused frame synthesis (kind 0 = read gamma)
+  SynthParams synth;
 };
+
+// LLR of variable i of frame f: from memory, or synthesised from
+// (seed, point, trial0 + f) when the call asked for fused synthesis.
+template <typename T, typename P>
+__device__ __forceinline__ T frame_llr(const P& p, long long f, int i) {
+  if (p.synth.kind != 0) return static_cast<T>(synth_llr(p.synth, p.synth.trial0 + f, i));
+  return p.gamma[f * p.ld_gamma + i];
+}
 
 template <int DVMAX>
 struct VarPos;
@@ -145,8 +156,7 @@ __global__ void __launch_bounds__(512) resident_decode_kernel(const ResidentPara
     if (f >= p.batch) break;
 
     // ---- frame setup: gamma/mu, zero (or given) state, messages ----
-    const T* g = p.gamma + f * p.ld_gamma;
-    for (int i = tid; i < N; i += NT) gm[i] = div_rn(g[i], p.mu);
+    for (int i = tid; i < N; i += NT) gm[i] = div_rn(frame_llr<T>(p, f, i), p.mu);
 #pragma unroll
     for (int q = 0; q < CPT; ++q) {
       const int c = tid + q * NT;

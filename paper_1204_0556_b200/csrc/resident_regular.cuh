@@ -91,9 +91,8 @@ __global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const Resid
     if (f >= p.batch) break;
 
     // ---- frame setup ----
-    const T* g = p.gamma + f * p.ld_gamma;
 #pragma unroll
-    for (int q = 0; q < VPT; ++q) gm[q] = vact[q] ? div_rn(g[tid + q * NT], p.mu) : T(0);
+    for (int q = 0; q < VPT; ++q) gm[q] = vact[q] ? div_rn(frame_llr<T>(p, f, tid + q * NT), p.mu) : T(0);
 #pragma unroll
     for (int q = 0; q < CPT; ++q) {
       const int c = tid + q * NT;

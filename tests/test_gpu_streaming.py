@@ -1,0 +1,138 @@
+"""Streaming engine (csrc/streaming.cuh) parity: forced onto the golden
+codes, and automatically on codes too large for the resident engine
+(BASELINE config 5, n = 16384), against the reference goldens / the oracle."""
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_code, load_golden
+from oracle import admm_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _frames(f, code, n, point=0):
+    rate = 1.0 - code.n_checks / code.n_vars
+    return np.array([O.trial_gamma_awgn(code.n_vars, float(f["snr_db"]), rate, 1, point, t) for t in range(n)])
+
+
+@pytest.mark.parametrize("name", ["decode_cfg1.npz", "decode_cfg2.npz", "decode_cfg4.npz"])
+def test_streaming_f64_matches_reference_golden(cuda_ok, name):
+    from paper_1204_0556_b200 import AdmmConfig, decode_batch
+
+    f = load_golden(name)
+    code = golden_code(f)
+    B = len(f["iterations"])
+    gam = _frames(f, code, B)
+    cfg = AdmmConfig(mu=float(f["mu"]), epsilon=float(f["epsilon"]), t_max=int(f["t_max"]), rho=float(f["rho"]))
+    res = decode_batch(gam, code, cfg, dtype=torch.float64, want_hard=True, engine="streaming")
+    assert res.info["engine"] == 3
+    want_hard = np.unpackbits(f["hard"], axis=1)[:, : code.n_vars]
+    fl = res.flags.cpu().numpy()
+    assert np.array_equal(res.iterations.cpu().numpy(), f["iterations"])
+    assert np.array_equal((fl & 1) != 0, f["converged"] != 0)
+    assert np.array_equal((fl & 2) != 0, f["integral"] != 0)
+    assert np.array_equal(((fl & 2) != 0) & ((fl & 4) != 0), f["certificate"] != 0)
+    assert np.array_equal(res.hard.cpu().numpy(), want_hard)
+    assert np.array_equal(res.weight.cpu().numpy(), want_hard.sum(1))
+    nx = len(f["x"])
+    assert np.abs(res.x[:nx].cpu().numpy() - f["x"]).max() <= 1e-9
+
+
+def test_streaming_equals_resident_f32(cuda_ok):
+    from paper_1204_0556_b200 import AdmmConfig, baseline_code, decode_batch
+
+    code = baseline_code("cfg2_n1008")
+    g = torch.randn(200, code.n_vars, device="cuda", generator=torch.Generator("cuda").manual_seed(1)) * 2.5 + 3.2
+    cfg = AdmmConfig(mu=5.0)
+    a = decode_batch(g, code, cfg, dtype=torch.float32, engine="resident")
+    b = decode_batch(g, code, cfg, dtype=torch.float32, engine="streaming")
+    same = (a.x > 0.5).eq(b.x > 0.5).all(dim=1).float().mean().item()
+    assert same >= 0.995
+    assert (a.iterations - b.iterations).abs().float().mean().item() <= 2.0
+
+
+def test_streaming_irregular_and_zero_degree(cuda_ok):
+    from paper_1204_0556_b200 import AdmmConfig, ParityCheckMatrix, decode_batch
+
+    codes = [
+        ParityCheckMatrix.from_dense([[1, 1, 0, 1, 1, 0, 0], [1, 0, 1, 1, 0, 1, 0], [0, 1, 1, 1, 0, 0, 1]]),
+        ParityCheckMatrix(6, [[0, 1, 2], [1, 2, 3, 4]]),
+        ParityCheckMatrix(20, [list(range(0, 9)), list(range(5, 20)), [0, 7, 19]]),
+    ]
+    rng = np.random.default_rng(4)
+    for code in codes:
+        gam = rng.normal(0.5, 1.2, (33, code.n_vars))
+        res = decode_batch(gam, code, AdmmConfig(mu=3.0, t_max=300), dtype=torch.float64, engine="streaming")
+        g = O.Graph.of(code)
+        for t in range(len(gam)):
+            r = O.decode(gam[t], g, O.Params(mu=3.0, t_max=300))
+            assert int(res.iterations[t]) == r.iterations
+            assert np.abs(res.x[t].cpu().numpy() - r.x).max() <= 1e-9
+
+
+def test_config5_large_block_matches_oracle(cuda_ok):
+    """n = 16384 does not fit one SM: the automatic engine is streaming."""
+    from paper_1204_0556_b200 import AdmmConfig, baseline_code, decode_batch
+
+    code = baseline_code("cfg5_n16384")
+    gam = np.stack([O.trial_gamma_bsc(code.n_vars, 0.04, 1, 0, t) for t in range(3)]
+                   + [O.trial_gamma_awgn(code.n_vars, 2.5, 0.5, 1, 1, t) for t in range(3)])
+    cfg = AdmmConfig(mu=5.0)
+    res = decode_batch(gam, code, cfg, dtype=torch.float64, want_hard=True)
+    assert res.info["engine"] == 3
+    g = O.Graph.of(code)
+    for t in range(len(gam)):
+        r = O.decode(gam[t], g, O.Params(mu=5.0))
+        assert int(res.iterations[t]) == r.iterations
+        assert np.abs(res.x[t].cpu().numpy() - r.x).max() <= 1e-9
+        assert np.array_equal(res.hard[t].cpu().numpy(), r.hard_decision)
+    r32 = decode_batch(gam, code, cfg, dtype=torch.float32, want_hard=True)
+    assert torch.equal(r32.hard, res.hard)
+
+
+def test_streaming_rejects_state_io(cuda_ok):
+    from paper_1204_0556_b200 import AdmmConfig, baseline_code, decode_batch
+
+    code = baseline_code("cfg1_n96")
+    with pytest.raises(RuntimeError):
+        decode_batch(np.zeros((1, 96)), code, AdmmConfig(), want_state=True, engine="streaming")
+
+
+@pytest.mark.parametrize("engine", ["auto", "streaming"])
+def test_fused_synthesis_equals_materialised_llrs(cuda_ok, engine):
+    """decode_synth (LLRs generated inside the decode kernel) == decode_batch
+    on the LLRs synth_llr writes out; trial-indexed, so any split agrees."""
+    from paper_1204_0556_b200 import AdmmConfig, Awgn, Bsc, baseline_code, decode_batch, decode_synth, synth_llr
+
+    code = baseline_code("cfg2_n1008")
+    cfg = AdmmConfig(mu=5.0)
+    for ch in (Awgn(2.25, code.design_rate), Bsc(0.04)):
+        for dt in (torch.float32, torch.float64):
+            a = decode_synth(code, ch, cfg, seed=7, point=3, trial0=100, batch=96, dtype=dt, want_x=True,
+                             engine=engine)
+            g = synth_llr(code.n_vars, ch, seed=7, point=3, trial0=100, batch=96, dtype=dt)
+            b = decode_batch(g, code, cfg, dtype=dt, engine=engine)
+            assert torch.equal(a.x, b.x) and torch.equal(a.iterations, b.iterations)
+            assert torch.equal(a.flags, b.flags) and torch.equal(a.weight, b.weight)
+            # shard invariance: trials 100..195 decoded as two calls
+            c1 = decode_synth(code, ch, cfg, seed=7, point=3, trial0=100, batch=40, dtype=dt, engine=engine)
+            c2 = decode_synth(code, ch, cfg, seed=7, point=3, trial0=140, batch=56, dtype=dt, engine=engine)
+            assert torch.equal(torch.cat([c1.iterations, c2.iterations]), a.iterations)
+
+
+def test_synth_llr_statistics(cuda_ok):
+    from paper_1204_0556_b200 import Awgn, Bsc, synth_llr
+
+    ch = Awgn(2.0, 0.5)
+    g = synth_llr(4096, ch, seed=1, point=0, trial0=0, batch=256, dtype=torch.float64)
+    var = ch.noise_variance
+    y = g * var / 2.0  # received samples, mean 1, sd sqrt(var)
+    assert abs(y.mean().item() - 1.0) < 0.01
+    assert abs(y.std().item() - var ** 0.5) < 0.01
+    b = synth_llr(4096, Bsc(0.04), seed=1, point=0, trial0=0, batch=256, dtype=torch.float64)
+    frac = (b < 0).double().mean().item()
+    assert abs(frac - 0.04) < 0.002
+    # different points / seeds give different frames, same ones repeat exactly
+    assert not torch.equal(g, synth_llr(4096, ch, seed=1, point=1, trial0=0, batch=256, dtype=torch.float64))
+    assert torch.equal(g, synth_llr(4096, ch, seed=1, point=0, trial0=0, batch=256, dtype=torch.float64))
