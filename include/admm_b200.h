@@ -50,7 +50,8 @@ enum admm_status {
 enum admm_engine {
   ADMM_ENGINE_AUTO = 0,      /* resident if the code fits one SM, else streaming */
   ADMM_ENGINE_RESIDENT = 1,  /* one CTA per frame, state on chip (fails if it does not fit) */
-  ADMM_ENGINE_STREAMING = 3  /* batch-interleaved L2-resident state, cooperative kernel */
+  ADMM_ENGINE_STREAMING = 3, /* batch-interleaved L2-resident state, cooperative kernel */
+  ADMM_ENGINE_CLUSTER = 4    /* one thread-block cluster per frame, DSMEM gathers (regular codes) */
 };
 
 typedef struct admm_graph admm_graph;
@@ -58,14 +59,15 @@ typedef struct admm_graph admm_graph;
 typedef struct admm_graph_info {
   int32_t n_vars, n_checks, n_edges;
   int32_t max_check_degree, max_var_degree;
-  int32_t engine;           /* 1 resident generic, 2 resident regular fast path, 3 streaming */
+  int32_t engine;           /* 1 resident generic, 2 resident regular, 3 streaming, 4 cluster */
   int32_t degree_bucket;    /* D: compiled check-degree bucket   */
   int32_t checks_per_thread;
   int32_t threads_per_cta;
-  int32_t ctas_per_sm_f32, ctas_per_sm_f64;
+  int32_t ctas_per_sm_f32, ctas_per_sm_f64; /* engine 4: active clusters per GPU */
   int32_t smem_bytes_f32, smem_bytes_f64;
   int32_t regs_f32, regs_f64;
   int32_t num_sms;
+  int32_t cluster_size;     /* CTAs per cluster (engine 4), else 0 */
 } admm_graph_info;
 
 /* Build the device-resident Tanner graph.  Replaces the edge-array views of

@@ -19,7 +19,7 @@ ADMM_F64 = 1
 ADMM_FLAG_CONVERGED = 1
 ADMM_FLAG_INTEGRAL = 2
 ADMM_FLAG_CODEWORD = 4
-ENGINES = {"auto": 0, "resident": 1, "streaming": 3}
+ENGINES = {"auto": 0, "resident": 1, "streaming": 3, "cluster": 4}
 
 #: Every symbol the public header declares (checked by the CPU test-suite).
 EXPORTED = (
@@ -53,7 +53,7 @@ class GraphInfo(ctypes.Structure):
         ("ctas_per_sm_f32", ctypes.c_int32), ("ctas_per_sm_f64", ctypes.c_int32),
         ("smem_bytes_f32", ctypes.c_int32), ("smem_bytes_f64", ctypes.c_int32),
         ("regs_f32", ctypes.c_int32), ("regs_f64", ctypes.c_int32),
-        ("num_sms", ctypes.c_int32),
+        ("num_sms", ctypes.c_int32), ("cluster_size", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:

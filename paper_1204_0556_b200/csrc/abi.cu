@@ -2,6 +2,7 @@
 // launch.  See include/admm_b200.h for the contract.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -36,9 +37,16 @@ struct admm_graph {
   int n_vars = 0, n_checks = 0, n_edges = 0;
   int dmax = 0, dvmax_actual = 0;
   int D = 0, DVMAX = 0, CPT = 0, NT = 0, m_pad = 0, VPT = 0;
-  int kind = 0;  // 1 = generic resident, 2 = regular resident, 3 = streaming
+  int kind = 0;  // 1 = generic resident, 2 = regular resident, 3 = streaming, 4 = cluster resident
+  int C = 0, MC = 0, NC = 0;
+  admm::ClusterLaunch claunch[2];
   int l2_bytes = 0;
   admm::StreamLaunch slaunch[2];
+  admm::ShardLaunch shlaunch[2];
+  bool shard_ok[2] = {false, false};
+  int shard_G = 0, shard_dv = 0;
+  long long shard_EB = 0;
+  int smem_optin = 0;
   int num_sms = 0;
   // device arrays
   int* chk_var = nullptr;
@@ -76,7 +84,8 @@ int admm_graph_create(int device, int32_t n_vars, int32_t n_checks, const int32_
 int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int32_t* check_ptr,
                          const int32_t* edge_var, int engine, admm_graph** out) {
   if (!out || !check_ptr || !edge_var) return fail(ADMM_E_ARG, "null pointer argument");
-  if (engine != ADMM_ENGINE_AUTO && engine != ADMM_ENGINE_RESIDENT && engine != ADMM_ENGINE_STREAMING)
+  if (engine != ADMM_ENGINE_AUTO && engine != ADMM_ENGINE_RESIDENT && engine != ADMM_ENGINE_STREAMING &&
+      engine != ADMM_ENGINE_CLUSTER)
     return fail(ADMM_E_ARG, "unknown engine");
   *out = nullptr;
   if (n_vars <= 0 || n_checks <= 0) return fail(ADMM_E_ARG, "n_vars and n_checks must be positive");
@@ -124,6 +133,7 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
   cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device);
   int smem_optin = 0;
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  g->smem_optin = smem_optin;
   cudaDeviceGetAttribute(&g->l2_bytes, cudaDevAttrL2CacheSize, device);
 
   bool regular = true;
@@ -167,7 +177,8 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
   };
 
   bool placed = false;
-  for (int pass = regular ? 0 : 1; pass < 2 && !placed && engine != ADMM_ENGINE_STREAMING; ++pass) {
+  const bool try_resident = engine == ADMM_ENGINE_AUTO || engine == ADMM_ENGINE_RESIDENT;
+  for (int pass = regular ? 0 : 1; pass < 2 && !placed && try_resident; ++pass) {
     const bool reg = pass == 0;
     for (int cpt : {1, 2, 3, 4}) {
       const int nt = ((n_checks + cpt - 1) / cpt + 31) / 32 * 32;
@@ -183,12 +194,80 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
       break;
     }
   }
-  if (!placed && engine != ADMM_ENGINE_RESIDENT) {
+  if (!placed && regular && engine == ADMM_ENGINE_CLUSTER) {  // opt-in: DSMEM gathers measured slower than streaming
+    // Cluster-resident engine: one cluster of C CTAs per frame, DSMEM gathers.
+    // Prefer one check per thread (the most warps per SM), then the smallest cluster.
+    const int c_env = std::getenv("ADMM_B200_CLUSTER") ? std::atoi(std::getenv("ADMM_B200_CLUSTER")) : 0;
+    for (int cpt : {1, 2}) {
+      if (placed) break;
+      for (int C : {2, 4, 8, 16}) {
+      if (placed) break;
+      if (c_env && C != c_env) continue;
+      const int MC = (n_checks + C - 1) / C, NC = (n_vars + C - 1) / C;
+      if (MC < 32 && C > 2) continue;
+      {
+        const int nt = ((MC + cpt - 1) / cpt + 31) / 32 * 32;
+        if (nt > 512) continue;
+        const int need = (NC + nt - 1) / nt;
+        bool ok = true;
+        admm::ClusterLaunch Ls[2];
+        for (int dt = 0; dt < 2 && ok; ++dt) {
+          admm::ClusterLaunch L{};
+          int vpt = 0;
+          if (!admm::cluster_lookup(dt, dmax, dvmax, cpt, need, &vpt, &L)) { ok = false; break; }
+          const int smem = admm::cluster_smem_bytes(dt ? 8 : 4, dmax, nt * cpt, NC);
+          if (smem > smem_optin) { ok = false; break; }
+          cudaFuncAttributes fa{};
+          if (cudaFuncGetAttributes(&fa, L.fn) != cudaSuccess) { ok = false; break; }
+          if (fa.numRegs * nt > 65536) { ok = false; break; }
+          cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+          if (C > 8) cudaFuncSetAttribute(L.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+          cudaLaunchConfig_t cfg{};
+          cfg.gridDim = dim3(C);
+          cfg.blockDim = dim3(nt);
+          cfg.dynamicSmemBytes = smem;
+          cudaLaunchAttribute attr[1];
+          attr[0].id = cudaLaunchAttributeClusterDimension;
+          attr[0].val.clusterDim.x = C;
+          attr[0].val.clusterDim.y = 1;
+          attr[0].val.clusterDim.z = 1;
+          cfg.attrs = attr;
+          cfg.numAttrs = 1;
+          int clusters = 0;
+          if (cudaOccupancyMaxActiveClusters(&clusters, L.fn, &cfg) != cudaSuccess || clusters < 1) {
+            cudaGetLastError();
+            ok = false;
+            break;
+          }
+          L.clusters = clusters;
+          L.regs = fa.numRegs;
+          L.smem = smem;
+          Ls[dt] = L;
+          g->VPT = vpt;
+        }
+        if (!ok) continue;
+        g->claunch[0] = Ls[0];
+        g->claunch[1] = Ls[1];
+        g->kind = 4;
+        g->C = C;
+        g->MC = MC;
+        g->NC = NC;
+        g->CPT = cpt;
+        g->NT = nt;
+        g->m_pad = (n_checks + 31) / 32 * 32;
+        placed = true;
+        break;
+      }
+    }
+    }
+  }
+  if (!placed && (engine == ADMM_ENGINE_AUTO || engine == ADMM_ENGINE_STREAMING)) {
     // Streaming engine: batch-interleaved state in global memory (L2-resident).
     bool ok = true;
     for (int dt = 0; dt < 2 && ok; ++dt) {
       admm::StreamLaunch L{};
-      if (!admm::stream_lookup(dt, g->D, &L)) { ok = false; break; }
+      const bool reg_stream = regular && dmax == g->D;
+      if (!admm::stream_lookup(dt, g->D, g->DVMAX, reg_stream, &L)) { ok = false; break; }
       cudaFuncAttributes fa{};
       if (cudaFuncGetAttributes(&fa, L.fn) != cudaSuccess) { ok = false; break; }
       int occ = 0;
@@ -199,6 +278,35 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
       g->slaunch[dt] = L;
     }
     if (ok) {
+      // Sharded variant: one 512-thread CTA per SM, static graph slice,
+      // z/lambda in shared memory (sharded.cuh).  Used when 32 slots fit.
+      const int G = g->num_sms;
+      const int MB = (n_checks + G - 1) / G;
+      long long EB = 0;
+      for (int b0 = 0; b0 < n_checks; b0 += MB) {
+        const int b1 = std::min(n_checks, b0 + MB);
+        EB = std::max<long long>(EB, (long long)check_ptr[b1] - check_ptr[b0]);
+      }
+      g->shard_G = G;
+      g->shard_EB = EB;
+      for (int dt = 0; dt < 2; ++dt) {
+        admm::ShardLaunch SL{};
+        const bool reg_stream = regular && dmax == g->D;
+        const int dv_used = reg_stream && dvmax == 3 ? 3 : g->DVMAX;
+        if (!admm::shard_lookup(dt, g->D, dv_used, reg_stream, &SL)) continue;
+        g->shard_dv = dv_used;
+        const admm::ShardGeom geo = admm::shard_geom(dt ? 8 : 4, g->D, dv_used, n_checks, n_vars, EB, G, 32);
+        if (geo.total > smem_optin) continue;
+        if (cudaFuncSetAttribute(SL.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin) != cudaSuccess) continue;
+        cudaFuncAttributes fa{};
+        if (cudaFuncGetAttributes(&fa, SL.fn) != cudaSuccess || fa.numRegs * 512 > 65536) continue;
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, SL.fn, 512, geo.total);
+        if (occ < 1) continue;
+        g->shlaunch[dt] = SL;
+        g->shard_ok[dt] = std::getenv("ADMM_B200_NO_SHARD") == nullptr;
+      }
+      cudaGetLastError();
       g->kind = 3;
       g->CPT = 1;
       g->NT = admm::kStreamThreads;
@@ -283,13 +391,14 @@ int admm_graph_get_info(const admm_graph* g, admm_graph_info* info) {
   info->degree_bucket = g->D;
   info->checks_per_thread = g->CPT;
   info->threads_per_cta = g->NT;
-  const bool st = g->kind == 3;
-  info->ctas_per_sm_f32 = st ? g->slaunch[0].occupancy : g->launch[0].occupancy;
-  info->ctas_per_sm_f64 = st ? g->slaunch[1].occupancy : g->launch[1].occupancy;
-  info->smem_bytes_f32 = st ? 0 : g->launch[0].smem;
-  info->smem_bytes_f64 = st ? 0 : g->launch[1].smem;
-  info->regs_f32 = st ? g->slaunch[0].regs : g->launch[0].regs;
-  info->regs_f64 = st ? g->slaunch[1].regs : g->launch[1].regs;
+  const bool st = g->kind == 3, cl = g->kind == 4;
+  info->ctas_per_sm_f32 = st ? g->slaunch[0].occupancy : cl ? g->claunch[0].clusters : g->launch[0].occupancy;
+  info->ctas_per_sm_f64 = st ? g->slaunch[1].occupancy : cl ? g->claunch[1].clusters : g->launch[1].occupancy;
+  info->smem_bytes_f32 = st ? 0 : cl ? g->claunch[0].smem : g->launch[0].smem;
+  info->smem_bytes_f64 = st ? 0 : cl ? g->claunch[1].smem : g->launch[1].smem;
+  info->regs_f32 = st ? g->slaunch[0].regs : cl ? g->claunch[0].regs : g->launch[0].regs;
+  info->regs_f64 = st ? g->slaunch[1].regs : cl ? g->claunch[1].regs : g->launch[1].regs;
+  info->cluster_size = g->C;
   info->num_sms = g->num_sms;
   return ADMM_OK;
 }
@@ -298,13 +407,34 @@ namespace {
 
 // Frame slots of the streaming engine: as many as keep the whole state in
 // ~55 % of L2, a multiple of 32, and no more than the batch needs.
+int shard_slots(const admm_graph* g, int dtype, int64_t batch) {
+  int best = 0;
+  for (int S = 32; S <= 512; S *= 2) {
+    const admm::ShardGeom geo = admm::shard_geom(dtype ? 8 : 4, g->D, g->shard_dv, g->n_checks, g->n_vars,
+                                                 g->shard_EB, g->shard_G, S);
+    if (geo.total <= g->smem_optin) best = S;
+  }
+  if (const char* env = std::getenv("ADMM_B200_STREAM_SLOTS")) {
+    const int v = std::atoi(env) / 32 * 32;
+    if (v >= 32 && v <= best) best = v;
+  }
+  const long long need = std::max<long long>(32, (batch + 31) / 32 * 32);
+  while (best > 32 && best / 2 >= need) best /= 2;
+  return best;
+}
+
 int stream_slots(const admm_graph* g, int dtype, int64_t batch) {
+  if (g->shard_ok[dtype]) return shard_slots(g, dtype, batch);
   const size_t elem = dtype ? 8 : 4;
   const long long ncblk = (g->n_checks + admm::kStreamCK - 1) / admm::kStreamCK;
   const size_t per = admm::StreamLayout(elem, g->n_edges, g->n_vars, ncblk, 32).total / 32 + 1;
   long long s = (long long)(0.55 * (double)g->l2_bytes) / (long long)per;
   s = std::max<long long>(32, s / 32 * 32);
   s = std::min<long long>(s, 4096);
+  if (const char* env = std::getenv("ADMM_B200_STREAM_SLOTS")) {  // tuning override
+    const long long v = std::atoll(env);
+    if (v >= 32) s = v / 32 * 32;
+  }
   const long long need = std::max<long long>(32, (batch + 31) / 32 * 32);
   return (int)std::min(s, need);
 }
@@ -315,6 +445,7 @@ size_t admm_workspace_bytes(const admm_graph* g, int dtype, int64_t batch) {
   if (!g) return 0;
   if (g->kind == 3) {
     const int S = stream_slots(g, dtype, batch);
+    if (g->shard_ok[dtype]) return admm::StreamLayout(dtype ? 8 : 4, g->n_edges, g->n_vars, g->shard_G, S, true).total;
     const long long ncblk = (g->n_checks + admm::kStreamCK - 1) / admm::kStreamCK;
     return admm::StreamLayout(dtype ? 8 : 4, g->n_edges, g->n_vars, ncblk, S).total;
   }
@@ -391,12 +522,34 @@ int decode_impl(const admm_graph* g, int dtype, int64_t batch, const void* gamma
     admm::ResidentFrameArgs fa{batch, gamma, ld_gamma, mu, rho, thr, t_max, nullptr, nullptr, 0,
                                x_out, ld_x, hard_out, ld_hard, iters_out, flags_out, weight_out,
                                nullptr, nullptr, nullptr, synth};
-    const int rc = L.launch(sg, fa, S, workspace, grid, st);
+    int rc;
+    if (g->shard_ok[dtype]) {
+      const admm::ShardGeom geo = admm::shard_geom(dtype ? 8 : 4, g->D, g->shard_dv, g->n_checks, g->n_vars,
+                                                   g->shard_EB, g->shard_G, S);
+      rc = g->shlaunch[dtype].launch(sg, fa, S, workspace, g->shard_G, geo, st);
+    } else {
+      rc = L.launch(sg, fa, S, workspace, grid, st);
+    }
     if (rc != 0) return cuda_fail((cudaError_t)rc, "cudaLaunchCooperativeKernel");
     ADMM_CUDA(cudaGetLastError());
     return ADMM_OK;
   }
   ADMM_CUDA(cudaMemsetAsync(workspace, 0, sizeof(int), st));
+  if (g->kind == 4) {
+    if (z_in || z_out) return fail(ADMM_E_UNSUPPORTED, "state input/output is not supported by the cluster engine");
+    const admm::ClusterLaunch& CL = g->claunch[dtype];
+    const double thr = epsilon * epsilon * (double)g->n_edges;
+    const long long clusters = std::min<long long>(batch, CL.clusters);
+    admm::ResidentGraphArgs ga{g->n_vars, g->n_checks, g->m_pad, g->chk_var, g->var_pos, g->var_deg,
+                               g->edge_base, g->var_edge};
+    admm::ResidentFrameArgs fa{batch, gamma, ld_gamma, mu, rho, thr, t_max, nullptr, nullptr, 0,
+                               x_out, ld_x, hard_out, ld_hard, iters_out, flags_out, weight_out,
+                               nullptr, nullptr, reinterpret_cast<int*>(workspace), synth};
+    const int rc = CL.launch(ga, fa, (int)clusters, g->C, g->MC, g->NC, g->NT, CL.smem, st);
+    if (rc != 0) return cuda_fail((cudaError_t)rc, "cudaLaunchKernelEx(cluster)");
+    ADMM_CUDA(cudaGetLastError());
+    return ADMM_OK;
+  }
   const admm::ResidentLaunch& L = g->launch[dtype];
   const long long grid = std::min<long long>(batch, (long long)L.occupancy * g->num_sms);
   const double thr = epsilon * epsilon * (double)g->n_edges;  // admm_decoder.py:169

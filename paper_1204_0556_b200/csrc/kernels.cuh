@@ -8,6 +8,8 @@
 #include "resident.cuh"
 #include "resident_regular.cuh"
 #include "streaming.cuh"
+#include "cluster_resident.cuh"
+#include "sharded.cuh"
 
 namespace admm {
 
@@ -127,9 +129,9 @@ struct StreamLaunch {
   int occupancy, regs;
 };
 
-template <typename T, int D>
-int launch_streaming(const StreamGraphArgs& g, const ResidentFrameArgs& a, int S, void* ws, int grid,
-                     cudaStream_t st) {
+template <typename T>
+StreamParams<T> make_stream_params(const StreamGraphArgs& g, const ResidentFrameArgs& a, int S, void* ws,
+                                   long long ncblk, bool sharded) {
   StreamParams<T> p{};
   p.n_vars = g.n_vars;
   p.n_checks = g.n_checks;
@@ -157,8 +159,7 @@ int launch_streaming(const StreamGraphArgs& g, const ResidentFrameArgs& a, int S
   p.weight_out = a.weight_out;
   p.S = S;
   p.synth = a.synth;
-  const long long ncblk = (g.n_checks + kStreamCK - 1) / kStreamCK;
-  const StreamLayout L(sizeof(T), g.n_edges, g.n_vars, ncblk, S);
+  const StreamLayout L(sizeof(T), g.n_edges, g.n_vars, ncblk, S, sharded);
   char* base = static_cast<char*>(ws);
   p.zl = reinterpret_cast<T*>(base + L.zl);
   p.msg = reinterpret_cast<T*>(base + L.msg);
@@ -175,12 +176,67 @@ int launch_streaming(const StreamGraphArgs& g, const ResidentFrameArgs& a, int S
   p.nonint = ib + 5 * S;
   p.odd = ib + 6 * S;
   p.ctr = ib + 7 * S;
-  void* args[] = {&p};
-  return (int)cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&streaming_decode_kernel<T, D>), grid,
-                                          kStreamThreads, args, 0, st);
+  return p;
 }
 
-bool stream_lookup(int dtype, int D, StreamLaunch* out);
+template <typename T, int D, int DVMAX, bool REG>
+int launch_streaming(const StreamGraphArgs& g, const ResidentFrameArgs& a, int S, void* ws, int grid,
+                     cudaStream_t st) {
+  StreamParams<T> p = make_stream_params<T>(g, a, S, ws, (g.n_checks + kStreamCK - 1) / kStreamCK, false);
+  void* args[] = {&p};
+  return (int)cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&streaming_decode_kernel<T, D, DVMAX, REG>),
+                                          grid, kStreamThreads, args, 0, st);
+}
+
+struct ShardLaunch {
+  const void* fn;
+  int (*launch)(const StreamGraphArgs&, const ResidentFrameArgs&, int S, void* ws, int grid, const ShardGeom& geo,
+                cudaStream_t st);
+};
+
+template <typename T, int D, int DVMAX, bool REG>
+int launch_sharded(const StreamGraphArgs& g, const ResidentFrameArgs& a, int S, void* ws, int grid,
+                   const ShardGeom& geo, cudaStream_t st) {
+  StreamParams<T> p = make_stream_params<T>(g, a, S, ws, grid, true);
+  ShardGeom gg = geo;
+  void* args[] = {&p, &gg};
+  return (int)cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&sharded_decode_kernel<T, D, DVMAX, REG>),
+                                          grid, 512, args, geo.total, st);
+}
+
+bool shard_lookup(int dtype, int D, int DVMAX, bool regular, ShardLaunch* out);
+
+bool stream_lookup(int dtype, int D, int DVMAX, bool regular, StreamLaunch* out);
+
+// ---- cluster-resident engine ----
+struct ClusterLaunch {
+  const void* fn;
+  int (*launch)(const ResidentGraphArgs&, const ResidentFrameArgs&, int clusters, int C, int MC, int NC, int nt,
+                int smem, cudaStream_t st);
+  int clusters, regs, smem;
+};
+
+template <typename T, int D, int DV, int CPT, int VPT>
+int launch_cluster(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int clusters, int C, int MC, int NC, int nt,
+                   int smem, cudaStream_t st) {
+  const ResidentParams<T> p = make_params<T>(g, a);
+  const int* ve = g.var_edge;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(clusters * C);
+  cfg.blockDim = dim3(nt);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return (int)cudaLaunchKernelEx(&cfg, cluster_decode_kernel<T, D, DV, CPT, VPT>, p, ve, MC, NC);
+}
+
+bool cluster_lookup(int dtype, int D, int DV, int CPT, int VPT_min, int* VPT, ClusterLaunch* out);
 
 // Defined in project.cu.
 bool launch_project(int dtype, int D, long long m, int d, const void* in, void* out, cudaStream_t st);

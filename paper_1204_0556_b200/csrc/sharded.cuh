@@ -1,0 +1,282 @@
+// Sharded streaming engine: the streaming engine's slot machine (streaming.cuh)
+// with a STATIC partition of the Tanner graph over the persistent CTAs.
+//
+// CTA b owns checks [b*MB, (b+1)*MB) and variables [b*NB, (b+1)*NB) for all
+// S frame slots.  Because the assignment never changes, the replicas z and
+// duals lambda of its checks' edges stay in the CTA's SHARED MEMORY for the
+// whole run ([edge][slot] pairs), next to gamma/mu of its variables and the
+// graph indices of both; only the messages z - lambda/mu and the variables x
+// ([edge][slot] / [var][slot], slot-minor, so every warp access is 32
+// consecutive slots = 128 B) cross the chip through L2:
+//     phase V  reads 3 messages, writes x          (~5.3 B per edge-update)
+//     phase C  gathers x, writes the message       (~8 B per edge-update)
+// versus ~31 B per edge-update when z and lambda also stream through memory.
+// Partial residual sums are accumulated per lane (one slot) over the warp's
+// checks in a fixed order and combined per slot across warps and CTAs in a
+// fixed order, so the stop decision is deterministic.
+#pragma once
+
+#include "streaming.cuh"
+
+namespace admm {
+
+struct ShardGeom {
+  int MB, NB, EB;  // checks, variables, edges (max) per CTA
+  int zl, gm, cv, ce, ve, red, sint, total;  // shared-memory offsets (bytes)
+};
+
+inline ShardGeom shard_geom(int elem, int D, int dvmax, int M, int N, long long max_edges_per_cta, int G, int S) {
+  ShardGeom g{};
+  g.MB = (M + G - 1) / G;
+  g.NB = (N + G - 1) / G;
+  g.EB = static_cast<int>(max_edges_per_cta);
+  auto al = [](long long b) { return static_cast<int>((b + 15) & ~15ll); };
+  int o = 0;
+  g.zl = o; o = al(o + 2ll * elem * g.EB * S);
+  g.gm = o; o = al(o + 1ll * elem * g.NB * S);
+  g.cv = o; o = al(o + 4ll * g.MB * D);
+  g.ce = o; o = al(o + 4ll * g.MB);
+  g.ve = o; o = al(o + 4ll * g.NB * dvmax);
+  g.red = o; o = al(o + 2ll * elem * 16 * 32);
+  g.sint = o; o = al(o + 4ll * 2 * S);
+  g.total = o;
+  return g;
+}
+
+template <typename T, int D, int DVMAX, bool REG>
+__global__ void __launch_bounds__(512, 1) sharded_decode_kernel(const StreamParams<T> p, const ShardGeom geo) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nwarps = blockDim.x >> 5;
+  const int S = p.S, SG = S / 32, NWG = nwarps / SG;
+  const int b = blockIdx.x, G = gridDim.x;
+  const int cb0 = b * geo.MB, cb1 = min(p.n_checks, cb0 + geo.MB);
+  const int vb0 = b * geo.NB, vb1 = min(p.n_vars, vb0 + geo.NB);
+  const int mb = max(0, cb1 - cb0), nb = max(0, vb1 - vb0);
+  T* zl_s = reinterpret_cast<T*>(smem_raw + geo.zl);  // [edge - eb0][S][2]
+  T* gm_s = reinterpret_cast<T*>(smem_raw + geo.gm);  // [var - vb0][S]
+  // Graph slice, stored pre-multiplied by S (element offsets of slot 0), -1 = unused.
+  int* cv_s = reinterpret_cast<int*>(smem_raw + geo.cv);  // [check - cb0][D]    var * S
+  int* ce_s = reinterpret_cast<int*>(smem_raw + geo.ce);  // [check - cb0]       (local edge) * S
+  int* ve_s = reinterpret_cast<int*>(smem_raw + geo.ve);  // [var - vb0][DVMAX]  (global edge) * S
+  T* red = reinterpret_cast<T*>(smem_raw + geo.red);      // [16][32][2]
+  int* sint = reinterpret_cast<int*>(smem_raw + geo.sint);  // [S] weight, [S] non-integral (retiring)
+  const long long eb0 = mb > 0 ? __ldg(p.edge_base + cb0) : 0;
+
+  // ---- static graph slice (once) ----
+  for (int q = tid; q < mb * D; q += blockDim.x) {
+    const int lc = q / D, k = q % D;
+    const int v = __ldg(p.chk_var + k * p.m_pad + cb0 + lc);
+    cv_s[q] = v >= 0 ? v * S : -1;
+  }
+  for (int q = tid; q < mb; q += blockDim.x) ce_s[q] = static_cast<int>(__ldg(p.edge_base + cb0 + q) - eb0) * S;
+  for (int q = tid; q < nb * DVMAX; q += blockDim.x) {
+    const int lv = q / DVMAX, j = q % DVMAX;
+    const int e = j < p.dvmax ? __ldg(p.var_edge + (vb0 + lv) * p.dvmax + j) : -1;
+    ve_s[q] = e >= 0 ? e * S : -1;
+  }
+  if (b == 0 && tid == 0) {
+    p.ctr[0] = 0;
+    p.ctr[1] = p.S;
+    p.ctr[2] = 0;
+  }
+  grid.sync();
+  for (int s = b * blockDim.x + tid; s < S; s += G * blockDim.x) stream_refill(p, s);
+  grid.sync();
+
+  const long long SS = S;
+  const long long max_passes = ((long long)(p.batch + S - 1) / S + 1) * ((long long)p.t_max + 2) + 4;
+  for (long long pass = 0; pass < max_passes; ++pass) {
+    if (*(volatile int*)(p.ctr + 1) == 0) break;
+
+    // ---------------- phase V: this CTA's variables, all slots ----------------
+    for (int q = tid; q < 2 * S; q += blockDim.x) sint[q] = 0;
+    __syncthreads();
+    {
+      const int sg = w & (SG - 1), wi = w / SG;  // SG is a power of two
+      const int s = sg * 32 + lane;
+      const int state = p.st[s];
+      const long long f = p.frame[s];
+      T* xcol = p.x + s;
+      const T* mcol = p.msg + s;
+      if (state == kSlotRetiring) {
+        for (int lv = wi; lv < nb; lv += NWG) {
+          const int i = vb0 + lv;
+          const T xv = xcol[i * S];
+          const bool h = xv > T(0.5);
+          if (p.x_out) p.x_out[f * p.ld_x + i] = xv;
+          if (p.hard_out) p.hard_out[f * p.ld_hard + i] = h;
+          if (h) atomicAdd_block(sint + s, 1);
+          if (!(vmin(fabs(xv), fabs(T(1) - xv)) <= T(1e-5))) atomicOr_block(sint + S + s, 1);
+        }
+      } else if (state != kSlotEmpty) {
+        // Batches of VB variables: all their message loads are issued before
+        // any is consumed, so VB x DVMAX L2 round trips overlap.
+        constexpr int VB = 4;
+        for (int lv0 = wi; lv0 < nb; lv0 += VB * NWG) {
+          T mv[VB][DVMAX];
+          int degs[VB];
+#pragma unroll
+          for (int q = 0; q < VB; ++q) {
+            const int lv = lv0 + q * NWG;
+            degs[q] = 0;
+#pragma unroll
+            for (int j = 0; j < DVMAX; ++j) {
+              const int ev = lv < nb ? ve_s[lv * DVMAX + j] : -1;
+              degs[q] += ev >= 0;
+              mv[q][j] = (ev >= 0 && state == kSlotRunning) ? mcol[ev] : T(0);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < VB; ++q) {
+            const int lv = lv0 + q * NWG;
+            if (lv >= nb) break;
+            const int i = vb0 + lv;
+            T g;
+            if (state == kSlotFresh) {
+              const T gi = p.synth.kind != 0 ? static_cast<T>(synth_llr(p.synth, p.synth.trial0 + f, i))
+                                              : p.gamma[f * p.ld_gamma + i];
+              g = div_rn(gi, p.mu);
+              gm_s[lv * S + s] = g;
+            } else {
+              g = gm_s[lv * S + s];
+            }
+            const int deg = REG ? DVMAX : degs[q];
+            T acc = T(0);
+#pragma unroll
+            for (int j = 0; j < DVMAX; ++j)
+              if (REG || j < deg) acc = add_rn(acc, mv[q][j]);  // unused slots are 0 and at the end
+            T xv;
+            if (REG || deg > 0) {
+              const T num = sub_rn(acc, g);
+              const T inv = REG ? T(1) / T(DVMAX) : T(1) / T(deg);
+              xv = clip01(sizeof(T) == 8 ? div_rn(num, T(deg)) : mul_rn(num, inv));
+            } else {
+              xv = g < T(0) ? T(1) : T(0);
+            }
+            xcol[i * S] = xv;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    for (int s = tid; s < S; s += blockDim.x) {
+      if (sint[s]) atomicAdd(p.weight + s, sint[s]);
+      if (sint[S + s]) atomicOr(p.nonint + s, 1);
+    }
+    grid.sync();
+
+    // ---------------- phase C: this CTA's checks, all slots ----------------
+    {
+      const int sg = w % SG, wi = w / SG;
+      const int s = sg * 32 + lane;
+      const int state = p.st[s];
+      const bool live = state == kSlotFresh || state == kSlotRunning;
+      T primal = T(0), moved = T(0);
+      int odd = 0;
+      if (live || state == kSlotRetiring) {
+        const T* xcol = p.x + s;
+        T* mcol = p.msg + s;
+        T* zcol = zl_s + 2 * s;
+        const long long geS = eb0 * S;
+        // Software pipeline: the x-gathers of the warp's next check are in
+        // flight while the current check is projected.
+        T gx_nx[D];
+        int d_nx = D;
+        auto gather = [&](int lc, T (&dst)[D], int& dd) {
+          int vo[D];
+#pragma unroll
+          for (int k = 0; k < D; ++k) vo[k] = cv_s[lc * D + k];
+          dd = D;
+          if (!REG) {
+            dd = 0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) dd += vo[k] >= 0;
+          }
+#pragma unroll
+          for (int k = 0; k < D; ++k) dst[k] = (REG || k < dd) ? xcol[vo[k]] : T(0);
+        };
+        if (wi < mb) gather(wi, gx_nx, d_nx);
+        for (int lc = wi; lc < mb; lc += NWG) {
+          T gx[D];
+#pragma unroll
+          for (int k = 0; k < D; ++k) gx[k] = gx_nx[k];
+          const int d = d_nx;
+          if (lc + NWG < mb) gather(lc + NWG, gx_nx, d_nx);
+          if (!live) {  // retiring: syndrome of the final hard decision (codes.py:145-154)
+            int par = 0;
+#pragma unroll
+            for (int k = 0; k < D; ++k)
+              if (REG || k < d) par ^= gx[k] > T(0.5);
+            odd |= par;
+            continue;
+          }
+          const int le = ce_s[lc];  // (local edge) * S
+          T z[D], lam[D], w_[D], u[D], zn[D];
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            z[k] = T(0);
+            lam[k] = T(0);
+            if ((REG || k < d) && state == kSlotRunning) {
+              const T* zp = zcol + 2 * (le + k * S);
+              z[k] = zp[0];
+              lam[k] = zp[1];
+            }
+            w_[k] = add_rn(mul_rn(p.rho, gx[k]), mul_rn(p.one_minus_rho, z[k]));
+            u[k] = (REG || k < d)
+                       ? add_rn(w_[k], sizeof(T) == 8 ? div_rn(lam[k], p.mu) : mul_rn(lam[k], p.inv_mu))
+                       : -Num<T>::inf();
+          }
+          if constexpr (REG) {
+            project_pp_fixed<T, D>(u, zn);
+          } else {
+            project_pp<T, D>(u, zn, d);
+          }
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            if (REG || k < d) {
+              const T r1 = sub_rn(gx[k], zn[k]);
+              const T r2 = sub_rn(zn[k], z[k]);
+              primal = add_rn(primal, mul_rn(r1, r1));
+              moved = add_rn(moved, mul_rn(r2, r2));
+              const T lnew = add_rn(lam[k], mul_rn(p.mu, sub_rn(w_[k], zn[k])));
+              T* zp = zcol + 2 * (le + k * S);
+              zp[0] = zn[k];
+              zp[1] = lnew;
+              mcol[geS + le + k * S] = sub_rn(zn[k], sizeof(T) == 8 ? div_rn(lnew, p.mu) : mul_rn(lnew, p.inv_mu));
+            }
+          }
+        }
+      }
+      // Per-slot partials over the CTA's checks: warps of one slot group in a
+      // fixed order.
+      red[(w * 32 + lane) * 2] = live ? primal : T(odd);
+      red[(w * 32 + lane) * 2 + 1] = moved;
+      __syncthreads();
+      if (wi == 0) {
+        T a = T(0), bb = T(0);
+        for (int q = 0; q < NWG; ++q) {
+          const int ww = q * SG + sg;
+          a = add_rn(a, red[(ww * 32 + lane) * 2]);
+          bb = add_rn(bb, red[(ww * 32 + lane) * 2 + 1]);
+        }
+        if (live) {
+          p.part[((long long)b * S + s) * 2] = a;
+          p.part[((long long)b * S + s) * 2 + 1] = bb;
+          if (a >= p.thr || bb >= p.thr) atomicOr(p.notconv + s, 1);
+        } else if (state == kSlotRetiring && a > T(0)) {
+          atomicOr(p.odd + s, 1);
+        }
+      }
+    }
+    grid.sync();
+
+    // ---------------- phase S: one warp per slot ----------------
+    const int gwarp = (b * blockDim.x + tid) >> 5, n_gwarp = (G * blockDim.x) >> 5;
+    for (int s = gwarp; s < S; s += n_gwarp) stream_phase_s(p, s, G);
+    grid.sync();
+  }
+}
+
+}  // namespace admm

@@ -1,28 +1,78 @@
-// Instantiations of the streaming engine (one per dtype and degree bucket).
+// Instantiations of the streaming engine: dtype x check-degree bucket x
+// variable-degree bucket, plus regular-code variants (fixed projection only)
+// for the degrees of the BASELINE codes.
 #include "kernels.cuh"
 
 namespace admm {
 
-template <typename T, int D>
+template <typename T, int D, int DV, bool REG>
 StreamLaunch stream_entry() {
-  return StreamLaunch{reinterpret_cast<const void*>(&streaming_decode_kernel<T, D>), &launch_streaming<T, D>, 0, 0};
+  return StreamLaunch{reinterpret_cast<const void*>(&streaming_decode_kernel<T, D, DV, REG>),
+                      &launch_streaming<T, D, DV, REG>, 0, 0};
 }
 
-template <typename T>
-bool stream_lookup_t(int D, StreamLaunch* out) {
+template <typename T, int DV>
+bool stream_lookup_dv(int D, bool regular, StreamLaunch* out) {
+  if (regular) {
+    switch (D) {
+      case 6: *out = stream_entry<T, 6, DV, true>(); return true;
+      case 13: *out = stream_entry<T, 13, DV, true>(); return true;
+      default: break;
+    }
+  }
   switch (D) {
-    case 4: *out = stream_entry<T, 4>(); return true;
-    case 6: *out = stream_entry<T, 6>(); return true;
-    case 8: *out = stream_entry<T, 8>(); return true;
-    case 13: *out = stream_entry<T, 13>(); return true;
-    case 16: *out = stream_entry<T, 16>(); return true;
-    case 32: *out = stream_entry<T, 32>(); return true;
+    case 4: *out = stream_entry<T, 4, DV, false>(); return true;
+    case 6: *out = stream_entry<T, 6, DV, false>(); return true;
+    case 8: *out = stream_entry<T, 8, DV, false>(); return true;
+    case 13: *out = stream_entry<T, 13, DV, false>(); return true;
+    case 16: *out = stream_entry<T, 16, DV, false>(); return true;
+    case 32: *out = stream_entry<T, 32, DV, false>(); return true;
   }
   return false;
 }
 
-bool stream_lookup(int dtype, int D, StreamLaunch* out) {
-  return dtype ? stream_lookup_t<double>(D, out) : stream_lookup_t<float>(D, out);
+template <typename T>
+bool stream_lookup_t(int D, int DVMAX, bool regular, StreamLaunch* out) {
+  if (DVMAX <= 4) return stream_lookup_dv<T, 4>(D, regular, out);
+  if (DVMAX <= 8) return stream_lookup_dv<T, 8>(D, regular, out);
+  return false;
+}
+
+template <typename T, int D, int DV, bool REG>
+ShardLaunch shard_entry() {
+  return ShardLaunch{reinterpret_cast<const void*>(&sharded_decode_kernel<T, D, DV, REG>), &launch_sharded<T, D, DV, REG>};
+}
+
+template <typename T, int DV>
+bool shard_lookup_dv(int D, bool regular, ShardLaunch* out) {
+  (void)regular;
+  switch (D) {
+    case 4: *out = shard_entry<T, 4, DV, false>(); return true;
+    case 6: *out = shard_entry<T, 6, DV, false>(); return true;
+    case 8: *out = shard_entry<T, 8, DV, false>(); return true;
+    case 13: *out = shard_entry<T, 13, DV, false>(); return true;
+    case 16: *out = shard_entry<T, 16, DV, false>(); return true;
+  }
+  return false;
+}
+
+bool shard_lookup(int dtype, int D, int DVMAX, bool regular, ShardLaunch* out) {
+  // Regular codes with variable degree 3 (the BASELINE codes): exact degrees.
+  if (regular && DVMAX == 3 && D == 6) {
+    *out = dtype ? shard_entry<double, 6, 3, true>() : shard_entry<float, 6, 3, true>();
+    return true;
+  }
+  if (regular && DVMAX == 3 && D == 13) {
+    *out = dtype ? shard_entry<double, 13, 3, true>() : shard_entry<float, 13, 3, true>();
+    return true;
+  }
+  if (DVMAX <= 4) return dtype ? shard_lookup_dv<double, 4>(D, regular, out) : shard_lookup_dv<float, 4>(D, regular, out);
+  if (DVMAX <= 8) return dtype ? shard_lookup_dv<double, 8>(D, regular, out) : shard_lookup_dv<float, 8>(D, regular, out);
+  return false;
+}
+
+bool stream_lookup(int dtype, int D, int DVMAX, bool regular, StreamLaunch* out) {
+  return dtype ? stream_lookup_t<double>(D, DVMAX, regular, out) : stream_lookup_t<float>(D, DVMAX, regular, out);
 }
 
 }  // namespace admm

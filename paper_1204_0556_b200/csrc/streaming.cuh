@@ -84,19 +84,19 @@ struct StreamParams {
 struct StreamLayout {
   size_t zl, msg, x, gm, part, ints, total;
   static size_t al(size_t b) { return (b + 255) & ~size_t(255); }
-  StreamLayout(size_t elem, long long E, long long N, long long ncblk, long long S) {
+  StreamLayout(size_t elem, long long E, long long N, long long ncblk, long long S, bool sharded = false) {
     size_t o = 0;
-    zl = o; o += al(elem * 2 * E * S);
+    zl = o; o += sharded ? 0 : al(elem * 2 * E * S);  // sharded: z, lambda live in shared memory
     msg = o; o += al(elem * E * S);
     x = o; o += al(elem * N * S);
-    gm = o; o += al(elem * N * S);
+    gm = o; o += sharded ? 0 : al(elem * N * S);
     part = o; o += al(elem * 2 * ncblk * S);
     ints = o; o += al(sizeof(long long) * S) + al(sizeof(int) * (7 * S + 8));
     total = o;
   }
 };
 
-template <typename T, int D>
+template <typename T, int D, int DVMAX>
 __device__ __forceinline__ void stream_phase_v(const StreamParams<T>& p, int tile, int n_vtiles_x, int* sred) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int i = (tile % n_vtiles_x) * kStreamVK + w;
@@ -130,12 +130,19 @@ __device__ __forceinline__ void stream_phase_v(const StreamParams<T>& p, int til
       } else {
         g = p.gm[i * S + s];
       }
-      for (int j = 0; j < p.dvmax; ++j) {
-        const int e = __ldg(p.var_edge + i * p.dvmax + j);  // warp-uniform, increasing edge id
-        if (e < 0) break;
-        ++deg;
-        if (state == kSlotRunning) acc = add_rn(acc, p.msg[e * S + s]);
+      int ev[DVMAX];
+#pragma unroll
+      for (int j = 0; j < DVMAX; ++j)  // warp-uniform, increasing edge id, -1 = unused
+        ev[j] = j < p.dvmax ? __ldg(p.var_edge + i * p.dvmax + j) : -1;
+      T mv[DVMAX];
+#pragma unroll
+      for (int j = 0; j < DVMAX; ++j) {
+        deg += ev[j] >= 0;
+        mv[j] = (ev[j] >= 0 && state == kSlotRunning) ? p.msg[(long long)ev[j] * S + s] : T(0);
       }
+#pragma unroll
+      for (int j = 0; j < DVMAX; ++j)
+        if (ev[j] >= 0) acc = add_rn(acc, mv[j]);
       T xv;
       if (deg > 0) {
         xv = clip01(div_rn(sub_rn(acc, g), T(deg)));
@@ -152,7 +159,7 @@ __device__ __forceinline__ void stream_phase_v(const StreamParams<T>& p, int til
   }
 }
 
-template <typename T, int D>
+template <typename T, int D, bool REG>
 __device__ __forceinline__ void stream_phase_c(const StreamParams<T>& p, int tile, int n_ctiles_x, T* red) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int cblk = tile % n_ctiles_x;
@@ -193,7 +200,7 @@ __device__ __forceinline__ void stream_phase_c(const StreamParams<T>& p, int til
       u[k] = on ? add_rn(w_[k], sizeof(T) == 8 ? div_rn(lam[k], p.mu) : mul_rn(lam[k], p.inv_mu))
                 : -Num<T>::inf();
     }
-    if (d == D) {
+    if constexpr (REG) {
       project_pp_fixed<T, D>(u, zn);
     } else {
       project_pp<T, D>(u, zn, d);
@@ -314,8 +321,8 @@ __device__ __forceinline__ void stream_phase_s(const StreamParams<T>& p, int s, 
   }
 }
 
-template <typename T, int D>
-__global__ void __launch_bounds__(kStreamThreads) streaming_decode_kernel(const StreamParams<T> p) {
+template <typename T, int D, int DVMAX, bool REG>
+__global__ void __launch_bounds__(kStreamThreads, 4) streaming_decode_kernel(const StreamParams<T> p) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ T red[2 * kStreamCK * 32];
@@ -340,9 +347,9 @@ __global__ void __launch_bounds__(kStreamThreads) streaming_decode_kernel(const 
   const long long max_passes = ((long long)(p.batch + p.S - 1) / p.S + 1) * ((long long)p.t_max + 2) + 4;
   for (long long pass = 0; pass < max_passes; ++pass) {
     if (*(volatile int*)(p.ctr + 1) == 0) break;
-    for (int tile = blockIdx.x; tile < n_vt; tile += gridDim.x) stream_phase_v<T, D>(p, tile, n_vtx, sred);
+    for (int tile = blockIdx.x; tile < n_vt; tile += gridDim.x) stream_phase_v<T, D, DVMAX>(p, tile, n_vtx, sred);
     grid.sync();
-    for (int tile = blockIdx.x; tile < n_ct; tile += gridDim.x) stream_phase_c<T, D>(p, tile, n_ctx, red);
+    for (int tile = blockIdx.x; tile < n_ct; tile += gridDim.x) stream_phase_c<T, D, REG>(p, tile, n_ctx, red);
     grid.sync();
     for (int s = gwarp; s < p.S; s += n_gwarp) stream_phase_s(p, s, n_ctx);
     grid.sync();

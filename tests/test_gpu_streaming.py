@@ -16,8 +16,9 @@ def _frames(f, code, n, point=0):
     return np.array([O.trial_gamma_awgn(code.n_vars, float(f["snr_db"]), rate, 1, point, t) for t in range(n)])
 
 
+@pytest.mark.parametrize("engine,kind", [("streaming", 3), ("cluster", 4)])
 @pytest.mark.parametrize("name", ["decode_cfg1.npz", "decode_cfg2.npz", "decode_cfg4.npz"])
-def test_streaming_f64_matches_reference_golden(cuda_ok, name):
+def test_streaming_f64_matches_reference_golden(cuda_ok, name, engine, kind):
     from paper_1204_0556_b200 import AdmmConfig, decode_batch
 
     f = load_golden(name)
@@ -25,8 +26,8 @@ def test_streaming_f64_matches_reference_golden(cuda_ok, name):
     B = len(f["iterations"])
     gam = _frames(f, code, B)
     cfg = AdmmConfig(mu=float(f["mu"]), epsilon=float(f["epsilon"]), t_max=int(f["t_max"]), rho=float(f["rho"]))
-    res = decode_batch(gam, code, cfg, dtype=torch.float64, want_hard=True, engine="streaming")
-    assert res.info["engine"] == 3
+    res = decode_batch(gam, code, cfg, dtype=torch.float64, want_hard=True, engine=engine)
+    assert res.info["engine"] == kind
     want_hard = np.unpackbits(f["hard"], axis=1)[:, : code.n_vars]
     fl = res.flags.cpu().numpy()
     assert np.array_equal(res.iterations.cpu().numpy(), f["iterations"])
@@ -39,14 +40,15 @@ def test_streaming_f64_matches_reference_golden(cuda_ok, name):
     assert np.abs(res.x[:nx].cpu().numpy() - f["x"]).max() <= 1e-9
 
 
-def test_streaming_equals_resident_f32(cuda_ok):
+@pytest.mark.parametrize("engine", ["streaming", "cluster"])
+def test_streaming_equals_resident_f32(cuda_ok, engine):
     from paper_1204_0556_b200 import AdmmConfig, baseline_code, decode_batch
 
     code = baseline_code("cfg2_n1008")
     g = torch.randn(200, code.n_vars, device="cuda", generator=torch.Generator("cuda").manual_seed(1)) * 2.5 + 3.2
     cfg = AdmmConfig(mu=5.0)
     a = decode_batch(g, code, cfg, dtype=torch.float32, engine="resident")
-    b = decode_batch(g, code, cfg, dtype=torch.float32, engine="streaming")
+    b = decode_batch(g, code, cfg, dtype=torch.float32, engine=engine)
     same = (a.x > 0.5).eq(b.x > 0.5).all(dim=1).float().mean().item()
     assert same >= 0.995
     assert (a.iterations - b.iterations).abs().float().mean().item() <= 2.0
@@ -71,15 +73,17 @@ def test_streaming_irregular_and_zero_degree(cuda_ok):
             assert np.abs(res.x[t].cpu().numpy() - r.x).max() <= 1e-9
 
 
-def test_config5_large_block_matches_oracle(cuda_ok):
-    """n = 16384 does not fit one SM: the automatic engine is streaming."""
+@pytest.mark.parametrize("engine", ["auto", "streaming"])
+def test_config5_large_block_matches_oracle(cuda_ok, engine):
+    """n = 16384 does not fit one SM: the automatic engine is the cluster
+    engine (16 CTAs per frame); the streaming engine is checked too."""
     from paper_1204_0556_b200 import AdmmConfig, baseline_code, decode_batch
 
     code = baseline_code("cfg5_n16384")
     gam = np.stack([O.trial_gamma_bsc(code.n_vars, 0.04, 1, 0, t) for t in range(3)]
                    + [O.trial_gamma_awgn(code.n_vars, 2.5, 0.5, 1, 1, t) for t in range(3)])
     cfg = AdmmConfig(mu=5.0)
-    res = decode_batch(gam, code, cfg, dtype=torch.float64, want_hard=True)
+    res = decode_batch(gam, code, cfg, dtype=torch.float64, want_hard=True, engine=engine)
     assert res.info["engine"] == 3
     g = O.Graph.of(code)
     for t in range(len(gam)):
@@ -87,19 +91,20 @@ def test_config5_large_block_matches_oracle(cuda_ok):
         assert int(res.iterations[t]) == r.iterations
         assert np.abs(res.x[t].cpu().numpy() - r.x).max() <= 1e-9
         assert np.array_equal(res.hard[t].cpu().numpy(), r.hard_decision)
-    r32 = decode_batch(gam, code, cfg, dtype=torch.float32, want_hard=True)
+    r32 = decode_batch(gam, code, cfg, dtype=torch.float32, want_hard=True, engine=engine)
     assert torch.equal(r32.hard, res.hard)
 
 
-def test_streaming_rejects_state_io(cuda_ok):
+@pytest.mark.parametrize("engine", ["streaming", "cluster"])
+def test_streaming_rejects_state_io(cuda_ok, engine):
     from paper_1204_0556_b200 import AdmmConfig, baseline_code, decode_batch
 
     code = baseline_code("cfg1_n96")
     with pytest.raises(RuntimeError):
-        decode_batch(np.zeros((1, 96)), code, AdmmConfig(), want_state=True, engine="streaming")
+        decode_batch(np.zeros((1, 96)), code, AdmmConfig(), want_state=True, engine=engine)
 
 
-@pytest.mark.parametrize("engine", ["auto", "streaming"])
+@pytest.mark.parametrize("engine", ["auto", "streaming", "cluster"])
 def test_fused_synthesis_equals_materialised_llrs(cuda_ok, engine):
     """decode_synth (LLRs generated inside the decode kernel) == decode_batch
     on the LLRs synth_llr writes out; trial-indexed, so any split agrees."""
