@@ -35,6 +35,7 @@ from .codes import (
     parse_alist,
 )
 from .parity_polytope import PARITY_TOL, project_batch
+from .simulator import DecoderRef, MlOutcome, TrialStats, ml_account, run_point, stats_to_csv, sweep
 
 __version__ = "0.1.0"
 
@@ -45,4 +46,5 @@ __all__ = [
     "AlistParseError", "CodeGenerationError", "ParityCheckMatrix", "baseline_code", "emit_alist",
     "gen_regular_ldpc", "is_codeword", "make_ldpc", "parse_alist",
     "PARITY_TOL", "project_batch",
+    "DecoderRef", "MlOutcome", "TrialStats", "ml_account", "run_point", "stats_to_csv", "sweep",
 ]

@@ -23,6 +23,9 @@ fixed_cfg1.npz     config-1 frames 0..15 decoded for a FIXED number of
                    iterations (epsilon=1e-300 so eps^2 == 0) T = 1, 50, 1000.
 decode_cfg2.npz    config-2 code (n=1008, girth 6) at 2.0 dB, 24 frames.
 decode_cfg4.npz    config-4 code ((3,13), n=1040, girth 6) at 4.0 dB, 24 frames.
+harness.npz        reference sweep()/run_point() CSV (timing=False) on the config-1
+                   code: fixed-count sweep over BSC 0.03 / AWGN 2.5 dB and a
+                   target-errors run (exact truncation), for the GPU harness.
 steps.npz          single-iteration state dumps (x, z, lam) after 1, 2, 3
                    iterations for one config-1 frame (x_update / z_update /
                    lambda_update driven directly, as test_admm.py:151-160).
@@ -141,12 +144,28 @@ def steps_fixture(code):
     np.savez_compressed(OUT / "steps.npz", n_vars=code.n_vars, check_ptr=ptr, edge_var=ev, **rec)
 
 
+def harness_fixture(code):
+    from polylp import Awgn, Bsc, DecoderRef, run_point, stats_to_csv, sweep
+
+    rc = ref_code(code)
+    dec = DecoderRef("admm", AdmmConfig(mu=3.0))
+    csv_sweep = stats_to_csv(sweep(rc, [Bsc(0.03), Awgn(2.5, rc.design_rate)], dec, n_trials=300, seed=107,
+                                   workers=1), timing=False)
+    csv_target = stats_to_csv([run_point(rc, Bsc(0.05), dec, target_errors=20, max_trials=5000, seed=108,
+                                         point_index=2)], timing=False)
+    ptr, ev = pack_checks(code)
+    np.savez_compressed(OUT / "harness.npz", n_vars=code.n_vars, check_ptr=ptr, edge_var=ev,
+                        csv_sweep=np.array(csv_sweep), csv_target=np.array(csv_target))
+    print(csv_sweep, csv_target)
+
+
 def main():
     projection_fixture()
     c1 = baseline_code("cfg1_n96")
     decode_fixture("decode_cfg1.npz", c1, 3.0, 1000, 200, AdmmConfig(mu=5.0))
     fixed_fixture(c1)
     steps_fixture(c1)
+    harness_fixture(c1)
     decode_fixture("decode_cfg2.npz", baseline_code("cfg2_n1008"), 2.0, 24, 24, AdmmConfig(mu=5.0))
     decode_fixture("decode_cfg4.npz", baseline_code("cfg4_n1040"), 4.0, 24, 24, AdmmConfig(mu=5.0))
 
