@@ -68,6 +68,7 @@ typedef struct admm_graph_info {
   int32_t regs_f32, regs_f64;
   int32_t num_sms;
   int32_t cluster_size;     /* CTAs per cluster (engine 4), else 0 */
+  double layout_cost_before, layout_cost_after; /* bank-conflict cost of the relabeling (engine 2) */
 } admm_graph_info;
 
 /* Build the device-resident Tanner graph.  Replaces the edge-array views of

@@ -54,6 +54,7 @@ class GraphInfo(ctypes.Structure):
         ("smem_bytes_f32", ctypes.c_int32), ("smem_bytes_f64", ctypes.c_int32),
         ("regs_f32", ctypes.c_int32), ("regs_f64", ctypes.c_int32),
         ("num_sms", ctypes.c_int32), ("cluster_size", ctypes.c_int32),
+        ("layout_cost_before", ctypes.c_double), ("layout_cost_after", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

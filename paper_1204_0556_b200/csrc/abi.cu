@@ -10,6 +10,7 @@
 
 #include "../../include/admm_b200.h"
 #include "kernels.cuh"
+#include "layout.h"
 
 namespace {
 
@@ -54,6 +55,10 @@ struct admm_graph {
   uint8_t* var_deg = nullptr;
   int* edge_base = nullptr;
   int* var_edge = nullptr;
+  int* var_orig = nullptr;      // relabeled regular layout (kind 2)
+  int* edge_ref = nullptr;
+  int* var_edge_int = nullptr;
+  double layout_cost[2] = {0, 0};
   // per-dtype launch data
   admm::ResidentLaunch launch[2];
 };
@@ -363,7 +368,38 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
   cudaError_t e3 = up((void**)&g->var_deg, var_deg.data(), var_deg.size());
   cudaError_t e4 = up((void**)&g->edge_base, edge_base.data(), edge_base.size() * sizeof(int));
   cudaError_t e5 = up((void**)&g->var_edge, var_edge.data(), var_edge.size() * sizeof(int));
-  for (cudaError_t e : {e1, e2, e3, e4, e5}) {
+  cudaError_t e6 = cudaSuccess, e7 = cudaSuccess, e8 = cudaSuccess;
+  if (g->kind == 2 && std::getenv("ADMM_B200_NO_RELABEL") == nullptr) {
+    // Bank-conflict-aware relabeling (layout.h): internal variable numbering
+    // and slot order inside each check chosen so each warp's shared-memory
+    // gathers spread over the 32 banks.  chk_var is rewritten in internal
+    // variables; the kernel maps back through var_orig / edge_ref.
+    const int ds = (dmax % 2 == 0) ? dmax + 1 : dmax;
+    long long moves = std::min<long long>(8000000, 2000ll * E);
+    if (const char* env = std::getenv("ADMM_B200_LAYOUT_MOVES")) moves = std::atoll(env);
+    const admm::Layout lay = admm::optimize_layout(rows, n_vars, dmax, dvmax, ds, moves, 12345);
+    g->layout_cost[0] = lay.cost_before;
+    g->layout_cost[1] = lay.cost_after;
+    std::vector<int> chk2((size_t)D * MP, -1), eref((size_t)MP * dmax, 0), vorig(n_vars), vint((size_t)n_vars * dvmax);
+    for (int c = 0; c < n_checks; ++c)
+      for (int r = 0; r < dmax; ++r) {
+        const int e = c * dmax + r, k = lay.edge_slot[e];
+        chk2[(size_t)k * MP + c] = lay.slot_of_var[rows[c][r]];
+        eref[(size_t)c * dmax + k] = check_ptr[c] + r;
+      }
+    std::vector<int> fill(n_vars, 0);
+    for (int c = 0; c < n_checks; ++c)  // increasing check order per variable
+      for (int r = 0; r < dmax; ++r) {
+        const int v = rows[c][r], i = lay.slot_of_var[v];
+        vint[(size_t)i * dvmax + fill[v]++] = c * dmax + lay.edge_slot[c * dmax + r];
+      }
+    for (int i = 0; i < n_vars; ++i) vorig[i] = lay.var_of_slot[i];
+    cudaMemcpy(g->chk_var, chk2.data(), chk2.size() * sizeof(int), cudaMemcpyHostToDevice);
+    e6 = up((void**)&g->var_orig, vorig.data(), vorig.size() * sizeof(int));
+    e7 = up((void**)&g->edge_ref, eref.data(), eref.size() * sizeof(int));
+    e8 = up((void**)&g->var_edge_int, vint.data(), vint.size() * sizeof(int));
+  }
+  for (cudaError_t e : {e1, e2, e3, e4, e5, e6, e7, e8}) {
     if (e != cudaSuccess) {
       admm_graph_destroy(g);
       return cuda_fail(e, "graph upload");
@@ -381,6 +417,9 @@ int admm_graph_destroy(admm_graph* g) {
   cudaFree(g->var_deg);
   cudaFree(g->edge_base);
   cudaFree(g->var_edge);
+  cudaFree(g->var_orig);
+  cudaFree(g->edge_ref);
+  cudaFree(g->var_edge_int);
   delete g;
   return ADMM_OK;
 }
@@ -405,6 +444,8 @@ int admm_graph_get_info(const admm_graph* g, admm_graph_info* info) {
   info->regs_f32 = st ? g->slaunch[0].regs : cl ? g->claunch[0].regs : g->launch[0].regs;
   info->regs_f64 = st ? g->slaunch[1].regs : cl ? g->claunch[1].regs : g->launch[1].regs;
   info->cluster_size = g->C;
+  info->layout_cost_before = g->layout_cost[0];
+  info->layout_cost_after = g->layout_cost[1];
   info->num_sms = g->num_sms;
   return ADMM_OK;
 }
@@ -547,7 +588,7 @@ int decode_impl(const admm_graph* g, int dtype, int64_t batch, const void* gamma
     const double thr = epsilon * epsilon * (double)g->n_edges;
     const long long clusters = std::min<long long>(batch, CL.clusters);
     admm::ResidentGraphArgs ga{g->n_vars, g->n_checks, g->m_pad, g->chk_var, g->var_pos, g->var_deg,
-                               g->edge_base, g->var_edge};
+                               g->edge_base, g->var_edge, nullptr, nullptr, nullptr};
     admm::ResidentFrameArgs fa{batch, gamma, ld_gamma, mu, rho, thr, t_max, nullptr, nullptr, 0,
                                x_out, ld_x, hard_out, ld_hard, iters_out, flags_out, weight_out,
                                nullptr, nullptr, reinterpret_cast<int*>(workspace), synth};
@@ -561,7 +602,7 @@ int decode_impl(const admm_graph* g, int dtype, int64_t batch, const void* gamma
   const double thr = epsilon * epsilon * (double)g->n_edges;  // admm_decoder.py:169
 
   admm::ResidentGraphArgs ga{g->n_vars, g->n_checks, g->m_pad, g->chk_var, g->var_pos, g->var_deg,
-                             g->edge_base, g->var_edge};
+                             g->edge_base, g->var_edge, g->var_orig, g->edge_ref, g->var_edge_int};
   admm::ResidentFrameArgs fa{batch, gamma, ld_gamma, mu, rho, thr, t_max, z_in, lam_in, ld_edge,
                              x_out, ld_x, hard_out, ld_hard, iters_out, flags_out, weight_out,
                              z_out, lam_out, reinterpret_cast<int*>(workspace), synth};

@@ -20,6 +20,9 @@ struct ResidentGraphArgs {
   const uint8_t* var_deg;
   const int* edge_base;
   const int* var_edge;  // [n_vars][DV] reference edge ids (regular kernels)
+  const int* var_orig;  // relabeled regular layout (layout.h), may be null
+  const int* edge_ref;
+  const int* var_edge_int;  // relabeled: [internal var][DV] internal edge c*D + k
 };
 
 struct ResidentFrameArgs {
@@ -63,6 +66,8 @@ ResidentParams<T> make_params(const ResidentGraphArgs& g, const ResidentFrameArg
   p.var_pos = g.var_pos;
   p.var_deg = g.var_deg;
   p.edge_base = g.edge_base;
+  p.var_orig = g.var_orig;
+  p.edge_ref = g.edge_ref;
   p.batch = a.batch;
   p.gamma = static_cast<const T*>(a.gamma);
   p.ld_gamma = a.ld_gamma;
@@ -98,7 +103,8 @@ void launch_resident(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int
 template <typename T, int D, int DV, int CPT, int VPT, int MINB>
 void launch_regular(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int grid, int nt, int smem,
                     cudaStream_t st) {
-  resident_regular_kernel<T, D, DV, CPT, VPT, MINB><<<grid, nt, smem, st>>>(make_params<T>(g, a), g.var_edge);
+  resident_regular_kernel<T, D, DV, CPT, VPT, MINB><<<grid, nt, smem, st>>>(
+      make_params<T>(g, a), g.var_edge_int ? g.var_edge_int : g.var_edge);
 }
 
 // Regular-code variants: (D, DV, CPT, VPT).  Returns false when none fits.

@@ -39,6 +39,8 @@ struct ResidentParams {
   const uint16_t* var_pos;    // [n_vars][DVMAX] msg positions of the variable's edges
   const uint8_t* var_deg;     // [n_vars]
   const int* edge_base;       // [n_checks]  reference edge id of slot 0 (check_ptr)
+  const int* var_orig;        // regular kernel: internal variable -> original variable (null = identity)
+  const int* edge_ref;        // regular kernel: [check][D] reference edge id of slot k (null = c*D + k)
   // frames
   long long batch;
   const T* gamma;

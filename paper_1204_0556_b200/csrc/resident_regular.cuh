@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const Resid
   }
   uint32_t vaddr[VPT][DV];
   uint32_t xst[VPT];
+  int vorig[VPT];  // original variable of each owned internal variable (layout.h relabeling)
   bool vact[VPT];
 #pragma unroll
   for (int q = 0; q < VPT; ++q) {
@@ -73,6 +74,7 @@ __global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const Resid
       vaddr[q][j] = msg_a + ES * ((e / D) * DS + (e % D));
     }
     xst[q] = xs_a + ES * i;
+    vorig[q] = (vact[q] && p.var_orig) ? __ldg(p.var_orig + i) : i;
   }
 
   const T inv_mu = p.inv_mu;
@@ -92,7 +94,7 @@ __global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const Resid
 
     // ---- frame setup ----
 #pragma unroll
-    for (int q = 0; q < VPT; ++q) gm[q] = vact[q] ? div_rn(frame_llr<T>(p, f, tid + q * NT), p.mu) : T(0);
+    for (int q = 0; q < VPT; ++q) gm[q] = vact[q] ? div_rn(frame_llr<T>(p, f, vorig[q]), p.mu) : T(0);
 #pragma unroll
     for (int q = 0; q < CPT; ++q) {
       const int c = tid + q * NT;
@@ -100,7 +102,7 @@ __global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const Resid
       for (int k = 0; k < D; ++k) {
         T z0 = T(0), l0 = T(0);
         if (p.z_in != nullptr && cact[q]) {
-          const long long e = f * p.ld_edge + (long long)c * D + k;
+          const long long e = f * p.ld_edge + (p.edge_ref ? __ldg(p.edge_ref + c * D + k) : c * D + k);
           z0 = p.z_in[e];
           l0 = p.lam_in[e];
         }
@@ -180,7 +182,7 @@ __global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const Resid
 #pragma unroll
     for (int q = 0; q < VPT; ++q) {
       if (vact[q]) {
-        const int i = tid + q * NT;
+        const int i = vorig[q];
         const T xv = lds(xst[q], T());
         const bool h = xv > T(0.5);
         ones += h;
@@ -201,7 +203,7 @@ __global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const Resid
         if (p.z_out) {
 #pragma unroll
           for (int k = 0; k < D; ++k) {
-            const long long e = f * p.ld_edge + (long long)c * D + k;
+            const long long e = f * p.ld_edge + (p.edge_ref ? __ldg(p.edge_ref + c * D + k) : c * D + k);
             p.z_out[e] = z[q][k];
             p.lam_out[e] = lam[q][k];
           }
