@@ -369,15 +369,20 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
   cudaError_t e4 = up((void**)&g->edge_base, edge_base.data(), edge_base.size() * sizeof(int));
   cudaError_t e5 = up((void**)&g->var_edge, var_edge.data(), var_edge.size() * sizeof(int));
   cudaError_t e6 = cudaSuccess, e7 = cudaSuccess, e8 = cudaSuccess;
-  if (g->kind == 2 && std::getenv("ADMM_B200_NO_RELABEL") == nullptr) {
-    // Bank-conflict-aware relabeling (layout.h): internal variable numbering
-    // and slot order inside each check chosen so each warp's shared-memory
-    // gathers spread over the 32 banks.  chk_var is rewritten in internal
+  if (g->kind == 2) {
+    // Bank-conflict-free layout (layout.h): internal variable numbering and
+    // the slot of every edge inside its check, with the message of edge
+    // (c, v) stored at msg[slot][pi(v)].  chk_var is rewritten in internal
     // variables; the kernel maps back through var_orig / edge_ref.
-    const int ds = (dmax % 2 == 0) ? dmax + 1 : dmax;
-    long long moves = std::min<long long>(8000000, 2000ll * E);
+    long long moves = std::min<long long>(20000000, 4000ll * E);
     if (const char* env = std::getenv("ADMM_B200_LAYOUT_MOVES")) moves = std::atoll(env);
-    const admm::Layout lay = admm::optimize_layout(rows, n_vars, dmax, dvmax, ds, moves, 12345);
+    admm::Layout lay = admm::optimize_layout(rows, n_vars, dmax, moves, 12345);
+    for (int retry = 1; retry < 4 && lay.clashes > 0; ++retry)
+      lay = admm::optimize_layout(rows, n_vars, dmax, moves * (retry + 1), 12345 + retry);
+    if (lay.clashes > 0) {
+      admm_graph_destroy(g);
+      return fail(ADMM_E_UNSUPPORTED, "no clash-free message layout found");
+    }
     g->layout_cost[0] = lay.cost_before;
     g->layout_cost[1] = lay.cost_after;
     std::vector<int> chk2((size_t)D * MP, -1), eref((size_t)MP * dmax, 0), vorig(n_vars), vint((size_t)n_vars * dvmax);

@@ -1,107 +1,111 @@
-// Bank-conflict-aware relabeling of the Tanner graph for the regular
-// resident kernel (host code, run once in admm_graph_create).
+// Bank-conflict-free layout of the Tanner graph for the regular resident
+// kernel (host code, run once in admm_graph_create).
 //
-// The kernel's shared-memory gathers are:
-//   x-gather   warp = 32 consecutive (internal) checks, slot k:   address x[pi(v)]
-//   msg-gather warp = 32 consecutive (internal) variables, edge j: address msg[c*DS + k(c,v)]
-// (fp32: bank = word address mod 32).  Both the internal variable numbering
-// pi and the slot k of every edge inside its check are free: the projection
-// is permutation-equivariant and a variable still sums its messages in
-// increasing check order, so results are unchanged.  This module searches
-// (pi, k) by simulated annealing to minimise sum over gather groups of
-// sum_bank count^2 -- 32 lanes on 32 distinct banks is one wavefront.
+// Shared-memory layout of the kernel (fp32 bank = word address mod 32):
+//     x   [Npad]            x of internal variable i at word i
+//     msg [D][Npad]         message of edge (c, v) at word k*Npad + pi(v),
+//                           k = the edge's slot inside check c
+// with Npad a multiple of 32.  The accesses are:
+//   var phase   a warp = 32 consecutive internal variables i; loads
+//               msg[k_j(i)][i] for j < DV and stores x[i]: bank = i mod 32,
+//               conflict-free BY CONSTRUCTION;
+//   check phase a warp = 32 consecutive checks; for slot k it loads x[pi(v)]
+//               and stores msg[k][pi(v)]: bank = pi(v) mod 32 for both.
+// So one constraint family remains: inside every (check-warp, slot k) column
+// the 32 variables must have distinct pi(v) mod 32.  The message buffer
+// additionally needs the DV edges of a variable in DISTINCT slots (they share
+// the word msg[k][pi(v)] otherwise).  Both the internal numbering pi and the
+// slot of every edge inside its check are free -- the projection is
+// permutation-equivariant and a variable still sums its messages in
+// increasing check order -- so results are unchanged.  Simulated annealing
+// over (pi swaps, in-check slot swaps) minimises
+//     sum over columns of sum_bank C(count, 2)  +  W * (slot clashes)
+// and reports the resulting wavefront histogram.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
-#include <algorithm>
 #include <random>
 #include <vector>
 
 namespace admm {
 
 struct Layout {
-  std::vector<int> var_of_slot;   // internal var index -> original var
-  std::vector<int> slot_of_var;   // original var -> internal var index
-  std::vector<int> edge_slot;     // per original edge (check-major, sorted rows): slot k inside its check
+  std::vector<int> var_of_slot;  // internal var index -> original var
+  std::vector<int> slot_of_var;  // original var -> internal var index
+  std::vector<int> edge_slot;    // per original edge (c*D + sorted position): slot k inside check c
   double cost_before = 0, cost_after = 0;
+  int clashes = 0;               // variables with two edges in one slot (must be 0 to use the layout)
+  int max_wavefronts = 0;        // worst column after optimisation
 };
 
-// rows[c] = sorted original variables of check c (all of size D); each
-// variable has degree DV.  ds = message row stride (odd).
-inline Layout optimize_layout(const std::vector<std::vector<int>>& rows, int n_vars, int D, int DV, int ds,
-                              long long moves, uint64_t seed) {
+inline Layout optimize_layout(const std::vector<std::vector<int>>& rows, int n_vars, int D, long long moves,
+                              uint64_t seed) {
   const int M = static_cast<int>(rows.size());
+  const int E = M * D;
   Layout L;
   std::mt19937_64 rng(seed);
-  // edges: e = c*D + (index in sorted row)
-  std::vector<int> ev(static_cast<size_t>(M) * D), ec(static_cast<size_t>(M) * D);
-  std::vector<std::vector<int>> var_edges(n_vars);  // increasing check order
+  std::vector<int> ev(E), ec(E);
+  std::vector<std::vector<int>> var_edges(n_vars);
   for (int c = 0; c < M; ++c)
     for (int r = 0; r < D; ++r) {
-      const int e = c * D + r;
-      ev[e] = rows[c][r];
-      ec[e] = c;
-      var_edges[rows[c][r]].push_back(e);
+      ev[c * D + r] = rows[c][r];
+      ec[c * D + r] = c;
+      var_edges[rows[c][r]].push_back(c * D + r);
     }
-  std::vector<int> jidx(static_cast<size_t>(M) * D);  // position of edge e in its variable's edge list
-  for (int v = 0; v < n_vars; ++v)
-    for (size_t j = 0; j < var_edges[v].size(); ++j) jidx[var_edges[v][j]] = static_cast<int>(j);
-
   L.slot_of_var.resize(n_vars);
   L.var_of_slot.resize(n_vars);
   for (int v = 0; v < n_vars; ++v) L.var_of_slot[v] = v;
   std::shuffle(L.var_of_slot.begin(), L.var_of_slot.end(), rng);
   for (int i = 0; i < n_vars; ++i) L.slot_of_var[L.var_of_slot[i]] = i;
-  L.edge_slot.resize(static_cast<size_t>(M) * D);
-  std::vector<int> slot_edge(static_cast<size_t>(M) * D);  // (c, k) -> edge
-  for (int e = 0; e < M * D; ++e) {
+  L.edge_slot.resize(E);
+  std::vector<int> slot_edge(E);
+  for (int e = 0; e < E; ++e) {
     L.edge_slot[e] = e % D;
     slot_edge[e] = e;
   }
-
-  // Histograms: group A (check-warp, slot) over banks of pi(v);
-  //             group B (var-warp, j)     over banks of (ds*c + k).
-  const int nA = (M + 31) / 32 * D, nB = (n_vars + 31) / 32 * DV;
-  std::vector<int> hA(static_cast<size_t>(nA) * 32, 0), hB(static_cast<size_t>(nB) * 32, 0);
-  auto keyA = [&](int c, int k) { return ((c >> 5) * D + k) * 32; };
-  auto keyB = [&](int slot, int j) { return ((slot >> 5) * DV + j) * 32; };
-  auto bankB = [&](int c, int k) { return (ds * c + k) & 31; };
-  for (int e = 0; e < M * D; ++e) {
-    const int c = ec[e], v = ev[e], k = L.edge_slot[e];
-    hA[keyA(c, k) + (L.slot_of_var[v] & 31)]++;
-    hB[keyB(L.slot_of_var[v], jidx[e]) + bankB(c, k)]++;
+  // Column histograms (check-warp, k) over banks, and per-variable slot use.
+  const int ncol = (M + 31) / 32 * D;
+  std::vector<int> h(static_cast<size_t>(ncol) * 32, 0), vs(static_cast<size_t>(n_vars) * D, 0);
+  auto col = [&](int c, int k) { return ((c >> 5) * D + k) * 32; };
+  for (int e = 0; e < E; ++e) {
+    h[col(ec[e], L.edge_slot[e]) + (L.slot_of_var[ev[e]] & 31)]++;
+    vs[static_cast<size_t>(ev[e]) * D + L.edge_slot[e]]++;
   }
+  const double W = 4.0;
   auto total = [&]() {
     double s = 0;
-    for (int x : hA) s += double(x) * x;
-    for (int x : hB) s += double(x) * x;
+    for (int x : h) s += 0.5 * x * (x - 1);
+    for (int x : vs) s += W * 0.5 * x * (x - 1);
     return s;
   };
-  L.cost_before = total();
-  // Changing one histogram entry by +-1 changes sum(count^2) by 2*count+1 / -2*count+1.
-  auto add = [](std::vector<int>& h, int idx, int d, double& delta) {
-    delta += d > 0 ? 2.0 * h[idx] + 1 : -2.0 * h[idx] + 1;
+  // +-1 on a count x changes C(x,2) by +x / -(x-1).
+  auto addh = [&](int idx, int d, double& delta) {
+    delta += d > 0 ? h[idx] : -(h[idx] - 1);
     h[idx] += d;
   };
+  auto addv = [&](size_t idx, int d, double& delta) {
+    delta += W * (d > 0 ? vs[idx] : -(vs[idx] - 1));
+    vs[idx] += d;
+  };
+  L.cost_before = total();
   std::uniform_real_distribution<double> U(0.0, 1.0);
-  double T = 2.0;
-  const double T_end = 0.02;
-  const double decay = std::pow(T_end / T, 1.0 / std::max<long long>(1, moves));
+  double T = 1.0;
+  const double decay = std::pow(0.02 / T, 1.0 / static_cast<double>(std::max<long long>(1, moves)));
   for (long long it = 0; it < moves; ++it, T *= decay) {
     double delta = 0;
-    if (U(rng) < 0.5) {
-      // swap internal slots of two variables
+    if (rng() & 1) {
+      // swap the internal indices of two variables (moves their banks)
       const int v1 = static_cast<int>(rng() % n_vars), v2 = static_cast<int>(rng() % n_vars);
       if (v1 == v2) continue;
       const int s1 = L.slot_of_var[v1], s2 = L.slot_of_var[v2];
+      if ((s1 & 31) == (s2 & 31)) continue;
       auto relocate = [&](int v, int from, int to, double& d) {
         for (int e : var_edges[v]) {
-          const int c = ec[e], k = L.edge_slot[e];
-          add(hA, keyA(c, k) + (from & 31), -1, d);
-          add(hA, keyA(c, k) + (to & 31), +1, d);
-          add(hB, keyB(from, jidx[e]) + bankB(c, k), -1, d);
-          add(hB, keyB(to, jidx[e]) + bankB(c, k), +1, d);
+          const int base = col(ec[e], L.edge_slot[e]);
+          addh(base + (from & 31), -1, d);
+          addh(base + (to & 31), +1, d);
         }
       };
       relocate(v1, s1, s2, delta);
@@ -122,15 +126,19 @@ inline Layout optimize_layout(const std::vector<std::vector<int>>& rows, int n_v
       const int k1 = static_cast<int>(rng() % D), k2 = static_cast<int>(rng() % D);
       if (k1 == k2) continue;
       const int e1 = slot_edge[c * D + k1], e2 = slot_edge[c * D + k2];
-      const int b1 = L.slot_of_var[ev[e1]], b2 = L.slot_of_var[ev[e2]];
-      auto place = [&](int e, int slot_v, int k, int sign) {
-        add(hA, keyA(c, k) + (slot_v & 31), sign, delta);
-        add(hB, keyB(slot_v, jidx[e]) + bankB(c, k), sign, delta);
+      const int b1 = L.slot_of_var[ev[e1]] & 31, b2 = L.slot_of_var[ev[e2]] & 31;
+      const size_t v1 = static_cast<size_t>(ev[e1]) * D, v2 = static_cast<size_t>(ev[e2]) * D;
+      auto apply = [&](int ka, int kb, double& d) {  // e1: ka -> kb, e2: kb -> ka
+        addh(col(c, ka) + b1, -1, d);
+        addh(col(c, kb) + b2, -1, d);
+        addh(col(c, kb) + b1, +1, d);
+        addh(col(c, ka) + b2, +1, d);
+        addv(v1 + ka, -1, d);
+        addv(v2 + kb, -1, d);
+        addv(v1 + kb, +1, d);
+        addv(v2 + ka, +1, d);
       };
-      place(e1, b1, k1, -1);
-      place(e2, b2, k2, -1);
-      place(e1, b1, k2, +1);
-      place(e2, b2, k1, +1);
+      apply(k1, k2, delta);
       if (delta <= 0 || U(rng) < std::exp(-delta / T)) {
         L.edge_slot[e1] = k2;
         L.edge_slot[e2] = k1;
@@ -138,18 +146,15 @@ inline Layout optimize_layout(const std::vector<std::vector<int>>& rows, int n_v
         slot_edge[c * D + k1] = e2;
       } else {
         double z = 0;
-        auto undo = [&](int e, int slot_v, int k, int sign) {
-          add(hA, keyA(c, k) + (slot_v & 31), sign, z);
-          add(hB, keyB(slot_v, jidx[e]) + bankB(c, k), sign, z);
-        };
-        undo(e1, b1, k2, -1);
-        undo(e2, b2, k1, -1);
-        undo(e1, b1, k1, +1);
-        undo(e2, b2, k2, +1);
+        apply(k2, k1, z);
       }
     }
   }
   L.cost_after = total();
+  L.clashes = 0;
+  for (int x : vs) L.clashes += x > 1;
+  L.max_wavefronts = 0;
+  for (int x : h) L.max_wavefronts = std::max(L.max_wavefronts, x);
   return L;
 }
 

@@ -128,6 +128,23 @@ __device__ __forceinline__ bool project_pp(const T (&u)[D], T (&z)[D], int d) {
   return true;
 }
 
+// Bitonic merger (ascending) for a V-shaped sequence of length D, padded
+// conceptually to the next power of two with +inf: compare-exchanges that
+// touch a padded slot are no-ops and are pruned at compile time (7 for
+// D = 6, 22 for D = 13, versus 12 / 48 for a full sorting network).
+constexpr int next_pow2(int d) { return d <= 1 ? 1 : 2 * next_pow2((d + 1) / 2); }
+
+template <typename T, int D>
+__device__ __forceinline__ void bitonic_merge_asc(T (&s)[D]) {
+  constexpr int P = next_pow2(D);
+#pragma unroll
+  for (int h = P / 2; h >= 1; h /= 2) {
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+      if ((i & h) == 0 && i + h < D) ce_asc(s[i], s[i + h]);
+  }
+}
+
 // Fixed-degree variant used by the regular-code kernels: d == D at compile
 // time, no padding, and branch-free -- a row that passes the facet test gets
 // beta = 0, and clip(u - 0 * f) is exactly the cube clip the reference
@@ -158,14 +175,17 @@ __device__ __forceinline__ void project_pp_fixed(const T (&u)[D], T (&z)[D]) {
   const T beta_max = (r <= D - 2) ? mul_rn(T(0.5), sub_rn(v_top, v_nxt)) : v_top;
   const bool inside = (r >= D) || (fz <= T(r) + Num<T>::kTol) || (beta_max <= T(0));
 
-  bool up[D];
+  // Activation shifts in SORTED order: s = v_k - 1 on the +1 block (k <= r,
+  // descending) then -v_k (ascending) -- a V-shaped sequence whatever r is,
+  // so a bitonic merger sorts it.
+  const int r2 = r >> 1;
   T s[D];
 #pragma unroll
-  for (int k = 0; k < D; ++k) {
-    up[k] = u[k] >= v_top;
-    s[k] = up[k] ? sub_rn(u[k], T(1)) : -u[k];
-  }
-  SortNet<D>::asc(s);
+  for (int k = 0; k < D; ++k) s[k] = (((k + 1) >> 1) <= r2) ? sub_rn(v[k], T(1)) : -v[k];
+  bitonic_merge_asc<T, D>(s);
+  bool up[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) up[k] = u[k] >= v_top;
   T beta = beta_max, p = T(1);
 #pragma unroll
   for (int j = 0; j < D; ++j) {

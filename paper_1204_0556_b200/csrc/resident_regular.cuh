@@ -9,9 +9,12 @@
 //     x-gather addresses of its checks, the DV message addresses of its
 //     variables, its own message row and x slots -- is computed once per CTA
 //     and kept in registers as a 32-bit shared address (bare LDS/STS);
-//   * the messages are stored check-major with an odd row stride
-//     (msg[c * DS + k], DS = D or D+1) so a warp's stores hit 32 distinct
-//     banks and the row offset is an instruction immediate;
+//   * shared memory holds x[Npad] and the messages msg[D][Npad], the message
+//     of edge (c, v) at msg[k][pi(v)] (k = the edge's slot in c, pi = the
+//     internal variable numbering).  With the layout chosen by layout.h the
+//     variable phase is bank-conflict-free by construction and the check
+//     phase's x-gather / message store (both bank pi(v) mod 32) are spread
+//     over the 32 banks (residual collisions reported by the optimiser);
 //   * each thread owns VPT variables whose LLR/mu stays in registers;
 //   * the stop rule runs as one barrier-reduction (__syncthreads_or): if any
 //     thread's own partial residual sum already reaches eps^2 * E the frame
@@ -32,22 +35,22 @@ struct MsgStride {
 template <typename T, int D, int DV, int CPT, int VPT, int MINB>
 __global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const ResidentParams<T> p,
                                                                      const int* __restrict__ var_edge) {
-  constexpr int DS = MsgStride<D>::value;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int N = p.n_vars, M = p.n_checks;
   const int tid = threadIdx.x, NT = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = NT >> 5;
-  const int MP = NT * CPT;
-  T* msg = reinterpret_cast<T*>(smem_raw);
-  T* xs = msg + MP * DS;
-  T* red = xs + ((N + 1) & ~1);
+  const int NP = (N + 31) & ~31;
+  T* xs = reinterpret_cast<T*>(smem_raw);
+  T* msg = xs + NP;
+  T* red = msg + D * NP;
   int* s_int = reinterpret_cast<int*>(red + 64);  // [0] frame, [1] weight
   const uint32_t msg_a = smem_u32(msg), xs_a = smem_u32(xs);
   constexpr uint32_t ES = sizeof(T);
+  // msg[k][pi(v)] sits at x-address of v + moff(k)
+  const uint32_t moff0 = msg_a - xs_a, mstride = ES * NP;
 
   // ---- per-thread graph registers (once per CTA) ----
   uint32_t xaddr[CPT][D];
-  uint32_t mrow[CPT];
   bool cact[CPT];
 #pragma unroll
   for (int q = 0; q < CPT; ++q) {
@@ -55,10 +58,9 @@ __global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const Resid
     cact[q] = c < M;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      const int v = cact[q] ? __ldg(p.chk_var + k * p.m_pad + c) : 0;
+      const int v = cact[q] ? __ldg(p.chk_var + k * p.m_pad + c) : 0;  // internal variable
       xaddr[q][k] = xs_a + ES * v;
     }
-    mrow[q] = msg_a + ES * (c * DS);
   }
   uint32_t vaddr[VPT][DV];
   uint32_t xst[VPT];
@@ -70,8 +72,8 @@ __global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const Resid
     vact[q] = i < N;
 #pragma unroll
     for (int j = 0; j < DV; ++j) {
-      const int e = vact[q] ? __ldg(var_edge + i * DV + j) : 0;  // reference edge id = c * D + k
-      vaddr[q][j] = msg_a + ES * ((e / D) * DS + (e % D));
+      const int e = vact[q] ? __ldg(var_edge + i * DV + j) : 0;  // internal edge c * D + k
+      vaddr[q][j] = msg_a + ES * ((e % D) * NP + i);
     }
     xst[q] = xs_a + ES * i;
     vorig[q] = (vact[q] && p.var_orig) ? __ldg(p.var_orig + i) : i;
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const Resid
         }
         z[q][k] = z0;
         lam[q][k] = l0;
-        if (cact[q]) sts(mrow[q] + ES * k, sub_rn(z0, kF64 ? div_rn(l0, p.mu) : mul_rn(l0, inv_mu)));
+        if (cact[q]) sts(xaddr[q][k] + moff0 + k * mstride, sub_rn(z0, kF64 ? div_rn(l0, p.mu) : mul_rn(l0, inv_mu)));
       }
     }
     __syncthreads();
@@ -153,7 +155,8 @@ __global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const Resid
             moved = add_rn(moved, mul_rn(r2, r2));
             lam[q][k] = add_rn(lam[q][k], mul_rn(p.mu, sub_rn(w[k], zn[k])));
             z[q][k] = zn[k];
-            sts(mrow[q] + ES * k, sub_rn(zn[k], kF64 ? div_rn(lam[q][k], p.mu) : mul_rn(lam[q][k], inv_mu)));
+            sts(xaddr[q][k] + moff0 + k * mstride,
+                sub_rn(zn[k], kF64 ? div_rn(lam[q][k], p.mu) : mul_rn(lam[q][k], inv_mu)));
           }
         }
       }
@@ -224,10 +227,11 @@ __global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const Resid
   }
 }
 
-// Shared memory of the regular kernel (bytes).
+// Shared memory of the regular kernel (bytes): x[Npad] | msg[D][Npad] | red | ints.
 inline int regular_smem_bytes(int elem, int D, int n_vars, int m_pad) {
-  const int ds = (D % 2 == 0) ? D + 1 : D;
-  return elem * (m_pad * ds + ((n_vars + 1) & ~1) + 64) + 16;
+  (void)m_pad;
+  const int np = (n_vars + 31) & ~31;
+  return elem * (np + D * np + 64) + 16;
 }
 
 }  // namespace admm
