@@ -1,35 +1,38 @@
-"""Benchmark: BASELINE config 2 sweep through the sm_100a ADMM-LP decoder.
+"""Benchmark of the sm_100a ADMM-LP decoder on the BASELINE.json workloads.
 
-One STEP = decoding the BASELINE.json config-2 workload once: the (3,6)
-n=1008 girth-6 code, all-zero codeword over BPSK/AWGN at Eb/N0 = 1.5, 1.75,
-..., 3.0 dB (7 points), 65536 frames per point, mu=5, eps=1e-5, T_max=1000,
-rho=1.9 (the reference default).  Inputs are seeded synthetic LLRs generated
-on the device before timing (1.85 GB fp32 per step -- far larger than the
-126 MB L2, so no L2 flush is needed between steps).
+Default (what the driver runs): BASELINE config 2 -- the (3,6) n=1008
+girth-6 code, all-zero codeword over BPSK/AWGN at Eb/N0 = 1.5, 1.75, ...,
+3.0 dB (7 points), 65536 frames per point, mu=5, eps=1e-5, T_max=1000,
+rho=1.9 (the reference default), fp32.  One STEP = decoding the whole
+workload once (458,752 frames per GPU).  Inputs are seeded synthetic LLRs
+generated on the device before timing (1.85 GB fp32 per step, far larger
+than the 126 MB L2, so no L2 flush is needed between steps).
+``--workload cfg1|cfg3|cfg4|cfg5`` selects the other BASELINE configs (cfg5,
+n=16384, uses LLRs synthesised inside the decode kernel: 1M frames/point).
 
 ``value`` = decoded frames/s of the whole job (all ranks), device-timed with
 CUDA events, inputs resident in HBM.  ``e2e`` = the same metric through the
 public pipelined host API (paper_1204_0556_b200.pipeline): pinned host LLRs
 in, host hard decisions / iterations / flags out, copies inside the timed
-region.  ``--impl reference`` times the CPU oracle (numpy restatement of the
-reference, oracle/admm_oracle.py) on the box's host cores on a bounded sample
-of the same workload.
+region.  ``cpu_baseline`` and ``--impl reference`` time the CPU oracle
+(numpy restatement of the reference, oracle/admm_oracle.py) on the box's
+host cores on a bounded, SNR-stratified sample of the same workload.
 
-Multi-GPU (torchrun): every rank decodes its own frames (weak scaling; trial
-indices are sharded by rank), and one NCCL all-reduce of int64 counters
-merges the statistics.
+Multi-GPU (torchrun): weak scaling for cfg1-4 (every rank decodes its own
+frames), strong scaling for cfg5 (1M frames/point sharded over the ranks);
+one NCCL all-reduce of int64 counters merges the statistics.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
 import sys
 import time
+from dataclasses import dataclass
 from pathlib import Path
 
 import numpy as np
@@ -37,11 +40,33 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-POINTS_DB = [1.5, 1.75, 2.0, 2.25, 2.5, 2.75, 3.0]
-FRAMES_PER_POINT = 65536
 MU, EPS, TMAX, RHO = 5.0, 1e-5, 1000, 1.9
-METRIC = "decoded frames/s (ADMM-LP, config 2 sweep)"
 BYTES_PER_EDGE_UPDATE = {"f32": 28, "f64": 56}  # 6s + 3s/d_v, d_v = 3
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    code: str          # paper_1204_0556_b200.codes.BASELINE_CODES key
+    points: tuple      # ("awgn", snr_db) or ("bsc", p)
+    frames: int        # frames per point (per GPU for weak scaling, total for strong)
+    scaling: str
+    source: str        # "memory" (device LLR arrays) or "synth" (in-kernel Philox)
+    text: str
+
+
+WORKLOADS = {
+    "cfg1": Workload("cfg1", "cfg1_n96", (("awgn", 3.0),), 1000, "weak", "memory",
+                     "cfg1: (3,6) n=96, AWGN 3.0 dB, 1000 frames"),
+    "cfg2": Workload("cfg2", "cfg2_n1008", tuple(("awgn", 1.5 + 0.25 * k) for k in range(7)), 65536, "weak",
+                     "memory", "cfg2 sweep: (3,6) n=1008 girth-6, AWGN 1.5-3.0 dB step 0.25, 65536 frames/point"),
+    "cfg3": Workload("cfg3", "cfg3_n2640", (("awgn", 2.0), ("awgn", 2.5), ("awgn", 3.0)), 262144, "weak", "memory",
+                     "cfg3: (3,6) n=2640 girth-6, AWGN 2.0/2.5/3.0 dB, 262144 frames/point"),
+    "cfg4": Workload("cfg4", "cfg4_n1040", tuple(("awgn", 3.5 + 0.5 * k) for k in range(4)), 262144, "weak",
+                     "memory", "cfg4: (3,13) n=1040 girth-6, AWGN 3.5-5.0 dB step 0.5, 262144 frames/point"),
+    "cfg5": Workload("cfg5", "cfg5_n16384", (("bsc", 0.04), ("awgn", 2.5)), 1048576, "strong", "synth",
+                     "cfg5: (3,6) n=16384 girth-6, BSC 0.04 + AWGN 2.5 dB, 1048576 frames/point total"),
+}
 
 
 def parse():
@@ -50,23 +75,26 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
     ap.add_argument("--dtype", choices=["f32", "f64"], default="f32")
-    ap.add_argument("--frames", type=int, default=FRAMES_PER_POINT, help="frames per SNR point per GPU")
+    ap.add_argument("--frames", type=int, default=0, help="frames per point (0 = the workload's)")
+    ap.add_argument("--chunk", type=int, default=65536, help="frames per decode call (synth workloads)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--cpu-frames", type=int, default=0, help="oracle frames per point (0 = auto)")
-    ap.add_argument("--workload", choices=["cfg2", "cfg5"], default="cfg2",
-                    help="cfg2: headline sweep (default); cfg5: n=16384 large-block case, 1M frames/point "
-                         "sharded over the ranks (strong scaling), fused on-GPU frame synthesis")
-    ap.add_argument("--chunk", type=int, default=65536, help="cfg5: frames per decode call")
     return ap.parse_args()
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def channel_of(pt, code):
+    from paper_1204_0556_b200 import Awgn, Bsc
+
+    kind, val = pt
+    return Bsc(val) if kind == "bsc" else Awgn(val, code.design_rate)
 
 
 # ---------------------------------------------------------------------------
@@ -98,11 +126,8 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        rows = []
-        for line in self.path.read_text().splitlines():
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 9:
-                rows.append(parts)
+        rows = [[p.strip() for p in line.split(",")] for line in self.path.read_text().splitlines()]
+        rows = [r for r in rows if len(r) >= 9]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
@@ -115,20 +140,25 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU leg (oracle) -- used for cpu_baseline and --impl reference
+# CPU leg (oracle) -- cpu_baseline and --impl reference
 # ---------------------------------------------------------------------------
-def cpu_sample(code, frames_per_point: int, workers: int, seed_base: int = 0):
+def cpu_sample(wl: Workload, code, frames_per_point: int, workers: int, seed_base: int = 0):
     """Decode a bounded, SNR-stratified sample of the workload with the CPU
     oracle over `workers` processes.  Returns (seconds, frames, edge_updates)."""
     from oracle import admm_oracle as O
 
     g = O.Graph.of(code)
     rate = 1.0 - code.n_checks / code.n_vars
-    gam = np.concatenate([
-        np.array([O.trial_gamma_awgn(code.n_vars, db, rate, 1, k, seed_base + t) for t in range(frames_per_point)])
-        for k, db in enumerate(POINTS_DB)])
+    gam = []
+    for k, (kind, val) in enumerate(wl.points):
+        for t in range(frames_per_point):
+            if kind == "bsc":
+                gam.append(O.trial_gamma_bsc(code.n_vars, val, 1, k, seed_base + t))
+            else:
+                gam.append(O.trial_gamma_awgn(code.n_vars, val, rate, 1, k, seed_base + t))
+    gam = np.array(gam)
     t0 = time.perf_counter()
-    iters, conv, hard = O.decode_parallel(gam, g, O.Params(mu=MU, epsilon=EPS, t_max=TMAX, rho=RHO), workers)
+    iters, _conv, _hard = O.decode_parallel(gam, g, O.Params(mu=MU, epsilon=EPS, t_max=TMAX, rho=RHO), workers)
     dt = time.perf_counter() - t0
     return dt, len(gam), int(iters.sum()) * code.n_edges
 
@@ -143,19 +173,24 @@ def cpu_model():
     return "unknown"
 
 
-def run_reference(args):
+def auto_cpu_frames(wl: Workload, code, workers: int) -> int:
+    """About 10-20 s of oracle work: scales with cores, inversely with block length."""
+    return max(4, int(16 * workers * 1008 / code.n_vars * 7 / len(wl.points)))
+
+
+def run_reference(args, wl: Workload):
     """--impl reference: the CPU oracle on the host cores, same metric."""
-    rank, world, _ = dist_env()
+    rank, _world, _ = dist_env()
     if rank != 0:
         return
     from paper_1204_0556_b200.codes import baseline_code
 
-    code = baseline_code("cfg2_n1008")
+    code = baseline_code(wl.code)
     workers = os.cpu_count() or 1
-    fpp = args.cpu_frames or 16 * workers
+    fpp = args.cpu_frames or auto_cpu_frames(wl, code, workers)
     times, frames, eus = [], 0, 0
     for s in range(args.warmup + args.steps):
-        dt, nf, eu = cpu_sample(code, fpp, workers, seed_base=s * fpp)
+        dt, nf, eu = cpu_sample(wl, code, fpp, workers, seed_base=s * fpp)
         if s >= args.warmup:
             times.append(dt)
             frames += nf
@@ -163,30 +198,36 @@ def run_reference(args):
     total = sum(times)
     val = frames / total
     line = {
-        "impl": "reference", "metric": METRIC, "value": val, "unit": "frames/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded AWGN LLRs, all-zero codeword)",
-        "config": {"workload": "cfg2 sweep (n=1008 (3,6) girth-6, 1.5-3.0 dB step 0.25, mu=5, eps=1e-5, "
-                               "T_max=1000, rho=1.9)", "sample_frames_per_point": fpp},
+        "impl": "reference", "metric": metric_name(wl), "value": val, "unit": "frames/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded AWGN/BSC LLRs, all-zero codeword)",
+        "config": {"workload": wl.text + " (mu=5, eps=1e-5, T_max=1000, rho=1.9)", "sample_frames_per_point": fpp},
         "edge_updates_per_s": eus / total,
         "cpu_baseline": {"value": val, "unit": "frames/s", "cores": workers, "kind": "port",
-                         "sample": f"{fpp} frames per SNR point x 7 points per step, oracle/admm_oracle.py "
-                                   f"(numpy restatement of polylp.decode), {workers} processes, {cpu_model()}"},
+                         "sample": f"{fpp} frames per channel point x {len(wl.points)} points per step, "
+                                   f"oracle/admm_oracle.py (numpy restatement of polylp.decode), {workers} processes, "
+                                   f"{cpu_model()}"},
         "e2e": {"value": val, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def metric_name(wl: Workload) -> str:
+    return "decoded frames/s (ADMM-LP, config 2 sweep)" if wl.name == "cfg2" else f"decoded frames/s (ADMM-LP, {wl.name})"
+
+
 # ---------------------------------------------------------------------------
 # GPU leg
 # ---------------------------------------------------------------------------
-def run_ours(args):
+def run_ours(args, wl: Workload):
     import torch
     import torch.distributed as dist
 
-    from paper_1204_0556_b200 import AdmmConfig, baseline_code, decode_batch
-    from paper_1204_0556_b200.channels import Awgn, awgn_gammas_device
+    from paper_1204_0556_b200 import AdmmConfig, baseline_code, decode_batch, decode_synth
+    from paper_1204_0556_b200.channels import awgn_gammas_device, bsc_gammas_device
+    from paper_1204_0556_b200.distributed import (allreduce_counters, counters_as_dict, counters_from_results,
+                                                  max_over_ranks, shard)
     from paper_1204_0556_b200.pipeline import HostPipeline
 
     rank, world, local = dist_env()
@@ -194,206 +235,62 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    code = baseline_code("cfg2_n1008")
+    code = baseline_code(wl.code)
     cfg = AdmmConfig(mu=MU, epsilon=EPS, t_max=TMAX, rho=RHO)
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
-    F = args.frames
-    # Seeded device-side LLRs; rank r owns trial block r (weak scaling).
-    gam = [awgn_gammas_device(F, code.n_vars, db, code.design_rate, seed=1000003 * (k + 1) + 7919 * rank,
-                              device=dev, dtype=tdt) for k, db in enumerate(POINTS_DB)]
+    F = args.frames or wl.frames
     stream = torch.cuda.current_stream(dev)
+    chans = [channel_of(pt, code) for pt in wl.points]
+    gam = None
 
-    def step(collect=False):
-        outs = []
-        for k in range(len(POINTS_DB)):
-            r = decode_batch(gam[k], code, cfg, dtype=tdt, want_x=True, validate=False, stream=stream)
-            outs.append(r)
-        return outs
+    if wl.source == "memory":
+        # Seeded device-side LLRs; rank r owns its own trial block (weak scaling).
+        gam = []
+        for k, pt in enumerate(wl.points):
+            seed = 1000003 * (k + 1) + 7919 * rank
+            if pt[0] == "bsc":
+                gam.append(bsc_gammas_device(F, code.n_vars, pt[1], seed=seed, device=dev, dtype=tdt))
+            else:
+                gam.append(awgn_gammas_device(F, code.n_vars, pt[1], code.design_rate, seed=seed, device=dev,
+                                              dtype=tdt))
+        frames_local = F * len(wl.points)
 
-    # warm-up (also builds the device graph) and the deterministic work count
-    outs = None
-    for _ in range(max(args.warmup, 1)):
-        outs = step()
-    torch.cuda.synchronize(dev)
-    iters_sum = sum(int(o.iterations.sum()) for o in outs)
-    edge_updates = iters_sum * code.n_edges
-    info = outs[0].info
+        def step(collect=False):
+            return [decode_batch(g, code, cfg, dtype=tdt, want_x=True, want_hard=collect, validate=False,
+                                 stream=stream) for g in gam]
+    else:
+        mine = shard(F, rank, world) if wl.scaling == "strong" else range(rank * F, (rank + 1) * F)
+        frames_local = len(mine) * len(wl.points)
 
-    # timed region: K steps, per-launch events for the roofline
-    clocks = ClockSampler(local)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    clocks.start()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps * len(POINTS_DB))]
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    n = 0
-    for s in range(args.steps):
-        for k in range(len(POINTS_DB)):
-            ev[n][0].record(stream)
-            decode_batch(gam[k], code, cfg, dtype=tdt, want_x=True, validate=False, stream=stream)
-            ev[n][1].record(stream)
-            n += 1
-    t1.record(stream)
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    clk = clocks.stop()
-    elapsed = t0.elapsed_time(t1) / 1e3
-    launch_s = sum(a.elapsed_time(b) for a, b in ev) / 1e3 / n
-    if world > 1:
-        t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
+        def step(collect=False):
+            outs = []
+            for k, ch in enumerate(chans):
+                for lo in range(mine.start, mine.stop, args.chunk):
+                    n = min(args.chunk, mine.stop - lo)
+                    outs.append(decode_synth(code, ch, cfg, seed=1, point=k, trial0=lo, batch=n, dtype=tdt,
+                                             want_hard=collect, stream=stream))
+            return outs
 
-    # statistics of one step, merged with ONE all-reduce of int64 counters
-    from paper_1204_0556_b200.distributed import allreduce_counters, counters_as_dict, counters_from_results
-
-    cnt = torch.zeros(8, dtype=torch.int64, device=dev)
-    for k in range(len(POINTS_DB)):
-        o = decode_batch(gam[k], code, cfg, dtype=tdt, want_x=False, want_hard=True, validate=False)
-        cost = (gam[k].to(torch.float64) * o.hard.to(torch.float64)).sum(dim=1)
-        cnt += counters_from_results(o.iterations, o.weight, o.converged, o.codeword, cost, code.n_edges)
-    cnt = counters_as_dict(allreduce_counters(cnt))
-
-    frames_per_step = F * len(POINTS_DB)
-    value = world * frames_per_step * args.steps / elapsed
-    eu_total = world * edge_updates * args.steps / elapsed
-
-    # roofline of the dominant kernel (the resident decode kernel is the only one)
-    peak_path = ROOT / "MEASURED_PEAKS.json"
-    peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
-    if peak_path.exists():
-        peak, peak_src = float(json.loads(peak_path.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-    bpe = BYTES_PER_EDGE_UPDATE[args.dtype]
-    per_launch_bytes = bpe * edge_updates / len(POINTS_DB)
-    achieved = per_launch_bytes / launch_s / 1e9
-    traffic = None
-    tpath = ROOT / "profiles" / "traffic.json"
-    if tpath.exists():
-        try:
-            bpf = json.loads(tpath.read_text()).get(f"bytes_per_frame_{args.dtype}")
-            traffic = None if bpf is None else bpf * F  # ncu DRAM bytes per frame x frames per launch
-        except Exception:
-            traffic = None
-
-    # e2e through the pipelined host API
-    e2e = None
-    if not args.no_e2e:
-        pipe = HostPipeline(code, cfg, dtype=tdt, device=dev, max_batch=F)
-        host = [g.cpu().pin_memory() for g in gam]
-        pipe.run(host[:2])  # warm
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for s in range(args.steps):
-            res = pipe.run(host)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        e_el = e0.elapsed_time(e1) / 1e3
-        if world > 1:
-            t = torch.tensor([e_el], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_el = float(t.item())
-        e2e = {"value": world * frames_per_step * args.steps / e_el, "unit": "frames/s",
-               "h2d_bytes_per_step": pipe.h2d_bytes_per_run(host),
-               "d2h_bytes_per_step": pipe.d2h_bytes_per_run(host)}
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        workers = os.cpu_count() or 1
-        fpp = args.cpu_frames or 16 * workers
-        dt, nf, eu = cpu_sample(code, fpp, workers)
-        cpu = {"value": nf / dt, "unit": "frames/s", "cores": workers, "kind": "port",
-               "edge_updates_per_s": eu / dt,
-               "sample": f"{fpp} frames per SNR point x 7 points (SNR-stratified sample of the same workload), "
-                         f"oracle/admm_oracle.py over {workers} processes, {cpu_model()}"}
-
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
-            "data": "synthetic (seeded device AWGN LLRs, all-zero codeword)",
-            "config": {"workload": "cfg2 sweep: (3,6) n=1008 girth-6 code, AWGN 1.5-3.0 dB step 0.25, "
-                                   f"{F} frames/point/GPU, mu=5, eps=1e-5, T_max=1000, rho=1.9",
-                       "frames_per_step_per_gpu": frames_per_step, "parallelism": f"frame-shard x{world}",
-                       "l2": "inputs 1.85 GB/step >> 126 MB L2 (no flush needed)",
-                       "engine": info},
-            "edge_updates_per_s": eu_total,
-            "mean_iterations": iters_sum / frames_per_step,
-            "stats_one_step_all_ranks": cnt,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "bytes_model": f"{bpe} B per edge-update (two-kernel HBM schedule, SURVEY 8d) x "
-                                        f"{edge_updates // len(POINTS_DB)} edge-updates per launch",
-                         "kernel": f"resident engine {info.get('engine')} (1 generic, 2 regular)",
-                         "avg_launch_ms": launch_s * 1e3,
-                         "note": "fused on-chip design: the HBM-model bytes are never moved (edge state stays in "
-                                 "registers/SMEM); `traffic` is the ncu DRAM bytes per launch; the real bound is SM "
-                                 "instruction issue (DESIGN.md 3.4)"},
-            "gpu_launches": args.steps * len(POINTS_DB),
-            "clocks": clk,
-            "e2e": e2e,
-            "cpu_baseline": cpu,
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
-
-
-def run_cfg5(args):
-    """BASELINE config 5: (3,6) n=16384 girth-6 code, BSC p=0.04 and AWGN 2.5 dB,
-    1,048,576 frames per point sharded over the ranks (strong scaling).  LLRs
-    are synthesised inside the decode kernel from (seed, point, trial), so
-    the statistics are identical for every GPU count."""
-    import torch
-    import torch.distributed as dist
-
-    from paper_1204_0556_b200 import AdmmConfig, Awgn, Bsc, baseline_code, decode_synth
-    from paper_1204_0556_b200.distributed import allreduce_counters, counters_as_dict, counters_from_results, shard
-
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    code = baseline_code("cfg5_n16384")
-    cfg = AdmmConfig(mu=MU, epsilon=EPS, t_max=TMAX, rho=RHO)
-    tdt = torch.float32 if args.dtype == "f32" else torch.float64
-    total = args.frames if args.frames != FRAMES_PER_POINT else 1048576
-    points = [Bsc(0.04), Awgn(2.5, code.design_rate)]
-    mine = shard(total, rank, world)
-    stream = torch.cuda.current_stream(dev)
-
-    def step(collect=False):
-        outs = []
-        for k, ch in enumerate(points):
-            for lo in range(mine.start, mine.stop, args.chunk):
-                n = min(args.chunk, mine.stop - lo)
-                r = decode_synth(code, ch, cfg, seed=1, point=k, trial0=lo, batch=n, dtype=tdt, stream=stream)
-                if collect:
-                    outs.append(r)
-        return outs
-
+    # warm-up (also builds the device graph), the deterministic work count and statistics
     outs = step(collect=True)
     for _ in range(max(args.warmup - 1, 0)):
         step()
     torch.cuda.synchronize(dev)
     iters_sum = sum(int(o.iterations.to(torch.int64).sum()) for o in outs)
     edge_updates = iters_sum * code.n_edges
+    n_launch = len(outs)
     cnt = torch.zeros(8, dtype=torch.int64, device=dev)
-    for o in outs:
-        cnt += counters_from_results(o.iterations, o.weight, o.converged, o.codeword,
-                                     torch.zeros(o.iterations.numel(), device=dev), code.n_edges)
+    for k, o in enumerate(outs):
+        if gam is not None:
+            cost = (gam[k].to(torch.float64) * o.hard.to(torch.float64)).sum(dim=1)
+        else:  # synthesised frames: ML accounting would need the LLRs back; not part of the timed path
+            cost = torch.zeros(o.iterations.numel(), dtype=torch.float64, device=dev)
+        cnt += counters_from_results(o.iterations, o.weight, o.converged, o.codeword, cost, code.n_edges)
     cnt = counters_as_dict(allreduce_counters(cnt))
     info = outs[0].info
+    del outs
+
+    # timed region: K steps
     clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
@@ -409,38 +306,90 @@ def run_cfg5(args):
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    elapsed = t0.elapsed_time(t1) / 1e3
-    n_launch = len(outs)
-    launch_s = elapsed / args.steps / n_launch
+    elapsed_local = t0.elapsed_time(t1) / 1e3
+    launch_s = elapsed_local / args.steps / n_launch
+    elapsed = max_over_ranks(elapsed_local, device=dev)
+    totals = torch.tensor([frames_local, edge_updates], dtype=torch.int64, device=dev)
     if world > 1:
-        t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
-        e = torch.tensor([edge_updates], dtype=torch.int64, device=dev)
-        dist.all_reduce(e)
-        edge_updates_all = int(e.item())
-    else:
-        edge_updates_all = edge_updates
-    peak = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]) \
-        if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
+        dist.all_reduce(totals)
+    frames_all, eu_all = int(totals[0]), int(totals[1])
+    value = frames_all * args.steps / elapsed
+
+    # roofline of the dominant kernel (one decode kernel per launch)
+    peak_path = ROOT / "MEASURED_PEAKS.json"
+    peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    if peak_path.exists():
+        peak, peak_src = float(json.loads(peak_path.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     bpe = BYTES_PER_EDGE_UPDATE[args.dtype]
     achieved = bpe * edge_updates / n_launch / launch_s / 1e9
+    traffic = None
+    tpath = ROOT / "profiles" / "traffic.json"
+    if tpath.exists() and wl.name == "cfg2":
+        try:
+            bpf = json.loads(tpath.read_text()).get(f"bytes_per_frame_{args.dtype}")
+            traffic = None if bpf is None else bpf * F  # ncu DRAM bytes per frame x frames per launch
+        except Exception:
+            traffic = None
+    kernel = {1: "resident_decode_kernel", 2: "resident_regular_kernel", 3: "sharded_decode_kernel",
+              4: "cluster_decode_kernel"}.get(info.get("engine"), "?")
+
+    # e2e through the pipelined host API (memory workloads)
+    e2e = None
+    if not args.no_e2e and gam is not None:
+        pipe = HostPipeline(code, cfg, dtype=tdt, device=dev, max_batch=F)
+        host = [g.cpu().pin_memory() for g in gam]
+        pipe.run(host[:1])
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            pipe.run(host)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e_el = max_over_ranks(e0.elapsed_time(e1) / 1e3, device=dev)
+        e2e = {"value": frames_all * args.steps / e_el, "unit": "frames/s",
+               "h2d_bytes_per_step": pipe.h2d_bytes_per_run(host), "d2h_bytes_per_step": pipe.d2h_bytes_per_run(host)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        workers = os.cpu_count() or 1
+        fpp = args.cpu_frames or auto_cpu_frames(wl, code, workers)
+        dt, nf, eu = cpu_sample(wl, code, fpp, workers)
+        cpu = {"value": nf / dt, "unit": "frames/s", "cores": workers, "kind": "port", "edge_updates_per_s": eu / dt,
+               "sample": f"{fpp} frames per channel point x {len(wl.points)} points (SNR-stratified sample of the "
+                         f"same workload), oracle/admm_oracle.py over {workers} processes, {cpu_model()}"}
+
     if rank == 0:
         line = {
-            "metric": "decoded frames/s (ADMM-LP, config 5 large block)", "value": len(points) * total * args.steps / elapsed,
-            "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (in-kernel Philox LLRs keyed by seed/point/trial)",
-            "config": {"workload": f"cfg5: (3,6) n=16384 girth-6, BSC 0.04 + AWGN 2.5 dB, {total} frames/point total",
-                       "parallelism": f"frame-shard x{world}", "chunk": args.chunk, "engine": info},
-            "edge_updates_per_s": edge_updates_all * args.steps / elapsed,
-            "mean_iterations": iters_sum / (len(points) * len(mine)),
+            "metric": metric_name(wl), "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+            "scaling": wl.scaling, "vs_baseline": None, "dtype": args.dtype,
+            "data": "synthetic (seeded device LLRs, all-zero codeword)" if gam is not None
+            else "synthetic (in-kernel Philox LLRs keyed by seed/point/trial, all-zero codeword)",
+            "config": {"workload": wl.text + f" ({F} frames/point{'/GPU' if wl.scaling == 'weak' else ''}; "
+                                             "mu=5, eps=1e-5, T_max=1000, rho=1.9)",
+                       "frames_per_step_per_gpu": frames_local, "parallelism": f"frame-shard x{world}",
+                       "l2": "inputs >> 126 MB L2 per step (no flush needed)" if gam is not None
+                       else "no LLR input (synthesised in the decode kernel)",
+                       "engine": info},
+            "edge_updates_per_s": eu_all * args.steps / elapsed,
+            "mean_iterations": iters_sum / frames_local,
             "stats_one_step_all_ranks": cnt,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "bytes_model": f"{bpe} B per edge-update (SURVEY 8d)",
-                         "kernel": "streaming_decode_kernel", "avg_launch_ms": launch_s * 1e3},
+                         "traffic": traffic, "peak_source": peak_src,
+                         "bytes_model": f"{bpe} B per edge-update (two-kernel HBM schedule, SURVEY 8d) x "
+                                        f"{edge_updates // n_launch} edge-updates per launch",
+                         "kernel": kernel, "avg_launch_ms": launch_s * 1e3,
+                         "note": "resident engines keep the edge state on chip, so the HBM-model bytes are never "
+                                 "moved and frac > 1 is expected; `traffic` is ncu DRAM bytes per launch; the real "
+                                 "bound is SM instruction issue / latency (DESIGN.md 3.4)"},
             "gpu_launches": args.steps * n_launch,
-            "clocks": clk, "e2e": None, "cpu_baseline": None,
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -449,13 +398,11 @@ def run_cfg5(args):
 
 def main():
     args = parse()
-    if args.workload == "cfg5" and args.impl == "ours":
-        run_cfg5(args)
-        return
+    wl = WORKLOADS[args.workload]
     if args.impl == "reference":
-        run_reference(args)
+        run_reference(args, wl)
     else:
-        run_ours(args)
+        run_ours(args, wl)
 
 
 if __name__ == "__main__":
