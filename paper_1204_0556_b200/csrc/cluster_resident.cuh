@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(512, 1) cluster_decode_kernel(const ResidentPa
 #pragma unroll
           for (int k = 0; k < D; ++k) {
             w[k] = add_rn(mul_rn(p.rho, gx[k]), mul_rn(p.one_minus_rho, z[q][k]));
-            u[k] = add_rn(w[k], kF64 ? div_rn(lam[q][k], p.mu) : mul_rn(lam[q][k], inv_mu));
+            u[k] = add_rn(w[k], lam[q][k]);  // scaled dual lambda/mu
           }
           project_pp_fixed<T, D>(u, zn);
 #pragma unroll
@@ -204,9 +204,9 @@ __global__ void __launch_bounds__(512, 1) cluster_decode_kernel(const ResidentPa
             const T r2 = sub_rn(zn[k], z[q][k]);
             primal = add_rn(primal, mul_rn(r1, r1));
             moved = add_rn(moved, mul_rn(r2, r2));
-            lam[q][k] = add_rn(lam[q][k], mul_rn(p.mu, sub_rn(w[k], zn[k])));
+            lam[q][k] = add_rn(lam[q][k], sub_rn(w[k], zn[k]));
             z[q][k] = zn[k];
-            sts(mrow[q] + ES * k, sub_rn(zn[k], kF64 ? div_rn(lam[q][k], p.mu) : mul_rn(lam[q][k], inv_mu)));
+            sts(mrow[q] + ES * k, sub_rn(zn[k], lam[q][k]));
           }
         }
       }

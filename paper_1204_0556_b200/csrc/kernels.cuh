@@ -100,10 +100,10 @@ void launch_resident(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int
   resident_decode_kernel<T, D, CPT, DVMAX><<<grid, nt, smem, st>>>(make_params<T>(g, a));
 }
 
-template <typename T, int D, int DV, int CPT, int VPT, int MINB>
+template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT>
 void launch_regular(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int grid, int nt, int smem,
                     cudaStream_t st) {
-  resident_regular_kernel<T, D, DV, CPT, VPT, MINB><<<grid, nt, smem, st>>>(
+  resident_regular_kernel<T, D, DV, CPT, VPT, MINB, MAXT><<<grid, nt, smem, st>>>(
       make_params<T>(g, a), g.var_edge_int ? g.var_edge_int : g.var_edge);
 }
 

@@ -168,11 +168,11 @@ __global__ void __launch_bounds__(512) resident_decode_kernel(const ResidentPara
         if (p.z_in != nullptr && vidx[q][k] >= 0) {
           const long long e = f * p.ld_edge + p.edge_base[c] + k;
           z0 = p.z_in[e];
-          l0 = p.lam_in[e];
+          l0 = div_rn(p.lam_in[e], p.mu);  // duals kept scaled: lambda / mu
         }
         z[q][k] = z0;
         lam[q][k] = l0;
-        if (vidx[q][k] >= 0) msg[k * MP + c] = sub_rn(z0, div_rn(l0, p.mu));
+        if (vidx[q][k] >= 0) msg[k * MP + c] = sub_rn(z0, l0);
       }
     }
     __syncthreads();
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(512) resident_decode_kernel(const ResidentPara
             const bool on = vidx[q][k] >= 0;
             gx[k] = on ? xs[vidx[q][k]] : T(0);
             w[k] = add_rn(mul_rn(p.rho, gx[k]), mul_rn(p.one_minus_rho, z[q][k]));
-            u[k] = on ? add_rn(w[k], div_rn(lam[q][k], p.mu)) : -Num<T>::inf();
+            u[k] = on ? add_rn(w[k], lam[q][k]) : -Num<T>::inf();
           }
           project_pp<T, D>(u, zn, cdeg[q]);
 #pragma unroll
@@ -221,9 +221,9 @@ __global__ void __launch_bounds__(512) resident_decode_kernel(const ResidentPara
               const T r2 = sub_rn(zn[k], z[q][k]);
               primal = add_rn(primal, mul_rn(r1, r1));
               moved = add_rn(moved, mul_rn(r2, r2));
-              lam[q][k] = add_rn(lam[q][k], mul_rn(p.mu, sub_rn(w[k], zn[k])));
+              lam[q][k] = add_rn(lam[q][k], sub_rn(w[k], zn[k]));
               z[q][k] = zn[k];
-              msg[k * MP + c] = sub_rn(zn[k], div_rn(lam[q][k], p.mu));
+              msg[k * MP + c] = sub_rn(zn[k], lam[q][k]);
             }
           }
         }
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(512) resident_decode_kernel(const ResidentPara
           if (vidx[q][k] >= 0) {
             const long long e = f * p.ld_edge + p.edge_base[c] + k;
             p.z_out[e] = z[q][k];
-            p.lam_out[e] = lam[q][k];
+            p.lam_out[e] = mul_rn(p.mu, lam[q][k]);
           }
         }
       }

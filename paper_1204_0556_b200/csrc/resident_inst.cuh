@@ -42,9 +42,13 @@ bool resident_lookup_t(int D, int CPT, int DVMAX, ResidentLaunch* out) {
 
 template <typename T, int D, int DV, int CPT, int VPT>
 ResidentLaunch make_regular() {
-  constexpr int MINB = (sizeof(T) == 4 && CPT == 1 && D <= 8) ? 2 : 1;
-  return ResidentLaunch{reinterpret_cast<const void*>(&resident_regular_kernel<T, D, DV, CPT, VPT, MINB>),
-                        &launch_regular<T, D, DV, CPT, VPT, MINB>, 0, 0, 0};
+  // CPT = 2, d <= 8, fp32: a 256-thread CTA bounded to 85 registers so three
+  // CTAs fit an SM (ADMM_B200_MINB3 selects it for A/B measurements).
+  constexpr bool k3 = sizeof(T) == 4 && CPT == 2 && D <= 8;
+  constexpr int MINB = (sizeof(T) == 4 && CPT == 1 && D <= 8) ? 2 : k3 ? 3 : 1;
+  constexpr int MAXT = k3 ? 256 : 512;
+  return ResidentLaunch{reinterpret_cast<const void*>(&resident_regular_kernel<T, D, DV, CPT, VPT, MINB, MAXT>),
+                        &launch_regular<T, D, DV, CPT, VPT, MINB, MAXT>, 0, 0, 0};
 }
 
 // The compiled regular shapes.  VPT is the smallest compiled value >= the

@@ -32,8 +32,8 @@ struct MsgStride {
   static constexpr int value = (D % 2 == 0) ? D + 1 : D;
 };
 
-template <typename T, int D, int DV, int CPT, int VPT, int MINB>
-__global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const ResidentParams<T> p,
+template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT = 512>
+__global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const ResidentParams<T> p,
                                                                      const int* __restrict__ var_edge) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int N = p.n_vars, M = p.n_checks;
@@ -79,8 +79,11 @@ __global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const Resid
     vorig[q] = (vact[q] && p.var_orig) ? __ldg(p.var_orig + i) : i;
   }
 
-  const T inv_mu = p.inv_mu;
   constexpr bool kF64 = sizeof(T) == 8;
+  // Duals are kept SCALED, l = lambda / mu (the reference's message-passing
+  // form, tests/test_admm.py:208-240): v = w + l, l' = l + (w - z'),
+  // message = z' - l'.  No division or multiply by mu in the loop; lambda
+  // is converted only at the state I/O boundary.
   T z[CPT][D], lam[CPT][D];
   T gm[VPT];
 
@@ -108,9 +111,10 @@ __global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const Resid
           z0 = p.z_in[e];
           l0 = p.lam_in[e];
         }
+        const T s0 = div_rn(l0, p.mu);
         z[q][k] = z0;
-        lam[q][k] = l0;
-        if (cact[q]) sts(xaddr[q][k] + moff0 + k * mstride, sub_rn(z0, kF64 ? div_rn(l0, p.mu) : mul_rn(l0, inv_mu)));
+        lam[q][k] = s0;
+        if (cact[q]) sts(xaddr[q][k] + moff0 + k * mstride, sub_rn(z0, s0));
       }
     }
     __syncthreads();
@@ -144,7 +148,7 @@ __global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const Resid
 #pragma unroll
           for (int k = 0; k < D; ++k) {
             w[k] = add_rn(mul_rn(p.rho, gx[k]), mul_rn(p.one_minus_rho, z[q][k]));
-            u[k] = add_rn(w[k], kF64 ? div_rn(lam[q][k], p.mu) : mul_rn(lam[q][k], inv_mu));
+            u[k] = add_rn(w[k], lam[q][k]);
           }
           project_pp_fixed<T, D>(u, zn);
 #pragma unroll
@@ -153,10 +157,9 @@ __global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const Resid
             const T r2 = sub_rn(zn[k], z[q][k]);
             primal = add_rn(primal, mul_rn(r1, r1));
             moved = add_rn(moved, mul_rn(r2, r2));
-            lam[q][k] = add_rn(lam[q][k], mul_rn(p.mu, sub_rn(w[k], zn[k])));
+            lam[q][k] = add_rn(lam[q][k], sub_rn(w[k], zn[k]));
             z[q][k] = zn[k];
-            sts(xaddr[q][k] + moff0 + k * mstride,
-                sub_rn(zn[k], kF64 ? div_rn(lam[q][k], p.mu) : mul_rn(lam[q][k], inv_mu)));
+            sts(xaddr[q][k] + moff0 + k * mstride, sub_rn(zn[k], lam[q][k]));
           }
         }
       }
@@ -208,7 +211,7 @@ __global__ void __launch_bounds__(512, MINB) resident_regular_kernel(const Resid
           for (int k = 0; k < D; ++k) {
             const long long e = f * p.ld_edge + (p.edge_ref ? __ldg(p.edge_ref + c * D + k) : c * D + k);
             p.z_out[e] = z[q][k];
-            p.lam_out[e] = lam[q][k];
+            p.lam_out[e] = mul_rn(p.mu, lam[q][k]);
           }
         }
       }

@@ -11,6 +11,7 @@
 //     phase V  reads 3 messages, writes x          (~5.3 B per edge-update)
 //     phase C  gathers x, writes the message       (~8 B per edge-update)
 // versus ~31 B per edge-update when z and lambda also stream through memory.
+// Duals are kept scaled (lambda / mu, the reference's message-passing form).
 // Partial residual sums are accumulated per lane (one slot) over the warp's
 // checks in a fixed order and combined per slot across warps and CTAs in a
 // fixed order, so the stop decision is deterministic.
@@ -224,9 +225,7 @@ __global__ void __launch_bounds__(512, 1) sharded_decode_kernel(const StreamPara
               lam[k] = zp[1];
             }
             w_[k] = add_rn(mul_rn(p.rho, gx[k]), mul_rn(p.one_minus_rho, z[k]));
-            u[k] = (REG || k < d)
-                       ? add_rn(w_[k], sizeof(T) == 8 ? div_rn(lam[k], p.mu) : mul_rn(lam[k], p.inv_mu))
-                       : -Num<T>::inf();
+            u[k] = (REG || k < d) ? add_rn(w_[k], lam[k]) : -Num<T>::inf();  // lam holds lambda/mu
           }
           if constexpr (REG) {
             project_pp_fixed<T, D>(u, zn);
@@ -240,11 +239,11 @@ __global__ void __launch_bounds__(512, 1) sharded_decode_kernel(const StreamPara
               const T r2 = sub_rn(zn[k], z[k]);
               primal = add_rn(primal, mul_rn(r1, r1));
               moved = add_rn(moved, mul_rn(r2, r2));
-              const T lnew = add_rn(lam[k], mul_rn(p.mu, sub_rn(w_[k], zn[k])));
+              const T lnew = add_rn(lam[k], sub_rn(w_[k], zn[k]));  // scaled dual lambda/mu
               T* zp = zcol + 2 * (le + k * S);
               zp[0] = zn[k];
               zp[1] = lnew;
-              mcol[geS + le + k * S] = sub_rn(zn[k], sizeof(T) == 8 ? div_rn(lnew, p.mu) : mul_rn(lnew, p.inv_mu));
+              mcol[geS + le + k * S] = sub_rn(zn[k], lnew);
             }
           }
         }

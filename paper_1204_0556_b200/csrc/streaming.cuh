@@ -197,8 +197,7 @@ __device__ __forceinline__ void stream_phase_c(const StreamParams<T>& p, int til
         }
       }
       w_[k] = add_rn(mul_rn(p.rho, gx[k]), mul_rn(p.one_minus_rho, z[k]));
-      u[k] = on ? add_rn(w_[k], sizeof(T) == 8 ? div_rn(lam[k], p.mu) : mul_rn(lam[k], p.inv_mu))
-                : -Num<T>::inf();
+      u[k] = on ? add_rn(w_[k], lam[k]) : -Num<T>::inf();  // lam holds the scaled dual lambda/mu
     }
     if constexpr (REG) {
       project_pp_fixed<T, D>(u, zn);
@@ -212,14 +211,14 @@ __device__ __forceinline__ void stream_phase_c(const StreamParams<T>& p, int til
         const T r2 = sub_rn(zn[k], z[k]);
         primal = add_rn(primal, mul_rn(r1, r1));
         moved = add_rn(moved, mul_rn(r2, r2));
-        const T lnew = add_rn(lam[k], mul_rn(p.mu, sub_rn(w_[k], zn[k])));
+        const T lnew = add_rn(lam[k], sub_rn(w_[k], zn[k]));
         const long long e = e0 + k;
         if constexpr (sizeof(T) == 4) {
           reinterpret_cast<float2*>(p.zl)[e * S + s] = make_float2(zn[k], lnew);
         } else {
           reinterpret_cast<double2*>(p.zl)[e * S + s] = make_double2(zn[k], lnew);
         }
-        p.msg[e * S + s] = sub_rn(zn[k], sizeof(T) == 8 ? div_rn(lnew, p.mu) : mul_rn(lnew, p.inv_mu));
+        p.msg[e * S + s] = sub_rn(zn[k], lnew);
       }
     }
   } else if (c < p.n_checks && state == kSlotRetiring) {
