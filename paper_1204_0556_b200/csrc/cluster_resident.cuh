@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(512, 1) cluster_decode_kernel(const ResidentPa
 #pragma unroll
           for (int j = 1; j < DV; ++j) acc = add_rn(acc, mv[j]);
           const T num = sub_rn(acc, gm[q]);
-          sts(xst[q], clip01(kF64 ? div_rn(num, T(DV)) : mul_rn(num, T(1) / T(DV))));
+          sts(xst[q], clip01(mul_rn(num, T(1) / T(DV))));
         }
       }
       cluster_barrier();

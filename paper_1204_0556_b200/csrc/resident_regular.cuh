@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
 #pragma unroll
           for (int j = 1; j < DV; ++j) acc = add_rn(acc, lds(vaddr[q][j], T()));
           const T num = sub_rn(acc, gm[q]);
-          const T xv = clip01(kF64 ? div_rn(num, T(DV)) : mul_rn(num, T(1) / T(DV)));
+          const T xv = clip01(mul_rn(num, T(1) / T(DV)));  // reciprocal of the degree (compile time)
           sts(xst[q], xv);
         }
       }

@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(512, 1) sharded_decode_kernel(const StreamPara
             if (REG || deg > 0) {
               const T num = sub_rn(acc, g);
               const T inv = REG ? T(1) / T(DVMAX) : T(1) / T(deg);
-              xv = clip01(sizeof(T) == 8 ? div_rn(num, T(deg)) : mul_rn(num, inv));
+              xv = clip01(mul_rn(num, inv));
             } else {
               xv = g < T(0) ? T(1) : T(0);
             }
