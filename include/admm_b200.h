@@ -138,6 +138,12 @@ int admm_synth_llr(int dtype, int64_t batch, int32_t n_vars, const admm_channel*
 int admm_project_batch(int dtype, int64_t m, int32_t d, const void* values, void* out,
                        void* stream);
 
+/* Phase profiler of the sharded engine (tracing aid): enable = 1 resets and
+ * turns on clock64() accumulation in CTA 0, 0 turns it off, -1 leaves it;
+ * cycles8 (host, may be NULL) receives {variable phase, grid sync, check
+ * phase, grid sync, slot phase, passes, 0, 0} accumulated so far. */
+int admm_phase_profile(int enable, uint64_t* cycles8);
+
 const char* admm_last_error(void);
 int admm_version(void);
 

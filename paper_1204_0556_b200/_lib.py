@@ -34,6 +34,7 @@ EXPORTED = (
     "admm_decode_synth",
     "admm_synth_llr",
     "admm_project_batch",
+    "admm_phase_profile",
 )
 
 
@@ -102,6 +103,8 @@ def load() -> ctypes.CDLL:
     lib.admm_synth_llr.argtypes = [ctypes.c_int, I64, I32, ctypes.POINTER(Channel), ctypes.c_uint64,
                                    ctypes.c_uint32, I64, P, I64, P]
     lib.admm_synth_llr.restype = ctypes.c_int
+    lib.admm_phase_profile.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]
+    lib.admm_phase_profile.restype = ctypes.c_int
     lib.admm_project_batch.argtypes = [ctypes.c_int, I64, I32, P, P, P]
     lib.admm_project_batch.restype = ctypes.c_int
     _lib = lib

@@ -310,9 +310,9 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
         if (geo.total > smem_optin) continue;
         if (cudaFuncSetAttribute(SL.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin) != cudaSuccess) continue;
         cudaFuncAttributes fa{};
-        if (cudaFuncGetAttributes(&fa, SL.fn) != cudaSuccess || fa.numRegs * 512 > 65536) continue;
+        if (cudaFuncGetAttributes(&fa, SL.fn) != cudaSuccess || fa.numRegs * (dt ? 512 : 1024) > 65536) continue;
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, SL.fn, 512, geo.total);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, SL.fn, dt ? 512 : 1024, geo.total);
         if (occ < 1) continue;
         g->shlaunch[dt] = SL;
         g->shard_ok[dt] = std::getenv("ADMM_B200_NO_SHARD") == nullptr;
@@ -656,6 +656,12 @@ int admm_synth_llr(int dtype, int64_t batch, int32_t n_vars, const admm_channel*
   if (!out) return fail(ADMM_E_ARG, "null output");
   admm::launch_synth(dtype, batch, n_vars, sp, out, ld, reinterpret_cast<cudaStream_t>(stream));
   ADMM_CUDA(cudaGetLastError());
+  return ADMM_OK;
+}
+
+int admm_phase_profile(int enable, uint64_t* cycles8) {
+  if (!admm::phase_profile(enable, reinterpret_cast<unsigned long long*>(cycles8)))
+    return fail(ADMM_E_CUDA, "phase profile: CUDA error");
   return ADMM_OK;
 }
 

@@ -182,6 +182,7 @@ StreamParams<T> make_stream_params(const StreamGraphArgs& g, const ResidentFrame
   p.nonint = ib + 5 * S;
   p.odd = ib + 6 * S;
   p.ctr = ib + 7 * S;
+  p.flagpad = reinterpret_cast<int*>(base + L.flags);
   return p;
 }
 
@@ -207,10 +208,11 @@ int launch_sharded(const StreamGraphArgs& g, const ResidentFrameArgs& a, int S, 
   ShardGeom gg = geo;
   void* args[] = {&p, &gg};
   return (int)cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&sharded_decode_kernel<T, D, DVMAX, REG>),
-                                          grid, 512, args, geo.total, st);
+                                          grid, ShardThreads<T>::value, args, geo.total, st);
 }
 
 bool shard_lookup(int dtype, int D, int DVMAX, bool regular, ShardLaunch* out);
+bool phase_profile(int enable, unsigned long long* out8);
 
 bool stream_lookup(int dtype, int D, int DVMAX, bool regular, StreamLaunch* out);
 

@@ -12,6 +12,13 @@
 //     phase C  gathers x, writes the message       (~8 B per edge-update)
 // versus ~31 B per edge-update when z and lambda also stream through memory.
 // Duals are kept scaled (lambda / mu, the reference's message-passing form).
+//
+// Slot management is REPLICATED: every CTA keeps the slot states, iteration
+// counters and frame indices in its own shared memory and takes the same
+// decisions from the same global inputs (the per-slot not-converged flags and
+// the fixed-order partial sums), refilling retired slots in slot order from a
+// replicated frame counter.  An iteration therefore needs two grid syncs
+// (after the variable phase and after the check phase), not three.
 // Partial residual sums are accumulated per lane (one slot) over the warp's
 // checks in a fixed order and combined per slot across warps and CTAs in a
 // fixed order, so the stop decision is deterministic.
@@ -21,9 +28,20 @@
 
 namespace admm {
 
+// One CTA per SM: 32 warps in fp32 (64 registers fit), 16 in fp64 (the
+// double-precision check update needs ~110 registers; at 64 it spills).
+template <typename T> struct ShardThreads { static constexpr int value = sizeof(T) == 4 ? 1024 : 512; };
+constexpr int kShardThreadsMax = 1024;
+
+// Phase profiler (admm_phase_profile): CTA 0, thread 0 accumulates clock64()
+// cycles per phase when enabled.  Slots: 0 variable phase, 1 grid sync after
+// it, 2 check phase, 3 grid sync after it, 4 slot phase, 5 passes.
+__device__ unsigned long long g_phase_cycles[8];
+__device__ int g_phase_on;
+
 struct ShardGeom {
   int MB, NB, EB;  // checks, variables, edges (max) per CTA
-  int zl, gm, cv, ce, ve, red, sint, total;  // shared-memory offsets (bytes)
+  int zl, gm, cv, ce, ve, red, sint, slot, total;  // shared-memory offsets (bytes)
 };
 
 inline ShardGeom shard_geom(int elem, int D, int dvmax, int M, int N, long long max_edges_per_cta, int G, int S) {
@@ -38,14 +56,15 @@ inline ShardGeom shard_geom(int elem, int D, int dvmax, int M, int N, long long 
   g.cv = o; o = al(o + 4ll * g.MB * D);
   g.ce = o; o = al(o + 4ll * g.MB);
   g.ve = o; o = al(o + 4ll * g.NB * dvmax);
-  g.red = o; o = al(o + 2ll * elem * 16 * 32);
+  g.red = o; o = al(o + 2ll * elem * (kShardThreadsMax / 32) * 32);
   g.sint = o; o = al(o + 4ll * 2 * S);
+  g.slot = o; o = al(o + 8ll * S + 4ll * 4 * S + 4 * (4 + 32) + 16);  // replicated slot machine
   g.total = o;
   return g;
 }
 
 template <typename T, int D, int DVMAX, bool REG>
-__global__ void __launch_bounds__(512, 1) sharded_decode_kernel(const StreamParams<T> p, const ShardGeom geo) {
+__global__ void __launch_bounds__(ShardThreads<T>::value, 1) sharded_decode_kernel(const StreamParams<T> p, const ShardGeom geo) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -77,56 +96,108 @@ __global__ void __launch_bounds__(512, 1) sharded_decode_kernel(const StreamPara
     const int e = j < p.dvmax ? __ldg(p.var_edge + (vb0 + lv) * p.dvmax + j) : -1;
     ve_s[q] = e >= 0 ? e * S : -1;
   }
-  if (b == 0 && tid == 0) {
-    p.ctr[0] = 0;
-    p.ctr[1] = p.S;
-    p.ctr[2] = 0;
+  // ---- replicated slot machine (shared memory, identical in every CTA) ----
+  long long* fr_s = reinterpret_cast<long long*>(smem_raw + geo.slot);  // [S] frame
+  int* st_s = reinterpret_cast<int*>(fr_s + S);                         // [S] state
+  int* t_s = st_s + S;                                                  // [S] iterations
+  int* cv_f = t_s + S;                                                  // [S] converged (retiring)
+  int* dec_s = cv_f + S;                                                // [S] decision scratch
+  int* misc = dec_s + S;  // [0] active slots, [2..3] next frame (int64), [4..35] warp scan
+  // not-converged flags, double-buffered by pass parity; slot s at [32 s] so
+  // the ~G atomics per slot and pass land on distinct L2 lines
+  int* ncb[2] = {p.flagpad, p.flagpad + 32 * S};
+  for (int s = tid; s < S; s += blockDim.x) {
+    const long long f = s;
+    fr_s[s] = f < p.batch ? f : -1;
+    st_s[s] = f < p.batch ? kSlotFresh : kSlotEmpty;
+    t_s[s] = 0;
+    cv_f[s] = 0;
+    if (b == 0) {
+      ncb[0][32 * s] = 0;
+      ncb[1][32 * s] = 0;
+      p.weight[s] = 0;
+      p.nonint[s] = 0;
+      p.odd[s] = 0;
+    }
+  }
+  if (tid == 0) {
+    const long long first = p.batch < S ? p.batch : S;
+    misc[0] = static_cast<int>(first);
+    *reinterpret_cast<long long*>(misc + 2) = first;
   }
   grid.sync();
-  for (int s = b * blockDim.x + tid; s < S; s += G * blockDim.x) stream_refill(p, s);
-  grid.sync();
 
-  const long long SS = S;
   const long long max_passes = ((long long)(p.batch + S - 1) / S + 1) * ((long long)p.t_max + 2) + 4;
   for (long long pass = 0; pass < max_passes; ++pass) {
-    if (*(volatile int*)(p.ctr + 1) == 0) break;
+    __syncthreads();
+    if (misc[0] == 0) break;
+    int* nc_now = ncb[pass & 1];
 
+    const bool prof = g_phase_on && b == 0 && tid == 0;
+    long long tp0 = prof ? clock64() : 0;
+    const long long SS = S;
     // ---------------- phase V: this CTA's variables, all slots ----------------
     for (int q = tid; q < 2 * S; q += blockDim.x) sint[q] = 0;
     __syncthreads();
+    long long tpa = prof ? clock64() : 0;
     {
       const int sg = w & (SG - 1), wi = w / SG;  // SG is a power of two
       const int s = sg * 32 + lane;
-      const int state = p.st[s];
-      const long long f = p.frame[s];
+      const int state = st_s[s];
+      const long long f = fr_s[s];
       T* xcol = p.x + s;
       const T* mcol = p.msg + s;
+      // Batches of VB variables: every global load of a batch (messages of
+      // RUNNING slots, gamma or synthesis of FRESH slots, the final x of
+      // RETIRING slots) is issued before any is consumed.
+      constexpr int VB = 4;
       if (state == kSlotRetiring) {
-        for (int lv = wi; lv < nb; lv += NWG) {
-          const int i = vb0 + lv;
-          const T xv = xcol[i * S];
-          const bool h = xv > T(0.5);
-          if (p.x_out) p.x_out[f * p.ld_x + i] = xv;
-          if (p.hard_out) p.hard_out[f * p.ld_hard + i] = h;
-          if (h) atomicAdd_block(sint + s, 1);
-          if (!(vmin(fabs(xv), fabs(T(1) - xv)) <= T(1e-5))) atomicOr_block(sint + S + s, 1);
+        for (int lv0 = wi; lv0 < nb; lv0 += VB * NWG) {
+          T xq[VB];
+#pragma unroll
+          for (int q = 0; q < VB; ++q) {
+            const int lv = lv0 + q * NWG;
+            xq[q] = lv < nb ? xcol[(vb0 + lv) * S] : T(0);
+          }
+#pragma unroll
+          for (int q = 0; q < VB; ++q) {
+            const int lv = lv0 + q * NWG;
+            if (lv >= nb) break;
+            const int i = vb0 + lv;
+            const T xv = xq[q];
+            const bool h = xv > T(0.5);
+            if (p.x_out) p.x_out[f * p.ld_x + i] = xv;
+            if (p.hard_out) p.hard_out[f * p.ld_hard + i] = h;
+            if (h) atomicAdd_block(sint + s, 1);
+            if (!(vmin(fabs(xv), fabs(T(1) - xv)) <= T(1e-5))) atomicOr_block(sint + S + s, 1);
+          }
         }
       } else if (state != kSlotEmpty) {
-        // Batches of VB variables: all their message loads are issued before
-        // any is consumed, so VB x DVMAX L2 round trips overlap.
-        constexpr int VB = 4;
+        const bool fresh = state == kSlotFresh;
+        long long tq0 = prof ? clock64() : 0;
         for (int lv0 = wi; lv0 < nb; lv0 += VB * NWG) {
           T mv[VB][DVMAX];
+          T gq[VB];
           int degs[VB];
 #pragma unroll
           for (int q = 0; q < VB; ++q) {
             const int lv = lv0 + q * NWG;
+            const bool inb = lv < nb;
             degs[q] = 0;
 #pragma unroll
             for (int j = 0; j < DVMAX; ++j) {
-              const int ev = lv < nb ? ve_s[lv * DVMAX + j] : -1;
+              const int ev = inb ? ve_s[lv * DVMAX + j] : -1;
               degs[q] += ev >= 0;
-              mv[q][j] = (ev >= 0 && state == kSlotRunning) ? mcol[ev] : T(0);
+              mv[q][j] = (ev >= 0 && !fresh) ? mcol[ev] : T(0);
+            }
+            if (!inb) {
+              gq[q] = T(0);
+            } else if (!fresh) {
+              gq[q] = gm_s[lv * S + s];
+            } else {
+              const int i = vb0 + lv;
+              gq[q] = p.synth.kind != 0 ? static_cast<T>(synth_llr(p.synth, p.synth.trial0 + f, i))
+                                        : p.gamma[f * p.ld_gamma + i];
             }
           }
 #pragma unroll
@@ -134,14 +205,10 @@ __global__ void __launch_bounds__(512, 1) sharded_decode_kernel(const StreamPara
             const int lv = lv0 + q * NWG;
             if (lv >= nb) break;
             const int i = vb0 + lv;
-            T g;
-            if (state == kSlotFresh) {
-              const T gi = p.synth.kind != 0 ? static_cast<T>(synth_llr(p.synth, p.synth.trial0 + f, i))
-                                              : p.gamma[f * p.ld_gamma + i];
-              g = div_rn(gi, p.mu);
+            T g = gq[q];
+            if (fresh) {
+              g = div_rn(g, p.mu);
               gm_s[lv * S + s] = g;
-            } else {
-              g = gm_s[lv * S + s];
             }
             const int deg = REG ? DVMAX : degs[q];
             T acc = T(0);
@@ -158,21 +225,32 @@ __global__ void __launch_bounds__(512, 1) sharded_decode_kernel(const StreamPara
             }
             xcol[i * S] = xv;
           }
+          if (prof && lv0 == wi) {
+            g_phase_cycles[6] += clock64() - tq0;  // first batch: loads issued and consumed
+            g_phase_cycles[7] += 1;
+          }
         }
       }
     }
+    long long tpb = prof ? clock64() : 0;
+    (void)tpa;
+    (void)tpb;
     __syncthreads();
     for (int s = tid; s < S; s += blockDim.x) {
       if (sint[s]) atomicAdd(p.weight + s, sint[s]);
       if (sint[S + s]) atomicOr(p.nonint + s, 1);
     }
+    long long tp1 = prof ? clock64() : 0;
     grid.sync();
+    long long tp2 = prof ? clock64() : 0;
 
     // ---------------- phase C: this CTA's checks, all slots ----------------
+    if (b == 0)  // the other flag buffer was last read in the previous pass's slot phase
+      for (int q = tid; q < S; q += blockDim.x) ncb[(pass + 1) & 1][32 * q] = 0;
     {
       const int sg = w % SG, wi = w / SG;
       const int s = sg * 32 + lane;
-      const int state = p.st[s];
+      const int state = st_s[s];
       const bool live = state == kSlotFresh || state == kSlotRunning;
       T primal = T(0), moved = T(0);
       int odd = 0;
@@ -263,17 +341,100 @@ __global__ void __launch_bounds__(512, 1) sharded_decode_kernel(const StreamPara
         if (live) {
           p.part[((long long)b * S + s) * 2] = a;
           p.part[((long long)b * S + s) * 2 + 1] = bb;
-          if (a >= p.thr || bb >= p.thr) atomicOr(p.notconv + s, 1);
+          if (a >= p.thr || bb >= p.thr) atomicOr(nc_now + 32 * s, 1);
         } else if (state == kSlotRetiring && a > T(0)) {
           atomicOr(p.odd + s, 1);
         }
       }
     }
+    long long tp3 = prof ? clock64() : 0;
     grid.sync();
+    long long tp4 = prof ? clock64() : 0;
 
-    // ---------------- phase S: one warp per slot ----------------
-    const int gwarp = (b * blockDim.x + tid) >> 5, n_gwarp = (G * blockDim.x) >> 5;
-    for (int s = gwarp; s < S; s += n_gwarp) stream_phase_s(p, s, G);
+    // ---------------- phase S: replicated in every CTA (no grid sync) ----------------
+    // (a) exact residual sums for the slots whose every partial is below the
+    //     threshold (admm_decoder.py:174-179): one warp per slot, fixed tree.
+    //     The flags are fetched for all slots at once first.
+    for (int q = tid; q < S; q += blockDim.x) dec_s[q] = nc_now[32 * q];
+    __syncthreads();
+    for (int q = w; q < S; q += nwarps) {
+      const int state = st_s[q];
+      int conv = 0;
+      if ((state == kSlotFresh || state == kSlotRunning) && dec_s[q] == 0) {
+        T a = T(0), bb = T(0);
+        for (int r = lane; r < G; r += 32) {
+          a = add_rn(a, p.part[((long long)r * S + q) * 2]);
+          bb = add_rn(bb, p.part[((long long)r * S + q) * 2 + 1]);
+        }
+        a = warp_allsum(a);
+        bb = warp_allsum(bb);
+        conv = a < p.thr && bb < p.thr;
+      }
+      __syncwarp();
+      if (lane == 0) dec_s[q] = conv;
+    }
+    __syncthreads();
+    // (b) state transitions; retired slots are refilled in slot order from the
+    //     replicated frame counter (a block-wide scan gives each its rank).
+    long long* next = reinterpret_cast<long long*>(misc + 2);
+    int* wscan = misc + 4;
+    for (int s0 = 0; s0 < S; s0 += blockDim.x) {
+      const int q = s0 + tid;
+      const int state = q < S ? st_s[q] : kSlotEmpty;
+      const bool retiring = state == kSlotRetiring;
+      if (q < S && retiring && b == 0) {
+        const long long f = fr_s[q];
+        if (p.iters_out) p.iters_out[f] = t_s[q];
+        if (p.flags_out) p.flags_out[f] = (cv_f[q] ? 1 : 0) | (p.nonint[q] ? 0 : 2) | (p.odd[q] ? 0 : 4);
+        if (p.weight_out) p.weight_out[f] = p.weight[q];
+        p.weight[q] = 0;
+        p.nonint[q] = 0;
+        p.odd[q] = 0;
+      }
+      if (q < S && (state == kSlotFresh || state == kSlotRunning)) {
+        const int t = t_s[q] + 1;
+        t_s[q] = t;
+        if (dec_s[q] || t >= p.t_max) {
+          cv_f[q] = dec_s[q];
+          st_s[q] = kSlotRetiring;
+        } else {
+          st_s[q] = kSlotRunning;
+        }
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, retiring);
+      if (lane == 0) wscan[w] = __popc(bal);
+      __syncthreads();
+      int before = 0, total = 0;
+      for (int ww = 0; ww < nwarps; ++ww) {
+        before += ww < w ? wscan[ww] : 0;
+        total += wscan[ww];
+      }
+      const long long base = *next;
+      if (retiring) {
+        const long long f = base + before + __popc(bal & ((1u << lane) - 1u));
+        t_s[q] = 0;
+        cv_f[q] = 0;
+        if (f < p.batch) {
+          fr_s[q] = f;
+          st_s[q] = kSlotFresh;
+        } else {
+          fr_s[q] = -1;
+          st_s[q] = kSlotEmpty;
+          atomicSub_block(misc, 1);
+        }
+      }
+      __syncthreads();
+      if (tid == 0) *next = base + total;
+    }
+    if (prof) {
+      const long long tp5 = clock64();
+      g_phase_cycles[0] += tp1 - tp0;
+      g_phase_cycles[1] += tp2 - tp1;
+      g_phase_cycles[2] += tp3 - tp2;
+      g_phase_cycles[3] += tp4 - tp3;
+      g_phase_cycles[4] += tp5 - tp4;
+      g_phase_cycles[5] += 1;
+    }
     grid.sync();
   }
 }

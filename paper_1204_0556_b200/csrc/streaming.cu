@@ -71,6 +71,19 @@ bool shard_lookup(int dtype, int D, int DVMAX, bool regular, ShardLaunch* out) {
   return false;
 }
 
+bool phase_profile(int enable, unsigned long long* out8) {
+  if (out8) {
+    if (cudaMemcpyFromSymbol(out8, g_phase_cycles, sizeof(unsigned long long) * 8) != cudaSuccess) return false;
+  }
+  if (enable >= 0) {
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const int on = enable > 0;
+    if (cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z)) != cudaSuccess) return false;
+    if (cudaMemcpyToSymbol(g_phase_on, &on, sizeof(int)) != cudaSuccess) return false;
+  }
+  return true;
+}
+
 bool stream_lookup(int dtype, int D, int DVMAX, bool regular, StreamLaunch* out) {
   return dtype ? stream_lookup_t<double>(D, DVMAX, regular, out) : stream_lookup_t<float>(D, DVMAX, regular, out);
 }

@@ -78,11 +78,12 @@ struct StreamParams {
   int* odd;           // [S] odd-parity flag (retiring)
   int* ctr;           // [0] queue, [1] active slots, [2] passes
   SynthParams synth;  // fused frame synthesis (kind 0 = read gamma)
+  int* flagpad;       // [4][S][32] not-converged flags, one cache line per slot (sharded engines)
 };
 
 // Bytes of streaming workspace for S slots.
 struct StreamLayout {
-  size_t zl, msg, x, gm, part, ints, total;
+  size_t zl, msg, x, gm, part, ints, flags, total;
   static size_t al(size_t b) { return (b + 255) & ~size_t(255); }
   StreamLayout(size_t elem, long long E, long long N, long long ncblk, long long S, bool sharded = false) {
     size_t o = 0;
@@ -92,6 +93,7 @@ struct StreamLayout {
     gm = o; o += sharded ? 0 : al(elem * N * S);
     part = o; o += al(elem * 2 * ncblk * S);
     ints = o; o += al(sizeof(long long) * S) + al(sizeof(int) * (7 * S + 8));
+    flags = o; o += al(sizeof(int) * 4 * 32 * S);  // per-slot flags, one 128-byte line each
     total = o;
   }
 };

@@ -141,3 +141,22 @@ def test_synth_llr_statistics(cuda_ok):
     # different points / seeds give different frames, same ones repeat exactly
     assert not torch.equal(g, synth_llr(4096, ch, seed=1, point=1, trial0=0, batch=256, dtype=torch.float64))
     assert torch.equal(g, synth_llr(4096, ch, seed=1, point=0, trial0=0, batch=256, dtype=torch.float64))
+
+
+def test_phase_profiler_counts_passes(cuda_ok):
+    """admm_phase_profile (tracing aid of the sharded engine) accumulates
+    cycles per phase and the number of passes."""
+    import ctypes
+
+    from paper_1204_0556_b200 import AdmmConfig, Bsc, _lib, baseline_code, decode_synth
+
+    lib = _lib.load()
+    code = baseline_code("cfg5_n16384")
+    _lib.check(lib.admm_phase_profile(1, None))
+    r = decode_synth(code, Bsc(0.04), AdmmConfig(mu=5.0), seed=3, batch=64, dtype=torch.float32)
+    torch.cuda.synchronize()
+    out = (ctypes.c_uint64 * 8)()
+    _lib.check(lib.admm_phase_profile(0, out))
+    assert r.info["engine"] == 3
+    assert out[5] >= int(r.iterations.max())          # at least one pass per iteration
+    assert out[0] > 0 and out[2] > 0 and out[4] > 0   # variable, check and slot phases ran
