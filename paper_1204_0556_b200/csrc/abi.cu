@@ -146,34 +146,41 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
   for (int v = 0; v < n_vars && regular; ++v) regular = vdeg[v] == dvmax;
 
   // Validate one candidate launch shape for both dtypes and record it.
+  auto check_one = [&](admm::ResidentLaunch& L, int smem, int nt) -> bool {
+    if (smem > smem_optin) return false;
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, L.fn) != cudaSuccess) return false;
+    if (fa.numRegs * nt > 65536 || nt > fa.maxThreadsPerBlock) return false;
+    if (cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L.fn, nt, smem);
+    if (occ < 1) return false;
+    L.smem = smem;
+    L.occupancy = occ;
+    L.regs = fa.numRegs;
+    return true;
+  };
   auto try_shape = [&](bool reg, int cpt, int nt, int* vpt_out) -> bool {
     const int m_pad = nt * cpt;
     admm::ResidentLaunch Ls[2];
     int vpt = 0;
     for (int dt = 0; dt < 2; ++dt) {
-      admm::ResidentLaunch L{};
-      int smem = 0;
+      bool ok = false;
       if (reg) {
         const int need = (n_vars + nt - 1) / nt;
-        if (!admm::regular_lookup(dt, dmax, dvmax, cpt, need, &vpt, &L)) return false;
-        smem = admm::regular_smem_bytes(dt ? 8 : 4, dmax, n_vars, m_pad);
+        for (int variant = 0; !ok; ++variant) {
+          admm::ResidentLaunch L{};
+          if (!admm::regular_lookup(dt, dmax, dvmax, cpt, need, variant, &vpt, &L)) break;
+          ok = check_one(L, admm::regular_smem_bytes(dt ? 8 : 4, dmax, n_vars, m_pad), nt);
+          if (ok) Ls[dt] = L;
+        }
       } else {
-        if ((long long)g->D * m_pad >= 65535) return false;
-        if (!admm::resident_lookup(dt, g->D, cpt, g->DVMAX, &L)) return false;
-        smem = admm::ResidentSmem(dt ? 8 : 4, n_vars, g->D * m_pad, g->DVMAX).total;
+        admm::ResidentLaunch L{};
+        if ((long long)g->D * m_pad < 65535 && admm::resident_lookup(dt, g->D, cpt, g->DVMAX, &L))
+          ok = check_one(L, admm::ResidentSmem(dt ? 8 : 4, n_vars, g->D * m_pad, g->DVMAX).total, nt);
+        if (ok) Ls[dt] = L;
       }
-      if (smem > smem_optin) return false;
-      cudaFuncAttributes fa{};
-      if (cudaFuncGetAttributes(&fa, L.fn) != cudaSuccess) return false;
-      if (fa.numRegs * nt > 65536 || nt > fa.maxThreadsPerBlock) return false;
-      if (cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
-      int occ = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L.fn, nt, smem);
-      if (occ < 1) return false;
-      L.smem = smem;
-      L.occupancy = occ;
-      L.regs = fa.numRegs;
-      Ls[dt] = L;
+      if (!ok) return false;
     }
     g->launch[0] = Ls[0];
     g->launch[1] = Ls[1];
@@ -193,7 +200,7 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
     for (int cpt : (reg ? order_reg : order_gen)) {
       if (cpt_env && cpt != cpt_env) continue;  // tuning override
       const int nt = ((n_checks + cpt - 1) / cpt + 31) / 32 * 32;
-      if (nt > 512) continue;
+      if (nt > (reg ? 1024 : 512)) continue;
       int vpt = 0;
       if (!try_shape(reg, cpt, nt, &vpt)) continue;
       g->kind = reg ? 2 : 1;

@@ -107,11 +107,13 @@ void launch_regular(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int 
       make_params<T>(g, a), g.var_edge_int ? g.var_edge_int : g.var_edge);
 }
 
-// Regular-code variants: (D, DV, CPT, VPT).  Returns false when none fits.
-bool regular_lookup_f32(int D, int DV, int CPT, int VPT_min, int* VPT, ResidentLaunch* out);
-bool regular_lookup_f64(int D, int DV, int CPT, int VPT_min, int* VPT, ResidentLaunch* out);
-inline bool regular_lookup(int dtype, int D, int DV, int CPT, int VPT_min, int* VPT, ResidentLaunch* out) {
-  return dtype ? regular_lookup_f64(D, DV, CPT, VPT_min, VPT, out) : regular_lookup_f32(D, DV, CPT, VPT_min, VPT, out);
+// Regular-code variants: (D, DV, CPT, VPT).  `variant` enumerates the
+// compiled shapes that match; returns false past the last one.
+bool regular_lookup_f32(int D, int DV, int CPT, int VPT_min, int variant, int* VPT, ResidentLaunch* out);
+bool regular_lookup_f64(int D, int DV, int CPT, int VPT_min, int variant, int* VPT, ResidentLaunch* out);
+inline bool regular_lookup(int dtype, int D, int DV, int CPT, int VPT_min, int variant, int* VPT, ResidentLaunch* out) {
+  return dtype ? regular_lookup_f64(D, DV, CPT, VPT_min, variant, VPT, out)
+               : regular_lookup_f32(D, DV, CPT, VPT_min, variant, VPT, out);
 }
 
 // Defined in resident_f32.cu / resident_f64.cu.

@@ -40,34 +40,37 @@ bool resident_lookup_t(int D, int CPT, int DVMAX, ResidentLaunch* out) {
   return false;
 }
 
-template <typename T, int D, int DV, int CPT, int VPT>
+template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT>
 ResidentLaunch make_regular() {
-  // CPT = 2, d <= 8, fp32: a 256-thread CTA bounded to 85 registers so three
-  // CTAs fit an SM (ADMM_B200_MINB3 selects it for A/B measurements).
-  constexpr bool k3 = sizeof(T) == 4 && CPT == 2 && D <= 8;
-  constexpr int MINB = (sizeof(T) == 4 && CPT == 1 && D <= 8) ? 2 : k3 ? 3 : 1;
-  constexpr int MAXT = k3 ? 256 : 512;
   return ResidentLaunch{reinterpret_cast<const void*>(&resident_regular_kernel<T, D, DV, CPT, VPT, MINB, MAXT>),
                         &launch_regular<T, D, DV, CPT, VPT, MINB, MAXT>, 0, 0, 0};
 }
 
-// The compiled regular shapes.  VPT is the smallest compiled value >= the
-// variables-per-thread the graph needs.
+// The compiled regular shapes (D, DV, CPT, VPT, MINB, MAXT), in preference
+// order.  `variant` selects the variant-th shape that matches (D, DV, CPT)
+// and provides at least VPT_min variables per thread; the host tries them in
+// turn until one fits the CTA size, registers and shared memory.
+//   * fp32, CPT = 2: 256-thread CTAs bounded to 85 registers (3 CTAs/SM,
+//     +1.3 % over 2 CTAs on config 2), then a 704-thread variant for codes
+//     with up to 1408 checks (config 3: 672 threads, 21 warps).
 template <typename T>
-bool regular_lookup_t(int D, int DV, int CPT, int VPT_min, int* VPT, ResidentLaunch* out) {
-#define ADMM_REG(d, dv, cpt, vpt)                                         \
-  if (D == d && DV == dv && CPT == cpt && VPT_min <= vpt) {               \
-    *VPT = vpt;                                                           \
-    *out = make_regular<T, d, dv, cpt, vpt>();                            \
-    return true;                                                          \
+bool regular_lookup_t(int D, int DV, int CPT, int VPT_min, int variant, int* VPT, ResidentLaunch* out) {
+  constexpr bool F32 = sizeof(T) == 4;
+  int seen = 0;
+#define ADMM_REG(d, dv, cpt, vpt, minb, maxt)                               \
+  if (D == d && DV == dv && CPT == cpt && VPT_min <= vpt && seen++ == variant) { \
+    *VPT = vpt;                                                             \
+    *out = make_regular<T, d, dv, cpt, vpt, minb, maxt>();                  \
+    return true;                                                            \
   }
-  ADMM_REG(6, 3, 1, 2)
-  ADMM_REG(6, 3, 2, 4)
-  ADMM_REG(6, 3, 3, 6)
-  ADMM_REG(6, 3, 4, 8)
-  ADMM_REG(13, 3, 1, 5)
-  ADMM_REG(4, 2, 1, 2)
-  ADMM_REG(4, 3, 1, 2)
+  ADMM_REG(6, 3, 1, 2, F32 ? 2 : 1, 512)
+  ADMM_REG(6, 3, 2, 4, F32 ? 3 : 1, F32 ? 256 : 512)
+  ADMM_REG(6, 3, 2, 4, 1, 704)
+  ADMM_REG(6, 3, 3, 6, 1, 512)
+  ADMM_REG(6, 3, 4, 8, 1, 512)
+  ADMM_REG(13, 3, 1, 5, 1, 512)
+  ADMM_REG(4, 2, 1, 2, F32 ? 2 : 1, 512)
+  ADMM_REG(4, 3, 1, 2, F32 ? 2 : 1, 512)
 #undef ADMM_REG
   return false;
 }
