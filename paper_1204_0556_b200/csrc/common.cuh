@@ -54,6 +54,18 @@ __device__ __forceinline__ float add_rn(float a, float b) { return a + b; }
 __device__ __forceinline__ float sub_rn(float a, float b) { return a - b; }
 __device__ __forceinline__ float div_rn(float a, float b) { return __fdividef(a, b); }
 
+// Packed fp32 pair arithmetic (sm_100 FADD2/FMUL2/FFMA2): the same IEEE
+// round-to-nearest operation in each lane, one instruction for two edges.
+__device__ __forceinline__ float2 fsub2_rn(float2 a, float2 b) {
+  unsigned long long ra, rb, rd;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(rb) : "f"(b.x), "f"(b.y));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(rd) : "l"(ra), "l"(rb));
+  float2 d;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(rd));
+  return d;
+}
+
 // Butterfly all-reduce inside a warp.  IEEE addition is commutative, so every
 // lane ends with a bitwise identical sum (lane i adds a_i + a_j, lane j adds
 // a_j + a_i at each level): the convergence decision is uniform.
