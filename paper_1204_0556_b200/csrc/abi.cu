@@ -58,6 +58,9 @@ struct admm_graph {
   int* var_orig = nullptr;      // relabeled regular layout (kind 2)
   int* edge_ref = nullptr;
   int* var_edge_int = nullptr;
+  int* cchk_var = nullptr;       // colored layout (fp32 regular kernels with DV | D)
+  int* cvar_orig = nullptr;
+  int* cedge_ref = nullptr;
   double layout_cost[2] = {0, 0};
   // per-dtype launch data
   admm::ResidentLaunch launch[2];
@@ -168,10 +171,12 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
       bool ok = false;
       if (reg) {
         const int need = (n_vars + nt - 1) / nt;
-        for (int variant = 0; !ok; ++variant) {
+        // tuning override: first fp32 variant to try
+        const char* venv = dt == 0 ? std::getenv("ADMM_B200_F32_VARIANT") : nullptr;
+        for (int variant = venv ? std::atoi(venv) : 0; !ok; ++variant) {
           admm::ResidentLaunch L{};
           if (!admm::regular_lookup(dt, dmax, dvmax, cpt, need, variant, &vpt, &L)) break;
-          ok = check_one(L, admm::regular_smem_bytes(dt ? 8 : 4, dmax, n_vars, m_pad), nt);
+          ok = check_one(L, admm::regular_smem_bytes(dt ? 8 : 4, dmax, dvmax, n_vars, L.colored, nt, vpt), nt);
           if (ok) Ls[dt] = L;
         }
       } else {
@@ -411,6 +416,32 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
     e7 = up((void**)&g->edge_ref, eref.data(), eref.size() * sizeof(int));
     e8 = up((void**)&g->var_edge_int, vint.data(), vint.size() * sizeof(int));
   }
+  if (g->kind == 2 && (g->launch[0].colored || g->launch[1].colored)) {
+    // Colored layout (layout.h): message of edge (c, v) at msgc[color][pi(v)].
+    long long moves = std::min<long long>(20000000, 4000ll * E);
+    if (const char* env = std::getenv("ADMM_B200_LAYOUT_MOVES")) moves = std::atoll(env);
+    const admm::Layout lay = admm::optimize_colored_layout(rows, n_vars, dmax, dvmax, moves, 777);
+    if (lay.clashes > 0) {
+      admm_graph_destroy(g);
+      return fail(ADMM_E_UNSUPPORTED, "no equitable edge coloring found");
+    }
+    g->layout_cost[0] = lay.cost_before;
+    g->layout_cost[1] = lay.cost_after;
+    std::vector<int> chk2((size_t)D * MP, -1), eref((size_t)MP * dmax, 0), vorig(n_vars);
+    for (int c = 0; c < n_checks; ++c)
+      for (int r = 0; r < dmax; ++r) {
+        const int k = lay.edge_slot[c * dmax + r];
+        chk2[(size_t)k * MP + c] = lay.slot_of_var[rows[c][r]];
+        eref[(size_t)c * dmax + k] = check_ptr[c] + r;
+      }
+    for (int i = 0; i < n_vars; ++i) vorig[i] = lay.var_of_slot[i];
+    cudaError_t c1 = up((void**)&g->cchk_var, chk2.data(), chk2.size() * sizeof(int));
+    cudaError_t c2 = up((void**)&g->cvar_orig, vorig.data(), vorig.size() * sizeof(int));
+    cudaError_t c3 = up((void**)&g->cedge_ref, eref.data(), eref.size() * sizeof(int));
+    if (e6 == cudaSuccess) e6 = c1;
+    if (e7 == cudaSuccess) e7 = c2;
+    if (e8 == cudaSuccess) e8 = c3;
+  }
   for (cudaError_t e : {e1, e2, e3, e4, e5, e6, e7, e8}) {
     if (e != cudaSuccess) {
       admm_graph_destroy(g);
@@ -432,6 +463,9 @@ int admm_graph_destroy(admm_graph* g) {
   cudaFree(g->var_orig);
   cudaFree(g->edge_ref);
   cudaFree(g->var_edge_int);
+  cudaFree(g->cchk_var);
+  cudaFree(g->cvar_orig);
+  cudaFree(g->cedge_ref);
   delete g;
   return ADMM_OK;
 }
@@ -615,6 +649,12 @@ int decode_impl(const admm_graph* g, int dtype, int64_t batch, const void* gamma
 
   admm::ResidentGraphArgs ga{g->n_vars, g->n_checks, g->m_pad, g->chk_var, g->var_pos, g->var_deg,
                              g->edge_base, g->var_edge, g->var_orig, g->edge_ref, g->var_edge_int};
+  if (L.colored) {
+    ga.chk_var = g->cchk_var;
+    ga.var_orig = g->cvar_orig;
+    ga.edge_ref = g->cedge_ref;
+    ga.var_edge_int = nullptr;
+  }
   admm::ResidentFrameArgs fa{batch, gamma, ld_gamma, mu, rho, thr, t_max, z_in, lam_in, ld_edge,
                              x_out, ld_x, hard_out, ld_hard, iters_out, flags_out, weight_out,
                              z_out, lam_out, reinterpret_cast<int*>(workspace), synth};

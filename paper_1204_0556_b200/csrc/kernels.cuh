@@ -54,6 +54,7 @@ struct ResidentLaunch {
   const void* fn;
   ResidentLaunchFn launch;
   int smem, occupancy, regs;
+  bool colored;  // regular kernel on the colored message layout (layout.h)
 };
 
 template <typename T>
@@ -100,10 +101,10 @@ void launch_resident(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int
   resident_decode_kernel<T, D, CPT, DVMAX><<<grid, nt, smem, st>>>(make_params<T>(g, a));
 }
 
-template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT>
+template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT, bool COL>
 void launch_regular(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int grid, int nt, int smem,
                     cudaStream_t st) {
-  resident_regular_kernel<T, D, DV, CPT, VPT, MINB, MAXT><<<grid, nt, smem, st>>>(
+  resident_regular_kernel<T, D, DV, CPT, VPT, MINB, MAXT, COL><<<grid, nt, smem, st>>>(
       make_params<T>(g, a), g.var_edge_int ? g.var_edge_int : g.var_edge);
 }
 

@@ -158,4 +158,168 @@ inline Layout optimize_layout(const std::vector<std::vector<int>>& rows, int n_v
   return L;
 }
 
+
+// Colored layout for regular codes with DV | D (the (3,6) codes): every edge
+// gets a color j in [0, DV) such that each variable has one edge of every
+// color and each check D/DV edges of every color, and the edges of color j
+// sit in the check slots k = j (mod DV).  The message of edge (c, v) of color
+// j is then stored at msgc[j][pi(v)]: a variable reads its messages at
+// compile-time offsets from its own x slot and a check writes slot k at a
+// compile-time offset from the x-gather address -- no per-edge addresses are
+// held anywhere.  Such a coloring always exists: split every check into D/DV
+// copies of degree DV; the resulting DV-regular bipartite graph is the union
+// of DV perfect matchings (Koenig), color j = the j-th matching.  The
+// annealer then moves variables (pi) and swaps same-color slots of one check
+// to spread every (check-warp, slot) column over the 32 banks.
+inline bool match_dfs(int v, const std::vector<std::vector<int>>& adj, const std::vector<char>& used_edge,
+                      const std::vector<int>& edge_copy, std::vector<int>& copy_match, std::vector<int>& seen,
+                      int stamp, std::vector<int>& var_match_edge) {
+  for (int e : adj[v]) {
+    if (used_edge[e]) continue;
+    const int cp = edge_copy[e];
+    if (seen[cp] == stamp) continue;
+    seen[cp] = stamp;
+    if (copy_match[cp] < 0 ||
+        match_dfs(copy_match[cp], adj, used_edge, edge_copy, copy_match, seen, stamp, var_match_edge)) {
+      copy_match[cp] = v;
+      var_match_edge[v] = e;
+      return true;
+    }
+  }
+  return false;
+}
+
+inline Layout optimize_colored_layout(const std::vector<std::vector<int>>& rows, int n_vars, int D, int DV,
+                                      long long moves, uint64_t seed) {
+  const int M = static_cast<int>(rows.size());
+  const int E = M * D, R = D / DV, NCOPY = M * R;
+  Layout L;
+  std::mt19937_64 rng(seed);
+  std::vector<int> ev(E), ec(E), edge_copy(E), color(E, -1);
+  std::vector<std::vector<int>> adj(n_vars);
+  for (int c = 0; c < M; ++c) {
+    std::vector<int> perm(D);
+    for (int r = 0; r < D; ++r) perm[r] = r;
+    std::shuffle(perm.begin(), perm.end(), rng);
+    for (int r = 0; r < D; ++r) {
+      const int e = c * D + r;
+      ev[e] = rows[c][r];
+      ec[e] = c;
+      edge_copy[e] = c * R + perm[r] / DV;
+      adj[ev[e]].push_back(e);
+    }
+  }
+  // DV successive perfect matchings between variables and check copies.
+  std::vector<char> used(E, 0);
+  std::vector<int> seen(NCOPY, -1);
+  int stamp = 0;
+  for (int j = 0; j < DV; ++j) {
+    std::vector<int> copy_match(NCOPY, -1), var_edge(n_vars, -1);
+    for (int v = 0; v < n_vars; ++v) {
+      if (!match_dfs(v, adj, used, edge_copy, copy_match, seen, stamp++, var_edge)) {
+        L.clashes = 1;  // cannot happen for a biregular graph with DV | D
+        return L;
+      }
+    }
+    for (int v = 0; v < n_vars; ++v) {
+      used[var_edge[v]] = 1;
+      color[var_edge[v]] = j;
+    }
+  }
+  // Slots: the color-j edges of check c take slots j, j + DV, j + 2 DV, ...
+  L.edge_slot.assign(E, -1);
+  std::vector<int> slot_edge(E);
+  for (int c = 0; c < M; ++c) {
+    int fill[32] = {0};
+    for (int r = 0; r < D; ++r) {
+      const int e = c * D + r, j = color[e];
+      const int k = j + DV * fill[j]++;
+      L.edge_slot[e] = k;
+      slot_edge[c * D + k] = e;
+    }
+  }
+  L.slot_of_var.resize(n_vars);
+  L.var_of_slot.resize(n_vars);
+  for (int v = 0; v < n_vars; ++v) L.var_of_slot[v] = v;
+  std::shuffle(L.var_of_slot.begin(), L.var_of_slot.end(), rng);
+  for (int i = 0; i < n_vars; ++i) L.slot_of_var[L.var_of_slot[i]] = i;
+  std::vector<std::vector<int>> var_edges(n_vars);
+  for (int e = 0; e < E; ++e) var_edges[ev[e]].push_back(e);
+  const int ncol = (M + 31) / 32 * D;
+  std::vector<int> h(static_cast<size_t>(ncol) * 32, 0);
+  auto col = [&](int c, int k) { return ((c >> 5) * D + k) * 32; };
+  for (int e = 0; e < E; ++e) h[col(ec[e], L.edge_slot[e]) + (L.slot_of_var[ev[e]] & 31)]++;
+  auto total = [&]() {
+    double t = 0;
+    for (int x : h) t += 0.5 * x * (x - 1);
+    return t;
+  };
+  auto addh = [&](int idx, int d, double& delta) {
+    delta += d > 0 ? h[idx] : -(h[idx] - 1);
+    h[idx] += d;
+  };
+  L.cost_before = total();
+  std::uniform_real_distribution<double> U(0.0, 1.0);
+  double T = 1.0;
+  const double decay = std::pow(0.02 / T, 1.0 / static_cast<double>(std::max<long long>(1, moves)));
+  for (long long it = 0; it < moves; ++it, T *= decay) {
+    double delta = 0;
+    if (R < 2 || (rng() & 1)) {
+      const int v1 = static_cast<int>(rng() % n_vars), v2 = static_cast<int>(rng() % n_vars);
+      if (v1 == v2) continue;
+      const int s1 = L.slot_of_var[v1], s2 = L.slot_of_var[v2];
+      if ((s1 & 31) == (s2 & 31)) continue;
+      auto relocate = [&](int v, int from, int to, double& d) {
+        for (int e : var_edges[v]) {
+          const int base = col(ec[e], L.edge_slot[e]);
+          addh(base + (from & 31), -1, d);
+          addh(base + (to & 31), +1, d);
+        }
+      };
+      relocate(v1, s1, s2, delta);
+      relocate(v2, s2, s1, delta);
+      if (delta <= 0 || U(rng) < std::exp(-delta / T)) {
+        L.slot_of_var[v1] = s2;
+        L.slot_of_var[v2] = s1;
+        L.var_of_slot[s2] = v1;
+        L.var_of_slot[s1] = v2;
+      } else {
+        double z = 0;
+        relocate(v1, s2, s1, z);
+        relocate(v2, s1, s2, z);
+      }
+    } else {
+      // swap two same-color slots of one check
+      const int c = static_cast<int>(rng() % M);
+      const int j = static_cast<int>(rng() % DV);
+      const int a = static_cast<int>(rng() % R), b = static_cast<int>(rng() % R);
+      if (a == b) continue;
+      const int k1 = j + DV * a, k2 = j + DV * b;
+      const int e1 = slot_edge[c * D + k1], e2 = slot_edge[c * D + k2];
+      const int b1 = L.slot_of_var[ev[e1]] & 31, b2 = L.slot_of_var[ev[e2]] & 31;
+      auto apply = [&](int ka, int kb, double& d) {
+        addh(col(c, ka) + b1, -1, d);
+        addh(col(c, kb) + b2, -1, d);
+        addh(col(c, kb) + b1, +1, d);
+        addh(col(c, ka) + b2, +1, d);
+      };
+      apply(k1, k2, delta);
+      if (delta <= 0 || U(rng) < std::exp(-delta / T)) {
+        L.edge_slot[e1] = k2;
+        L.edge_slot[e2] = k1;
+        slot_edge[c * D + k2] = e1;
+        slot_edge[c * D + k1] = e2;
+      } else {
+        double z = 0;
+        apply(k2, k1, z);
+      }
+    }
+  }
+  L.cost_after = total();
+  L.clashes = 0;
+  L.max_wavefronts = 0;
+  for (int x : h) L.max_wavefronts = std::max(L.max_wavefronts, x);
+  return L;
+}
+
 }  // namespace admm

@@ -40,37 +40,46 @@ bool resident_lookup_t(int D, int CPT, int DVMAX, ResidentLaunch* out) {
   return false;
 }
 
-template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT>
+template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT, bool COL>
 ResidentLaunch make_regular() {
-  return ResidentLaunch{reinterpret_cast<const void*>(&resident_regular_kernel<T, D, DV, CPT, VPT, MINB, MAXT>),
-                        &launch_regular<T, D, DV, CPT, VPT, MINB, MAXT>, 0, 0, 0};
+  return ResidentLaunch{reinterpret_cast<const void*>(&resident_regular_kernel<T, D, DV, CPT, VPT, MINB, MAXT, COL>),
+                        &launch_regular<T, D, DV, CPT, VPT, MINB, MAXT, COL>, 0, 0, 0, COL};
 }
 
-// The compiled regular shapes (D, DV, CPT, VPT, MINB, MAXT), in preference
-// order.  `variant` selects the variant-th shape that matches (D, DV, CPT)
-// and provides at least VPT_min variables per thread; the host tries them in
-// turn until one fits the CTA size, registers and shared memory.
-//   * fp32, CPT = 2: 256-thread CTAs bounded to 85 registers (3 CTAs/SM,
-//     +1.3 % over 2 CTAs on config 2), then a 704-thread variant for codes
-//     with up to 1408 checks (config 3: 672 threads, 21 warps).
+// The compiled regular shapes (D, DV, CPT, VPT, MINB, MAXT, COL), in
+// preference order.  `variant` selects the variant-th shape that matches
+// (D, DV, CPT) and provides at least VPT_min variables per thread; the host
+// tries them in turn until one fits the CTA size, registers and shared memory.
+//   * fp32 (3,6): colored message layout first (layout.h; no per-edge
+//     addresses, no activity predicates in the loop: +10 % on config 2),
+//     256-thread CTAs at 3 CTAs/SM (4 CTAs/SM = 64 registers spills: -8 %),
+//     then a 704-thread variant for codes with up to 1408
+//     checks (config 3);
+//   * the slot layout (per-edge message addresses) for everything else and
+//     for fp64, whose variable sums must follow the reference's edge order.
 template <typename T>
 bool regular_lookup_t(int D, int DV, int CPT, int VPT_min, int variant, int* VPT, ResidentLaunch* out) {
   constexpr bool F32 = sizeof(T) == 4;
   int seen = 0;
-#define ADMM_REG(d, dv, cpt, vpt, minb, maxt)                               \
+#define ADMM_REG(d, dv, cpt, vpt, minb, maxt, col)                               \
   if (D == d && DV == dv && CPT == cpt && VPT_min <= vpt && seen++ == variant) { \
-    *VPT = vpt;                                                             \
-    *out = make_regular<T, d, dv, cpt, vpt, minb, maxt>();                  \
-    return true;                                                            \
+    *VPT = vpt;                                                                  \
+    *out = make_regular<T, d, dv, cpt, vpt, minb, maxt, col>();                  \
+    return true;                                                                 \
   }
-  ADMM_REG(6, 3, 1, 2, F32 ? 2 : 1, 512)
-  ADMM_REG(6, 3, 2, 4, F32 ? 3 : 1, F32 ? 256 : 512)
-  ADMM_REG(6, 3, 2, 4, 1, 704)
-  ADMM_REG(6, 3, 3, 6, 1, 512)
-  ADMM_REG(6, 3, 4, 8, 1, 512)
-  ADMM_REG(13, 3, 1, 5, 1, 512)
-  ADMM_REG(4, 2, 1, 2, F32 ? 2 : 1, 512)
-  ADMM_REG(4, 3, 1, 2, F32 ? 2 : 1, 512)
+  if constexpr (F32) {
+    ADMM_REG(6, 3, 2, 4, 3, 256, true)
+    ADMM_REG(6, 3, 2, 4, 1, 704, true)
+    ADMM_REG(6, 3, 1, 2, 2, 512, true)
+  }
+  ADMM_REG(6, 3, 1, 2, F32 ? 2 : 1, 512, false)
+  ADMM_REG(6, 3, 2, 4, F32 ? 3 : 1, F32 ? 256 : 512, false)
+  ADMM_REG(6, 3, 2, 4, 1, 704, false)
+  ADMM_REG(6, 3, 3, 6, 1, 512, false)
+  ADMM_REG(6, 3, 4, 8, 1, 512, false)
+  ADMM_REG(13, 3, 1, 5, 1, 512, false)
+  ADMM_REG(4, 2, 1, 2, F32 ? 2 : 1, 512, false)
+  ADMM_REG(4, 3, 1, 2, F32 ? 2 : 1, 512, false)
 #undef ADMM_REG
   return false;
 }

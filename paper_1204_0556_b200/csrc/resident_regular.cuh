@@ -32,22 +32,36 @@ struct MsgStride {
   static constexpr int value = (D % 2 == 0) ? D + 1 : D;
 };
 
-template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT = 512>
+// Padded variable count of the shared-memory arrays.  COL kernels also give
+// every idle thread slot (variables i >= N, checks c >= M) real storage so the
+// hot loop carries no activity predicates: idle variables occupy slots
+// [N, VPT * NT) and idle checks gather from / write to the spare slot N.
+__host__ __device__ inline int regular_np(int n_vars, bool col, int nt, int vpt) {
+  if (!col) return (n_vars + 31) & ~31;
+  const int need = (n_vars + 1 > vpt * nt ? n_vars + 1 : vpt * nt);
+  return (need + 31) & ~31;
+}
+
+template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT = 512, bool COL = false>
 __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const ResidentParams<T> p,
                                                                      const int* __restrict__ var_edge) {
+  static_assert(!COL || (D % DV == 0 && sizeof(T) == 4), "colored layout: fp32, DV | D");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int N = p.n_vars, M = p.n_checks;
   const int tid = threadIdx.x, NT = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = NT >> 5;
-  const int NP = (N + 31) & ~31;
+  const int NP = COL ? regular_np(N, true, NT, VPT) : (N + 31) & ~31;
+  constexpr int kRows = COL ? DV : D;  // message rows: colors (COL) or check slots
   T* xs = reinterpret_cast<T*>(smem_raw);
   T* msg = xs + NP;
-  T* red = msg + D * NP;
+  T* red = msg + kRows * NP;
   int* s_int = reinterpret_cast<int*>(red + 64);  // [0] frame, [1] weight
   const uint32_t msg_a = smem_u32(msg), xs_a = smem_u32(xs);
   constexpr uint32_t ES = sizeof(T);
   // msg[k][pi(v)] sits at x-address of v + moff(k)
   const uint32_t moff0 = msg_a - xs_a, mstride = ES * NP;
+  // shared-address offset of the message of check slot k from the x slot of its variable
+  auto moff = [&](int k) -> uint32_t { return moff0 + (COL ? k % DV : k) * mstride; };
 
   // ---- per-thread graph registers (once per CTA) ----
   uint32_t xaddr[CPT][D];
@@ -58,11 +72,11 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
     cact[q] = c < M;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      const int v = cact[q] ? __ldg(p.chk_var + k * p.m_pad + c) : 0;  // internal variable
+      const int v = cact[q] ? __ldg(p.chk_var + k * p.m_pad + c) : (COL ? N : 0);  // internal variable
       xaddr[q][k] = xs_a + ES * v;
     }
   }
-  uint32_t vaddr[VPT][DV];
+  uint32_t vaddr[COL ? 1 : VPT][DV];
   uint32_t xst[VPT];
   int vorig[VPT];  // original variable of each owned internal variable (layout.h relabeling)
   bool vact[VPT];
@@ -70,10 +84,12 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
   for (int q = 0; q < VPT; ++q) {
     const int i = tid + q * NT;
     vact[q] = i < N;
+    if constexpr (!COL) {
 #pragma unroll
-    for (int j = 0; j < DV; ++j) {
-      const int e = vact[q] ? __ldg(var_edge + i * DV + j) : 0;  // internal edge c * D + k
-      vaddr[q][j] = msg_a + ES * ((e % D) * NP + i);
+      for (int j = 0; j < DV; ++j) {
+        const int e = vact[q] ? __ldg(var_edge + i * DV + j) : 0;  // internal edge c * D + k
+        vaddr[q][j] = msg_a + ES * ((e % D) * NP + i);
+      }
     }
     xst[q] = xs_a + ES * i;
     vorig[q] = (vact[q] && p.var_orig) ? __ldg(p.var_orig + i) : i;
@@ -117,7 +133,7 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
         const T s0 = div_rn(l0, p.mu);
         z[q][k] = z0;
         lam[q][k] = s0;
-        if (cact[q]) sts(xaddr[q][k] + moff0 + k * mstride, sub_rn(z0, s0));
+        if (cact[q]) sts(xaddr[q][k] + moff(k), sub_rn(z0, s0));
       }
     }
     __syncthreads();
@@ -129,10 +145,12 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
       // ---- x-update (admm_decoder.py:108-124): edges summed in edge order ----
 #pragma unroll
       for (int q = 0; q < VPT; ++q) {
-        if (vact[q]) {
-          T acc = lds(vaddr[q][0], T());
+        if (COL || vact[q]) {
+          // COL: message of color j at a fixed offset from the variable's x slot
+          auto va = [&](int j) -> uint32_t { return COL ? xst[q] + moff0 + j * mstride : vaddr[COL ? 0 : q][j]; };
+          T acc = lds(va(0), T());
 #pragma unroll
-          for (int j = 1; j < DV; ++j) acc = add_rn(acc, lds(vaddr[q][j], T()));
+          for (int j = 1; j < DV; ++j) acc = add_rn(acc, lds(va(j), T()));
           const T num = sub_rn(acc, gm[q]);
           const T xv = clip01(mul_rn(num, T(1) / T(DV)));  // reciprocal of the degree (compile time)
           sts(xst[q], xv);
@@ -150,7 +168,9 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
         float2 pr2 = make_float2(0.f, 0.f), mv2 = make_float2(0.f, 0.f);
 #pragma unroll
         for (int q = 0; q < CPT; ++q) {
-          if (cact[q]) {
+          // COL: idle checks run on the spare slot; their residuals are dropped
+          const float2 pr_in = pr2, mv_in = mv2;
+          if (COL || cact[q]) {
             float2 gx2[D / 2], w2[D / 2], z2[D / 2], l2[D / 2];
 #pragma unroll
             for (int j = 0; j < D / 2; ++j) {
@@ -180,9 +200,13 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
               lam[q][2 * j + 1] = ln.y;
               z[q][2 * j] = zn2.x;
               z[q][2 * j + 1] = zn2.y;
-              sts(xaddr[q][2 * j] + moff0 + (2 * j) * mstride, m2.x);
-              sts(xaddr[q][2 * j + 1] + moff0 + (2 * j + 1) * mstride, m2.y);
+              sts(xaddr[q][2 * j] + moff(2 * j), m2.x);
+              sts(xaddr[q][2 * j + 1] + moff(2 * j + 1), m2.y);
             }
+          }
+          if (COL && !cact[q]) {
+            pr2 = pr_in;
+            mv2 = mv_in;
           }
         }
         primal = pr2.x + pr2.y;
@@ -208,7 +232,7 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
             moved = add_rn(moved, mul_rn(r2, r2));
             lam[q][k] = add_rn(lam[q][k], sub_rn(w[k], zn[k]));
             z[q][k] = zn[k];
-            sts(xaddr[q][k] + moff0 + k * mstride, sub_rn(zn[k], lam[q][k]));
+            sts(xaddr[q][k] + moff(k), sub_rn(zn[k], lam[q][k]));
           }
         }
       }
@@ -280,11 +304,11 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
   }
 }
 
-// Shared memory of the regular kernel (bytes): x[Npad] | msg[D][Npad] | red | ints.
-inline int regular_smem_bytes(int elem, int D, int n_vars, int m_pad) {
-  (void)m_pad;
-  const int np = (n_vars + 31) & ~31;
-  return elem * (np + D * np + 64) + 16;
+// Shared memory of the regular kernel (bytes): x[Npad] | msg[rows][Npad] | red | ints,
+// rows = D (slot layout) or DV (colored layout).
+inline int regular_smem_bytes(int elem, int D, int DV, int n_vars, bool col, int nt, int vpt) {
+  const int np = regular_np(n_vars, col, nt, vpt);
+  return elem * (np + (col ? DV : D) * np + 64) + 16;
 }
 
 }  // namespace admm
