@@ -149,14 +149,21 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
   for (int v = 0; v < n_vars && regular; ++v) regular = vdeg[v] == dvmax;
 
   // Validate one candidate launch shape for both dtypes and record it.
+  const bool dbg = std::getenv("ADMM_B200_DEBUG") != nullptr;
   auto check_one = [&](admm::ResidentLaunch& L, int smem, int nt) -> bool {
     if (smem > smem_optin) return false;
     cudaFuncAttributes fa{};
-    if (cudaFuncGetAttributes(&fa, L.fn) != cudaSuccess) return false;
+    const cudaError_t ge = cudaFuncGetAttributes(&fa, L.fn);
+    if (dbg)
+      std::fprintf(stderr, "[admm] candidate fn=%p nt=%d smem=%d colored=%d np_fixed=%d: %s regs=%d maxthr=%d\n",
+                   L.fn, nt, smem, (int)L.colored, L.np_fixed, cudaGetErrorString(ge), fa.numRegs,
+                   fa.maxThreadsPerBlock);
+    if (ge != cudaSuccess) return false;
     if (fa.numRegs * nt > 65536 || nt > fa.maxThreadsPerBlock) return false;
     if (cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L.fn, nt, smem);
+    if (dbg) std::fprintf(stderr, "[admm]   occupancy %d\n", occ);
     if (occ < 1) return false;
     L.smem = smem;
     L.occupancy = occ;
@@ -175,8 +182,10 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
         const char* venv = dt == 0 ? std::getenv("ADMM_B200_F32_VARIANT") : nullptr;
         for (int variant = venv ? std::atoi(venv) : 0; !ok; ++variant) {
           admm::ResidentLaunch L{};
-          if (!admm::regular_lookup(dt, dmax, dvmax, cpt, need, variant, &vpt, &L)) break;
-          ok = check_one(L, admm::regular_smem_bytes(dt ? 8 : 4, dmax, dvmax, n_vars, L.colored, nt, vpt), nt);
+          if (!admm::regular_lookup(dt, dmax, dvmax, cpt, need, nt, n_vars, variant, &vpt, &L)) break;
+          const int smem = L.np_fixed ? 4 * (L.np_fixed * (1 + dvmax) + 64) + 16
+                                      : admm::regular_smem_bytes(dt ? 8 : 4, dmax, dvmax, n_vars, L.colored, nt, vpt);
+          ok = check_one(L, smem, nt);
           if (ok) Ls[dt] = L;
         }
       } else {

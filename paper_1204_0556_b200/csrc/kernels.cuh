@@ -55,6 +55,7 @@ struct ResidentLaunch {
   ResidentLaunchFn launch;
   int smem, occupancy, regs;
   bool colored;  // regular kernel on the colored message layout (layout.h)
+  int np_fixed;  // compile-time padded variable count (0 = computed from n_vars)
 };
 
 template <typename T>
@@ -101,20 +102,23 @@ void launch_resident(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int
   resident_decode_kernel<T, D, CPT, DVMAX><<<grid, nt, smem, st>>>(make_params<T>(g, a));
 }
 
-template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT, bool COL>
+template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT, bool COL, int NPC, int NTC>
 void launch_regular(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int grid, int nt, int smem,
                     cudaStream_t st) {
-  resident_regular_kernel<T, D, DV, CPT, VPT, MINB, MAXT, COL><<<grid, nt, smem, st>>>(
+  resident_regular_kernel<T, D, DV, CPT, VPT, MINB, MAXT, COL, NPC, NTC><<<grid, nt, smem, st>>>(
       make_params<T>(g, a), g.var_edge_int ? g.var_edge_int : g.var_edge);
 }
 
 // Regular-code variants: (D, DV, CPT, VPT).  `variant` enumerates the
 // compiled shapes that match; returns false past the last one.
-bool regular_lookup_f32(int D, int DV, int CPT, int VPT_min, int variant, int* VPT, ResidentLaunch* out);
-bool regular_lookup_f64(int D, int DV, int CPT, int VPT_min, int variant, int* VPT, ResidentLaunch* out);
-inline bool regular_lookup(int dtype, int D, int DV, int CPT, int VPT_min, int variant, int* VPT, ResidentLaunch* out) {
-  return dtype ? regular_lookup_f64(D, DV, CPT, VPT_min, variant, VPT, out)
-               : regular_lookup_f32(D, DV, CPT, VPT_min, variant, VPT, out);
+bool regular_lookup_f32(int D, int DV, int CPT, int VPT_min, int nt, int n_vars, int variant, int* VPT,
+                        ResidentLaunch* out);
+bool regular_lookup_f64(int D, int DV, int CPT, int VPT_min, int nt, int n_vars, int variant, int* VPT,
+                        ResidentLaunch* out);
+inline bool regular_lookup(int dtype, int D, int DV, int CPT, int VPT_min, int nt, int n_vars, int variant,
+                           int* VPT, ResidentLaunch* out) {
+  return dtype ? regular_lookup_f64(D, DV, CPT, VPT_min, nt, n_vars, variant, VPT, out)
+               : regular_lookup_f32(D, DV, CPT, VPT_min, nt, n_vars, variant, VPT, out);
 }
 
 // Defined in resident_f32.cu / resident_f64.cu.

@@ -40,10 +40,11 @@ bool resident_lookup_t(int D, int CPT, int DVMAX, ResidentLaunch* out) {
   return false;
 }
 
-template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT, bool COL>
+template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT, bool COL, int NPC = 0, int NTC = 0>
 ResidentLaunch make_regular() {
-  return ResidentLaunch{reinterpret_cast<const void*>(&resident_regular_kernel<T, D, DV, CPT, VPT, MINB, MAXT, COL>),
-                        &launch_regular<T, D, DV, CPT, VPT, MINB, MAXT, COL>, 0, 0, 0, COL};
+  return ResidentLaunch{
+      reinterpret_cast<const void*>(&resident_regular_kernel<T, D, DV, CPT, VPT, MINB, MAXT, COL, NPC, NTC>),
+      &launch_regular<T, D, DV, CPT, VPT, MINB, MAXT, COL, NPC, NTC>, 0, 0, 0, COL, NPC};
 }
 
 // The compiled regular shapes (D, DV, CPT, VPT, MINB, MAXT, COL), in
@@ -58,7 +59,8 @@ ResidentLaunch make_regular() {
 //   * the slot layout (per-edge message addresses) for everything else and
 //     for fp64, whose variable sums must follow the reference's edge order.
 template <typename T>
-bool regular_lookup_t(int D, int DV, int CPT, int VPT_min, int variant, int* VPT, ResidentLaunch* out) {
+bool regular_lookup_t(int D, int DV, int CPT, int VPT_min, int nt, int n_vars, int variant, int* VPT,
+                      ResidentLaunch* out) {
   constexpr bool F32 = sizeof(T) == 4;
   int seen = 0;
 #define ADMM_REG(d, dv, cpt, vpt, minb, maxt, col)                               \
@@ -67,7 +69,17 @@ bool regular_lookup_t(int D, int DV, int CPT, int VPT_min, int variant, int* VPT
     *out = make_regular<T, d, dv, cpt, vpt, minb, maxt, col>();                  \
     return true;                                                                 \
   }
+  // compile-time geometry: exactly nt threads and at most npc padded variables
+#define ADMM_REG_FIXED(d, dv, cpt, vpt, minb, npc, ntc)                                       \
+  if (D == d && DV == dv && CPT == cpt && VPT_min <= vpt && nt == ntc &&                      \
+      regular_np(n_vars, true, ntc, vpt) <= npc && seen++ == variant) {                       \
+    *VPT = vpt;                                                                               \
+    *out = make_regular<T, d, dv, cpt, vpt, minb, ntc, true, npc, ntc>();                     \
+    return true;                                                                              \
+  }
   if constexpr (F32) {
+    ADMM_REG_FIXED(6, 3, 2, 4, 3, 1024, 256)
+    ADMM_REG_FIXED(6, 3, 2, 4, 1, 2688, 672)
     ADMM_REG(6, 3, 2, 4, 3, 256, true)
     ADMM_REG(6, 3, 2, 4, 1, 704, true)
     ADMM_REG(6, 3, 1, 2, 2, 512, true)
@@ -81,6 +93,7 @@ bool regular_lookup_t(int D, int DV, int CPT, int VPT_min, int variant, int* VPT
   ADMM_REG(4, 2, 1, 2, F32 ? 2 : 1, 512, false)
   ADMM_REG(4, 3, 1, 2, F32 ? 2 : 1, 512, false)
 #undef ADMM_REG
+#undef ADMM_REG_FIXED
   return false;
 }
 

@@ -42,15 +42,20 @@ __host__ __device__ inline int regular_np(int n_vars, bool col, int nt, int vpt)
   return (need + 31) & ~31;
 }
 
-template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT = 512, bool COL = false>
+// NPC / NTC > 0 fix the padded variable count and the CTA size at compile
+// time (COL only): every shared address in the hot loop is then a register
+// plus an immediate offset.
+template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT = 512, bool COL = false, int NPC = 0,
+          int NTC = 0>
 __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const ResidentParams<T> p,
                                                                      const int* __restrict__ var_edge) {
   static_assert(!COL || (D % DV == 0 && sizeof(T) == 4), "colored layout: fp32, DV | D");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int N = p.n_vars, M = p.n_checks;
-  const int tid = threadIdx.x, NT = blockDim.x;
+  static_assert(COL || (NPC == 0 && NTC == 0), "compile-time geometry needs the colored layout");
+  const int tid = threadIdx.x, NT = NTC ? NTC : blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = NT >> 5;
-  const int NP = COL ? regular_np(N, true, NT, VPT) : (N + 31) & ~31;
+  const int NP = NPC ? NPC : COL ? regular_np(N, true, NT, VPT) : (N + 31) & ~31;
   constexpr int kRows = COL ? DV : D;  // message rows: colors (COL) or check slots
   T* xs = reinterpret_cast<T*>(smem_raw);
   T* msg = xs + NP;
@@ -59,7 +64,7 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
   const uint32_t msg_a = smem_u32(msg), xs_a = smem_u32(xs);
   constexpr uint32_t ES = sizeof(T);
   // msg[k][pi(v)] sits at x-address of v + moff(k)
-  const uint32_t moff0 = msg_a - xs_a, mstride = ES * NP;
+  const uint32_t moff0 = NPC ? ES * NPC : msg_a - xs_a, mstride = ES * NP;
   // shared-address offset of the message of check slot k from the x slot of its variable
   auto moff = [&](int k) -> uint32_t { return moff0 + (COL ? k % DV : k) * mstride; };
 
@@ -91,7 +96,7 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
         vaddr[q][j] = msg_a + ES * ((e % D) * NP + i);
       }
     }
-    xst[q] = xs_a + ES * i;
+    xst[q] = xs_a + ES * tid + ES * q * NT;
     vorig[q] = (vact[q] && p.var_orig) ? __ldg(p.var_orig + i) : i;
   }
 

@@ -173,3 +173,17 @@ def test_empty_batch_and_shape_errors(cuda_ok):
         decode_batch(np.zeros((3, 95)), code)
     with pytest.raises(ValueError):
         decode_batch(np.full((2, 96), np.nan), code)
+
+
+@pytest.mark.parametrize("name,ctas", [("cfg1_n96", 1), ("cfg2_n1008", 3), ("cfg3_n2640", 1), ("cfg4_n1040", 1)])
+def test_baseline_codes_take_the_regular_resident_kernels(cuda_ok, name, ctas):
+    """Guards the engine choice: every BASELINE code that fits one SM must land
+    on the regular resident kernels (engine 2), with the CTA occupancy the
+    fp32 fast path was tuned for -- a silent fall-back to the generic kernel
+    still decodes correctly and would otherwise only show up as a slow bench."""
+    from paper_1204_0556_b200 import baseline_code
+    from paper_1204_0556_b200.admm_decoder import DeviceGraph
+
+    info = DeviceGraph(baseline_code(name), 0).info
+    assert info["engine"] == 2, info
+    assert info["ctas_per_sm_f32"] >= ctas, info
