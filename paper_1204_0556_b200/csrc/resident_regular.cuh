@@ -49,7 +49,7 @@ template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT = 512,
           int NTC = 0>
 __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const ResidentParams<T> p,
                                                                      const int* __restrict__ var_edge) {
-  static_assert(!COL || (D % DV == 0 && sizeof(T) == 4), "colored layout: fp32, DV | D");
+  static_assert(!COL || (D % DV == 0 && sizeof(T) == 4 && VPT % 2 == 0), "colored layout: fp32, DV | D, VPT even");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int N = p.n_vars, M = p.n_checks;
   static_assert(COL || (NPC == 0 && NTC == 0), "compile-time geometry needs the colored layout");
@@ -87,7 +87,9 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
   bool vact[VPT];
 #pragma unroll
   for (int q = 0; q < VPT; ++q) {
-    const int i = tid + q * NT;
+    // COL: variables in adjacent pairs (2 tid + 2 NT p, +1) so the variable
+    // phase moves two of them per 8-byte shared access
+    const int i = COL ? 2 * tid + 2 * NT * (q >> 1) + (q & 1) : tid + q * NT;
     vact[q] = i < N;
     if constexpr (!COL) {
 #pragma unroll
@@ -96,7 +98,7 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
         vaddr[q][j] = msg_a + ES * ((e % D) * NP + i);
       }
     }
-    xst[q] = xs_a + ES * tid + ES * q * NT;
+    xst[q] = COL ? xs_a + ES * 2 * tid + ES * (2 * NT * (q >> 1) + (q & 1)) : xs_a + ES * tid + ES * q * NT;
     vorig[q] = (vact[q] && p.var_orig) ? __ldg(p.var_orig + i) : i;
   }
 
@@ -105,9 +107,20 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
   // form, tests/test_admm.py:208-240): v = w + l, l' = l + (w - z'),
   // message = z' - l'.  No division or multiply by mu in the loop; lambda
   // is converted only at the state I/O boundary.
-  T z[CPT][D], lam[CPT][D];
-  T gm[VPT];
   constexpr bool kPacked = !kF64 && (D % 2 == 0);
+  // fp32 keeps the state as packed edge pairs (kPacked) so the loop-carried
+  // registers are the FFMA2/FADD2 operand pairs themselves.
+  T z[kPacked ? 1 : CPT][D], lam[kPacked ? 1 : CPT][D];
+  float2 zp[CPT][kPacked ? D / 2 : 1], lp[CPT][kPacked ? D / 2 : 1];
+  auto zget = [&](int q, int k) -> T {
+    if constexpr (kPacked) return (k & 1) ? zp[q][k >> 1].y : zp[q][k >> 1].x;
+    else return z[q][k];
+  };
+  auto lget = [&](int q, int k) -> T {
+    if constexpr (kPacked) return (k & 1) ? lp[q][k >> 1].y : lp[q][k >> 1].x;
+    else return lam[q][k];
+  };
+  T gm[VPT];
   const float2 rho2 = make_float2(float(p.rho), float(p.rho));
   const float2 omr2 = make_float2(float(p.one_minus_rho), float(p.one_minus_rho));
 
@@ -136,8 +149,18 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
           l0 = p.lam_in[e];
         }
         const T s0 = div_rn(l0, p.mu);
-        z[q][k] = z0;
-        lam[q][k] = s0;
+        if constexpr (kPacked) {
+          if (k & 1) {
+            zp[q][k >> 1].y = z0;
+            lp[q][k >> 1].y = s0;
+          } else {
+            zp[q][k >> 1].x = z0;
+            lp[q][k >> 1].x = s0;
+          }
+        } else {
+          z[q][k] = z0;
+          lam[q][k] = s0;
+        }
         if (cact[q]) sts(xaddr[q][k] + moff(k), sub_rn(z0, s0));
       }
     }
@@ -148,8 +171,20 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
     while (t < p.t_max) {
       ++t;
       // ---- x-update (admm_decoder.py:108-124): edges summed in edge order ----
+      if constexpr (COL) {
+        // pairs of variables: 8-byte loads/stores, packed sums (color order)
 #pragma unroll
-      for (int q = 0; q < VPT; ++q) {
+        for (int h = 0; h < VPT / 2; ++h) {
+          const uint32_t a = xst[2 * h];
+          float2 acc = lds2(a + moff0);
+#pragma unroll
+          for (int j = 1; j < DV; ++j) acc = __fadd2_rn(acc, lds2(a + moff0 + j * mstride));
+          const float2 num = fsub2_rn(acc, make_float2(gm[2 * h], gm[2 * h + 1]));
+          sts2(a, make_float2(clip01(num.x * (1.f / DV)), clip01(num.y * (1.f / DV))));
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < (COL ? 0 : VPT); ++q) {
         if (COL || vact[q]) {
           // COL: message of color j at a fixed offset from the variable's x slot
           auto va = [&](int j) -> uint32_t { return COL ? xst[q] + moff0 + j * mstride : vaddr[COL ? 0 : q][j]; };
@@ -180,8 +215,8 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
 #pragma unroll
             for (int j = 0; j < D / 2; ++j) {
               gx2[j] = make_float2(lds(xaddr[q][2 * j], T()), lds(xaddr[q][2 * j + 1], T()));
-              z2[j] = make_float2(z[q][2 * j], z[q][2 * j + 1]);
-              l2[j] = make_float2(lam[q][2 * j], lam[q][2 * j + 1]);
+              z2[j] = zp[q][j];
+              l2[j] = lp[q][j];
             }
             T u[D], zn[D];
 #pragma unroll
@@ -201,10 +236,8 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
               mv2 = __ffma2_rn(r2, r2, mv2);
               const float2 ln = __fadd2_rn(l2[j], fsub2_rn(w2[j], zn2));
               const float2 m2 = fsub2_rn(zn2, ln);
-              lam[q][2 * j] = ln.x;
-              lam[q][2 * j + 1] = ln.y;
-              z[q][2 * j] = zn2.x;
-              z[q][2 * j + 1] = zn2.y;
+              lp[q][j] = ln;
+              zp[q][j] = zn2;
               sts(xaddr[q][2 * j] + moff(2 * j), m2.x);
               sts(xaddr[q][2 * j + 1] + moff(2 * j + 1), m2.y);
             }
@@ -225,19 +258,19 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
           for (int k = 0; k < D; ++k) gx[k] = lds(xaddr[q][k], T());
 #pragma unroll
           for (int k = 0; k < D; ++k) {
-            w[k] = add_rn(mul_rn(p.rho, gx[k]), mul_rn(p.one_minus_rho, z[q][k]));
-            u[k] = add_rn(w[k], lam[q][k]);
+            w[k] = add_rn(mul_rn(p.rho, gx[k]), mul_rn(p.one_minus_rho, z[kPacked ? 0 : q][k]));
+            u[k] = add_rn(w[k], lam[kPacked ? 0 : q][k]);
           }
           project_pp_fixed<T, D>(u, zn);
 #pragma unroll
           for (int k = 0; k < D; ++k) {
             const T r1 = sub_rn(gx[k], zn[k]);
-            const T r2 = sub_rn(zn[k], z[q][k]);
+            const T r2 = sub_rn(zn[k], z[kPacked ? 0 : q][k]);
             primal = add_rn(primal, mul_rn(r1, r1));
             moved = add_rn(moved, mul_rn(r2, r2));
-            lam[q][k] = add_rn(lam[q][k], sub_rn(w[k], zn[k]));
-            z[q][k] = zn[k];
-            sts(xaddr[q][k] + moff(k), sub_rn(zn[k], lam[q][k]));
+            lam[kPacked ? 0 : q][k] = add_rn(lam[kPacked ? 0 : q][k], sub_rn(w[k], zn[k]));
+            z[kPacked ? 0 : q][k] = zn[k];
+            sts(xaddr[q][k] + moff(k), sub_rn(zn[k], lam[kPacked ? 0 : q][k]));
           }
         }
       }
@@ -289,8 +322,8 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
 #pragma unroll
           for (int k = 0; k < D; ++k) {
             const long long e = f * p.ld_edge + (p.edge_ref ? __ldg(p.edge_ref + c * D + k) : c * D + k);
-            p.z_out[e] = z[q][k];
-            p.lam_out[e] = mul_rn(p.mu, lam[q][k]);
+            p.z_out[e] = zget(q, k);
+            p.lam_out[e] = mul_rn(p.mu, lget(q, k));
           }
         }
       }
