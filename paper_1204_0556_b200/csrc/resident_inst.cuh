@@ -78,6 +78,7 @@ bool regular_lookup_t(int D, int DV, int CPT, int VPT_min, int nt, int n_vars, i
     return true;                                                                              \
   }
   if constexpr (F32) {
+    ADMM_REG_FIXED(6, 3, 2, 4, 4, 1024, 256)
     ADMM_REG_FIXED(6, 3, 2, 4, 3, 1024, 256)
     ADMM_REG_FIXED(6, 3, 2, 4, 1, 2688, 672)
     ADMM_REG(6, 3, 2, 4, 3, 256, true)

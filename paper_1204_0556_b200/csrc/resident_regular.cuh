@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
           // COL: idle checks run on the spare slot; their residuals are dropped
           const float2 pr_in = pr2, mv_in = mv2;
           if (COL || cact[q]) {
-            float2 gx2[D / 2], w2[D / 2], z2[D / 2], l2[D / 2];
+            float2 gx2[D / 2], u2[D / 2], z2[D / 2], l2[D / 2];
 #pragma unroll
             for (int j = 0; j < D / 2; ++j) {
               gx2[j] = make_float2(lds(xaddr[q][2 * j], T()), lds(xaddr[q][2 * j + 1], T()));
@@ -221,10 +221,9 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
             T u[D], zn[D];
 #pragma unroll
             for (int j = 0; j < D / 2; ++j) {
-              w2[j] = __ffma2_rn(rho2, gx2[j], __fmul2_rn(omr2, z2[j]));
-              const float2 u2 = __fadd2_rn(w2[j], l2[j]);
-              u[2 * j] = u2.x;
-              u[2 * j + 1] = u2.y;
+              u2[j] = __fadd2_rn(__ffma2_rn(rho2, gx2[j], __fmul2_rn(omr2, z2[j])), l2[j]);
+              u[2 * j] = u2[j].x;
+              u[2 * j + 1] = u2[j].y;
             }
             project_pp_fixed<T, D>(u, zn);
 #pragma unroll
@@ -234,7 +233,9 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
               const float2 r2 = fsub2_rn(zn2, z2[j]);
               pr2 = __ffma2_rn(r1, r1, pr2);
               mv2 = __ffma2_rn(r2, r2, mv2);
-              const float2 ln = __fadd2_rn(l2[j], fsub2_rn(w2[j], zn2));
+              // reassociated dual update l' = (w + l) - z' = u - z' (fp32
+              // throughput mode): w and l are dead once u is formed
+              const float2 ln = fsub2_rn(u2[j], zn2);
               const float2 m2 = fsub2_rn(zn2, ln);
               lp[q][j] = ln;
               zp[q][j] = zn2;
