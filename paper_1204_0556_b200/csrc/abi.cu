@@ -183,8 +183,8 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
         for (int variant = venv ? std::atoi(venv) : 0; !ok; ++variant) {
           admm::ResidentLaunch L{};
           if (!admm::regular_lookup(dt, dmax, dvmax, cpt, need, nt, n_vars, variant, &vpt, &L)) break;
-          const int smem = L.np_fixed ? 4 * (L.np_fixed * (1 + dvmax) + 64) + 16
-                                      : admm::regular_smem_bytes(dt ? 8 : 4, dmax, dvmax, n_vars, L.colored, nt, vpt);
+          const int smem = admm::regular_smem_bytes(dt ? 8 : 4, dmax, dvmax, n_vars, L.colored, L.gm_smem, nt, vpt,
+                                                    L.np_fixed);
           ok = check_one(L, smem, nt);
           if (ok) Ls[dt] = L;
         }

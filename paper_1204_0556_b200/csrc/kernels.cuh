@@ -56,6 +56,7 @@ struct ResidentLaunch {
   int smem, occupancy, regs;
   bool colored;  // regular kernel on the colored message layout (layout.h)
   int np_fixed;  // compile-time padded variable count (0 = computed from n_vars)
+  bool gm_smem;  // LLR steps in shared memory (regular_gm_smem)
 };
 
 template <typename T>

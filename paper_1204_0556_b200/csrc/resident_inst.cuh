@@ -44,7 +44,7 @@ template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT, bool 
 ResidentLaunch make_regular() {
   return ResidentLaunch{
       reinterpret_cast<const void*>(&resident_regular_kernel<T, D, DV, CPT, VPT, MINB, MAXT, COL, NPC, NTC>),
-      &launch_regular<T, D, DV, CPT, VPT, MINB, MAXT, COL, NPC, NTC>, 0, 0, 0, COL, NPC};
+      &launch_regular<T, D, DV, CPT, VPT, MINB, MAXT, COL, NPC, NTC>, 0, 0, 0, COL, NPC, regular_gm_smem(COL, MINB)};
 }
 
 // The compiled regular shapes (D, DV, CPT, VPT, MINB, MAXT, COL), in
