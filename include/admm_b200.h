@@ -144,6 +144,24 @@ int admm_project_batch(int dtype, int64_t m, int32_t d, const void* values, void
  * phase, grid sync, slot phase, passes, 0, 0} accumulated so far. */
 int admm_phase_profile(int enable, uint64_t* cycles8);
 
+/* Flooding sum-product BP on the same graph handle (the comparison baseline,
+ * SURVEY.md 8f #4).  Replaces posterior_llrs / decode_bp
+ * (bp_decoder.py:55-112) with BpConfig (t_max, llr_clip, early_stop)
+ * (bp_decoder.py:22-34) for a batch of frames:
+ *   gamma        [batch][ld_gamma] device LLRs (dtype)
+ *   beliefs_out  [batch][ld_beliefs] posterior LLRs (may be NULL)
+ *   x_out        [batch][ld_x] bit-1 probabilities 0.5 (1 - tanh(b / 2)) (may be NULL)
+ *   hard_out, iters_out, flags_out, weight_out as admm_decode_batch;
+ *   flags: CONVERGED = early exit on a codeword, INTEGRAL as the reference's
+ *   decode_bp, CODEWORD = zero syndrome of the hard decision.
+ *   workspace    >= 16 bytes of device scratch.
+ * Codes whose per-frame state does not fit one SM return ADMM_E_UNSUPPORTED. */
+int admm_bp_decode_batch(const admm_graph* g, int dtype, int64_t batch, const void* gamma, int64_t ld_gamma,
+                         int32_t t_max, double llr_clip, int32_t early_stop, void* beliefs_out,
+                         int64_t ld_beliefs, void* x_out, int64_t ld_x, uint8_t* hard_out, int64_t ld_hard,
+                         int32_t* iters_out, uint8_t* flags_out, int32_t* weight_out, void* workspace,
+                         size_t workspace_bytes, void* stream);
+
 const char* admm_last_error(void);
 int admm_version(void);
 

@@ -22,6 +22,7 @@ from .admm_decoder import (
     synth_llr,
     run_iterations,
 )
+from .bp_decoder import BpBatchResult, BpConfig, decode_bp, decode_bp_batch, posterior_llrs
 from .channels import Awgn, Bsc, llr, transmit, trial_gamma, trial_gammas
 from .codes import (
     AlistParseError,
@@ -42,6 +43,7 @@ __version__ = "0.1.0"
 __all__ = [
     "AdmmConfig", "BatchResult", "DecodeOutput", "INTEGRALITY_TOL", "STATUS_CONVERGED",
     "STATUS_MAX_ITERS", "decode", "decode_batch", "decode_synth", "device_graph", "synth_llr", "run_iterations",
+    "BpBatchResult", "BpConfig", "decode_bp", "decode_bp_batch", "posterior_llrs",
     "Awgn", "Bsc", "llr", "transmit", "trial_gamma", "trial_gammas",
     "AlistParseError", "CodeGenerationError", "ParityCheckMatrix", "baseline_code", "emit_alist",
     "gen_regular_ldpc", "is_codeword", "make_ldpc", "parse_alist",

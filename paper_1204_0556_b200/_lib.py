@@ -35,6 +35,7 @@ EXPORTED = (
     "admm_synth_llr",
     "admm_project_batch",
     "admm_phase_profile",
+    "admm_bp_decode_batch",
 )
 
 
@@ -107,6 +108,11 @@ def load() -> ctypes.CDLL:
     lib.admm_phase_profile.restype = ctypes.c_int
     lib.admm_project_batch.argtypes = [ctypes.c_int, I64, I32, P, P, P]
     lib.admm_project_batch.restype = ctypes.c_int
+    lib.admm_bp_decode_batch.argtypes = [
+        P, ctypes.c_int, I64, P, I64, I32, D, I32,
+        P, I64, P, I64, P, I64, P, P, P, P, SZ, P,
+    ]
+    lib.admm_bp_decode_batch.restype = ctypes.c_int
     _lib = lib
     return lib
 

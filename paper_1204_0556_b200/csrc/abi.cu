@@ -5,10 +5,13 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
 #include "../../include/admm_b200.h"
+#include "bp_launch.h"
 #include "kernels.cuh"
 #include "layout.h"
 
@@ -61,6 +64,11 @@ struct admm_graph {
   int* cchk_var = nullptr;       // colored layout (fp32 regular kernels with DV | D)
   int* cvar_orig = nullptr;
   int* cedge_ref = nullptr;
+  int* chk_var_ref = nullptr;    // original numbering when chk_var is relabeled (kind 2), else == chk_var
+  // BP (bp.cuh): its own CTA shape on the same graph arrays
+  admm::BpLaunch bp_launch[2];
+  bool bp_ok[2] = {false, false};
+  int bp_nt = 0;
   double layout_cost[2] = {0, 0};
   // per-dtype launch data
   admm::ResidentLaunch launch[2];
@@ -69,6 +77,23 @@ struct admm_graph {
 namespace {
 
 const int kBuckets[] = {4, 6, 8, 13, 16, 32};
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per kernel and process-wide,
+// while one kernel serves many graphs with different shared-memory sizes:
+// only ever raise it, so a graph placed earlier with a larger size stays
+// launchable after a smaller one was placed.
+cudaError_t ensure_smem(const void* fn, int smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> granted;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  int& cur = granted[{dev, fn}];
+  if (smem <= cur) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) cur = smem;
+  return e;
+}
 
 int pick_bucket(int d) {
   for (int b : kBuckets)
@@ -160,7 +185,7 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
                    fa.maxThreadsPerBlock);
     if (ge != cudaSuccess) return false;
     if (fa.numRegs * nt > 65536 || nt > fa.maxThreadsPerBlock) return false;
-    if (cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
+    if (ensure_smem(L.fn, smem) != cudaSuccess) return false;
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L.fn, nt, smem);
     if (dbg) std::fprintf(stderr, "[admm]   occupancy %d\n", occ);
@@ -252,7 +277,7 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
           cudaFuncAttributes fa{};
           if (cudaFuncGetAttributes(&fa, L.fn) != cudaSuccess) { ok = false; break; }
           if (fa.numRegs * nt > 65536) { ok = false; break; }
-          cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+          ensure_smem(L.fn, smem);
           if (C > 8) cudaFuncSetAttribute(L.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
           cudaLaunchConfig_t cfg{};
           cfg.gridDim = dim3(C);
@@ -329,7 +354,7 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
         g->shard_dv = dv_used;
         const admm::ShardGeom geo = admm::shard_geom(dt ? 8 : 4, g->D, dv_used, n_checks, n_vars, EB, G, 32);
         if (geo.total > smem_optin) continue;
-        if (cudaFuncSetAttribute(SL.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin) != cudaSuccess) continue;
+        if (ensure_smem(SL.fn, smem_optin) != cudaSuccess) continue;
         cudaFuncAttributes fa{};
         if (cudaFuncGetAttributes(&fa, SL.fn) != cudaSuccess || fa.numRegs * (dt ? 512 : 1024) > 65536) continue;
         int occ = 0;
@@ -390,6 +415,35 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
   cudaError_t e4 = up((void**)&g->edge_base, edge_base.data(), edge_base.size() * sizeof(int));
   cudaError_t e5 = up((void**)&g->var_edge, var_edge.data(), var_edge.size() * sizeof(int));
   cudaError_t e6 = cudaSuccess, e7 = cudaSuccess, e8 = cudaSuccess;
+  g->chk_var_ref = g->chk_var;
+  if (g->kind == 2 && e1 == cudaSuccess)
+    e1 = up((void**)&g->chk_var_ref, chk_var.data(), chk_var.size() * sizeof(int));
+  // BP placement: generic check-degree bucket, one or two checks per thread.
+  for (int dt = 0; dt < 2; ++dt) {
+    for (int cpt : {1, 2}) {
+      const int nt = ((n_checks + cpt - 1) / cpt + 31) / 32 * 32;
+      if (nt > 512) continue;
+      if (g->bp_nt && nt != g->bp_nt) continue;  // one CTA shape for both dtypes
+      admm::BpLaunch L{};
+      if (!admm::bp_lookup(dt, D, cpt, g->DVMAX, &L)) continue;
+      const int smem = admm::bp_smem_bytes(dt ? 8 : 4, n_vars, D * MP, g->DVMAX);
+      if (smem > smem_optin) continue;
+      cudaFuncAttributes fa{};
+      if (cudaFuncGetAttributes(&fa, L.fn) != cudaSuccess || fa.numRegs * nt > 65536) continue;
+      if (ensure_smem(L.fn, smem) != cudaSuccess) continue;
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, L.fn, nt, smem);
+      if (occ < 1) continue;
+      L.smem = smem;
+      L.occupancy = occ;
+      L.regs = fa.numRegs;
+      g->bp_launch[dt] = L;
+      g->bp_ok[dt] = true;
+      g->bp_nt = nt;
+      break;
+    }
+  }
+  cudaGetLastError();
   if (g->kind == 2) {
     // Bank-conflict-free layout (layout.h): internal variable numbering and
     // the slot of every edge inside its check, with the message of edge
@@ -475,6 +529,7 @@ int admm_graph_destroy(admm_graph* g) {
   cudaFree(g->cchk_var);
   cudaFree(g->cvar_orig);
   cudaFree(g->cedge_ref);
+  if (g->chk_var_ref != g->chk_var) cudaFree(g->chk_var_ref);
   delete g;
   return ADMM_OK;
 }
@@ -711,6 +766,39 @@ int admm_synth_llr(int dtype, int64_t batch, int32_t n_vars, const admm_channel*
   if (batch == 0) return ADMM_OK;
   if (!out) return fail(ADMM_E_ARG, "null output");
   admm::launch_synth(dtype, batch, n_vars, sp, out, ld, reinterpret_cast<cudaStream_t>(stream));
+  ADMM_CUDA(cudaGetLastError());
+  return ADMM_OK;
+}
+
+int admm_bp_decode_batch(const admm_graph* g, int dtype, int64_t batch, const void* gamma, int64_t ld_gamma,
+                         int32_t t_max, double llr_clip, int32_t early_stop, void* beliefs_out,
+                         int64_t ld_beliefs, void* x_out, int64_t ld_x, uint8_t* hard_out, int64_t ld_hard,
+                         int32_t* iters_out, uint8_t* flags_out, int32_t* weight_out, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  if (!g) return fail(ADMM_E_ARG, "null graph");
+  if (dtype != ADMM_F32 && dtype != ADMM_F64) return fail(ADMM_E_ARG, "dtype must be ADMM_F32 or ADMM_F64");
+  if (batch < 0) return fail(ADMM_E_ARG, "negative batch");
+  if (t_max < 1) return fail(ADMM_E_ARG, "t_max must be at least 1");          // bp_decoder.py:31-32
+  if (!(llr_clip > 0)) return fail(ADMM_E_ARG, "llr_clip must be positive");   // bp_decoder.py:33-34
+  if (batch == 0) return ADMM_OK;
+  if (!gamma) return fail(ADMM_E_ARG, "null gamma");
+  if (ld_gamma < g->n_vars) return fail(ADMM_E_ARG, "ld_gamma < n_vars");
+  if (beliefs_out && ld_beliefs < g->n_vars) return fail(ADMM_E_ARG, "ld_beliefs < n_vars");
+  if (x_out && ld_x < g->n_vars) return fail(ADMM_E_ARG, "ld_x < n_vars");
+  if (hard_out && ld_hard < g->n_vars) return fail(ADMM_E_ARG, "ld_hard < n_vars");
+  if (!workspace || workspace_bytes < 16) return fail(ADMM_E_WORKSPACE, "workspace too small (16 bytes)");
+  if (!g->bp_ok[dtype]) return fail(ADMM_E_UNSUPPORTED, "BP: the graph does not fit one SM");
+  if (batch > (1ll << 31) - 1024) return fail(ADMM_E_ARG, "batch too large for one call");
+  ADMM_CUDA(cudaSetDevice(g->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  ADMM_CUDA(cudaMemsetAsync(workspace, 0, sizeof(int), st));
+  const admm::BpLaunch& L = g->bp_launch[dtype];
+  const long long grid = std::min<long long>(batch, (long long)L.occupancy * g->num_sms);
+  admm::BpGraphArgs ga{g->n_vars, g->n_checks, g->m_pad, g->chk_var_ref, g->var_pos, g->var_deg};
+  admm::BpFrameArgs fa{batch, gamma, ld_gamma, llr_clip, t_max, early_stop ? 1 : 0, beliefs_out, ld_beliefs,
+                       x_out, ld_x, hard_out, ld_hard, iters_out, flags_out, weight_out,
+                       reinterpret_cast<int*>(workspace), admm::SynthParams{}};
+  L.launch(ga, fa, (int)grid, g->bp_nt, L.smem, st);
   ADMM_CUDA(cudaGetLastError());
   return ADMM_OK;
 }

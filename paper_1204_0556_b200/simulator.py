@@ -20,9 +20,9 @@ one ``decode`` call per trial in a process pool.  Two frame sources:
   statistically the same channel, not bit-identical to numpy.
 
 In both modes a trial's result depends only on (seed, point, trial), never on
-the batch size or the number of GPUs.  Only the ADMM decoder is implemented
-on the GPU; ``DecoderRef("bp")`` / ``("dual-ascent")`` raise (the reference's
-baselines are out of scope).  Timing columns report each trial's share of its
+the batch size or the number of GPUs.  ``DecoderRef("admm")`` and
+``DecoderRef("bp")`` (flooding sum-product, csrc/bp.cuh) run on the GPU;
+``("dual-ascent")`` raises (that reference baseline is out of scope).  Timing columns report each trial's share of its
 batch's wall time.
 """
 
@@ -39,7 +39,8 @@ import numpy as np
 import torch
 from numpy.typing import ArrayLike, NDArray
 
-from .admm_decoder import AdmmConfig, DecodeOutput, decode, decode_batch, decode_synth
+from .admm_decoder import AdmmConfig, DecodeOutput, decode, decode_batch, decode_synth, synth_llr
+from .bp_decoder import BpConfig, decode_bp, decode_bp_batch
 from .channels import Awgn, Bsc, ChannelModel, llr, transmit, trial_rng
 from .codes import ParityCheckMatrix, as_code, is_codeword
 
@@ -54,23 +55,28 @@ ALGORITHMS = ("admm", "bp", "dual-ascent")
 
 @dataclass(frozen=True)
 class DecoderRef:
-    """Decoder selection (simulator.py:53-72).  Only ``"admm"`` runs here."""
+    """Decoder selection (simulator.py:53-72): ``"admm"`` and ``"bp"`` run on the GPU."""
 
     algo: str = "admm"
-    config: AdmmConfig | None = None
+    config: AdmmConfig | BpConfig | None = None
 
     def __post_init__(self) -> None:
         if self.algo not in ALGORITHMS:
             raise ValueError(f"unknown decoder {self.algo!r}; use one of {ALGORITHMS}")
 
-    def admm_config(self) -> AdmmConfig:
-        if self.algo != "admm":
-            raise NotImplementedError(
-                f"decoder {self.algo!r} is a CPU baseline of the reference; only 'admm' runs on the GPU")
-        return self.config if self.config is not None else AdmmConfig()
+    def admm_config(self) -> AdmmConfig | BpConfig:
+        """The decoder's config (defaults as simulator.py:64-72)."""
+        if self.algo == "admm":
+            return self.config if self.config is not None else AdmmConfig()
+        if self.algo == "bp":
+            return self.config if self.config is not None else BpConfig()
+        raise NotImplementedError(
+            f"decoder {self.algo!r} is a CPU baseline of the reference; 'admm' and 'bp' run on the GPU")
 
     def bind(self, code) -> Callable[[NDArray[np.float64]], DecodeOutput]:
         cfg = self.admm_config()
+        if self.algo == "bp":
+            return lambda g: decode_bp(g, code, cfg)
         return lambda g: decode(g, code, cfg)
 
 
@@ -143,19 +149,30 @@ def _decode_wave(code, channel, cfg, sent, seed, point, trials: range, *, frames
     B = len(trials)
     t0 = time.perf_counter()
     all_zero = not np.any(sent)
+    bp = isinstance(cfg, BpConfig)
     if frames == "device":
         if not all_zero:
             raise ValueError("frames='device' synthesises the all-zero codeword only")
-        res = decode_synth(code, channel, cfg, seed=seed, point=point, trial0=trials.start, batch=B,
-                           dtype=dtype, device=device, want_hard=True, engine=engine)
-        gam = None
+        if bp:
+            gam = synth_llr(code.n_vars, channel, seed=seed, point=point, trial0=trials.start, batch=B,
+                            dtype=dtype, device=device)
+            res = decode_bp_batch(gam, code, cfg, dtype=dtype, device=device, want_beliefs=False, want_x=False,
+                                  validate=False)
+        else:
+            res = decode_synth(code, channel, cfg, seed=seed, point=point, trial0=trials.start, batch=B,
+                               dtype=dtype, device=device, want_hard=True, engine=engine)
+            gam = None
     elif frames == "reference":
         gam_np = np.empty((B, code.n_vars))
         for k, t in enumerate(trials):
             gam_np[k] = llr(transmit(sent, channel, trial_rng(seed, point, t)), channel)
         gam = torch.from_numpy(gam_np).to(device)
-        res = decode_batch(gam, code, cfg, dtype=dtype, device=device, want_x=False, want_hard=True,
-                           validate=False, engine=engine)
+        if bp:
+            res = decode_bp_batch(gam, code, cfg, dtype=dtype, device=device, want_beliefs=False, want_x=False,
+                                  validate=False)
+        else:
+            res = decode_batch(gam, code, cfg, dtype=dtype, device=device, want_x=False, want_hard=True,
+                               validate=False, engine=engine)
     else:
         raise ValueError("frames must be 'reference' or 'device'")
     hard = res.hard
@@ -163,8 +180,6 @@ def _decode_wave(code, channel, cfg, sent, seed, point, trials: range, *, frames
     bit_err = (hard != sent_t).sum(dim=1).to(torch.int64)
     word_err = bit_err > 0
     if gam is None:
-        from .admm_decoder import synth_llr
-
         gam = synth_llr(code.n_vars, channel, seed=seed, point=point, trial0=trials.start, batch=B,
                         dtype=torch.float64, device=device)
     cost_est = (gam.to(torch.float64) * hard.to(torch.float64)).sum(dim=1)

@@ -29,6 +29,15 @@ harness.npz        reference sweep()/run_point() CSV (timing=False) on the confi
 steps.npz          single-iteration state dumps (x, z, lam) after 1, 2, 3
                    iterations for one config-1 frame (x_update / z_update /
                    lambda_update driven directly, as test_admm.py:151-160).
+bp.npz             the reference's BP (bp_decoder.py): config-1 code at 2.5 dB,
+                   200 frames with the default BpConfig (beliefs, iterations,
+                   found, decode_bp x / integral / status), 16 frames for a
+                   FIXED 1 / 5 / 30 iterations (early_stop=False); a mixed-degree
+                   code; 25 random tree codes (the reference's
+                   tests/oracles.py:random_tree_code, seed 0) with their
+                   exact marginals (oracles.exact_marginals) and the BP beliefs
+                   after 40 iterations at llr_clip=500 (test_bp.py:31-42);
+                   config-2 code at 1.75 dB, 24 frames (iterations, found, hard).
 """
 
 from __future__ import annotations
@@ -159,6 +168,72 @@ def harness_fixture(code):
     print(csv_sweep, csv_target)
 
 
+def bp_fixture():
+    from polylp import BpConfig, decode_bp, posterior_llrs
+
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    import oracles  # noqa: E402  (the reference's own test oracles)
+
+    rec = {}
+    c1 = baseline_code("cfg1_n96")
+    rc = ref_code(c1)
+    gam = awgn_frames(c1, 2.5, seed=1, point=0, trials=range(200))
+    bel, it, fd, xs, integ, stat = [], [], [], [], [], []
+    for g in gam:
+        b, t, f = posterior_llrs(g, rc, BpConfig())
+        o = decode_bp(g, rc, BpConfig())
+        bel.append(b); it.append(t); fd.append(f); xs.append(o.x); integ.append(o.integral)
+        stat.append(o.status == polylp.STATUS_CONVERGED)
+    ptr, ev = pack_checks(c1)
+    rec.update(c1_check_ptr=ptr, c1_edge_var=ev, c1_n_vars=c1.n_vars, c1_gamma=gam, c1_beliefs=np.array(bel),
+               c1_iterations=np.array(it), c1_found=np.array(fd), c1_x=np.array(xs), c1_integral=np.array(integ),
+               c1_status=np.array(stat))
+    for T in (1, 5, 30):
+        rec[f"c1_fixed_T{T}"] = np.array([posterior_llrs(g, rc, BpConfig(t_max=T, early_stop=False))[0]
+                                          for g in gam[:16]])
+    # mixed check degrees (2 .. 7) and a degree-1 variable
+    rng = np.random.default_rng(77)
+    mixed = [sorted(rng.choice(40, size=int(rng.integers(2, 8)), replace=False).tolist()) for _ in range(22)]
+    mcode = polylp.ParityCheckMatrix(40, [np.array(c) for c in mixed])
+    mg = rng.normal(0.8, 1.3, size=(12, 40))
+    rec["mx_checks"] = np.array([len(c) for c in mixed])
+    rec["mx_flat"] = np.concatenate(mixed)
+    rec["mx_gamma"] = mg
+    rec["mx_beliefs_T7"] = np.array([posterior_llrs(g, mcode, BpConfig(t_max=7, early_stop=False, llr_clip=12.0))[0]
+                                     for g in mg])
+    out = [posterior_llrs(g, mcode, BpConfig(t_max=60)) for g in mg]
+    rec["mx_beliefs"] = np.array([o[0] for o in out])
+    rec["mx_iterations"] = np.array([o[1] for o in out])
+    rec["mx_found"] = np.array([o[2] for o in out])
+    # tree codes: BP is exact (test_bp.py:31-42)
+    trng = np.random.default_rng(0)
+    for k in range(25):
+        tc = oracles.random_tree_code(trng, n_max=12)
+        g = trng.normal(0.0, 1.5, tc.n_vars)
+        b, _, _ = posterior_llrs(g, tc, BpConfig(t_max=40, llr_clip=500.0, early_stop=False))
+        rec[f"tree{k}_n"] = tc.n_vars
+        rec[f"tree{k}_lens"] = np.array([len(c) for c in tc.check_neighborhoods])
+        rec[f"tree{k}_flat"] = np.concatenate([np.asarray(c) for c in tc.check_neighborhoods])
+        rec[f"tree{k}_gamma"] = g
+        rec[f"tree{k}_beliefs"] = b
+        rec[f"tree{k}_exact"] = oracles.exact_marginals(g, tc)
+    c2 = baseline_code("cfg2_n1008")
+    rc2 = ref_code(c2)
+    g2 = awgn_frames(c2, 1.75, seed=1, point=0, trials=range(24))
+    o2 = [decode_bp(g, rc2, BpConfig(t_max=200)) for g in g2]
+    rec.update(c2_gamma=g2, c2_iterations=np.array([o.iterations for o in o2]),
+               c2_found=np.array([o.status == polylp.STATUS_CONVERGED for o in o2]),
+               c2_hard=np.packbits(np.array([o.hard_decision for o in o2]), axis=1))
+    from polylp import Bsc, DecoderRef, stats_to_csv, sweep
+
+    rec["c1_csv_bp"] = np.array(stats_to_csv(sweep(rc, [Bsc(0.04), polylp.Awgn(2.0, rc.design_rate)],
+                                                   DecoderRef("bp", BpConfig(t_max=100)), n_trials=200,
+                                                   seed=109, workers=1), timing=False))
+    np.savez_compressed(OUT / "bp.npz", **rec)
+    print("bp: cfg1 mean iters", np.mean(it), "found", int(np.sum(fd)), "cfg2 found",
+          int(rec["c2_found"].sum()), "iters", rec["c2_iterations"])
+
+
 def main():
     projection_fixture()
     c1 = baseline_code("cfg1_n96")
@@ -170,5 +245,13 @@ def main():
     decode_fixture("decode_cfg4.npz", baseline_code("cfg4_n1040"), 4.0, 24, 24, AdmmConfig(mu=5.0))
 
 
+def main_bp():
+    bp_fixture()
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["bp"]:
+        main_bp()
+    else:
+        main()
+        bp_fixture()

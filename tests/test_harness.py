@@ -29,7 +29,10 @@ def test_merge_and_validation():
     with pytest.raises(ValueError):
         DecoderRef("nope")
     with pytest.raises(NotImplementedError):
-        DecoderRef("bp").admm_config()
+        DecoderRef("dual-ascent").admm_config()
+    from paper_1204_0556_b200 import BpConfig
+
+    assert DecoderRef("bp").admm_config() == BpConfig()
 
 
 @pytest.mark.gpu
