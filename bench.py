@@ -385,7 +385,7 @@ def run_ours(args, wl: Workload):
                          "kernel": kernel, "avg_launch_ms": launch_s * 1e3,
                          "note": "resident engines keep the edge state on chip, so the HBM-model bytes are never "
                                  "moved and frac > 1 is expected; `traffic` is ncu DRAM bytes per launch; the real "
-                                 "bound is SM instruction issue / latency (DESIGN.md 3.4)"},
+                                 "bound is SM instruction issue / latency (DESIGN.md 3.6)"},
             "gpu_launches": args.steps * n_launch,
             "clocks": clk,
             "e2e": e2e,
