@@ -435,7 +435,11 @@ __global__ void __launch_bounds__(ShardThreads<T>::value, 1) sharded_decode_kern
       g_phase_cycles[4] += tp5 - tp4;
       g_phase_cycles[5] += 1;
     }
-    grid.sync();
+    // No grid sync here: every cross-CTA read of the next pass is separated
+    // from the last write it depends on by the sync after its variable phase
+    // (p.part, the flag buffers, the weight/odd/non-integral counters of the
+    // slots that retired in this pass) or after this pass's check phase
+    // (messages, x).
   }
 }
 
