@@ -209,7 +209,7 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
           admm::ResidentLaunch L{};
           if (!admm::regular_lookup(dt, dmax, dvmax, cpt, need, nt, n_vars, variant, &vpt, &L)) break;
           const int smem = admm::regular_smem_bytes(dt ? 8 : 4, dmax, dvmax, n_vars, L.colored, L.gm_smem, nt, vpt,
-                                                    L.np_fixed);
+                                                    L.np_fixed, L.zs_cpt);
           ok = check_one(L, smem, nt);
           if (ok) Ls[dt] = L;
         }
@@ -235,20 +235,37 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
     // Two checks per thread first on the regular path: the second check's
     // independent instruction stream hides the sorting networks' ALU-pipe
     // bursts (measured +9 % over one check per thread on config 2).
+    // The regular path keeps the shape with the most resident fp32 warps per
+    // SM (ties: the order below), e.g. config 3: three checks per thread with
+    // the edge state in shared memory, 2 x 14 warps, over two checks per
+    // thread in registers, 1 x 21 warps.
     const int order_reg[4] = {2, 1, 3, 4}, order_gen[4] = {1, 2, 3, 4};
+    int best_cpt = 0, best_warps = 0;
     for (int cpt : (reg ? order_reg : order_gen)) {
       if (cpt_env && cpt != cpt_env) continue;  // tuning override
       const int nt = ((n_checks + cpt - 1) / cpt + 31) / 32 * 32;
       if (nt > (reg ? 1024 : 512)) continue;
       int vpt = 0;
       if (!try_shape(reg, cpt, nt, &vpt)) continue;
-      g->kind = reg ? 2 : 1;
-      g->CPT = cpt;
-      g->NT = nt;
-      g->m_pad = nt * cpt;
-      g->VPT = vpt;
-      placed = true;
-      break;
+      const int warps = g->launch[0].occupancy * nt / 32;
+      if (dbg) std::fprintf(stderr, "[admm] shape cpt=%d nt=%d: %d fp32 warps/SM\n", cpt, nt, warps);
+      if (warps > best_warps) {
+        best_warps = warps;
+        best_cpt = cpt;
+      }
+      if (!reg) break;  // generic kernels: first fit
+    }
+    if (best_cpt) {
+      const int nt = ((n_checks + best_cpt - 1) / best_cpt + 31) / 32 * 32;
+      int vpt = 0;
+      if (try_shape(reg, best_cpt, nt, &vpt)) {
+        g->kind = reg ? 2 : 1;
+        g->CPT = best_cpt;
+        g->NT = nt;
+        g->m_pad = nt * best_cpt;
+        g->VPT = vpt;
+        placed = true;
+      }
     }
   }
   if (!placed && regular && engine == ADMM_ENGINE_CLUSTER) {  // opt-in: DSMEM gathers measured slower than streaming

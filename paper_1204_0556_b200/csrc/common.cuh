@@ -98,6 +98,15 @@ __device__ __forceinline__ void sts(uint32_t a, float v) {
 __device__ __forceinline__ void sts(uint32_t a, double v) {
   asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
+// Four adjacent fp32 words (16-byte aligned address).
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts4(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
 // Two adjacent fp32 words (8-byte aligned address).
 __device__ __forceinline__ float2 lds2(uint32_t a) {
   float2 v;

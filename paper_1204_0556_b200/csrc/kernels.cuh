@@ -57,6 +57,7 @@ struct ResidentLaunch {
   bool colored;  // regular kernel on the colored message layout (layout.h)
   int np_fixed;  // compile-time padded variable count (0 = computed from n_vars)
   bool gm_smem;  // LLR steps in shared memory (regular_gm_smem)
+  int zs_cpt;    // > 0: edge state in shared memory for this many checks per thread
 };
 
 template <typename T>
@@ -103,10 +104,10 @@ void launch_resident(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int
   resident_decode_kernel<T, D, CPT, DVMAX><<<grid, nt, smem, st>>>(make_params<T>(g, a));
 }
 
-template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT, bool COL, int NPC, int NTC>
+template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT, bool COL, int NPC, int NTC, bool ZS>
 void launch_regular(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int grid, int nt, int smem,
                     cudaStream_t st) {
-  resident_regular_kernel<T, D, DV, CPT, VPT, MINB, MAXT, COL, NPC, NTC><<<grid, nt, smem, st>>>(
+  resident_regular_kernel<T, D, DV, CPT, VPT, MINB, MAXT, COL, NPC, NTC, ZS><<<grid, nt, smem, st>>>(
       make_params<T>(g, a), g.var_edge_int ? g.var_edge_int : g.var_edge);
 }
 

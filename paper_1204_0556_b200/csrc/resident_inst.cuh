@@ -40,11 +40,13 @@ bool resident_lookup_t(int D, int CPT, int DVMAX, ResidentLaunch* out) {
   return false;
 }
 
-template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT, bool COL, int NPC = 0, int NTC = 0>
+template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT, bool COL, int NPC = 0, int NTC = 0,
+          bool ZS = false>
 ResidentLaunch make_regular() {
   return ResidentLaunch{
-      reinterpret_cast<const void*>(&resident_regular_kernel<T, D, DV, CPT, VPT, MINB, MAXT, COL, NPC, NTC>),
-      &launch_regular<T, D, DV, CPT, VPT, MINB, MAXT, COL, NPC, NTC>, 0, 0, 0, COL, NPC, regular_gm_smem(COL, MINB)};
+      reinterpret_cast<const void*>(&resident_regular_kernel<T, D, DV, CPT, VPT, MINB, MAXT, COL, NPC, NTC, ZS>),
+      &launch_regular<T, D, DV, CPT, VPT, MINB, MAXT, COL, NPC, NTC, ZS>, 0, 0, 0, COL, NPC,
+      regular_gm_smem(COL, MINB), ZS ? CPT : 0};
 }
 
 // The compiled regular shapes (D, DV, CPT, VPT, MINB, MAXT, COL), in
@@ -77,7 +79,16 @@ bool regular_lookup_t(int D, int DV, int CPT, int VPT_min, int nt, int n_vars, i
     *out = make_regular<T, d, dv, cpt, vpt, minb, ntc, true, npc, ntc>();                     \
     return true;                                                                              \
   }
+  // ... with the edge state in shared memory (ZS)
+#define ADMM_REG_FIXED_ZS(d, dv, cpt, vpt, minb, npc, ntc)                                    \
+  if (D == d && DV == dv && CPT == cpt && VPT_min <= vpt && nt == ntc &&                      \
+      regular_np(n_vars, true, ntc, vpt) <= npc && seen++ == variant) {                       \
+    *VPT = vpt;                                                                               \
+    *out = make_regular<T, d, dv, cpt, vpt, minb, ntc, true, npc, ntc, true>();               \
+    return true;                                                                              \
+  }
   if constexpr (F32) {
+    ADMM_REG_FIXED_ZS(6, 3, 3, 6, 2, 2688, 448)
     ADMM_REG_FIXED(6, 3, 2, 4, 4, 1024, 256)
     ADMM_REG_FIXED(6, 3, 2, 4, 3, 1024, 256)
     ADMM_REG_FIXED(6, 3, 2, 4, 1, 2688, 672)
@@ -95,6 +106,7 @@ bool regular_lookup_t(int D, int DV, int CPT, int VPT_min, int nt, int n_vars, i
   ADMM_REG(4, 3, 1, 2, F32 ? 2 : 1, 512, false)
 #undef ADMM_REG
 #undef ADMM_REG_FIXED
+#undef ADMM_REG_FIXED_ZS
   return false;
 }
 

@@ -47,8 +47,12 @@ __host__ __device__ inline int regular_np(int n_vars, bool col, int nt, int vpt)
 // NPC / NTC > 0 fix the padded variable count and the CTA size at compile
 // time (COL only): every shared address in the hot loop is then a register
 // plus an immediate offset.
+// ZS keeps the edge state (z, lambda) in shared memory instead of registers
+// (colored fp32 kernels): zs[q][j][NT] float4 {z_2j, z_2j+1, l_2j, l_2j+1},
+// 16-byte accesses, conflict-free.  It buys registers for more resident warps
+// where the register file, not shared memory, caps the CTAs per SM.
 template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT = 512, bool COL = false, int NPC = 0,
-          int NTC = 0>
+          int NTC = 0, bool ZS = false>
 __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const ResidentParams<T> p,
                                                                      const int* __restrict__ var_edge) {
   static_assert(!COL || (D % DV == 0 && sizeof(T) == 4 && VPT % 2 == 0), "colored layout: fp32, DV | D, VPT even");
@@ -59,7 +63,11 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
   const int lane = tid & 31, warp = tid >> 5, nwarps = NT >> 5;
   const int NP = NPC ? NPC : COL ? regular_np(N, true, NT, VPT) : (N + 31) & ~31;
   constexpr int kRows = COL ? DV : D;  // message rows: colors (COL) or check slots
-  T* xs = reinterpret_cast<T*>(smem_raw);
+  static_assert(!ZS || (COL && D % 2 == 0), "shared-memory edge state: colored fp32 kernels");
+  const int zs_bytes = ZS ? CPT * (D / 2) * NT * 16 : 0;
+  const uint32_t zs_a = smem_u32(smem_raw) + 16u * tid;  // this thread's float4 column
+  auto zsa = [&](int q, int j) -> uint32_t { return zs_a + 16u * ((q * (D / 2) + j) * NT); };
+  T* xs = reinterpret_cast<T*>(smem_raw + zs_bytes);
   T* msg = xs + NP;
   // kGmSmem (colored kernels built for >= 4 CTAs/SM): the LLR steps gamma/mu
   // live in shared memory after the messages, read as pairs next to them --
@@ -117,14 +125,26 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
   // fp32 keeps the state as packed edge pairs (kPacked) so the loop-carried
   // registers are the FFMA2/FADD2 operand pairs themselves.
   T z[kPacked ? 1 : CPT][D], lam[kPacked ? 1 : CPT][D];
-  float2 zp[CPT][kPacked ? D / 2 : 1], lp[CPT][kPacked ? D / 2 : 1];
+  float2 zp[ZS ? 1 : CPT][kPacked && !ZS ? D / 2 : 1], lp[ZS ? 1 : CPT][kPacked && !ZS ? D / 2 : 1];
   auto zget = [&](int q, int k) -> T {
-    if constexpr (kPacked) return (k & 1) ? zp[q][k >> 1].y : zp[q][k >> 1].x;
-    else return z[q][k];
+    if constexpr (ZS) {
+      const float4 v = lds4(zsa(q, k >> 1));
+      return (k & 1) ? v.y : v.x;
+    } else if constexpr (kPacked) {
+      return (k & 1) ? zp[q][k >> 1].y : zp[q][k >> 1].x;
+    } else {
+      return z[q][k];
+    }
   };
   auto lget = [&](int q, int k) -> T {
-    if constexpr (kPacked) return (k & 1) ? lp[q][k >> 1].y : lp[q][k >> 1].x;
-    else return lam[q][k];
+    if constexpr (ZS) {
+      const float4 v = lds4(zsa(q, k >> 1));
+      return (k & 1) ? v.w : v.z;
+    } else if constexpr (kPacked) {
+      return (k & 1) ? lp[q][k >> 1].y : lp[q][k >> 1].x;
+    } else {
+      return lam[q][k];
+    }
   };
   T gm[kGmSmem ? 1 : VPT];
   const float2 rho2 = make_float2(float(p.rho), float(p.rho));
@@ -159,7 +179,17 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
           l0 = p.lam_in[e];
         }
         const T s0 = div_rn(l0, p.mu);
-        if constexpr (kPacked) {
+        if constexpr (ZS) {
+          // pairs are written once both halves are known
+          if (k & 1) {
+            zp[0][0].y = z0;
+            lp[0][0].y = s0;
+            sts4(zsa(q, k >> 1), make_float4(zp[0][0].x, z0, lp[0][0].x, s0));
+          } else {
+            zp[0][0].x = z0;
+            lp[0][0].x = s0;
+          }
+        } else if constexpr (kPacked) {
           if (k & 1) {
             zp[q][k >> 1].y = z0;
             lp[q][k >> 1].y = s0;
@@ -226,8 +256,14 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
 #pragma unroll
             for (int j = 0; j < D / 2; ++j) {
               gx2[j] = make_float2(lds(xaddr[q][2 * j], T()), lds(xaddr[q][2 * j + 1], T()));
-              z2[j] = zp[q][j];
-              l2[j] = lp[q][j];
+              if constexpr (ZS) {
+                const float4 v = lds4(zsa(q, j));
+                z2[j] = make_float2(v.x, v.y);
+                l2[j] = make_float2(v.z, v.w);
+              } else {
+                z2[j] = zp[q][j];
+                l2[j] = lp[q][j];
+              }
             }
             T u[D], zn[D];
 #pragma unroll
@@ -248,8 +284,12 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
               // throughput mode): w and l are dead once u is formed
               const float2 ln = fsub2_rn(u2[j], zn2);
               const float2 m2 = fsub2_rn(zn2, ln);
-              lp[q][j] = ln;
-              zp[q][j] = zn2;
+              if constexpr (ZS) {
+                sts4(zsa(q, j), make_float4(zn2.x, zn2.y, ln.x, ln.y));
+              } else {
+                lp[q][j] = ln;
+                zp[q][j] = zn2;
+              }
               sts(xaddr[q][2 * j] + moff(2 * j), m2.x);
               sts(xaddr[q][2 * j + 1] + moff(2 * j + 1), m2.y);
             }
@@ -357,9 +397,9 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
 // Shared memory of the regular kernel (bytes): x[Npad] | msg[rows][Npad] | red | ints,
 // rows = D (slot layout) or DV (colored layout).
 inline int regular_smem_bytes(int elem, int D, int DV, int n_vars, bool col, bool gm_smem, int nt, int vpt,
-                              int np_fixed = 0) {
+                              int np_fixed = 0, int zs_cpt = 0) {
   const int np = np_fixed ? np_fixed : regular_np(n_vars, col, nt, vpt);
-  return elem * (np + (col ? DV : D) * np + (gm_smem ? np : 0) + 64) + 16;
+  return zs_cpt * (D / 2) * nt * 16 + elem * (np + (col ? DV : D) * np + (gm_smem ? np : 0) + 64) + 16;
 }
 
 }  // namespace admm
