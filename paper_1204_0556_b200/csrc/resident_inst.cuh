@@ -46,7 +46,7 @@ ResidentLaunch make_regular() {
   return ResidentLaunch{
       reinterpret_cast<const void*>(&resident_regular_kernel<T, D, DV, CPT, VPT, MINB, MAXT, COL, NPC, NTC, ZS>),
       &launch_regular<T, D, DV, CPT, VPT, MINB, MAXT, COL, NPC, NTC, ZS>, 0, 0, 0, COL, NPC,
-      regular_gm_smem(COL, MINB), ZS ? CPT : 0};
+      regular_gm_smem(COL, MINB, ZS), ZS ? CPT : 0};
 }
 
 // The compiled regular shapes (D, DV, CPT, VPT, MINB, MAXT, COL), in
@@ -58,6 +58,10 @@ ResidentLaunch make_regular() {
 //     256-thread CTAs at 3 CTAs/SM (4 CTAs/SM = 64 registers spills: -8 %),
 //     then a 704-thread variant for codes with up to 1408
 //     checks (config 3);
+//   * shared-memory edge state (ZS) only where registers cap the CTAs per SM
+//     (config 3: 2 x 448 threads); on config 2 it measured slower at both 5
+//     CTAs/SM (712 G) and one check per thread (602 G) than 4 CTAs/SM with
+//     the state in registers (836 G);
 //   * the slot layout (per-edge message addresses) for everything else and
 //     for fp64, whose variable sums must follow the reference's edge order.
 template <typename T>

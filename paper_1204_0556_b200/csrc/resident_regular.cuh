@@ -36,7 +36,7 @@ struct MsgStride {
 // every idle thread slot (variables i >= N, checks c >= M) real storage so the
 // hot loop carries no activity predicates: idle variables occupy slots
 // [N, VPT * NT) and idle checks gather from / write to the spare slot N.
-__host__ __device__ constexpr bool regular_gm_smem(bool col, int minb) { return col && minb >= 4; }
+__host__ __device__ constexpr bool regular_gm_smem(bool col, int minb, bool zs = false) { return col && minb >= 4 && !zs; }
 
 __host__ __device__ inline int regular_np(int n_vars, bool col, int nt, int vpt) {
   if (!col) return (n_vars + 31) & ~31;
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
   // kGmSmem (colored kernels built for >= 4 CTAs/SM): the LLR steps gamma/mu
   // live in shared memory after the messages, read as pairs next to them --
   // four fewer registers (+1.5 % at 4 CTAs/SM; -3 % at one CTA per SM).
-  constexpr bool kGmSmem = regular_gm_smem(COL, MINB);
+  constexpr bool kGmSmem = regular_gm_smem(COL, MINB, ZS);
   T* red = msg + kRows * NP + (kGmSmem ? NP : 0);
   int* s_int = reinterpret_cast<int*>(red + 64);  // [0] frame, [1] weight
   const uint32_t msg_a = smem_u32(msg), xs_a = smem_u32(xs);
