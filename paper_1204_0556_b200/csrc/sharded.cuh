@@ -12,6 +12,10 @@
 //     phase C  gathers x, writes the message       (~8 B per edge-update)
 // versus ~31 B per edge-update when z and lambda also stream through memory.
 // Duals are kept scaled (lambda / mu, the reference's message-passing form).
+// The cross-CTA gathers use ld.global.cg: with ~205 KB of the unified L1 given
+// to shared memory, L1-allocating loads can only keep ~150 line misses in
+// flight per SM, while L2-only loads keep the whole batch in flight (an L2
+// round trip under full load is ~2.7k cycles, tools/micro/l2mlp.cu).
 //
 // Slot management is REPLICATED: every CTA keeps the slot states, iteration
 // counters and frame indices in its own shared memory and takes the same
@@ -157,7 +161,7 @@ __global__ void __launch_bounds__(ShardThreads<T>::value, 1) sharded_decode_kern
 #pragma unroll
           for (int q = 0; q < VB; ++q) {
             const int lv = lv0 + q * NWG;
-            xq[q] = lv < nb ? xcol[(vb0 + lv) * S] : T(0);
+            xq[q] = lv < nb ? __ldcg(xcol + (vb0 + lv) * S) : T(0);
           }
 #pragma unroll
           for (int q = 0; q < VB; ++q) {
@@ -188,7 +192,7 @@ __global__ void __launch_bounds__(ShardThreads<T>::value, 1) sharded_decode_kern
             for (int j = 0; j < DVMAX; ++j) {
               const int ev = inb ? ve_s[lv * DVMAX + j] : -1;
               degs[q] += ev >= 0;
-              mv[q][j] = (ev >= 0 && !fresh) ? mcol[ev] : T(0);
+              mv[q][j] = (ev >= 0 && !fresh) ? __ldcg(mcol + ev) : T(0);
             }
             if (!inb) {
               gq[q] = T(0);
@@ -274,7 +278,7 @@ __global__ void __launch_bounds__(ShardThreads<T>::value, 1) sharded_decode_kern
             for (int k = 0; k < D; ++k) dd += vo[k] >= 0;
           }
 #pragma unroll
-          for (int k = 0; k < D; ++k) dst[k] = (REG || k < dd) ? xcol[vo[k]] : T(0);
+          for (int k = 0; k < D; ++k) dst[k] = (REG || k < dd) ? __ldcg(xcol + vo[k]) : T(0);
         };
         if (wi < mb) gather(wi, gx_nx, d_nx);
         for (int lc = wi; lc < mb; lc += NWG) {
