@@ -23,11 +23,16 @@ template <> struct Num<double> {
 };
 
 __device__ __forceinline__ float clip01(float v) { return __saturatef(v); }  // [0,1]; -inf -> 0
-__device__ __forceinline__ double clip01(double v) { return fmin(fmax(v, 0.0), 1.0); }
+// fp64 min/max as compare + select: CUDA's fmin/fmax for double carry NaN
+// semantics that expand to DSETP.MIN/MAX + SEL + FSEL + LOP3 and register
+// moves (~3x the instructions of the whole projection); the decoder never
+// sees NaNs, and for non-NaN inputs the results are identical in value (only
+// the sign of a zero may differ, which no later operation observes).
+__device__ __forceinline__ double clip01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
 __device__ __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
 __device__ __forceinline__ float vmin(float a, float b) { return fminf(a, b); }
-__device__ __forceinline__ double vmax(double a, double b) { return fmax(a, b); }
-__device__ __forceinline__ double vmin(double a, double b) { return fmin(a, b); }
+__device__ __forceinline__ double vmax(double a, double b) { return a > b ? a : b; }
+__device__ __forceinline__ double vmin(double a, double b) { return a < b ? a : b; }
 
 // Compare-exchange primitives used by the generated sorting networks.
 template <typename T> __device__ __forceinline__ void ce_desc(T& a, T& b) {
@@ -37,6 +42,19 @@ template <typename T> __device__ __forceinline__ void ce_desc(T& a, T& b) {
 }
 template <typename T> __device__ __forceinline__ void ce_asc(T& a, T& b) {
   const T lo = vmin(a, b), hi = vmax(a, b);
+  a = lo;
+  b = hi;
+}
+// fp64: one comparison drives both selects
+template <> __device__ __forceinline__ void ce_desc<double>(double& a, double& b) {
+  const bool sw = a < b;
+  const double hi = sw ? b : a, lo = sw ? a : b;
+  a = hi;
+  b = lo;
+}
+template <> __device__ __forceinline__ void ce_asc<double>(double& a, double& b) {
+  const bool sw = b < a;
+  const double lo = sw ? b : a, hi = sw ? a : b;
   a = lo;
   b = hi;
 }
