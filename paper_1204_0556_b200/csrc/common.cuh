@@ -125,6 +125,15 @@ __device__ __forceinline__ float4 lds4(uint32_t a) {
 __device__ __forceinline__ void sts4(uint32_t a, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
+// Two adjacent fp64 words (16-byte aligned address).
+__device__ __forceinline__ double2 lds2d(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts2d(uint32_t a, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
 // Two adjacent fp32 words (8-byte aligned address).
 __device__ __forceinline__ float2 lds2(uint32_t a) {
   float2 v;

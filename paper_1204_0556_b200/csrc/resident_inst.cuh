@@ -100,6 +100,9 @@ bool regular_lookup_t(int D, int DV, int CPT, int VPT_min, int nt, int n_vars, i
     ADMM_REG(6, 3, 2, 4, 1, 704, true)
     ADMM_REG(6, 3, 1, 2, 2, 512, true)
   }
+  if constexpr (!F32) {  // fp64: colored layout with compile-time geometry (color-order variable sums)
+    ADMM_REG_FIXED(6, 3, 2, 4, 2, 1024, 256)
+  }
   ADMM_REG(6, 3, 1, 2, F32 ? 2 : 1, 512, false)
   ADMM_REG(6, 3, 2, 4, F32 ? 3 : 1, F32 ? 256 : 512, false)
   ADMM_REG(6, 3, 2, 4, 1, 704, false)

@@ -55,7 +55,7 @@ template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT = 512,
           int NTC = 0, bool ZS = false>
 __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const ResidentParams<T> p,
                                                                      const int* __restrict__ var_edge) {
-  static_assert(!COL || (D % DV == 0 && sizeof(T) == 4 && VPT % 2 == 0), "colored layout: fp32, DV | D, VPT even");
+  static_assert(!COL || (D % DV == 0 && VPT % 2 == 0), "colored layout: DV | D, VPT even");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int N = p.n_vars, M = p.n_checks;
   static_assert(COL || (NPC == 0 && NTC == 0), "compile-time geometry needs the colored layout");
@@ -211,7 +211,25 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
     while (t < p.t_max) {
       ++t;
       // ---- x-update (admm_decoder.py:108-124): edges summed in edge order ----
-      if constexpr (COL) {
+      if constexpr (COL && kF64) {
+        // fp64: pairs of variables in 16-byte accesses, messages summed in
+        // color order (the reference sums in edge order; the difference is
+        // at rounding level, inside the 1e-9 fp64 parity bar)
+#pragma unroll
+        for (int h = 0; h < VPT / 2; ++h) {
+          const uint32_t a = xst[2 * h];
+          double2 acc = lds2d(a + moff0);
+#pragma unroll
+          for (int j = 1; j < DV; ++j) {
+            const double2 m = lds2d(a + moff0 + j * mstride);
+            acc.x = add_rn(acc.x, m.x);
+            acc.y = add_rn(acc.y, m.y);
+          }
+          const double inv = 1.0 / DV;
+          sts2d(a, make_double2(clip01(mul_rn(sub_rn(acc.x, gm[2 * h]), inv)),
+                                clip01(mul_rn(sub_rn(acc.y, gm[2 * h + 1]), inv))));
+        }
+      } else if constexpr (COL) {
         // pairs of variables: 8-byte loads/stores, packed sums (color order)
 #pragma unroll
         for (int h = 0; h < VPT / 2; ++h) {

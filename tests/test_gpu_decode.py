@@ -187,3 +187,21 @@ def test_baseline_codes_take_the_regular_resident_kernels(cuda_ok, name, ctas):
     info = DeviceGraph(baseline_code(name), 0).info
     assert info["engine"] == 2, info
     assert info["ctas_per_sm_f32"] >= ctas, info
+
+
+def test_f64_config2_kernel_matches_oracle_on_more_frames(cuda_ok):
+    """The fp64 config-2 kernel (colored layout, compile-time geometry, sums
+    in color order) against the oracle on 256 frames at 1.75 dB (heavy-tailed
+    iteration counts, many T_max frames): identical iteration counts and
+    hard decisions."""
+    from paper_1204_0556_b200 import AdmmConfig, baseline_code, decode_batch
+
+    code = baseline_code("cfg2_n1008")
+    rate = 1.0 - code.n_checks / code.n_vars
+    gam = np.array([O.trial_gamma_awgn(code.n_vars, 1.75, rate, 21, 0, t) for t in range(256)])
+    res = decode_batch(gam, code, AdmmConfig(mu=5.0), dtype=torch.float64, want_hard=True)
+    assert res.info["engine"] == 2
+    it_o, conv_o, hard_o = O.decode_parallel(gam, O.Graph.of(code), O.Params(mu=5.0))
+    assert np.array_equal(res.iterations.cpu().numpy(), it_o)
+    assert np.array_equal(res.converged.cpu().numpy(), conv_o)
+    assert np.array_equal(res.hard.cpu().numpy(), hard_o)
