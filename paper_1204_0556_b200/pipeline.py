@@ -5,8 +5,11 @@ and returns host results per block, overlapping three streams:
 
     copy-in  (H2D of block i+1)  |  decode (block i)  |  copy-out (D2H of block i-1)
 
-Device buffers are allocated once (two input slots, two output slots), so
-the steady state allocates nothing.  This is the batched counterpart of the
+Device buffers are allocated once (two input slots, two output slots).  With
+``reuse_outputs=True`` the pinned host result buffers are allocated once per
+chunk position and reused by the next ``run`` (results stay valid until
+then), so the steady state allocates nothing -- pinned allocations are
+synchronous and cost milliseconds each.  This is the batched counterpart of the
 reference's per-trial loop ``decode_fn(gamma)`` (simulator.py:172-177),
 where the host produces LLRs and consumes hard decisions.
 """
@@ -32,7 +35,7 @@ class HostResult:
 
 class HostPipeline:
     def __init__(self, code, config: AdmmConfig, *, dtype=torch.float32, device=None, max_batch: int,
-                 want_hard: bool = True):
+                 want_hard: bool = True, reuse_outputs: bool = False):
         self.code = as_code(code)
         self.cfg = config
         self.dev = torch.device(device if device is not None else "cuda")
@@ -52,6 +55,22 @@ class HostPipeline:
         self.ws = mk(ws, dt=torch.uint8)
         self.s_in = torch.cuda.Stream(self.dev)
         self.s_out = torch.cuda.Stream(self.dev)
+        self.reuse_outputs = reuse_outputs
+        self._host_out: dict[tuple[int, int], HostResult] = {}
+
+    def _host_result(self, i: int, B: int) -> HostResult:
+        key = (i, B)
+        if self.reuse_outputs and key in self._host_out:
+            return self._host_out[key]
+        res = HostResult(
+            iterations=torch.empty(B, dtype=torch.int32, pin_memory=True),
+            flags=torch.empty(B, dtype=torch.uint8, pin_memory=True),
+            weight=torch.empty(B, dtype=torch.int32, pin_memory=True),
+            hard=torch.empty((B, self.code.n_vars), dtype=torch.uint8, pin_memory=True)
+            if self.want_hard else None)
+        if self.reuse_outputs:
+            self._host_out[key] = res
+        return res
 
     def h2d_bytes_per_run(self, chunks) -> int:
         return sum(c.shape[0] * c.shape[1] * torch.tensor([], dtype=self.tdt).element_size() for c in chunks)
@@ -88,14 +107,9 @@ class HostPipeline:
             ev = torch.cuda.Event()
             ev.record(comp)
             slot_free[k] = ev
+            res = self._host_result(i, B)
             with torch.cuda.stream(self.s_out):
                 self.s_out.wait_event(ev)
-                res = HostResult(
-                    iterations=torch.empty(B, dtype=torch.int32, pin_memory=True),
-                    flags=torch.empty(B, dtype=torch.uint8, pin_memory=True),
-                    weight=torch.empty(B, dtype=torch.int32, pin_memory=True),
-                    hard=torch.empty((B, self.code.n_vars), dtype=torch.uint8, pin_memory=True)
-                    if self.want_hard else None)
                 res.iterations.copy_(self.iters[k][:B], non_blocking=True)
                 res.flags.copy_(self.flags[k][:B], non_blocking=True)
                 res.weight.copy_(self.weight[k][:B], non_blocking=True)

@@ -34,3 +34,23 @@ def test_host_pipeline_matches_decode_batch(cuda_ok, dtype):
     assert all(torch.equal(a.hard, b.hard) for a, b in zip(out, out2))
     with pytest.raises(ValueError):
         pipe.run([torch.zeros((601, code.n_vars), dtype=dtype).pin_memory()])
+
+
+def test_host_pipeline_reused_outputs(cuda_ok):
+    from paper_1204_0556_b200 import AdmmConfig, baseline_code, decode_batch
+    from paper_1204_0556_b200.channels import awgn_gammas_device
+    from paper_1204_0556_b200.pipeline import HostPipeline
+
+    code = baseline_code("cfg1_n96")
+    g = awgn_gammas_device(200, code.n_vars, 2.0, code.design_rate, seed=4, dtype=torch.float32)
+    host = [g[:120].cpu().pin_memory(), g[120:].cpu().pin_memory()]
+    pipe = HostPipeline(code, AdmmConfig(mu=5.0), dtype=torch.float32, max_batch=128, reuse_outputs=True)
+    a = pipe.run(host)
+    torch.cuda.synchronize()
+    first = [r.hard.clone() for r in a]
+    b = pipe.run(host)
+    torch.cuda.synchronize()
+    assert all(x.hard.data_ptr() == y.hard.data_ptr() for x, y in zip(a, b))  # buffers reused
+    ref = decode_batch(g, code, AdmmConfig(mu=5.0), dtype=torch.float32, want_x=False, want_hard=True)
+    assert torch.equal(torch.cat([r.hard for r in b]), ref.hard.cpu())
+    assert all(torch.equal(x, y.hard) for x, y in zip(first, b))
