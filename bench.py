@@ -80,6 +80,7 @@ def parse():
     ap.add_argument("--frames", type=int, default=0, help="frames per point (0 = the workload's)")
     ap.add_argument("--chunk", type=int, default=65536, help="frames per decode call (synth workloads)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-block", type=int, default=65536, help="frames per host block of the e2e pipeline")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--cpu-frames", type=int, default=0, help="oracle frames per point (0 = auto)")
     return ap.parse_args()
@@ -336,8 +337,11 @@ def run_ours(args, wl: Workload):
     # e2e through the pipelined host API (memory workloads)
     e2e = None
     if not args.no_e2e and gam is not None:
-        pipe = HostPipeline(code, cfg, dtype=tdt, device=dev, max_batch=F, reuse_outputs=True)
-        host = [g.cpu().pin_memory() for g in gam]
+        # host blocks of --e2e-block frames: a short pipeline fill (first H2D)
+        # and drain (last D2H) per step
+        blk = min(F, args.e2e_block)
+        pipe = HostPipeline(code, cfg, dtype=tdt, device=dev, max_batch=blk, reuse_outputs=True)
+        host = [h for g in gam for h in g.cpu().pin_memory().split(blk)]
         pipe.run(host)  # warm-up: allocates the pinned result buffers reused by the timed runs
         torch.cuda.synchronize(dev)
         if world > 1:
