@@ -64,6 +64,7 @@ struct admm_graph {
   int* cchk_var = nullptr;       // colored layout (fp32 regular kernels with DV | D)
   int* cvar_orig = nullptr;
   int* cedge_ref = nullptr;
+  int* ccheck_rot = nullptr;     // colored layout, D mod DV = 1: per-check rotation
   int* chk_var_ref = nullptr;    // original numbering when chk_var is relabeled (kind 2), else == chk_var
   // BP (bp.cuh): its own CTA shape on the same graph arrays
   admm::BpLaunch bp_launch[2];
@@ -518,6 +519,11 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
     cudaError_t c1 = up((void**)&g->cchk_var, chk2.data(), chk2.size() * sizeof(int));
     cudaError_t c2 = up((void**)&g->cvar_orig, vorig.data(), vorig.size() * sizeof(int));
     cudaError_t c3 = up((void**)&g->cedge_ref, eref.data(), eref.size() * sizeof(int));
+    if (c3 == cudaSuccess && dmax % dvmax != 0) {
+      std::vector<int> rot((size_t)MP, 0);
+      for (int c = 0; c < n_checks; ++c) rot[c] = lay.check_rot[c];
+      c3 = up((void**)&g->ccheck_rot, rot.data(), rot.size() * sizeof(int));
+    }
     if (e6 == cudaSuccess) e6 = c1;
     if (e7 == cudaSuccess) e7 = c2;
     if (e8 == cudaSuccess) e8 = c3;
@@ -546,6 +552,7 @@ int admm_graph_destroy(admm_graph* g) {
   cudaFree(g->cchk_var);
   cudaFree(g->cvar_orig);
   cudaFree(g->cedge_ref);
+  cudaFree(g->ccheck_rot);
   if (g->chk_var_ref != g->chk_var) cudaFree(g->chk_var_ref);
   delete g;
   return ADMM_OK;
@@ -735,6 +742,7 @@ int decode_impl(const admm_graph* g, int dtype, int64_t batch, const void* gamma
     ga.var_orig = g->cvar_orig;
     ga.edge_ref = g->cedge_ref;
     ga.var_edge_int = nullptr;
+    ga.check_rot = g->ccheck_rot;
   }
   admm::ResidentFrameArgs fa{batch, gamma, ld_gamma, mu, rho, thr, t_max, z_in, lam_in, ld_edge,
                              x_out, ld_x, hard_out, ld_hard, iters_out, flags_out, weight_out,

@@ -23,6 +23,7 @@ struct ResidentGraphArgs {
   const int* var_orig;  // relabeled regular layout (layout.h), may be null
   const int* edge_ref;
   const int* var_edge_int;  // relabeled: [internal var][DV] internal edge c*D + k
+  const int* check_rot;     // colored layout rotations (null = none)
 };
 
 struct ResidentFrameArgs {
@@ -72,6 +73,7 @@ ResidentParams<T> make_params(const ResidentGraphArgs& g, const ResidentFrameArg
   p.edge_base = g.edge_base;
   p.var_orig = g.var_orig;
   p.edge_ref = g.edge_ref;
+  p.check_rot = g.check_rot;
   p.batch = a.batch;
   p.gamma = static_cast<const T*>(a.gamma);
   p.ld_gamma = a.ld_gamma;

@@ -35,6 +35,7 @@ struct Layout {
   std::vector<int> var_of_slot;  // internal var index -> original var
   std::vector<int> slot_of_var;  // original var -> internal var index
   std::vector<int> edge_slot;    // per original edge (c*D + sorted position): slot k inside check c
+  std::vector<int> check_rot;    // colored layout: rotation r_c (slot k has color (k + r_c) mod DV)
   double cost_before = 0, cost_after = 0;
   int clashes = 0;               // variables with two edges in one slot (must be 0 to use the layout)
   int max_wavefronts = 0;        // worst column after optimisation
@@ -159,18 +160,23 @@ inline Layout optimize_layout(const std::vector<std::vector<int>>& rows, int n_v
 }
 
 
-// Colored layout for regular codes with DV | D (the (3,6) codes): every edge
-// gets a color j in [0, DV) such that each variable has one edge of every
-// color and each check D/DV edges of every color, and the edges of color j
-// sit in the check slots k = j (mod DV).  The message of edge (c, v) of color
-// j is then stored at msgc[j][pi(v)]: a variable reads its messages at
-// compile-time offsets from its own x slot and a check writes slot k at a
-// compile-time offset from the x-gather address -- no per-edge addresses are
-// held anywhere.  Such a coloring always exists: split every check into D/DV
-// copies of degree DV; the resulting DV-regular bipartite graph is the union
-// of DV perfect matchings (Koenig), color j = the j-th matching.  The
-// annealer then moves variables (pi) and swaps same-color slots of one check
-// to spread every (check-warp, slot) column over the 32 banks.
+// Colored layout for regular codes with D = q DV + rem, rem in {0, 1} (the
+// (3,6) and (3,13) codes): every edge gets a color j in [0, DV) such that
+// each variable has one edge of every color and each check q edges of every
+// color plus, when rem = 1, one more edge of its ROTATION color r_c; the
+// check's color-j edges sit in the slots k with (k + r_c) mod DV = j.  The
+// message of edge (c, v) of color j is stored at msgc[j][pi(v)]: a variable
+// reads its messages at compile-time offsets from its own x slot and a check
+// writes slot k at offset (k + r_c) mod DV from the address it gathered x
+// from -- no per-edge message addresses anywhere.
+//
+// Existence (Koenig): split every check into q copies of degree DV and, when
+// rem = 1, one copy of degree 1 padded with DV - 1 edges to M (DV - 1) / DV
+// dummy variables of degree DV.  The result is a DV-regular bipartite
+// multigraph, i.e. the union of DV perfect matchings; color j = matching j,
+// and r_c = the color of the check's degree-1 copy.  The annealer then moves
+// variables (pi) and swaps same-color slots of one check to spread every
+// (check-warp, slot) column over the 32 banks.
 inline bool match_dfs(int v, const std::vector<std::vector<int>>& adj, const std::vector<char>& used_edge,
                       const std::vector<int>& edge_copy, std::vector<int>& copy_match, std::vector<int>& seen,
                       int stamp, std::vector<int>& var_match_edge) {
@@ -189,14 +195,27 @@ inline bool match_dfs(int v, const std::vector<std::vector<int>>& adj, const std
   return false;
 }
 
+inline bool colored_layout_supported(int M, int D, int DV) {
+  const int rem = D % DV;
+  return DV >= 1 && D >= DV && (rem == 0 || (rem == 1 && (M * (DV - 1)) % DV == 0));
+}
+
 inline Layout optimize_colored_layout(const std::vector<std::vector<int>>& rows, int n_vars, int D, int DV,
                                       long long moves, uint64_t seed) {
   const int M = static_cast<int>(rows.size());
-  const int E = M * D, R = D / DV, NCOPY = M * R;
+  const int E = M * D, Q = D / DV, rem = D % DV;
   Layout L;
+  if (!colored_layout_supported(M, D, DV)) {
+    L.clashes = 1;
+    return L;
+  }
   std::mt19937_64 rng(seed);
-  std::vector<int> ev(E), ec(E), edge_copy(E), color(E, -1);
-  std::vector<std::vector<int>> adj(n_vars);
+  const int CPC = Q + (rem ? 1 : 0);           // copies per check
+  const int NCOPY = M * CPC;
+  const int ND = rem ? M * (DV - 1) / DV : 0;  // dummy variables
+  const int ED = rem ? M * (DV - 1) : 0;       // dummy edges
+  std::vector<int> ev(E + ED), ec(E), edge_copy(E + ED), color(E + ED, -1);
+  std::vector<std::vector<int>> adj(n_vars + ND);
   for (int c = 0; c < M; ++c) {
     std::vector<int> perm(D);
     for (int r = 0; r < D; ++r) perm[r] = r;
@@ -205,35 +224,54 @@ inline Layout optimize_colored_layout(const std::vector<std::vector<int>>& rows,
       const int e = c * D + r;
       ev[e] = rows[c][r];
       ec[e] = c;
-      edge_copy[e] = c * R + perm[r] / DV;
+      edge_copy[e] = c * CPC + perm[r] / DV;  // perm == D - 1 (rem = 1) -> the degree-1 copy
       adj[ev[e]].push_back(e);
     }
   }
-  // DV successive perfect matchings between variables and check copies.
-  std::vector<char> used(E, 0);
+  for (int t = 0; t < ED; ++t) {  // pad every degree-1 copy with DV - 1 dummy edges
+    const int c = t / (DV - 1), e = E + t, d = n_vars + t / DV;
+    ev[e] = d;
+    edge_copy[e] = c * CPC + Q;
+    adj[d].push_back(e);
+  }
+  // DV successive perfect matchings of the DV-regular multigraph.
+  const int NL = n_vars + ND;
+  std::vector<char> used(E + ED, 0);
   std::vector<int> seen(NCOPY, -1);
   int stamp = 0;
   for (int j = 0; j < DV; ++j) {
-    std::vector<int> copy_match(NCOPY, -1), var_edge(n_vars, -1);
-    for (int v = 0; v < n_vars; ++v) {
+    std::vector<int> copy_match(NCOPY, -1), var_edge(NL, -1);
+    for (int v = 0; v < NL; ++v) {
       if (!match_dfs(v, adj, used, edge_copy, copy_match, seen, stamp++, var_edge)) {
-        L.clashes = 1;  // cannot happen for a biregular graph with DV | D
+        L.clashes = 1;  // cannot happen for a biregular graph (Koenig)
         return L;
       }
     }
-    for (int v = 0; v < n_vars; ++v) {
+    for (int v = 0; v < NL; ++v) {
       used[var_edge[v]] = 1;
       color[var_edge[v]] = j;
     }
   }
-  // Slots: the color-j edges of check c take slots j, j + DV, j + 2 DV, ...
+  // Rotations and slots: the color-j edges of check c take the slots k with
+  // (k + r_c) mod DV == j, in increasing k.
+  L.check_rot.assign(M, 0);
+  if (rem)
+    for (int e = 0; e < E; ++e)
+      if (edge_copy[e] == ec[e] * CPC + Q) L.check_rot[ec[e]] = color[e];
   L.edge_slot.assign(E, -1);
   std::vector<int> slot_edge(E);
+  std::vector<std::vector<std::vector<int>>> color_slots(M);  // [c][j] -> slots
   for (int c = 0; c < M; ++c) {
-    int fill[32] = {0};
+    color_slots[c].assign(DV, {});
+    for (int k = 0; k < D; ++k) color_slots[c][(k + L.check_rot[c]) % DV].push_back(k);
+    std::vector<int> fill(DV, 0);
     for (int r = 0; r < D; ++r) {
       const int e = c * D + r, j = color[e];
-      const int k = j + DV * fill[j]++;
+      if (fill[j] >= static_cast<int>(color_slots[c][j].size())) {
+        L.clashes = 1;
+        return L;
+      }
+      const int k = color_slots[c][j][fill[j]++];
       L.edge_slot[e] = k;
       slot_edge[c * D + k] = e;
     }
@@ -264,7 +302,7 @@ inline Layout optimize_colored_layout(const std::vector<std::vector<int>>& rows,
   const double decay = std::pow(0.02 / T, 1.0 / static_cast<double>(std::max<long long>(1, moves)));
   for (long long it = 0; it < moves; ++it, T *= decay) {
     double delta = 0;
-    if (R < 2 || (rng() & 1)) {
+    if (Q < 2 || (rng() & 1)) {
       const int v1 = static_cast<int>(rng() % n_vars), v2 = static_cast<int>(rng() % n_vars);
       if (v1 == v2) continue;
       const int s1 = L.slot_of_var[v1], s2 = L.slot_of_var[v2];
@@ -291,10 +329,10 @@ inline Layout optimize_colored_layout(const std::vector<std::vector<int>>& rows,
     } else {
       // swap two same-color slots of one check
       const int c = static_cast<int>(rng() % M);
-      const int j = static_cast<int>(rng() % DV);
-      const int a = static_cast<int>(rng() % R), b = static_cast<int>(rng() % R);
+      const std::vector<int>& cs = color_slots[c][rng() % DV];
+      const int a = static_cast<int>(rng() % cs.size()), b = static_cast<int>(rng() % cs.size());
       if (a == b) continue;
-      const int k1 = j + DV * a, k2 = j + DV * b;
+      const int k1 = cs[a], k2 = cs[b];
       const int e1 = slot_edge[c * D + k1], e2 = slot_edge[c * D + k2];
       const int b1 = L.slot_of_var[ev[e1]] & 31, b2 = L.slot_of_var[ev[e2]] & 31;
       auto apply = [&](int ka, int kb, double& d) {

@@ -41,6 +41,7 @@ struct ResidentParams {
   const int* edge_base;       // [n_checks]  reference edge id of slot 0 (check_ptr)
   const int* var_orig;        // regular kernel: internal variable -> original variable (null = identity)
   const int* edge_ref;        // regular kernel: [check][D] reference edge id of slot k (null = c*D + k)
+  const int* check_rot;       // colored regular kernel, D mod DV = 1: rotation of each check (null = 0)
   // frames
   long long batch;
   const T* gamma;

@@ -96,6 +96,7 @@ bool regular_lookup_t(int D, int DV, int CPT, int VPT_min, int nt, int n_vars, i
     ADMM_REG_FIXED(6, 3, 2, 4, 4, 1024, 256)
     ADMM_REG_FIXED(6, 3, 2, 4, 3, 1024, 256)
     ADMM_REG_FIXED(6, 3, 2, 4, 1, 2688, 672)
+    ADMM_REG_FIXED(13, 3, 1, 6, 2, 1536, 256)
     ADMM_REG(6, 3, 2, 4, 3, 256, true)
     ADMM_REG(6, 3, 2, 4, 1, 704, true)
     ADMM_REG(6, 3, 1, 2, 2, 512, true)

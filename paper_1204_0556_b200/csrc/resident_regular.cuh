@@ -55,7 +55,7 @@ template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT = 512,
           int NTC = 0, bool ZS = false>
 __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const ResidentParams<T> p,
                                                                      const int* __restrict__ var_edge) {
-  static_assert(!COL || (D % DV == 0 && VPT % 2 == 0), "colored layout: DV | D, VPT even");
+  static_assert(!COL || (D % DV <= 1 && VPT % 2 == 0), "colored layout: D mod DV in {0, 1}, VPT even");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int N = p.n_vars, M = p.n_checks;
   static_assert(COL || (NPC == 0 && NTC == 0), "compile-time geometry needs the colored layout");
@@ -79,8 +79,16 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
   constexpr uint32_t ES = sizeof(T);
   // msg[k][pi(v)] sits at x-address of v + moff(k)
   const uint32_t moff0 = NPC ? ES * NPC : msg_a - xs_a, mstride = ES * NP;
-  // shared-address offset of the message of check slot k from the x slot of its variable
-  auto moff = [&](int k) -> uint32_t { return moff0 + (COL ? k % DV : k) * mstride; };
+  // kRot: colored layout with D = q DV + 1 (the (3,13) code): slot k of a
+  // check with rotation r has color (k + r) mod DV, so each check keeps its
+  // DV color offsets in registers (rot_off).
+  constexpr bool kRot = COL && (D % DV != 0);
+  uint32_t rot_off[CPT][kRot ? DV : 1];
+  // shared-address offset of the message of slot k of check q from the x slot of its variable
+  auto moff = [&](int q, int k) -> uint32_t {
+    if constexpr (kRot) return rot_off[q][k % DV];
+    else return moff0 + (COL ? k % DV : k) * mstride;
+  };
 
   // ---- per-thread graph registers (once per CTA) ----
   uint32_t xaddr[CPT][D];
@@ -89,6 +97,11 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
   for (int q = 0; q < CPT; ++q) {
     const int c = tid + q * NT;
     cact[q] = c < M;
+    if constexpr (kRot) {
+      const int r = cact[q] && p.check_rot ? __ldg(p.check_rot + c) : 0;
+#pragma unroll
+      for (int j = 0; j < DV; ++j) rot_off[q][j] = moff0 + ((j + r) % DV) * mstride;
+    }
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       const int v = cact[q] ? __ldg(p.chk_var + k * p.m_pad + c) : (COL ? N : 0);  // internal variable
@@ -201,7 +214,7 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
           z[q][k] = z0;
           lam[q][k] = s0;
         }
-        if (cact[q]) sts(xaddr[q][k] + moff(k), sub_rn(z0, s0));
+        if (cact[q]) sts(xaddr[q][k] + moff(q, k), sub_rn(z0, s0));
       }
     }
     __syncthreads();
@@ -308,8 +321,8 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
                 lp[q][j] = ln;
                 zp[q][j] = zn2;
               }
-              sts(xaddr[q][2 * j] + moff(2 * j), m2.x);
-              sts(xaddr[q][2 * j + 1] + moff(2 * j + 1), m2.y);
+              sts(xaddr[q][2 * j] + moff(q, 2 * j), m2.x);
+              sts(xaddr[q][2 * j + 1] + moff(q, 2 * j + 1), m2.y);
             }
           }
           if (COL && !cact[q]) {
@@ -340,7 +353,7 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
             moved = add_rn(moved, mul_rn(r2, r2));
             lam[kPacked ? 0 : q][k] = add_rn(lam[kPacked ? 0 : q][k], sub_rn(w[k], zn[k]));
             z[kPacked ? 0 : q][k] = zn[k];
-            sts(xaddr[q][k] + moff(k), sub_rn(zn[k], lam[kPacked ? 0 : q][k]));
+            sts(xaddr[q][k] + moff(q, k), sub_rn(zn[k], lam[kPacked ? 0 : q][k]));
           }
         }
       }

@@ -205,3 +205,25 @@ def test_f64_config2_kernel_matches_oracle_on_more_frames(cuda_ok):
     assert np.array_equal(res.iterations.cpu().numpy(), it_o)
     assert np.array_equal(res.converged.cpu().numpy(), conv_o)
     assert np.array_equal(res.hard.cpu().numpy(), hard_o)
+
+
+@pytest.mark.parametrize("name,snr", [("cfg2_n1008", 2.0), ("cfg3_n2640", 2.0), ("cfg4_n1040", 4.0)])
+def test_f32_kernels_of_the_baseline_shapes_match_f64(cuda_ok, name, snr):
+    """The fp32 fast paths that only the BASELINE shapes take (compile-time
+    geometry, colored / rotated-colored layouts, shared-memory edge state):
+    >= 99.9 % identical hard decisions against the fp64 parity mode on 4096
+    frames, frame errors within 2 standard errors."""
+    from paper_1204_0556_b200 import AdmmConfig, Awgn, baseline_code, decode_batch, synth_llr
+
+    code = baseline_code(name)
+    cfg = AdmmConfig(mu=5.0)
+    g64 = synth_llr(code.n_vars, Awgn(snr, code.design_rate), seed=17, point=0, trial0=0, batch=4096,
+                    dtype=torch.float64)
+    r64 = decode_batch(g64, code, cfg, dtype=torch.float64, want_x=False, want_hard=True)
+    r32 = decode_batch(g64.float(), code, cfg, dtype=torch.float32, want_x=False, want_hard=True)
+    h64, h32 = r64.hard.cpu().numpy(), r32.hard.cpu().numpy()
+    assert (h64 == h32).all(axis=1).mean() >= 0.999
+    n = len(h64)
+    fe32, fe64 = int((h32.sum(1) > 0).sum()), int((h64.sum(1) > 0).sum())
+    w = max(fe64, 1) / n
+    assert abs(fe32 - fe64) / n <= 2 * np.sqrt(2 * w * (1 - w) / n) + 1e-3
