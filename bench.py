@@ -332,7 +332,7 @@ def run_ours(args, wl: Workload):
         except Exception:
             traffic = None
     kernel = {1: "resident_decode_kernel", 2: "resident_regular_kernel", 3: "sharded_decode_kernel",
-              4: "cluster_decode_kernel"}.get(info.get("engine"), "?")
+              4: "cluster_decode_kernel", 5: "wide_decode_kernel"}.get(info.get("kernel", info.get("engine")), "?")
 
     # e2e through the pipelined host API (memory workloads)
     e2e = None

@@ -51,7 +51,17 @@ enum admm_engine {
   ADMM_ENGINE_AUTO = 0,      /* resident if the code fits one SM, else streaming */
   ADMM_ENGINE_RESIDENT = 1,  /* one CTA per frame, state on chip (fails if it does not fit) */
   ADMM_ENGINE_STREAMING = 3, /* batch-interleaved L2-resident state, cooperative kernel */
-  ADMM_ENGINE_CLUSTER = 4    /* one thread-block cluster per frame, DSMEM gathers (regular codes) */
+  ADMM_ENGINE_CLUSTER = 4,   /* one thread-block cluster per frame, DSMEM gathers (regular codes) */
+  ADMM_ENGINE_WIDE = 5       /* streaming placement, wide HBM-streaming kernel for every batch size */
+};
+
+/* Kernel ids reported by admm_decode_kernel. */
+enum admm_kernel {
+  ADMM_KERNEL_RESIDENT = 1,  /* generic resident (one CTA per frame)              */
+  ADMM_KERNEL_REGULAR = 2,   /* regular-code resident                              */
+  ADMM_KERNEL_SHARDED = 3,   /* sharded / L2 streaming (codes beyond one SM)       */
+  ADMM_KERNEL_CLUSTER = 4,   /* cluster resident                                   */
+  ADMM_KERNEL_WIDE = 5       /* wide HBM streaming (large batches beyond one SM)   */
 };
 
 typedef struct admm_graph admm_graph;
@@ -82,6 +92,11 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
                          const int32_t* edge_var, int engine, admm_graph** out);
 int admm_graph_destroy(admm_graph* g);
 int admm_graph_get_info(const admm_graph* g, admm_graph_info* info);
+
+/* Which kernel admm_decode_batch / admm_decode_synth run for `batch` frames
+ * (enum admm_kernel), or a negative error code.  Codes beyond one SM switch
+ * from the sharded kernel to the wide kernel at large batches. */
+int admm_decode_kernel(const admm_graph* g, int dtype, int64_t batch);
 
 /* Bytes of device workspace admm_decode_batch needs for `batch` frames. */
 size_t admm_workspace_bytes(const admm_graph* g, int dtype, int64_t batch);

@@ -19,7 +19,9 @@ ADMM_F64 = 1
 ADMM_FLAG_CONVERGED = 1
 ADMM_FLAG_INTEGRAL = 2
 ADMM_FLAG_CODEWORD = 4
-ENGINES = {"auto": 0, "resident": 1, "streaming": 3, "cluster": 4}
+ENGINES = {"auto": 0, "resident": 1, "streaming": 3, "cluster": 4, "wide": 5}
+#: Kernel ids of admm_decode_kernel (enum admm_kernel).
+KERNELS = {1: "resident", 2: "regular", 3: "sharded", 4: "cluster", 5: "wide"}
 
 #: Every symbol the public header declares (checked by the CPU test-suite).
 EXPORTED = (
@@ -30,6 +32,7 @@ EXPORTED = (
     "admm_graph_destroy",
     "admm_graph_get_info",
     "admm_workspace_bytes",
+    "admm_decode_kernel",
     "admm_decode_batch",
     "admm_decode_synth",
     "admm_synth_llr",
@@ -90,6 +93,8 @@ def load() -> ctypes.CDLL:
     lib.admm_graph_get_info.restype = ctypes.c_int
     lib.admm_workspace_bytes.argtypes = [P, ctypes.c_int, I64]
     lib.admm_workspace_bytes.restype = SZ
+    lib.admm_decode_kernel.argtypes = [P, ctypes.c_int, I64]
+    lib.admm_decode_kernel.restype = ctypes.c_int
     lib.admm_decode_batch.argtypes = [
         P, ctypes.c_int, I64, P, I64, D, D, I32, D,
         P, I64, P, I64, P, P, P,

@@ -95,6 +95,12 @@ class DeviceGraph:
     def workspace_bytes(self, dtype_code: int, batch: int) -> int:
         return int(_lib.load().admm_workspace_bytes(self._h, dtype_code, batch))
 
+    def call_info(self, dtype_code: int, batch: int) -> dict:
+        """Graph info plus the kernel a call with ``batch`` frames runs
+        (``kernel``: admm_decode_kernel id, ``kernel_name``)."""
+        k = int(_lib.load().admm_decode_kernel(self._h, dtype_code, batch))
+        return dict(self.info, kernel=k, kernel_name=_lib.KERNELS.get(k, "?"))
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
@@ -264,7 +270,7 @@ def decode_batch(
            lam_out=lo, workspace=ws, stream=st)
     # keep inputs alive until the kernel has consumed them
     res = BatchResult(iterations=iters, flags=flags, weight=weight, x=x, hard=hard, z=zo, lam=lo,
-                      info=dg.info)
+                      info=dg.call_info(code_dt, B))
     res._keepalive = (g, zi, li, ws)  # type: ignore[attr-defined]
     return res
 
@@ -362,6 +368,6 @@ def decode_synth(code, channel, config: AdmmConfig = AdmmConfig(), *, seed: int,
             float(config.mu), float(config.epsilon), int(config.t_max), float(config.rho),
             _ptr(x), N, _ptr(hard), N, iters.data_ptr(), flags.data_ptr(), weight.data_ptr(),
             ws.data_ptr(), ws_bytes, st.cuda_stream))
-    res = BatchResult(iterations=iters, flags=flags, weight=weight, x=x, hard=hard, info=dg.info)
+    res = BatchResult(iterations=iters, flags=flags, weight=weight, x=x, hard=hard, info=dg.call_info(code_dt, batch))
     res._keepalive = (ws,)  # type: ignore[attr-defined]
     return res

@@ -48,6 +48,11 @@ struct admm_graph {
   admm::StreamLaunch slaunch[2];
   admm::ShardLaunch shlaunch[2];
   bool shard_ok[2] = {false, false};
+  admm::WideLaunch wlaunch[2];
+  bool wide_ok[2] = {false, false};
+  int* wctbl = nullptr;  // wide engine index tables (wide.cuh)
+  int* wvtbl = nullptr;
+  int engine_req = 0;
   int shard_G = 0, shard_dv = 0;
   long long shard_EB = 0;
   int smem_optin = 0;
@@ -119,7 +124,7 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
                          const int32_t* edge_var, int engine, admm_graph** out) {
   if (!out || !check_ptr || !edge_var) return fail(ADMM_E_ARG, "null pointer argument");
   if (engine != ADMM_ENGINE_AUTO && engine != ADMM_ENGINE_RESIDENT && engine != ADMM_ENGINE_STREAMING &&
-      engine != ADMM_ENGINE_CLUSTER)
+      engine != ADMM_ENGINE_CLUSTER && engine != ADMM_ENGINE_WIDE)
     return fail(ADMM_E_ARG, "unknown engine");
   *out = nullptr;
   if (n_vars <= 0 || n_checks <= 0) return fail(ADMM_E_ARG, "n_vars and n_checks must be positive");
@@ -148,6 +153,7 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
 
   auto* g = new admm_graph();
   g->device = device;
+  g->engine_req = engine;
   g->n_vars = n_vars;
   g->n_checks = n_checks;
   g->n_edges = E;
@@ -336,7 +342,7 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
     }
     }
   }
-  if (!placed && (engine == ADMM_ENGINE_AUTO || engine == ADMM_ENGINE_STREAMING)) {
+  if (!placed && (engine == ADMM_ENGINE_AUTO || engine == ADMM_ENGINE_STREAMING || engine == ADMM_ENGINE_WIDE)) {
     // Streaming engine: batch-interleaved state in global memory (L2-resident).
     bool ok = true;
     for (int dt = 0; dt < 2 && ok; ++dt) {
@@ -382,6 +388,26 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
         g->shard_ok[dt] = std::getenv("ADMM_B200_NO_SHARD") == nullptr;
       }
       cudaGetLastError();
+      // Wide HBM-streaming kernel (wide.cuh) for large batches.
+      for (int dt = 0; dt < 2; ++dt) {
+        admm::WideLaunch WL{};
+        const bool reg_stream = regular && dmax == g->D;
+        if (!admm::wide_lookup(dt, g->D, reg_stream && dvmax == 3 ? 3 : g->DVMAX, reg_stream, &WL)) continue;
+        cudaFuncAttributes fa{};
+        if (cudaFuncGetAttributes(&fa, WL.fn) != cudaSuccess) continue;
+        if (WL.smem > smem_optin || ensure_smem(WL.fn, WL.smem) != cudaSuccess) continue;
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, WL.fn, admm::kWideThreads, WL.smem);
+        if (occ < 1) continue;
+        WL.occupancy = occ;
+        WL.regs = fa.numRegs;
+        g->wlaunch[dt] = WL;
+        g->wide_ok[dt] = std::getenv("ADMM_B200_NO_WIDE") == nullptr;
+      }
+      if (engine == ADMM_ENGINE_WIDE && !g->wide_ok[0] && !g->wide_ok[1]) {
+        delete g;
+        return fail(ADMM_E_UNSUPPORTED, "no wide streaming kernel for this graph");
+      }
       g->kind = 3;
       g->CPT = 1;
       g->NT = admm::kStreamThreads;
@@ -416,6 +442,27 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
         var_edge[(size_t)v * dvmax + fill[v]++] = check_ptr[c] + (int)k;  // increasing edge id
       }
   }
+  // Index tables of the wide kernel's work items (wide.cuh ItemFeed).
+  std::vector<int> wct, wvt;
+  if (g->kind == 3 && (g->wide_ok[0] || g->wide_ok[1])) {
+    const int dt = g->wide_ok[0] ? 0 : 1;
+    const int WD = g->wlaunch[dt].D, WDV = g->wlaunch[dt].DV;
+    if (g->wide_ok[1 - dt] && (g->wlaunch[1 - dt].D != WD || g->wlaunch[1 - dt].DV != WDV)) g->wide_ok[1 - dt] = false;
+    const int CT = admm::wide_ct(WD), VT = admm::wide_vt(WDV), CB = admm::kWideCB, VB = admm::kWideVB;
+    const int ncb = (n_checks + CB - 1) / CB, nvb = (n_vars + VB - 1) / VB;
+    wct.assign((size_t)ncb * CT, -1);
+    wvt.assign((size_t)nvb * VT, -1);
+    for (int cb = 0; cb < ncb; ++cb)
+      for (int q = 0; q < CB; ++q) wct[(size_t)cb * CT + WD * CB + q] = 0;
+    for (int c = 0; c < n_checks; ++c) {
+      const size_t base = (size_t)(c / CB) * CT;
+      for (size_t k = 0; k < rows[c].size(); ++k) wct[base + k * CB + c % CB] = rows[c][k];
+      wct[base + WD * CB + c % CB] = check_ptr[c];
+    }
+    for (int v = 0; v < n_vars; ++v)
+      for (int j = 0; j < std::min(dvmax, WDV); ++j)
+        wvt[(size_t)(v / VB) * VT + (v % VB) * WDV + j] = var_edge[(size_t)v * dvmax + j];
+  }
   std::vector<uint16_t> var_pos((size_t)n_vars * g->DVMAX, 0);
   std::vector<uint8_t> var_deg(n_vars);
   for (int v = 0; v < n_vars; ++v) {
@@ -432,6 +479,8 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
   cudaError_t e3 = up((void**)&g->var_deg, var_deg.data(), var_deg.size());
   cudaError_t e4 = up((void**)&g->edge_base, edge_base.data(), edge_base.size() * sizeof(int));
   cudaError_t e5 = up((void**)&g->var_edge, var_edge.data(), var_edge.size() * sizeof(int));
+  if (e5 == cudaSuccess && !wct.empty()) e5 = up((void**)&g->wctbl, wct.data(), wct.size() * sizeof(int));
+  if (e5 == cudaSuccess && !wvt.empty()) e5 = up((void**)&g->wvtbl, wvt.data(), wvt.size() * sizeof(int));
   cudaError_t e6 = cudaSuccess, e7 = cudaSuccess, e8 = cudaSuccess;
   g->chk_var_ref = g->chk_var;
   if (g->kind == 2 && e1 == cudaSuccess)
@@ -546,6 +595,8 @@ int admm_graph_destroy(admm_graph* g) {
   cudaFree(g->var_deg);
   cudaFree(g->edge_base);
   cudaFree(g->var_edge);
+  cudaFree(g->wctbl);
+  cudaFree(g->wvtbl);
   cudaFree(g->var_orig);
   cudaFree(g->edge_ref);
   cudaFree(g->var_edge_int);
@@ -604,6 +655,28 @@ int shard_slots(const admm_graph* g, int dtype, int64_t batch) {
   return best;
 }
 
+// Wide kernel for this call?  Large batches of codes beyond one SM: the
+// sharded kernel holds ~64 slots and is latency-bound, the wide kernel
+// streams thousands of slots through HBM (wide.cuh).
+bool use_wide(const admm_graph* g, int dtype, int64_t batch) {
+  if (g->kind != 3 || !g->wide_ok[dtype]) return false;
+  if (g->engine_req == ADMM_ENGINE_WIDE) return true;
+  long long min_batch = 2048;
+  if (const char* env = std::getenv("ADMM_B200_WIDE_MIN")) min_batch = std::atoll(env);
+  return batch >= min_batch;
+}
+
+// Slots of the wide kernel: a multiple of the stripe width, up to 4096
+// (ADMM_B200_WIDE_SLOTS overrides), no more than the batch needs.
+int wide_slots(const admm_graph* g, int dtype, int64_t batch) {
+  const long long W = 32ll * g->wlaunch[dtype].vs;
+  long long s = 4096;
+  if (const char* env = std::getenv("ADMM_B200_WIDE_SLOTS")) s = std::max<long long>(W, std::atoll(env));
+  s = s / W * W;
+  const long long need = std::max<long long>(W, (batch + W - 1) / W * W);
+  return (int)std::min(s, need);
+}
+
 int stream_slots(const admm_graph* g, int dtype, int64_t batch) {
   if (g->shard_ok[dtype]) return shard_slots(g, dtype, batch);
   const size_t elem = dtype ? 8 : 4;
@@ -622,9 +695,21 @@ int stream_slots(const admm_graph* g, int dtype, int64_t batch) {
 
 }  // namespace
 
+int admm_decode_kernel(const admm_graph* g, int dtype, int64_t batch) {
+  if (!g) return fail(ADMM_E_ARG, "null graph");
+  if (dtype != ADMM_F32 && dtype != ADMM_F64) return fail(ADMM_E_ARG, "dtype must be ADMM_F32 or ADMM_F64");
+  if (g->kind == 3 && use_wide(g, dtype, batch)) return ADMM_KERNEL_WIDE;
+  return g->kind;
+}
+
 size_t admm_workspace_bytes(const admm_graph* g, int dtype, int64_t batch) {
   if (!g) return 0;
   if (g->kind == 3) {
+    if (dtype < 0 || dtype > 1) return 0;
+    if (use_wide(g, dtype, batch)) {
+      const int S = wide_slots(g, dtype, batch);
+      return admm::WideLayout(dtype ? 8 : 4, g->n_edges, g->n_vars, admm::wide_ncb(g->n_checks), S).total;
+    }
     const int S = stream_slots(g, dtype, batch);
     if (g->shard_ok[dtype]) return admm::StreamLayout(dtype ? 8 : 4, g->n_edges, g->n_vars, g->shard_G, S, true).total;
     const long long ncblk = (g->n_checks + admm::kStreamCK - 1) / admm::kStreamCK;
@@ -695,11 +780,23 @@ int decode_impl(const admm_graph* g, int dtype, int64_t batch, const void* gamma
   if (g->kind == 3) {
     if (z_in || z_out) return fail(ADMM_E_UNSUPPORTED, "state input/output is not supported by the streaming engine");
     const double thr = epsilon * epsilon * (double)g->n_edges;  // admm_decoder.py:169
+    admm::StreamGraphArgs sg{g->n_vars, g->n_checks, g->n_edges, g->m_pad, g->dvmax_actual,
+                             g->chk_var, g->edge_base, g->var_edge};
+    if (use_wide(g, dtype, batch)) {
+      const admm::WideLaunch& WL = g->wlaunch[dtype];
+      sg.ctbl = g->wctbl;
+      sg.vtbl = g->wvtbl;
+      admm::ResidentFrameArgs fa{batch, gamma, ld_gamma, mu, rho, thr, t_max, nullptr, nullptr, 0,
+                                 x_out, ld_x, hard_out, ld_hard, iters_out, flags_out, weight_out,
+                                 nullptr, nullptr, nullptr, synth};
+      const int rc = WL.launch(sg, fa, wide_slots(g, dtype, batch), workspace, WL.occupancy * g->num_sms, st);
+      if (rc != 0) return cuda_fail((cudaError_t)rc, "cudaLaunchCooperativeKernel(wide)");
+      ADMM_CUDA(cudaGetLastError());
+      return ADMM_OK;
+    }
     const int S = stream_slots(g, dtype, batch);
     const admm::StreamLaunch& L = g->slaunch[dtype];
     const int grid = L.occupancy * g->num_sms;
-    admm::StreamGraphArgs sg{g->n_vars, g->n_checks, g->n_edges, g->m_pad, g->dvmax_actual,
-                             g->chk_var, g->edge_base, g->var_edge};
     admm::ResidentFrameArgs fa{batch, gamma, ld_gamma, mu, rho, thr, t_max, nullptr, nullptr, 0,
                                x_out, ld_x, hard_out, ld_hard, iters_out, flags_out, weight_out,
                                nullptr, nullptr, nullptr, synth};

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <stdint.h>
 
 #include "resident.cuh"
@@ -10,6 +11,7 @@
 #include "streaming.cuh"
 #include "cluster_resident.cuh"
 #include "sharded.cuh"
+#include "wide.cuh"
 
 namespace admm {
 
@@ -138,6 +140,8 @@ struct StreamGraphArgs {
   const int* chk_var;
   const int* edge_base;
   const int* var_edge;
+  const int* ctbl = nullptr;  // wide engine index tables
+  const int* vtbl = nullptr;
 };
 
 struct StreamLaunch {
@@ -260,5 +264,77 @@ bool cluster_lookup(int dtype, int D, int DV, int CPT, int VPT_min, int* VPT, Cl
 // Defined in project.cu.
 bool launch_project(int dtype, int D, long long m, int d, const void* in, void* out, cudaStream_t st);
 void launch_synth(int dtype, long long batch, int n, const SynthParams& s, void* out, long long ld, cudaStream_t st);
+
+
+// ---- wide streaming engine (wide.cuh) ----
+struct WideLaunch {
+  const void* fn;
+  int (*launch)(const StreamGraphArgs&, const ResidentFrameArgs&, int S, void* ws, int grid, cudaStream_t st);
+  int occupancy, regs, vs, smem, D, DV;
+};
+
+inline long long wide_ncb(int n_checks) { return (n_checks + kWideCB - 1) / kWideCB; }
+
+template <typename T>
+WideParams<T> make_wide_params(const StreamGraphArgs& g, const ResidentFrameArgs& a, int S, void* ws) {
+  WideParams<T> p{};
+  p.n_vars = g.n_vars;
+  p.n_checks = g.n_checks;
+  p.n_edges = g.n_edges;
+  p.m_pad = g.m_pad;
+  p.dvmax = g.dvmax;
+  p.chk_var = g.chk_var;
+  p.edge_base = g.edge_base;
+  p.var_edge = g.var_edge;
+  p.ctbl = g.ctbl;
+  p.vtbl = g.vtbl;
+  p.batch = a.batch;
+  p.gamma = static_cast<const T*>(a.gamma);
+  p.ld_gamma = a.ld_gamma;
+  p.mu = T(a.mu);
+  p.rho = T(a.rho);
+  p.one_minus_rho = T(1.0 - a.rho);
+  p.thr = T(a.thr);
+  p.t_max = a.t_max;
+  p.x_out = static_cast<T*>(a.x_out);
+  p.ld_x = a.ld_x;
+  p.hard_out = a.hard_out;
+  p.ld_hard = a.ld_hard;
+  p.iters_out = a.iters_out;
+  p.flags_out = a.flags_out;
+  p.weight_out = a.weight_out;
+  p.S = S;
+  p.ncb = static_cast<int>(wide_ncb(g.n_checks));
+  p.static_items = std::getenv("ADMM_B200_WIDE_STATIC") != nullptr;
+  p.synth = a.synth;
+  const WideLayout L(sizeof(T), g.n_edges, g.n_vars, p.ncb, S);
+  char* base = static_cast<char*>(ws);
+  p.zl = reinterpret_cast<T*>(base + L.zl);
+  p.msg = reinterpret_cast<T*>(base + L.msg);
+  p.x = reinterpret_cast<T*>(base + L.x);
+  p.gm = reinterpret_cast<T*>(base + L.gm);
+  p.part = reinterpret_cast<T*>(base + L.part);
+  p.frame = reinterpret_cast<long long*>(base + L.frame);
+  int* ib = reinterpret_cast<int*>(base + L.ints);
+  p.st = ib;
+  p.tcount = ib + S;
+  p.conv = ib + 2 * S;
+  p.weight = ib + 3 * S;
+  p.nonint = ib + 4 * S;
+  p.odd = ib + 5 * S;
+  p.ctr = ib + 6 * S;
+  return p;
+}
+
+template <typename T, int VS, int D, int DVMAX, bool REG, int NS, int MINB>
+int launch_wide(const StreamGraphArgs& g, const ResidentFrameArgs& a, int S, void* ws, int grid, cudaStream_t st) {
+  WideParams<T> p = make_wide_params<T>(g, a, S, ws);
+  void* args[] = {&p};
+  return (int)cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&wide_decode_kernel<T, VS, D, DVMAX, REG, NS, MINB>),
+                                          grid, kWideThreads, args, wide_smem_bytes<T, VS, D, DVMAX, NS>(), st);
+}
+
+// Defined in wide.cu.
+bool wide_lookup(int dtype, int D, int DVMAX, bool regular, WideLaunch* out);
 
 }  // namespace admm

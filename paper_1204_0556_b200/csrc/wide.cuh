@@ -1,0 +1,724 @@
+// Wide streaming engine: large batches of frames of codes that do not fit one
+// SM (BASELINE config 5, n = 16384), with the decoder state in HBM.
+//
+// The sharded engine (sharded.cuh) keeps z/lambda in shared memory and can
+// therefore hold only ~64 frame slots; its passes are short (~25 us) and
+// bound by L2 latency and grid syncs.  This engine instead streams the whole
+// state through HBM every pass over S = 2048-8192 slots, so each phase is a
+// long, fully parallel, bandwidth-bound sweep -- the two-kernel HBM schedule
+// of SURVEY.md 8d (28 B per edge-update in fp32):
+//
+//   phase V (variables)  read msg (DV per var) + gamma/mu, write x
+//   phase C (checks)     gather x (L2-resident, see below), read z/lambda,
+//                        write z/lambda and msg = z - lambda/mu
+//   phase S (slots)      exact stop rule, retirement, refill
+//
+// Layout: slots are grouped in STRIPES of W = 32*VS consecutive slots, one
+// stripe per warp access; every array is stripe-major, then row (edge or
+// variable), then the stripe's 32 lanes x VS slots:
+//     zl  [stripe][E][32][2][VS]   z and lambda/mu of a lane: 2 adjacent vectors
+//     msg [stripe][E][32][VS]      x, gm [stripe][N][32][VS]
+//     part[stripe][ncb][2][32][VS] per-check-block residual partials
+// so a warp's access to one row is 32 lanes x 16 B = 512 B contiguous
+// (1 KB for z/lambda), each thread moving VS slots with one 128-bit access.
+// Within a stripe the rows of the checks of one work item are contiguous.
+//
+// Work items are (stripe, block of rows), distributed round-robin over all
+// warps in stripe-major order, so at any moment the grid works on a few
+// stripes: their x rows (N x 512 B = 8 MB per stripe at n = 16384) stay in
+// L2 while the D-fold reuse of the x gathers happens.  No __syncthreads in
+// the phases; phases are separated by grid syncs of the cooperative kernel.
+//
+// Slot life (as in streaming.cuh): FRESH (z = lambda = 0 implicit) ->
+// RUNNING -> RETIRING (the next V/C pass computes the outputs from the final
+// x) -> next frame or EMPTY.  The stop rule is exact: the S phase sums the
+// per-block partials of every running slot in a fixed order (lane-strided
+// blocks + butterfly), so decisions are deterministic and independent of
+// the batch composition.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "projection.cuh"
+#include "streaming.cuh"
+#include "synth.cuh"
+
+namespace admm {
+
+template <typename T, int VS>
+struct alignas(sizeof(T) * VS) WVec {
+  T v[VS];
+};
+
+constexpr int kWideThreads = 256;
+constexpr int kWideCB = 8;   // checks per phase-C work item (one warp)
+constexpr int kWideVB = 16;  // variables per phase-V work item (one warp)
+
+template <typename T>
+struct WideParams {
+  int n_vars, n_checks, n_edges, m_pad, dvmax;
+  const int* chk_var;    // [D][m_pad], -1 = unused
+  const int* edge_base;  // [n_checks]
+  const int* var_edge;   // [n_vars][dvmax], -1 = unused
+  const int* ctbl;       // [ncb][wide_ct(D)] check-block index tables
+  const int* vtbl;       // [nvb][wide_vt(DVMAX)] variable-block index tables
+  long long batch;
+  const T* gamma;
+  long long ld_gamma;
+  T mu, rho, one_minus_rho, thr;
+  int t_max;
+  T* x_out;
+  long long ld_x;
+  uint8_t* hard_out;
+  long long ld_hard;
+  int* iters_out;
+  uint8_t* flags_out;
+  int* weight_out;
+  int S, ncb;
+  int static_items;  // debug: static round-robin work items instead of the atomic feed
+  T* zl;
+  T* msg;
+  T* x;
+  T* gm;
+  T* part;
+  long long* frame;
+  int *st, *tcount, *conv, *weight, *nonint, *odd, *ctr;
+  SynthParams synth;
+};
+
+struct WideLayout {
+  size_t zl, msg, x, gm, part, frame, ints, total;
+  static size_t al(size_t b) { return (b + 255) & ~size_t(255); }
+  WideLayout(size_t elem, long long E, long long N, long long ncb, long long S) {
+    size_t o = 0;
+    zl = o; o += al(elem * 2 * E * S);
+    msg = o; o += al(elem * E * S);
+    x = o; o += al(elem * N * S);
+    gm = o; o += al(elem * N * S);
+    part = o; o += al(elem * 2 * ncb * S);
+    frame = o; o += al(sizeof(long long) * S);
+    ints = o; o += al(sizeof(int) * (6 * S + 8));
+    total = o;
+  }
+};
+
+template <typename V>
+__device__ __forceinline__ V wld(const V* p) { return *p; }
+template <typename V>
+__device__ __forceinline__ void wst(V* p, const V& v) { *p = v; }
+
+// Streaming accesses (ld/st.global.cs: evict-first in L1 and L2) for the
+// state that is touched once per pass -- z/lambda, messages, gamma/mu -- so
+// that L2 keeps the x rows of the stripes in flight for their D-fold reuse.
+template <typename V>
+__device__ __forceinline__ V ld_cs(const V* p) {
+  static_assert(sizeof(V) == 32 || sizeof(V) == 16 || sizeof(V) == 8 || sizeof(V) == 4, "vector size");
+  V r;
+  if constexpr (sizeof(V) == 32) {
+    const float4 t0 = __ldcs(reinterpret_cast<const float4*>(p));
+    const float4 t1 = __ldcs(reinterpret_cast<const float4*>(p) + 1);
+    memcpy(&r, &t0, 16);
+    memcpy(reinterpret_cast<char*>(&r) + 16, &t1, 16);
+  } else if constexpr (sizeof(V) == 16) {
+    const float4 t = __ldcs(reinterpret_cast<const float4*>(p));
+    memcpy(&r, &t, 16);
+  } else if constexpr (sizeof(V) == 8) {
+    const float2 t = __ldcs(reinterpret_cast<const float2*>(p));
+    memcpy(&r, &t, 8);
+  } else {
+    const float t = __ldcs(reinterpret_cast<const float*>(p));
+    memcpy(&r, &t, 4);
+  }
+  return r;
+}
+template <typename V>
+__device__ __forceinline__ void st_cs(V* p, const V& v) {
+  if constexpr (sizeof(V) == 32) {
+    float4 t0, t1;
+    memcpy(&t0, &v, 16);
+    memcpy(&t1, reinterpret_cast<const char*>(&v) + 16, 16);
+    __stcs(reinterpret_cast<float4*>(p), t0);
+    __stcs(reinterpret_cast<float4*>(p) + 1, t1);
+  } else if constexpr (sizeof(V) == 16) {
+    float4 t;
+    memcpy(&t, &v, 16);
+    __stcs(reinterpret_cast<float4*>(p), t);
+  } else if constexpr (sizeof(V) == 8) {
+    float2 t;
+    memcpy(&t, &v, 8);
+    __stcs(reinterpret_cast<float2*>(p), t);
+  } else {
+    float t;
+    memcpy(&t, &v, 4);
+    __stcs(reinterpret_cast<float*>(p), t);
+  }
+}
+
+// ---- per-warp cp.async pipeline ----
+// Every lane copies its own vectors into its warp's ring of NS stages and
+// reads back only what it copied, so a stage needs no barrier: wait_group
+// makes a lane's copies visible to it.  The loads of task t+NS-1 are in
+// flight while task t computes, and the in-flight bytes live in shared
+// memory instead of registers.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async_vec(uint32_t dst, const void* src) {
+  if constexpr (BYTES == 32) {
+    cp_async16(dst, src);
+    cp_async16(dst + 16, static_cast<const char*>(src) + 16);
+  } else if constexpr (BYTES == 16) {
+    cp_async16(dst, src);
+  } else if constexpr (BYTES == 8) {
+    cp_async8(dst, src);
+  } else {
+    static_assert(BYTES == 4, "vector size");
+    cp_async4(dst, src);
+  }
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+template <typename V>
+__device__ __forceinline__ V lds_vec(const unsigned char* p) {
+  return *reinterpret_cast<const V*>(p);
+}
+
+// Stripe flags, rebuilt in shared memory by every CTA at the start of a pass.
+enum : int { kStripeActive = 1, kStripeRetiring = 2, kStripeFresh = 4 };
+constexpr int kWideMaxStripes = 256;
+
+// Stage geometry.  A stage holds one task: the item's slot states (32 lanes
+// x VS ints), then for a check task D x-rows and D z/lambda rows, for a
+// variable task VBB variables x (DVMAX message rows, gamma/mu, x) -- each
+// row 32 lanes x one vector.
+template <typename T, int VS, int D, int DVMAX>
+struct WideStage {
+  static constexpr int VB = VS * static_cast<int>(sizeof(T));  // bytes per lane per row
+  static constexpr int HB = 32 * VS * 4;                        // slot states
+  static constexpr int CX = HB, CZ = HB + D * 32 * VB;          // check task: x rows, z/lambda rows
+  static constexpr int CBYTES = D * 32 * 3 * VB;
+  static constexpr int VBB = (3 * D) / (DVMAX + 2) > 0 ? (3 * D) / (DVMAX + 2) : 1;
+  static constexpr int VROWS = DVMAX + 2;                       // messages, gamma/mu, x
+  static constexpr int VBYTES = VBB * VROWS * 32 * VB;
+  static constexpr int bytes = (HB + (CBYTES > VBYTES ? CBYTES : VBYTES) + 15) / 16 * 16;
+};
+
+
+// ---- work items ----
+// Items are (stripe, block of kWideVB variables) in phase V and (stripe,
+// block of kWideCB checks) in phase C, numbered stripe-major.  Warps take
+// them dynamically from a global counter (ctr[2] / ctr[3]): item costs vary
+// (fresh frames synthesise their LLRs, retiring frames write outputs,
+// empty stripes cost nothing), and a static split left a quarter of the SM
+// time waiting at the grid syncs.  The graph indices of a block are a
+// precomputed table (wide_ct / wide_vt ints) loaded with one coalesced
+// access per lane and published to the warp's shared-memory table slot, so
+// no address computation waits on a dependent index load.
+__host__ __device__ constexpr int wide_ct(int D) { return ((D + 1) * kWideCB + 31) / 32 * 32; }
+__host__ __device__ constexpr int wide_vt(int DV) { return (kWideVB * DV + 31) / 32 * 32; }
+
+template <int TB>
+struct ItemFeed {
+  static constexpr int NR = TB / 32;
+  const int* tbl;  // [n_blocks][TB]
+  int* ctr;
+  int n_items, nblk;
+  int stat_next, stat_step;  // static assignment (debug): stat_step > 0
+  int id1;         // next item (its table is in reg)
+  int raw2;        // lane 0: atomic result for the item after (in flight)
+  int reg[NR];
+
+  __device__ __forceinline__ int grab_raw() {
+    if (stat_step > 0) {
+      const int v = stat_next;
+      stat_next += stat_step;
+      return v;
+    }
+    return (threadIdx.x & 31) == 0 ? atomicAdd(ctr, 1) : 0;
+  }
+  __device__ __forceinline__ void load(int id) {
+    if (id < n_items) {
+      const int* t = tbl + (long long)(id % nblk) * TB + (threadIdx.x & 31);
+#pragma unroll
+      for (int r = 0; r < NR; ++r) reg[r] = __ldg(t + r * 32);
+    }
+  }
+  __device__ __forceinline__ void publish(int* slot, int id) {
+    __syncwarp();  // every lane is done reading the slot's previous table
+#pragma unroll
+    for (int r = 0; r < NR; ++r) slot[r * 32 + (threadIdx.x & 31)] = reg[r];
+    if ((threadIdx.x & 31) == 0) slot[TB] = id;
+    __syncwarp();
+  }
+  // First item: published into slot0; returns its id.
+  __device__ __forceinline__ int start(int* slot0) {
+    const int a = __shfl_sync(0xffffffffu, grab_raw(), 0);
+    id1 = __shfl_sync(0xffffffffu, grab_raw(), 0);
+    load(a);
+    publish(slot0, a);
+    load(id1);
+    raw2 = grab_raw();
+    return a;
+  }
+  // Move to the next item: publish it into `slot`, prefetch the one after.
+  __device__ __forceinline__ int advance(int* slot) {
+    const int cur = id1;
+    publish(slot, cur);
+    id1 = __shfl_sync(0xffffffffu, raw2, 0);
+    load(id1);
+    raw2 = grab_raw();
+    return cur;
+  }
+};
+
+// Shared memory: stripe flags, then per warp two index-table slots and the
+// ring of NS stages.
+template <int D, int DVMAX>
+__host__ __device__ constexpr int wide_tstride() {
+  return (wide_ct(D) > wide_vt(DVMAX) ? wide_ct(D) : wide_vt(DVMAX)) + 4;
+}
+template <typename T, int VS, int D, int DVMAX, int NS>
+__host__ __device__ constexpr int wide_warp_bytes() {
+  return 2 * 4 * wide_tstride<D, DVMAX>() + NS * WideStage<T, VS, D, DVMAX>::bytes;
+}
+template <typename T, int VS, int D, int DVMAX, int NS>
+__host__ __device__ constexpr int wide_smem_bytes() {
+  return kWideMaxStripes * 4 + (kWideThreads / 32) * wide_warp_bytes<T, VS, D, DVMAX, NS>();
+}
+
+// ---- phase V: x = clip((sum msg - gamma/mu) / deg) (admm_decoder.py:108-124) ----
+template <typename T, int VS, int D, int DVMAX, int NS>
+__device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned char* ring, int* tslot, int tstride,
+                                             const int* sflag, int n_vi, int n_vb) {
+  using V = WVec<T, VS>;
+  using VI = WVec<int, VS>;
+  using G = WideStage<T, VS, D, DVMAX>;
+  constexpr int W = 32 * VS, VBB = G::VBB, TPI = (kWideVB + VBB - 1) / VBB, VB = G::VB, TB = wide_vt(DVMAX);
+  const int lane = threadIdx.x & 31;
+  const long long E = p.n_edges, N = p.n_vars;
+  const V* msg = reinterpret_cast<const V*>(p.msg);
+  V* x = reinterpret_cast<V*>(p.x);
+  V* gm = reinterpret_cast<V*>(p.gm);
+  const uint32_t ring_s = smem_u32(ring);
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  ItemFeed<TB> feed{p.vtbl, p.ctr + 2, n_vi, n_vb, gw, p.static_items ? (int)((gridDim.x * blockDim.x) >> 5) : 0};
+  int ik = 0, iq = 0, ti = 0;
+  int iid = feed.start(tslot);
+
+  auto issue_next = [&]() {
+    if (iid < n_vi) {
+      const int stripe = iid / n_vb, vb = iid % n_vb;
+      const int fl = sflag[stripe];
+      const int i0 = vb * kWideVB + iq * VBB, i1 = min(p.n_vars, min((vb + 1) * kWideVB, i0 + VBB));
+      if ((fl & kStripeActive) && i0 < i1) {
+        const int* tb = tslot + (ik & 1) * tstride;
+        const uint32_t st = ring_s + (ti % NS) * G::bytes;
+        cp_async_vec<4 * VS>(st + lane * 4 * VS, p.st + stripe * W + lane * VS);
+        const long long rb = (long long)stripe * N * 32 + lane;
+#pragma unroll
+        for (int b = 0; b < VBB; ++b) {
+          const int i = i0 + b;
+          if (i < i1) {
+            const uint32_t rowb = st + G::HB + b * G::VROWS * 32 * VB + lane * VB;
+#pragma unroll
+            for (int j = 0; j < DVMAX; ++j) {
+              const int e = tb[(iq * VBB + b) * DVMAX + j];
+              if (e >= 0) cp_async_vec<VB>(rowb + j * 32 * VB, msg + ((long long)stripe * E + e) * 32 + lane);
+            }
+            cp_async_vec<VB>(rowb + DVMAX * 32 * VB, gm + rb + (long long)i * 32);
+            if (fl & kStripeRetiring) cp_async_vec<VB>(rowb + (DVMAX + 1) * 32 * VB, x + rb + (long long)i * 32);
+          }
+        }
+      }
+    }
+    cp_commit();
+    ++ti;
+    if (++iq == TPI) {
+      iq = 0;
+      ++ik;
+      iid = feed.advance(tslot + (ik & 1) * tstride);
+    }
+  };
+
+#pragma unroll
+  for (int t = 0; t < NS - 1; ++t) issue_next();
+  for (int t = 0;; ++t) {
+    const int ck = t / TPI, cq = t % TPI;
+    const int* tb = tslot + (ck & 1) * tstride;
+    const int cid = tb[TB];
+    if (cid >= n_vi) break;
+    issue_next();
+    cp_wait<NS - 1>();
+    const int stripe = cid / n_vb, vb = cid % n_vb;
+    const int fl = sflag[stripe];
+    const int i0 = vb * kWideVB + cq * VBB, i1 = min(p.n_vars, min((vb + 1) * kWideVB, i0 + VBB));
+    if (!(fl & kStripeActive) || i0 >= i1) continue;
+    const unsigned char* st = ring + (t % NS) * G::bytes;
+    const VI stv = lds_vec<VI>(st + lane * 4 * VS);
+    const int s0 = stripe * W + lane * VS;
+    bool anyupd = false, anyfresh = false, anyret = false;
+    long long fr[VS];
+#pragma unroll
+    for (int l = 0; l < VS; ++l) {
+      anyupd |= stv.v[l] == kSlotRunning || stv.v[l] == kSlotFresh;
+      anyfresh |= stv.v[l] == kSlotFresh;
+      anyret |= stv.v[l] == kSlotRetiring;
+      fr[l] = (stv.v[l] == kSlotFresh || stv.v[l] == kSlotRetiring) ? p.frame[s0 + l] : 0;
+    }
+    int wsum[VS], nonint[VS];
+#pragma unroll
+    for (int l = 0; l < VS; ++l) wsum[l] = nonint[l] = 0;
+    const long long rb = (long long)stripe * N * 32 + lane;
+#pragma unroll
+    for (int b = 0; b < VBB; ++b) {
+      const int i = i0 + b;
+      if (i >= i1) break;
+      const unsigned char* rowb = st + G::HB + b * G::VROWS * 32 * VB + lane * VB;
+      int deg = 0;
+      V mv[DVMAX];
+#pragma unroll
+      for (int j = 0; j < DVMAX; ++j) {
+        const bool on = tb[(cq * VBB + b) * DVMAX + j] >= 0;
+        deg += on;
+        if (on) mv[j] = lds_vec<V>(rowb + j * 32 * VB);
+      }
+      V g = lds_vec<V>(rowb + DVMAX * 32 * VB);
+      V xn;
+      if (anyret) xn = lds_vec<V>(rowb + (DVMAX + 1) * 32 * VB);
+#pragma unroll
+      for (int l = 0; l < VS; ++l) {
+        const int state = stv.v[l];
+        if (state == kSlotRetiring) {
+          // Output statistics of the final iterate (make_output, :92-105); x stays.
+          const T xv = xn.v[l];
+          const bool h = xv > T(0.5);
+          if (p.x_out) p.x_out[fr[l] * p.ld_x + i] = xv;
+          if (p.hard_out) p.hard_out[fr[l] * p.ld_hard + i] = h;
+          wsum[l] += h;
+          if (!(vmin(fabs(xv), fabs(T(1) - xv)) <= T(1e-5))) nonint[l] = 1;
+        } else if (state == kSlotRunning || state == kSlotFresh) {
+          T acc = T(0);
+          if (state == kSlotFresh) {
+            const T gi = p.synth.kind != 0 ? static_cast<T>(synth_llr(p.synth, p.synth.trial0 + fr[l], i))
+                                            : p.gamma[fr[l] * p.ld_gamma + i];
+            g.v[l] = div_rn(gi, p.mu);
+          } else {
+#pragma unroll
+            for (int j = 0; j < DVMAX; ++j)
+              if (j < deg) acc = add_rn(acc, mv[j].v[l]);  // increasing edge id (np.bincount order)
+          }
+          xn.v[l] = deg > 0 ? clip01(div_rn(sub_rn(acc, g.v[l]), T(deg))) : (g.v[l] < T(0) ? T(1) : T(0));
+        }
+      }
+      if (anyupd) wst(x + rb + (long long)i * 32, xn);
+      if (anyfresh) st_cs(gm + rb + (long long)i * 32, g);
+    }
+    if (anyret) {
+#pragma unroll
+      for (int l = 0; l < VS; ++l) {
+        if (stv.v[l] != kSlotRetiring) continue;
+        if (wsum[l]) atomicAdd(p.weight + s0 + l, wsum[l]);
+        if (nonint[l]) atomicOr(p.nonint + s0 + l, 1);
+      }
+    }
+  }
+  cp_wait<0>();
+}
+
+// ---- phase C: fused z-update, projection, residuals, lambda-update, message
+// (admm_decoder.py:127-149, parity_polytope.py:352-421) ----
+template <typename T, int VS, int D, int DVMAX, bool REG, int NS>
+__device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned char* ring, int* tslot, int tstride,
+                                             const int* sflag, int n_ci) {
+  using V = WVec<T, VS>;
+  using VI = WVec<int, VS>;
+  using V2 = WVec<T, 2 * VS>;
+  using G = WideStage<T, VS, D, DVMAX>;
+  constexpr int W = 32 * VS, CB = kWideCB, VB = G::VB, TB = wide_ct(D);
+  const int lane = threadIdx.x & 31;
+  const long long E = p.n_edges, N = p.n_vars;
+  const V* x = reinterpret_cast<const V*>(p.x);
+  V2* zl = reinterpret_cast<V2*>(p.zl);
+  V* msg = reinterpret_cast<V*>(p.msg);
+  const int ncb = p.ncb;
+  const uint32_t ring_s = smem_u32(ring);
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  ItemFeed<TB> feed{p.ctbl, p.ctr + 3, n_ci, ncb, gw, p.static_items ? (int)((gridDim.x * blockDim.x) >> 5) : 0};
+  int ik = 0, iq = 0, ti = 0;
+  int iid = feed.start(tslot);
+
+  auto issue_next = [&]() {
+    if (iid < n_ci) {
+      const int stripe = iid / ncb, c = (iid % ncb) * CB + iq;
+      if ((sflag[stripe] & kStripeActive) && c < p.n_checks) {
+        const int* tb = tslot + (ik & 1) * tstride;
+        const uint32_t st = ring_s + (ti % NS) * G::bytes;
+        cp_async_vec<4 * VS>(st + lane * 4 * VS, p.st + stripe * W + lane * VS);
+        const long long e0 = tb[D * CB + iq];
+        const long long xb = (long long)stripe * N * 32 + lane, eb = (long long)stripe * E * 32 + lane;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          const int v = tb[k * CB + iq];
+          if (v >= 0) {
+            cp_async_vec<VB>(st + G::CX + (k * 32 + lane) * VB, x + xb + (long long)v * 32);
+            cp_async_vec<2 * VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zl + eb + (e0 + k) * 32);
+          }
+        }
+      }
+    }
+    cp_commit();
+    ++ti;
+    if (++iq == CB) {
+      iq = 0;
+      ++ik;
+      iid = feed.advance(tslot + (ik & 1) * tstride);
+    }
+  };
+
+  T primal[VS], moved[VS];
+  int odd[VS];
+#pragma unroll
+  for (int l = 0; l < VS; ++l) {
+    primal[l] = moved[l] = T(0);
+    odd[l] = 0;
+  }
+#pragma unroll
+  for (int t = 0; t < NS - 1; ++t) issue_next();
+  for (int t = 0;; ++t) {
+    const int ck = t / CB, cq = t % CB;
+    const int* tb = tslot + (ck & 1) * tstride;
+    const int cid = tb[TB];
+    if (cid >= n_ci) break;
+    issue_next();
+    cp_wait<NS - 1>();
+    const int stripe = cid / ncb, cb = cid % ncb, c = cb * CB + cq;
+    if (!(sflag[stripe] & kStripeActive) || c >= p.n_checks) continue;
+    const unsigned char* st = ring + (t % NS) * G::bytes;
+    const VI stv = lds_vec<VI>(st + lane * 4 * VS);
+    bool anyupd = false, anyret = false;
+#pragma unroll
+    for (int l = 0; l < VS; ++l) {
+      anyupd |= stv.v[l] == kSlotRunning || stv.v[l] == kSlotFresh;
+      anyret |= stv.v[l] == kSlotRetiring;
+    }
+    int d = 0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) d += tb[k * CB + cq] >= 0;
+    const long long e0 = tb[D * CB + cq];
+    const long long eb = (long long)stripe * E * 32 + lane;
+    V gx[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k)
+      if (k < d) gx[k] = lds_vec<V>(st + G::CX + (k * 32 + lane) * VB);
+    if (anyret) {
+      // Syndrome of the final hard decision (is_codeword, codes.py:145-154).
+#pragma unroll
+      for (int k = 0; k < D; ++k)
+        if (k < d) {
+#pragma unroll
+          for (int l = 0; l < VS; ++l) odd[l] ^= gx[k].v[l] > T(0.5);
+        }
+    }
+    if (anyupd) {
+      V2 zlv[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k)
+        if (k < d) zlv[k] = lds_vec<V2>(st + G::CZ + (k * 32 + lane) * 2 * VB);
+#pragma unroll
+      for (int l = 0; l < VS; ++l) {
+        const bool run = stv.v[l] == kSlotRunning;
+        T w_[D], u[D], zn[D], zo[D], lo[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          const bool on = k < d;
+          zo[k] = (on && run) ? zlv[k].v[l] : T(0);
+          lo[k] = (on && run) ? zlv[k].v[VS + l] : T(0);  // scaled dual lambda/mu
+          const T g = on ? gx[k].v[l] : T(0);
+          w_[k] = add_rn(mul_rn(p.rho, g), mul_rn(p.one_minus_rho, zo[k]));
+          u[k] = on ? add_rn(w_[k], lo[k]) : -Num<T>::inf();
+        }
+        if constexpr (REG) {
+          project_pp_fixed<T, D>(u, zn);
+        } else {
+          project_pp<T, D>(u, zn, d);
+        }
+        const bool act = run || stv.v[l] == kSlotFresh;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          if (k < d) {
+            const T r1 = sub_rn(gx[k].v[l], zn[k]);
+            const T r2 = sub_rn(zn[k], zo[k]);
+            if (act) {
+              primal[l] = add_rn(primal[l], mul_rn(r1, r1));
+              moved[l] = add_rn(moved[l], mul_rn(r2, r2));
+            }
+            const T lnew = add_rn(lo[k], sub_rn(w_[k], zn[k]));
+            zlv[k].v[l] = zn[k];
+            zlv[k].v[VS + l] = lnew;
+            gx[k].v[l] = sub_rn(zn[k], lnew);  // message
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < D; ++k)
+        if (k < d) {
+          st_cs(zl + eb + (e0 + k) * 32, zlv[k]);
+          st_cs(msg + eb + (e0 + k) * 32, gx[k]);
+        }
+    }
+    if (cq == CB - 1 || c + 1 >= p.n_checks) {
+      // End of the item: per-slot partials of its checks (fixed order).
+      if (anyupd) {
+        V* part = reinterpret_cast<V*>(p.part) + ((long long)stripe * ncb + cb) * 64 + lane;
+        V a, b;
+#pragma unroll
+        for (int l = 0; l < VS; ++l) {
+          a.v[l] = primal[l];
+          b.v[l] = moved[l];
+        }
+        wst(part, a);
+        wst(part + 32, b);
+      }
+      if (anyret) {
+        const int s0 = stripe * W + lane * VS;
+#pragma unroll
+        for (int l = 0; l < VS; ++l)
+          if (stv.v[l] == kSlotRetiring && odd[l]) atomicOr(p.odd + s0 + l, 1);
+      }
+#pragma unroll
+      for (int l = 0; l < VS; ++l) {
+        primal[l] = moved[l] = T(0);
+        odd[l] = 0;
+      }
+    }
+  }
+  cp_wait<0>();
+}
+
+template <typename T>
+__device__ __forceinline__ void wide_refill(const WideParams<T>& p, int s) {
+  const int f = atomicAdd(p.ctr + 0, 1);
+  p.tcount[s] = 0;
+  p.weight[s] = 0;
+  p.nonint[s] = 0;
+  p.odd[s] = 0;
+  p.conv[s] = 0;
+  if (f < p.batch) {
+    p.frame[s] = f;
+    p.st[s] = kSlotFresh;
+  } else {
+    p.frame[s] = -1;
+    p.st[s] = kSlotEmpty;
+    atomicSub(p.ctr + 1, 1);
+  }
+}
+
+// ---- phase S: one warp per slot ----
+template <typename T, int VS>
+__device__ __forceinline__ void wide_phase_s(const WideParams<T>& p, int s) {
+  constexpr int W = 32 * VS;
+  const int lane = threadIdx.x & 31;
+  const int state = __shfl_sync(0xffffffffu, lane == 0 ? p.st[s] : 0, 0);
+  if (state == kSlotEmpty) return;
+  if (state == kSlotRetiring) {
+    if (lane == 0) {
+      const long long f = p.frame[s];
+      if (p.iters_out) p.iters_out[f] = p.tcount[s];
+      if (p.flags_out) p.flags_out[f] = (p.conv[s] ? 1 : 0) | (p.nonint[s] ? 0 : 2) | (p.odd[s] ? 0 : 4);
+      if (p.weight_out) p.weight_out[f] = p.weight[s];
+      wide_refill(p, s);
+    }
+    return;
+  }
+  // Exact residual sums (admm_decoder.py:174-176), fixed order.
+  const int stripe = s / W, r = s % W;
+  const T* part = p.part + (long long)stripe * p.ncb * 2 * W + r;
+  T a = T(0), b = T(0);
+#pragma unroll 4
+  for (int q = lane; q < p.ncb; q += 32) {
+    a = add_rn(a, part[(long long)q * 2 * W]);
+    b = add_rn(b, part[(long long)q * 2 * W + W]);
+  }
+  a = warp_allsum(a);
+  b = warp_allsum(b);
+  if (lane == 0) {
+    const bool converged = a < p.thr && b < p.thr;  // admm_decoder.py:169, 179 (strict)
+    const int t = p.tcount[s] + 1;
+    p.tcount[s] = t;
+    if (converged || t >= p.t_max) {
+      p.conv[s] = converged;
+      p.st[s] = kSlotRetiring;
+    } else {
+      p.st[s] = kSlotRunning;
+    }
+  }
+}
+
+template <typename T, int VS, int D, int DVMAX, bool REG, int NS, int MINB>
+__global__ void __launch_bounds__(kWideThreads, MINB) wide_decode_kernel(const WideParams<T> p) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char wide_smem[];
+  constexpr int W = 32 * VS, TS = wide_tstride<D, DVMAX>();
+  int* sflag = reinterpret_cast<int*>(wide_smem);
+  unsigned char* wbase = wide_smem + kWideMaxStripes * 4 + (threadIdx.x >> 5) * wide_warp_bytes<T, VS, D, DVMAX, NS>();
+  int* tslot = reinterpret_cast<int*>(wbase);
+  unsigned char* ring = wbase + 2 * 4 * TS;
+  const int n_stripes = p.S / W;
+  const int n_vb = (p.n_vars + kWideVB - 1) / kWideVB;
+  const int n_vi = n_vb * n_stripes, n_ci = p.ncb * n_stripes;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int n_gwarp = (gridDim.x * blockDim.x) >> 5;
+
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.ctr[0] = 0;
+    p.ctr[1] = p.S;
+    p.ctr[2] = 0;
+    p.ctr[3] = 0;
+  }
+  grid.sync();
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < p.S; s += gridDim.x * blockDim.x) wide_refill(p, s);
+  grid.sync();
+
+  const long long max_passes = ((long long)(p.batch + p.S - 1) / p.S + 1) * ((long long)p.t_max + 2) + 4;
+  for (long long pass = 0; pass < max_passes; ++pass) {
+    if (*(volatile int*)(p.ctr + 1) == 0) break;
+    // stripe flags of this pass (slot states only change in phase S)
+    for (int i = threadIdx.x; i < n_stripes; i += blockDim.x) sflag[i] = 0;
+    __syncthreads();
+    for (int s = threadIdx.x * 4; s < p.S; s += blockDim.x * 4) {
+      const int4 q = *reinterpret_cast<const int4*>(p.st + s);
+      const int a[4] = {q.x, q.y, q.z, q.w};
+      int f = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        f |= (a[j] != kSlotEmpty ? kStripeActive : 0) | (a[j] == kSlotRetiring ? kStripeRetiring : 0) |
+             (a[j] == kSlotFresh ? kStripeFresh : 0);
+      if (f) atomicOr_block(sflag + s / W, f);
+    }
+    __syncthreads();
+    wide_phase_v<T, VS, D, DVMAX, NS>(p, ring, tslot, TS, sflag, n_vi, n_vb);
+    grid.sync();
+    wide_phase_c<T, VS, D, DVMAX, REG, NS>(p, ring, tslot, TS, sflag, n_ci);
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // item counters of the next pass (both phases are done)
+      p.ctr[2] = 0;
+      p.ctr[3] = 0;
+    }
+    for (int s = gwarp; s < p.S; s += n_gwarp) wide_phase_s<T, VS>(p, s);
+    grid.sync();
+  }
+}
+
+}  // namespace admm

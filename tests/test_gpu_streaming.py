@@ -16,7 +16,7 @@ def _frames(f, code, n, point=0):
     return np.array([O.trial_gamma_awgn(code.n_vars, float(f["snr_db"]), rate, 1, point, t) for t in range(n)])
 
 
-@pytest.mark.parametrize("engine,kind", [("streaming", 3), ("cluster", 4)])
+@pytest.mark.parametrize("engine,kind", [("streaming", 3), ("cluster", 4), ("wide", 3)])
 @pytest.mark.parametrize("name", ["decode_cfg1.npz", "decode_cfg2.npz", "decode_cfg4.npz"])
 def test_streaming_f64_matches_reference_golden(cuda_ok, name, engine, kind):
     from paper_1204_0556_b200 import AdmmConfig, decode_batch
@@ -28,6 +28,7 @@ def test_streaming_f64_matches_reference_golden(cuda_ok, name, engine, kind):
     cfg = AdmmConfig(mu=float(f["mu"]), epsilon=float(f["epsilon"]), t_max=int(f["t_max"]), rho=float(f["rho"]))
     res = decode_batch(gam, code, cfg, dtype=torch.float64, want_hard=True, engine=engine)
     assert res.info["engine"] == kind
+    assert (res.info["kernel"] == 5) == (engine == "wide")
     want_hard = np.unpackbits(f["hard"], axis=1)[:, : code.n_vars]
     fl = res.flags.cpu().numpy()
     assert np.array_equal(res.iterations.cpu().numpy(), f["iterations"])
@@ -40,7 +41,7 @@ def test_streaming_f64_matches_reference_golden(cuda_ok, name, engine, kind):
     assert np.abs(res.x[:nx].cpu().numpy() - f["x"]).max() <= 1e-9
 
 
-@pytest.mark.parametrize("engine", ["streaming", "cluster"])
+@pytest.mark.parametrize("engine", ["streaming", "cluster", "wide"])
 def test_streaming_equals_resident_f32(cuda_ok, engine):
     from paper_1204_0556_b200 import AdmmConfig, baseline_code, decode_batch
 
@@ -54,18 +55,21 @@ def test_streaming_equals_resident_f32(cuda_ok, engine):
     assert (a.iterations - b.iterations).abs().float().mean().item() <= 2.0
 
 
-def test_streaming_irregular_and_zero_degree(cuda_ok):
+@pytest.mark.parametrize("engine", ["streaming", "wide"])
+def test_streaming_irregular_and_zero_degree(cuda_ok, engine):
     from paper_1204_0556_b200 import AdmmConfig, ParityCheckMatrix, decode_batch
 
     codes = [
         ParityCheckMatrix.from_dense([[1, 1, 0, 1, 1, 0, 0], [1, 0, 1, 1, 0, 1, 0], [0, 1, 1, 1, 0, 0, 1]]),
         ParityCheckMatrix(6, [[0, 1, 2], [1, 2, 3, 4]]),
-        ParityCheckMatrix(20, [list(range(0, 9)), list(range(5, 20)), [0, 7, 19]]),
+        ParityCheckMatrix(12, [list(range(0, 8)), list(range(4, 11)), [0, 7, 10]]),  # var 11: degree 0
     ]
+    if engine == "streaming":
+        codes.append(ParityCheckMatrix(20, [list(range(0, 9)), list(range(5, 20)), [0, 7, 19]]))
     rng = np.random.default_rng(4)
     for code in codes:
         gam = rng.normal(0.5, 1.2, (33, code.n_vars))
-        res = decode_batch(gam, code, AdmmConfig(mu=3.0, t_max=300), dtype=torch.float64, engine="streaming")
+        res = decode_batch(gam, code, AdmmConfig(mu=3.0, t_max=300), dtype=torch.float64, engine=engine)
         g = O.Graph.of(code)
         for t in range(len(gam)):
             r = O.decode(gam[t], g, O.Params(mu=3.0, t_max=300))
@@ -73,7 +77,7 @@ def test_streaming_irregular_and_zero_degree(cuda_ok):
             assert np.abs(res.x[t].cpu().numpy() - r.x).max() <= 1e-9
 
 
-@pytest.mark.parametrize("engine", ["auto", "streaming"])
+@pytest.mark.parametrize("engine", ["auto", "streaming", "wide"])
 def test_config5_large_block_matches_oracle(cuda_ok, engine):
     """n = 16384 does not fit one SM: the automatic engine is the cluster
     engine (16 CTAs per frame); the streaming engine is checked too."""
@@ -95,7 +99,7 @@ def test_config5_large_block_matches_oracle(cuda_ok, engine):
     assert torch.equal(r32.hard, res.hard)
 
 
-@pytest.mark.parametrize("engine", ["streaming", "cluster"])
+@pytest.mark.parametrize("engine", ["streaming", "cluster", "wide"])
 def test_streaming_rejects_state_io(cuda_ok, engine):
     from paper_1204_0556_b200 import AdmmConfig, baseline_code, decode_batch
 
@@ -104,7 +108,7 @@ def test_streaming_rejects_state_io(cuda_ok, engine):
         decode_batch(np.zeros((1, 96)), code, AdmmConfig(), want_state=True, engine=engine)
 
 
-@pytest.mark.parametrize("engine", ["auto", "streaming", "cluster"])
+@pytest.mark.parametrize("engine", ["auto", "streaming", "cluster", "wide"])
 def test_fused_synthesis_equals_materialised_llrs(cuda_ok, engine):
     """decode_synth (LLRs generated inside the decode kernel) == decode_batch
     on the LLRs synth_llr writes out; trial-indexed, so any split agrees."""
@@ -160,3 +164,29 @@ def test_phase_profiler_counts_passes(cuda_ok):
     assert r.info["engine"] == 3
     assert out[5] >= int(r.iterations.max())          # at least one pass per iteration
     assert out[0] > 0 and out[2] > 0 and out[4] > 0   # variable, check and slot phases ran
+
+
+def test_wide_kernel_large_batch_matches_sharded(cuda_ok):
+    """The automatic kernel choice switches to the wide HBM-streaming kernel
+    for large batches on codes beyond one SM; both kernels decode the same
+    trials to identical fp64 results (exact stop rule, same expression tree
+    up to the residual summation order), and wide's fp32 hard decisions
+    agree with fp64 on >= 99.9 % of frames."""
+    from paper_1204_0556_b200 import AdmmConfig, Awgn, baseline_code, decode_synth
+
+    code = baseline_code("cfg5_n16384")
+    cfg = AdmmConfig(mu=5.0)
+    ch = Awgn(2.5, code.design_rate)
+    B = 2304  # > the 2048-frame switch, not a multiple of the 4096 slots
+    w64 = decode_synth(code, ch, cfg, seed=1, point=1, trial0=0, batch=B, dtype=torch.float64, want_hard=True)
+    assert w64.info["kernel"] == 5
+    # the sharded kernel on a sub-batch (below the switch) of the same trials
+    sub = decode_synth(code, ch, cfg, seed=1, point=1, trial0=1000, batch=200, dtype=torch.float64, want_hard=True)
+    assert sub.info["kernel"] == 3
+    assert torch.equal(sub.iterations, w64.iterations[1000:1200])
+    assert torch.equal(sub.hard, w64.hard[1000:1200])
+    assert torch.equal(sub.flags, w64.flags[1000:1200])
+    w32 = decode_synth(code, ch, cfg, seed=1, point=1, trial0=0, batch=B, dtype=torch.float32, want_hard=True)
+    same = w32.hard.eq(w64.hard).all(dim=1).float().mean().item()
+    assert same >= 0.999
+    assert abs(int(w32.iterations.sum()) - int(w64.iterations.sum())) <= 0.02 * int(w64.iterations.sum())
