@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdlib>
 #include <stdint.h>
 
@@ -306,6 +307,10 @@ WideParams<T> make_wide_params(const StreamGraphArgs& g, const ResidentFrameArgs
   p.S = S;
   p.ncb = static_cast<int>(wide_ncb(g.n_checks));
   p.static_items = std::getenv("ADMM_B200_WIDE_STATIC") != nullptr;
+  const char* ck = std::getenv("ADMM_B200_WIDE_CHUNK");
+  p.chunk = ck ? std::max(1, std::atoi(ck)) : 1;
+  const char* ef = std::getenv("ADMM_B200_WIDE_L2EF");
+  p.l2_evict_first = ef ? std::atoi(ef) : 0;
   p.synth = a.synth;
   const WideLayout L(sizeof(T), g.n_edges, g.n_vars, p.ncb, S);
   char* base = static_cast<char*>(ws);

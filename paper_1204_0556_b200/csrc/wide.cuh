@@ -77,6 +77,8 @@ struct WideParams {
   int* weight_out;
   int S, ncb;
   int static_items;  // debug: static round-robin work items instead of the atomic feed
+  int chunk;         // work items per atomic grab
+  int l2_evict_first;  // L2 evict-first policy on the streamed rows
   T* zl;
   T* msg;
   T* x;
@@ -92,7 +94,7 @@ struct WideLayout {
   static size_t al(size_t b) { return (b + 255) & ~size_t(255); }
   WideLayout(size_t elem, long long E, long long N, long long ncb, long long S) {
     size_t o = 0;
-    zl = o; o += al(elem * 2 * E * S);
+    zl = o; o += al(elem * (elem == 4 ? 1 : 2) * E * S);  // fp32: z only (the message array holds z - lambda/mu)
     msg = o; o += al(elem * E * S);
     x = o; o += al(elem * N * S);
     gm = o; o += al(elem * N * S);
@@ -163,6 +165,35 @@ __device__ __forceinline__ void st_cs(V* p, const V& v) {
 // memory instead of registers.
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+// Same, with an L2 cache policy (evict_first for rows touched once per pass).
+__device__ __forceinline__ void cp_async16p(uint32_t dst, const void* src, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void cp_async8p(uint32_t dst, const void* src, uint64_t pol) {
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint64_t l2_evict_first_policy(bool on) {
+  uint64_t pol;
+  if (on)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async_vec_ef(uint32_t dst, const void* src, uint64_t pol) {
+  if constexpr (BYTES == 32) {
+    cp_async16p(dst, src, pol);
+    cp_async16p(dst + 16, static_cast<const char*>(src) + 16, pol);
+  } else if constexpr (BYTES == 16) {
+    cp_async16p(dst, src, pol);
+  } else if constexpr (BYTES == 8) {
+    cp_async8p(dst, src, pol);
+  } else {
+    static_assert(BYTES == 4, "vector size");
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "l"(pol) : "memory");
+  }
 }
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
@@ -235,6 +266,7 @@ struct ItemFeed {
   int* ctr;
   int n_items, nblk;
   int stat_next, stat_step;  // static assignment (debug): stat_step > 0
+  int chunk;
   int id1;         // next item (its table is in reg)
   int raw2;        // lane 0: atomic result for the item after (in flight)
   int reg[NR];
@@ -258,26 +290,43 @@ struct ItemFeed {
     __syncwarp();  // every lane is done reading the slot's previous table
 #pragma unroll
     for (int r = 0; r < NR; ++r) slot[r * 32 + (threadIdx.x & 31)] = reg[r];
-    if ((threadIdx.x & 31) == 0) slot[TB] = id;
+    if ((threadIdx.x & 31) == 0) {
+      slot[TB] = id;
+      slot[TB + 1] = id / nblk;  // stripe
+      slot[TB + 2] = id % nblk;  // block within the stripe
+    }
     __syncwarp();
+  }
+  // Items come in chunks of `chunk` consecutive ids per atomic (the
+  // counter is one address hammered by every warp); the next chunk's
+  // atomic is always in flight one chunk ahead.
+  int cbase, pos;
+  __device__ __forceinline__ int pull() {
+    if (pos == chunk) {
+      cbase = __shfl_sync(0xffffffffu, raw2, 0);
+      raw2 = grab_raw();
+      pos = 0;
+    }
+    return cbase * chunk + pos++;
   }
   // First item: published into slot0; returns its id.
   __device__ __forceinline__ int start(int* slot0) {
-    const int a = __shfl_sync(0xffffffffu, grab_raw(), 0);
-    id1 = __shfl_sync(0xffffffffu, grab_raw(), 0);
+    cbase = __shfl_sync(0xffffffffu, grab_raw(), 0);
+    pos = 0;
+    raw2 = grab_raw();
+    const int a = pull();
     load(a);
     publish(slot0, a);
+    id1 = pull();
     load(id1);
-    raw2 = grab_raw();
     return a;
   }
   // Move to the next item: publish it into `slot`, prefetch the one after.
   __device__ __forceinline__ int advance(int* slot) {
     const int cur = id1;
     publish(slot, cur);
-    id1 = __shfl_sync(0xffffffffu, raw2, 0);
+    id1 = pull();
     load(id1);
-    raw2 = grab_raw();
     return cur;
   }
 };
@@ -286,7 +335,7 @@ struct ItemFeed {
 // ring of NS stages.
 template <int D, int DVMAX>
 __host__ __device__ constexpr int wide_tstride() {
-  return (wide_ct(D) > wide_vt(DVMAX) ? wide_ct(D) : wide_vt(DVMAX)) + 4;
+  return (wide_ct(D) > wide_vt(DVMAX) ? wide_ct(D) : wide_vt(DVMAX)) + 4;  // + id, stripe, block
 }
 template <typename T, int VS, int D, int DVMAX, int NS>
 __host__ __device__ constexpr int wide_warp_bytes() {
@@ -298,7 +347,7 @@ __host__ __device__ constexpr int wide_smem_bytes() {
 }
 
 // ---- phase V: x = clip((sum msg - gamma/mu) / deg) (admm_decoder.py:108-124) ----
-template <typename T, int VS, int D, int DVMAX, int NS>
+template <typename T, int VS, int D, int DVMAX, bool REG, int NS>
 __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned char* ring, int* tslot, int tstride,
                                              const int* sflag, int n_vi, int n_vb) {
   using V = WVec<T, VS>;
@@ -312,17 +361,19 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
   V* gm = reinterpret_cast<V*>(p.gm);
   const uint32_t ring_s = smem_u32(ring);
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  ItemFeed<TB> feed{p.vtbl, p.ctr + 2, n_vi, n_vb, gw, p.static_items ? (int)((gridDim.x * blockDim.x) >> 5) : 0};
+  const uint64_t pol = l2_evict_first_policy(p.l2_evict_first);
+  ItemFeed<TB> feed{p.vtbl, p.ctr + 2, n_vi, n_vb, gw, p.static_items ? (int)((gridDim.x * blockDim.x) >> 5) : 0,
+                    p.chunk};
   int ik = 0, iq = 0, ti = 0;
   int iid = feed.start(tslot);
 
   auto issue_next = [&]() {
     if (iid < n_vi) {
-      const int stripe = iid / n_vb, vb = iid % n_vb;
+      const int* tb = tslot + (ik & 1) * tstride;
+      const int stripe = tb[TB + 1], vb = tb[TB + 2];
       const int fl = sflag[stripe];
       const int i0 = vb * kWideVB + iq * VBB, i1 = min(p.n_vars, min((vb + 1) * kWideVB, i0 + VBB));
       if ((fl & kStripeActive) && i0 < i1) {
-        const int* tb = tslot + (ik & 1) * tstride;
         const uint32_t st = ring_s + (ti % NS) * G::bytes;
         cp_async_vec<4 * VS>(st + lane * 4 * VS, p.st + stripe * W + lane * VS);
         const long long rb = (long long)stripe * N * 32 + lane;
@@ -334,9 +385,9 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
 #pragma unroll
             for (int j = 0; j < DVMAX; ++j) {
               const int e = tb[(iq * VBB + b) * DVMAX + j];
-              if (e >= 0) cp_async_vec<VB>(rowb + j * 32 * VB, msg + ((long long)stripe * E + e) * 32 + lane);
+              if (e >= 0) cp_async_vec_ef<VB>(rowb + j * 32 * VB, msg + ((long long)stripe * E + e) * 32 + lane, pol);
             }
-            cp_async_vec<VB>(rowb + DVMAX * 32 * VB, gm + rb + (long long)i * 32);
+            cp_async_vec_ef<VB>(rowb + DVMAX * 32 * VB, gm + rb + (long long)i * 32, pol);
             if (fl & kStripeRetiring) cp_async_vec<VB>(rowb + (DVMAX + 1) * 32 * VB, x + rb + (long long)i * 32);
           }
         }
@@ -360,17 +411,18 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
     if (cid >= n_vi) break;
     issue_next();
     cp_wait<NS - 1>();
-    const int stripe = cid / n_vb, vb = cid % n_vb;
+    const int stripe = tb[TB + 1], vb = tb[TB + 2];
     const int fl = sflag[stripe];
     const int i0 = vb * kWideVB + cq * VBB, i1 = min(p.n_vars, min((vb + 1) * kWideVB, i0 + VBB));
     if (!(fl & kStripeActive) || i0 >= i1) continue;
     const unsigned char* st = ring + (t % NS) * G::bytes;
     const VI stv = lds_vec<VI>(st + lane * 4 * VS);
     const int s0 = stripe * W + lane * VS;
-    bool anyupd = false, anyfresh = false, anyret = false;
+    bool anyupd = false, anyfresh = false, anyret = false, allrun = true;
     long long fr[VS];
 #pragma unroll
     for (int l = 0; l < VS; ++l) {
+      allrun &= stv.v[l] == kSlotRunning;
       anyupd |= stv.v[l] == kSlotRunning || stv.v[l] == kSlotFresh;
       anyfresh |= stv.v[l] == kSlotFresh;
       anyret |= stv.v[l] == kSlotRetiring;
@@ -389,13 +441,26 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
       V mv[DVMAX];
 #pragma unroll
       for (int j = 0; j < DVMAX; ++j) {
-        const bool on = tb[(cq * VBB + b) * DVMAX + j] >= 0;
+        const bool on = REG || tb[(cq * VBB + b) * DVMAX + j] >= 0;
         deg += on;
         if (on) mv[j] = lds_vec<V>(rowb + j * 32 * VB);
       }
       V g = lds_vec<V>(rowb + DVMAX * 32 * VB);
       V xn;
       if (anyret) xn = lds_vec<V>(rowb + (DVMAX + 1) * 32 * VB);
+      if (allrun) {
+        // every slot of the thread running: the plain x-update
+#pragma unroll
+        for (int l = 0; l < VS; ++l) {
+          T acc = T(0);
+#pragma unroll
+          for (int j = 0; j < DVMAX; ++j)
+            if (j < deg) acc = add_rn(acc, mv[j].v[l]);  // increasing edge id (np.bincount order)
+          xn.v[l] = deg > 0 ? clip01(div_rn(sub_rn(acc, g.v[l]), T(deg))) : (g.v[l] < T(0) ? T(1) : T(0));
+        }
+        wst(x + rb + (long long)i * 32, xn);
+        continue;
+      }
 #pragma unroll
       for (int l = 0; l < VS; ++l) {
         const int state = stv.v[l];
@@ -436,6 +501,20 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
   cp_wait<0>();
 }
 
+// Edge-state store of phase C: (z, lambda/mu) pairs, or z alone (ZM).
+template <typename T, int VS, bool ZM>
+__device__ __forceinline__ void wide_store_z(WVec<T, 2 * VS>* zl, WVec<T, VS>* zv, long long row,
+                                             const WVec<T, 2 * VS>& v) {
+  if constexpr (ZM) {
+    WVec<T, VS> z;
+#pragma unroll
+    for (int l = 0; l < VS; ++l) z.v[l] = v.v[l];
+    st_cs(zv + row, z);
+  } else {
+    st_cs(zl + row, v);
+  }
+}
+
 // ---- phase C: fused z-update, projection, residuals, lambda-update, message
 // (admm_decoder.py:127-149, parity_polytope.py:352-421) ----
 template <typename T, int VS, int D, int DVMAX, bool REG, int NS>
@@ -449,20 +528,27 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
   const int lane = threadIdx.x & 31;
   const long long E = p.n_edges, N = p.n_vars;
   const V* x = reinterpret_cast<const V*>(p.x);
+  // fp32 keeps (z, message) per edge and recovers lambda/mu = z - message:
+  // 20 instead of 24 bytes of edge state traffic per edge-update.  fp64 (the
+  // parity mode) keeps (z, lambda/mu) and writes the message separately.
+  constexpr bool ZM = sizeof(T) == 4;
   V2* zl = reinterpret_cast<V2*>(p.zl);
+  V* zv = reinterpret_cast<V*>(p.zl);
   V* msg = reinterpret_cast<V*>(p.msg);
   const int ncb = p.ncb;
   const uint32_t ring_s = smem_u32(ring);
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  ItemFeed<TB> feed{p.ctbl, p.ctr + 3, n_ci, ncb, gw, p.static_items ? (int)((gridDim.x * blockDim.x) >> 5) : 0};
+  const uint64_t pol = l2_evict_first_policy(p.l2_evict_first);
+  ItemFeed<TB> feed{p.ctbl, p.ctr + 3, n_ci, ncb, gw, p.static_items ? (int)((gridDim.x * blockDim.x) >> 5) : 0,
+                    p.chunk};
   int ik = 0, iq = 0, ti = 0;
   int iid = feed.start(tslot);
 
   auto issue_next = [&]() {
     if (iid < n_ci) {
-      const int stripe = iid / ncb, c = (iid % ncb) * CB + iq;
+      const int* tb = tslot + (ik & 1) * tstride;
+      const int stripe = tb[TB + 1], c = tb[TB + 2] * CB + iq;
       if ((sflag[stripe] & kStripeActive) && c < p.n_checks) {
-        const int* tb = tslot + (ik & 1) * tstride;
         const uint32_t st = ring_s + (ti % NS) * G::bytes;
         cp_async_vec<4 * VS>(st + lane * 4 * VS, p.st + stripe * W + lane * VS);
         const long long e0 = tb[D * CB + iq];
@@ -472,7 +558,12 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
           const int v = tb[k * CB + iq];
           if (v >= 0) {
             cp_async_vec<VB>(st + G::CX + (k * 32 + lane) * VB, x + xb + (long long)v * 32);
-            cp_async_vec<2 * VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zl + eb + (e0 + k) * 32);
+            if constexpr (ZM) {
+              cp_async_vec_ef<VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zv + eb + (e0 + k) * 32, pol);
+              cp_async_vec_ef<VB>(st + G::CZ + (k * 32 + lane) * 2 * VB + VB, msg + eb + (e0 + k) * 32, pol);
+            } else {
+              cp_async_vec_ef<2 * VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zl + eb + (e0 + k) * 32, pol);
+            }
           }
         }
       }
@@ -502,19 +593,22 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
     if (cid >= n_ci) break;
     issue_next();
     cp_wait<NS - 1>();
-    const int stripe = cid / ncb, cb = cid % ncb, c = cb * CB + cq;
+    const int stripe = tb[TB + 1], cb = tb[TB + 2], c = cb * CB + cq;
     if (!(sflag[stripe] & kStripeActive) || c >= p.n_checks) continue;
     const unsigned char* st = ring + (t % NS) * G::bytes;
     const VI stv = lds_vec<VI>(st + lane * 4 * VS);
-    bool anyupd = false, anyret = false;
+    bool anyupd = false, anyret = false, allrun = true;
 #pragma unroll
     for (int l = 0; l < VS; ++l) {
+      allrun &= stv.v[l] == kSlotRunning;
       anyupd |= stv.v[l] == kSlotRunning || stv.v[l] == kSlotFresh;
       anyret |= stv.v[l] == kSlotRetiring;
     }
-    int d = 0;
+    int d = REG ? D : 0;
+    if constexpr (!REG) {
 #pragma unroll
-    for (int k = 0; k < D; ++k) d += tb[k * CB + cq] >= 0;
+      for (int k = 0; k < D; ++k) d += tb[k * CB + cq] >= 0;
+    }
     const long long e0 = tb[D * CB + cq];
     const long long eb = (long long)stripe * E * 32 + lane;
     V gx[D];
@@ -530,11 +624,54 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
           for (int l = 0; l < VS; ++l) odd[l] ^= gx[k].v[l] > T(0.5);
         }
     }
-    if (anyupd) {
+    if (REG && allrun) {
+      // every slot of the thread running: the plain fused check update
+      V2 zlv[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        zlv[k] = lds_vec<V2>(st + G::CZ + (k * 32 + lane) * 2 * VB);
+        if constexpr (ZM) {
+#pragma unroll
+          for (int l = 0; l < VS; ++l) zlv[k].v[VS + l] = sub_rn(zlv[k].v[l], zlv[k].v[VS + l]);
+        }
+      }
+#pragma unroll
+      for (int l = 0; l < VS; ++l) {
+        T w_[D], u[D], zn[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          w_[k] = add_rn(mul_rn(p.rho, gx[k].v[l]), mul_rn(p.one_minus_rho, zlv[k].v[l]));
+          u[k] = add_rn(w_[k], zlv[k].v[VS + l]);  // scaled dual lambda/mu
+        }
+        project_pp_fixed<T, D>(u, zn);
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          const T r1 = sub_rn(gx[k].v[l], zn[k]);
+          const T r2 = sub_rn(zn[k], zlv[k].v[l]);
+          primal[l] = add_rn(primal[l], mul_rn(r1, r1));
+          moved[l] = add_rn(moved[l], mul_rn(r2, r2));
+          const T lnew = add_rn(zlv[k].v[VS + l], sub_rn(w_[k], zn[k]));
+          zlv[k].v[l] = zn[k];
+          zlv[k].v[VS + l] = lnew;
+          gx[k].v[l] = sub_rn(zn[k], lnew);  // message
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        wide_store_z<T, VS, ZM>(zl, zv, eb + (e0 + k) * 32, zlv[k]);
+        st_cs(msg + eb + (e0 + k) * 32, gx[k]);
+      }
+    } else if (anyupd) {
       V2 zlv[D];
 #pragma unroll
       for (int k = 0; k < D; ++k)
-        if (k < d) zlv[k] = lds_vec<V2>(st + G::CZ + (k * 32 + lane) * 2 * VB);
+        if (k < d) {
+          zlv[k] = lds_vec<V2>(st + G::CZ + (k * 32 + lane) * 2 * VB);
+          if constexpr (ZM) {
+#pragma unroll
+            for (int l = 0; l < VS; ++l) zlv[k].v[VS + l] = sub_rn(zlv[k].v[l], zlv[k].v[VS + l]);
+          }
+        }
 #pragma unroll
       for (int l = 0; l < VS; ++l) {
         const bool run = stv.v[l] == kSlotRunning;
@@ -573,7 +710,7 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
 #pragma unroll
       for (int k = 0; k < D; ++k)
         if (k < d) {
-          st_cs(zl + eb + (e0 + k) * 32, zlv[k]);
+          wide_store_z<T, VS, ZM>(zl, zv, eb + (e0 + k) * 32, zlv[k]);
           st_cs(msg + eb + (e0 + k) * 32, gx[k]);
         }
     }
@@ -708,7 +845,7 @@ __global__ void __launch_bounds__(kWideThreads, MINB) wide_decode_kernel(const W
       if (f) atomicOr_block(sflag + s / W, f);
     }
     __syncthreads();
-    wide_phase_v<T, VS, D, DVMAX, NS>(p, ring, tslot, TS, sflag, n_vi, n_vb);
+    wide_phase_v<T, VS, D, DVMAX, REG, NS>(p, ring, tslot, TS, sflag, n_vi, n_vb);
     grid.sync();
     wide_phase_c<T, VS, D, DVMAX, REG, NS>(p, ring, tslot, TS, sflag, n_ci);
     grid.sync();
