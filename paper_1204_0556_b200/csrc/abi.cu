@@ -708,7 +708,8 @@ size_t admm_workspace_bytes(const admm_graph* g, int dtype, int64_t batch) {
     if (dtype < 0 || dtype > 1) return 0;
     if (use_wide(g, dtype, batch)) {
       const int S = wide_slots(g, dtype, batch);
-      return admm::WideLayout(dtype ? 8 : 4, g->n_edges, g->n_vars, admm::wide_ncb(g->n_checks), S).total;
+      // upper bound: the synthesis buffer is only laid out for admm_decode_synth
+      return admm::WideLayout(dtype ? 8 : 4, g->n_edges, g->n_vars, admm::wide_ncb(g->n_checks), S, true).total;
     }
     const int S = stream_slots(g, dtype, batch);
     if (g->shard_ok[dtype]) return admm::StreamLayout(dtype ? 8 : 4, g->n_edges, g->n_vars, g->shard_G, S, true).total;

@@ -307,19 +307,16 @@ WideParams<T> make_wide_params(const StreamGraphArgs& g, const ResidentFrameArgs
   p.S = S;
   p.ncb = static_cast<int>(wide_ncb(g.n_checks));
   p.static_items = std::getenv("ADMM_B200_WIDE_STATIC") != nullptr;
-  const char* ck = std::getenv("ADMM_B200_WIDE_CHUNK");
-  p.chunk = ck ? std::max(1, std::atoi(ck)) : 1;
-  const char* ef = std::getenv("ADMM_B200_WIDE_L2EF");
-  p.l2_evict_first = ef ? std::atoi(ef) : 0;
+
   p.synth = a.synth;
-  const WideLayout L(sizeof(T), g.n_edges, g.n_vars, p.ncb, S);
+  const WideLayout L(sizeof(T), g.n_edges, g.n_vars, p.ncb, S, a.synth.kind != 0);
   char* base = static_cast<char*>(ws);
   p.zl = reinterpret_cast<T*>(base + L.zl);
   p.msg = reinterpret_cast<T*>(base + L.msg);
   p.x = reinterpret_cast<T*>(base + L.x);
   p.gm = reinterpret_cast<T*>(base + L.gm);
   p.part = reinterpret_cast<T*>(base + L.part);
-  p.frame = reinterpret_cast<long long*>(base + L.frame);
+  p.gfr = a.synth.kind != 0 ? reinterpret_cast<T*>(base + L.gfr) : nullptr;
   int* ib = reinterpret_cast<int*>(base + L.ints);
   p.st = ib;
   p.tcount = ib + S;
@@ -327,7 +324,10 @@ WideParams<T> make_wide_params(const StreamGraphArgs& g, const ResidentFrameArgs
   p.weight = ib + 3 * S;
   p.nonint = ib + 4 * S;
   p.odd = ib + 5 * S;
-  p.ctr = ib + 6 * S;
+  p.frame = ib + 6 * S;
+  p.fnext = ib + 7 * S;
+  p.slist = ib + 8 * S;
+  p.ctr = ib + 9 * S;
   return p;
 }
 

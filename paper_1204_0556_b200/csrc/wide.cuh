@@ -77,30 +77,31 @@ struct WideParams {
   int* weight_out;
   int S, ncb;
   int static_items;  // debug: static round-robin work items instead of the atomic feed
-  int chunk;         // work items per atomic grab
-  int l2_evict_first;  // L2 evict-first policy on the streamed rows
   T* zl;
   T* msg;
   T* x;
   T* gm;
   T* part;
-  long long* frame;
+  T* gfr;    // [S][N] LLRs of the slots' next frames (in-kernel synthesis only)
+  int* frame;  // [S] frame of the slot
+  int* fnext;  // [S] frame that follows a retiring slot's frame (-1 = none)
+  int* slist;  // [S] slots whose next frame's LLRs are synthesised in the coming pass
   int *st, *tcount, *conv, *weight, *nonint, *odd, *ctr;
   SynthParams synth;
 };
 
 struct WideLayout {
-  size_t zl, msg, x, gm, part, frame, ints, total;
+  size_t zl, msg, x, gm, part, gfr, ints, total;
   static size_t al(size_t b) { return (b + 255) & ~size_t(255); }
-  WideLayout(size_t elem, long long E, long long N, long long ncb, long long S) {
+  WideLayout(size_t elem, long long E, long long N, long long ncb, long long S, bool synth) {
     size_t o = 0;
     zl = o; o += al(elem * (elem == 4 ? 1 : 2) * E * S);  // fp32: z only (the message array holds z - lambda/mu)
     msg = o; o += al(elem * E * S);
     x = o; o += al(elem * N * S);
     gm = o; o += al(elem * N * S);
     part = o; o += al(elem * 2 * ncb * S);
-    frame = o; o += al(sizeof(long long) * S);
-    ints = o; o += al(sizeof(int) * (6 * S + 8));
+    gfr = o; o += synth ? al(elem * N * S) : 0;
+    ints = o; o += al(sizeof(int) * (9 * S + 16));
     total = o;
   }
 };
@@ -226,50 +227,56 @@ __device__ __forceinline__ V lds_vec(const unsigned char* p) {
 }
 
 // Stripe flags, rebuilt in shared memory by every CTA at the start of a pass.
-enum : int { kStripeActive = 1, kStripeRetiring = 2, kStripeFresh = 4 };
+enum : int { kStripeActive = 1 };
 constexpr int kWideMaxStripes = 256;
 
-// Stage geometry.  A stage holds one task: the item's slot states (32 lanes
-// x VS ints), then for a check task D x-rows and D z/lambda rows, for a
-// variable task VBB variables x (DVMAX message rows, gamma/mu, x) -- each
-// row 32 lanes x one vector.
+// Stage geometry.  A stage holds one task: for a check task D x-rows and D
+// edge-state rows, for a variable task VBB variables x (DVMAX message rows,
+// gamma/mu, x, fresh LLR) -- each row 32 lanes x one vector.
 template <typename T, int VS, int D, int DVMAX>
 struct WideStage {
   static constexpr int VB = VS * static_cast<int>(sizeof(T));  // bytes per lane per row
-  static constexpr int HB = 32 * VS * 4;                        // slot states
-  static constexpr int CX = HB, CZ = HB + D * 32 * VB;          // check task: x rows, z/lambda rows
+  static constexpr int CX = 0, CZ = D * 32 * VB;                 // check task: x rows, edge-state rows
   static constexpr int CBYTES = D * 32 * 3 * VB;
-  static constexpr int VBB = (3 * D) / (DVMAX + 2) > 0 ? (3 * D) / (DVMAX + 2) : 1;
-  static constexpr int VROWS = DVMAX + 2;                       // messages, gamma/mu, x
+  static constexpr int VROWS = DVMAX + 3;                        // messages, gamma/mu, x, fresh LLRs
+  static constexpr int VBB = (3 * D) / VROWS > 0 ? (3 * D) / VROWS : 1;
   static constexpr int VBYTES = VBB * VROWS * 32 * VB;
-  static constexpr int bytes = (HB + (CBYTES > VBYTES ? CBYTES : VBYTES) + 15) / 16 * 16;
+  static constexpr int bytes = ((CBYTES > VBYTES ? CBYTES : VBYTES) + 15) / 16 * 16;
 };
-
 
 // ---- work items ----
 // Items are (stripe, block of kWideVB variables) in phase V and (stripe,
 // block of kWideCB checks) in phase C, numbered stripe-major.  Warps take
-// them dynamically from a global counter (ctr[2] / ctr[3]): item costs vary
-// (fresh frames synthesise their LLRs, retiring frames write outputs,
-// empty stripes cost nothing), and a static split left a quarter of the SM
-// time waiting at the grid syncs.  The graph indices of a block are a
-// precomputed table (wide_ct / wide_vt ints) loaded with one coalesced
-// access per lane and published to the warp's shared-memory table slot, so
-// no address computation waits on a dependent index load.
+// them dynamically from a global counter (ctr[2] / ctr[3]): a static split
+// left a quarter of the SM time waiting at the grid syncs.  For the item
+// after the current one the feed prefetches (into registers) the block's
+// precomputed index table (wide_ct / wide_vt ints, one coalesced access per
+// lane) and the lane's slot states and frames, and publishes them to the
+// warp's shared-memory table slot when the item starts: no copy issue and
+// no compute step ever waits on a dependent index or state load.
 __host__ __device__ constexpr int wide_ct(int D) { return ((D + 1) * kWideCB + 31) / 32 * 32; }
 __host__ __device__ constexpr int wide_vt(int DV) { return (kWideVB * DV + 31) / 32 * 32; }
 
-template <int TB>
+// Table slot: [TB index ints][id, stripe, block, -][32 x VS states][32 x VS frames]
+template <int D, int DVMAX, int VS>
+__host__ __device__ constexpr int wide_tstride() {
+  return (wide_ct(D) > wide_vt(DVMAX) ? wide_ct(D) : wide_vt(DVMAX)) + 4 + 64 * VS;
+}
+
+template <int TB, int VS>
 struct ItemFeed {
   static constexpr int NR = TB / 32;
+  using VI = WVec<int, VS>;
   const int* tbl;  // [n_blocks][TB]
   int* ctr;
-  int n_items, nblk;
+  int n_items, nblk, W;
+  const int* st;
+  const int* frame;
   int stat_next, stat_step;  // static assignment (debug): stat_step > 0
-  int chunk;
-  int id1;         // next item (its table is in reg)
-  int raw2;        // lane 0: atomic result for the item after (in flight)
+  int id1;                   // next item (its table/states are in registers)
+  int raw2;                  // lane 0: atomic result for the item after (in flight)
   int reg[NR];
+  VI sreg, freg;
 
   __device__ __forceinline__ int grab_raw() {
     if (stat_step > 0) {
@@ -281,72 +288,88 @@ struct ItemFeed {
   }
   __device__ __forceinline__ void load(int id) {
     if (id < n_items) {
-      const int* t = tbl + (long long)(id % nblk) * TB + (threadIdx.x & 31);
+      const int lane = threadIdx.x & 31;
+      const int* t = tbl + (long long)(id % nblk) * TB + lane;
 #pragma unroll
       for (int r = 0; r < NR; ++r) reg[r] = __ldg(t + r * 32);
+      const int s0 = (id / nblk) * W + lane * VS;
+      sreg = *reinterpret_cast<const VI*>(st + s0);
+      freg = *reinterpret_cast<const VI*>(frame + s0);
     }
   }
   __device__ __forceinline__ void publish(int* slot, int id) {
-    __syncwarp();  // every lane is done reading the slot's previous table
+    const int lane = threadIdx.x & 31;
+    __syncwarp();  // every lane is done reading the slot's previous contents
 #pragma unroll
-    for (int r = 0; r < NR; ++r) slot[r * 32 + (threadIdx.x & 31)] = reg[r];
-    if ((threadIdx.x & 31) == 0) {
+    for (int r = 0; r < NR; ++r) slot[r * 32 + lane] = reg[r];
+    if (lane == 0) {
       slot[TB] = id;
       slot[TB + 1] = id / nblk;  // stripe
       slot[TB + 2] = id % nblk;  // block within the stripe
     }
+    *reinterpret_cast<VI*>(slot + TB + 4 + lane * VS) = sreg;
+    *reinterpret_cast<VI*>(slot + TB + 4 + 32 * VS + lane * VS) = freg;
     __syncwarp();
-  }
-  // Items come in chunks of `chunk` consecutive ids per atomic (the
-  // counter is one address hammered by every warp); the next chunk's
-  // atomic is always in flight one chunk ahead.
-  int cbase, pos;
-  __device__ __forceinline__ int pull() {
-    if (pos == chunk) {
-      cbase = __shfl_sync(0xffffffffu, raw2, 0);
-      raw2 = grab_raw();
-      pos = 0;
-    }
-    return cbase * chunk + pos++;
   }
   // First item: published into slot0; returns its id.
   __device__ __forceinline__ int start(int* slot0) {
-    cbase = __shfl_sync(0xffffffffu, grab_raw(), 0);
-    pos = 0;
-    raw2 = grab_raw();
-    const int a = pull();
+    const int a = __shfl_sync(0xffffffffu, grab_raw(), 0);
+    id1 = __shfl_sync(0xffffffffu, grab_raw(), 0);
     load(a);
     publish(slot0, a);
-    id1 = pull();
     load(id1);
+    raw2 = grab_raw();
     return a;
   }
   // Move to the next item: publish it into `slot`, prefetch the one after.
   __device__ __forceinline__ int advance(int* slot) {
     const int cur = id1;
     publish(slot, cur);
-    id1 = pull();
+    id1 = __shfl_sync(0xffffffffu, raw2, 0);
     load(id1);
+    raw2 = grab_raw();
     return cur;
   }
 };
 
-// Shared memory: stripe flags, then per warp two index-table slots and the
-// ring of NS stages.
-template <int D, int DVMAX>
-__host__ __device__ constexpr int wide_tstride() {
-  return (wide_ct(D) > wide_vt(DVMAX) ? wide_ct(D) : wide_vt(DVMAX)) + 4;  // + id, stripe, block
-}
+// Shared memory: stripe flags, then per warp two table slots and the ring of
+// NS stages.
 template <typename T, int VS, int D, int DVMAX, int NS>
 __host__ __device__ constexpr int wide_warp_bytes() {
-  return 2 * 4 * wide_tstride<D, DVMAX>() + NS * WideStage<T, VS, D, DVMAX>::bytes;
+  return 2 * 4 * wide_tstride<D, DVMAX, VS>() + NS * WideStage<T, VS, D, DVMAX>::bytes;
 }
 template <typename T, int VS, int D, int DVMAX, int NS>
 __host__ __device__ constexpr int wide_smem_bytes() {
   return kWideMaxStripes * 4 + (kWideThreads / 32) * wide_warp_bytes<T, VS, D, DVMAX, NS>();
 }
 
+// LLRs of the next frames of the slots retired in the last pass (in-kernel
+// synthesis): written slot-major, one lane per variable, while the slots
+// spend their retiring pass, so the first x-update of the new frame reads
+// them like a stored LLR vector instead of running Philox + Box-Muller on a
+// few lanes of every warp.
+constexpr int kWideSynthChunk = 2048;
+
+template <typename T>
+__device__ __forceinline__ void wide_synth_items(const WideParams<T>& p, int nlist) {
+  const int lane = threadIdx.x & 31;
+  const int nch = (p.n_vars + kWideSynthChunk - 1) / kWideSynthChunk;
+  const int n = nlist * nch;
+  for (;;) {
+    const int q = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(p.ctr + 4, 1) : 0, 0);
+    if (q >= n) break;
+    const int s = p.slist[q / nch], c = q % nch;
+    const int f = p.fnext[s];
+    const int i1 = min(p.n_vars, (c + 1) * kWideSynthChunk);
+    for (int i = c * kWideSynthChunk + lane; i < i1; i += 32)
+      p.gfr[(long long)s * p.n_vars + i] = static_cast<T>(synth_llr(p.synth, p.synth.trial0 + f, i));
+  }
+}
+
 // ---- phase V: x = clip((sum msg - gamma/mu) / deg) (admm_decoder.py:108-124) ----
+// One code path for every slot state (per-lane selects): a FRESH slot sums no
+// messages and takes gamma/mu from its frame's LLR vector; a RETIRING slot
+// keeps x and accumulates the output statistics (make_output, :92-105).
 template <typename T, int VS, int D, int DVMAX, bool REG, int NS>
 __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned char* ring, int* tslot, int tstride,
                                              const int* sflag, int n_vi, int n_vb) {
@@ -354,6 +377,7 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
   using VI = WVec<int, VS>;
   using G = WideStage<T, VS, D, DVMAX>;
   constexpr int W = 32 * VS, VBB = G::VBB, TPI = (kWideVB + VBB - 1) / VBB, VB = G::VB, TB = wide_vt(DVMAX);
+  constexpr int ES = static_cast<int>(sizeof(T));
   const int lane = threadIdx.x & 31;
   const long long E = p.n_edges, N = p.n_vars;
   const V* msg = reinterpret_cast<const V*>(p.msg);
@@ -361,9 +385,8 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
   V* gm = reinterpret_cast<V*>(p.gm);
   const uint32_t ring_s = smem_u32(ring);
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t pol = l2_evict_first_policy(p.l2_evict_first);
-  ItemFeed<TB> feed{p.vtbl, p.ctr + 2, n_vi, n_vb, gw, p.static_items ? (int)((gridDim.x * blockDim.x) >> 5) : 0,
-                    p.chunk};
+  ItemFeed<TB, VS> feed{p.vtbl, p.ctr + 2, n_vi, n_vb, W, p.st, p.frame, gw,
+                        p.static_items ? (int)((gridDim.x * blockDim.x) >> 5) : 0};
   int ik = 0, iq = 0, ti = 0;
   int iid = feed.start(tslot);
 
@@ -371,24 +394,34 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
     if (iid < n_vi) {
       const int* tb = tslot + (ik & 1) * tstride;
       const int stripe = tb[TB + 1], vb = tb[TB + 2];
-      const int fl = sflag[stripe];
       const int i0 = vb * kWideVB + iq * VBB, i1 = min(p.n_vars, min((vb + 1) * kWideVB, i0 + VBB));
-      if ((fl & kStripeActive) && i0 < i1) {
+      if ((sflag[stripe] & kStripeActive) && i0 < i1) {
+        const VI stv = *reinterpret_cast<const VI*>(tb + TB + 4 + lane * VS);
+        const VI frv = *reinterpret_cast<const VI*>(tb + TB + 4 + 32 * VS + lane * VS);
+        bool anyret = false;
+#pragma unroll
+        for (int l = 0; l < VS; ++l) anyret |= stv.v[l] == kSlotRetiring;
         const uint32_t st = ring_s + (ti % NS) * G::bytes;
-        cp_async_vec<4 * VS>(st + lane * 4 * VS, p.st + stripe * W + lane * VS);
         const long long rb = (long long)stripe * N * 32 + lane;
 #pragma unroll
         for (int b = 0; b < VBB; ++b) {
           const int i = i0 + b;
           if (i < i1) {
-            const uint32_t rowb = st + G::HB + b * G::VROWS * 32 * VB + lane * VB;
+            const uint32_t rowb = st + b * G::VROWS * 32 * VB + lane * VB;
 #pragma unroll
             for (int j = 0; j < DVMAX; ++j) {
               const int e = tb[(iq * VBB + b) * DVMAX + j];
-              if (e >= 0) cp_async_vec_ef<VB>(rowb + j * 32 * VB, msg + ((long long)stripe * E + e) * 32 + lane, pol);
+              if (e >= 0) cp_async_vec<VB>(rowb + j * 32 * VB, msg + ((long long)stripe * E + e) * 32 + lane);
             }
-            cp_async_vec_ef<VB>(rowb + DVMAX * 32 * VB, gm + rb + (long long)i * 32, pol);
-            if (fl & kStripeRetiring) cp_async_vec<VB>(rowb + (DVMAX + 1) * 32 * VB, x + rb + (long long)i * 32);
+            cp_async_vec<VB>(rowb + DVMAX * 32 * VB, gm + rb + (long long)i * 32);
+            if (anyret) cp_async_vec<VB>(rowb + (DVMAX + 1) * 32 * VB, x + rb + (long long)i * 32);
+#pragma unroll
+            for (int l = 0; l < VS; ++l) {
+              if (stv.v[l] != kSlotFresh) continue;
+              const T* src = p.synth.kind != 0 ? p.gfr + (long long)(stripe * W + lane * VS + l) * N + i
+                                               : p.gamma + (long long)frv.v[l] * p.ld_gamma + i;
+              cp_async_vec<ES>(rowb + (DVMAX + 2) * 32 * VB + l * ES, src);
+            }
           }
         }
       }
@@ -412,21 +445,18 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
     issue_next();
     cp_wait<NS - 1>();
     const int stripe = tb[TB + 1], vb = tb[TB + 2];
-    const int fl = sflag[stripe];
     const int i0 = vb * kWideVB + cq * VBB, i1 = min(p.n_vars, min((vb + 1) * kWideVB, i0 + VBB));
-    if (!(fl & kStripeActive) || i0 >= i1) continue;
+    if (!(sflag[stripe] & kStripeActive) || i0 >= i1) continue;
     const unsigned char* st = ring + (t % NS) * G::bytes;
-    const VI stv = lds_vec<VI>(st + lane * 4 * VS);
+    const VI stv = *reinterpret_cast<const VI*>(tb + TB + 4 + lane * VS);
+    const VI frv = *reinterpret_cast<const VI*>(tb + TB + 4 + 32 * VS + lane * VS);
     const int s0 = stripe * W + lane * VS;
-    bool anyupd = false, anyfresh = false, anyret = false, allrun = true;
-    long long fr[VS];
+    bool anyupd = false, anyfresh = false, anyret = false;
 #pragma unroll
     for (int l = 0; l < VS; ++l) {
-      allrun &= stv.v[l] == kSlotRunning;
-      anyupd |= stv.v[l] == kSlotRunning || stv.v[l] == kSlotFresh;
+      anyupd |= stv.v[l] != kSlotEmpty;
       anyfresh |= stv.v[l] == kSlotFresh;
       anyret |= stv.v[l] == kSlotRetiring;
-      fr[l] = (stv.v[l] == kSlotFresh || stv.v[l] == kSlotRetiring) ? p.frame[s0 + l] : 0;
     }
     int wsum[VS], nonint[VS];
 #pragma unroll
@@ -436,7 +466,7 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
     for (int b = 0; b < VBB; ++b) {
       const int i = i0 + b;
       if (i >= i1) break;
-      const unsigned char* rowb = st + G::HB + b * G::VROWS * 32 * VB + lane * VB;
+      const unsigned char* rowb = st + b * G::VROWS * 32 * VB + lane * VB;
       int deg = 0;
       V mv[DVMAX];
 #pragma unroll
@@ -446,45 +476,35 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
         if (on) mv[j] = lds_vec<V>(rowb + j * 32 * VB);
       }
       V g = lds_vec<V>(rowb + DVMAX * 32 * VB);
+      V xo, gf;
+      if (anyret) xo = lds_vec<V>(rowb + (DVMAX + 1) * 32 * VB);
+      if (anyfresh) gf = lds_vec<V>(rowb + (DVMAX + 2) * 32 * VB);
       V xn;
-      if (anyret) xn = lds_vec<V>(rowb + (DVMAX + 1) * 32 * VB);
-      if (allrun) {
-        // every slot of the thread running: the plain x-update
-#pragma unroll
-        for (int l = 0; l < VS; ++l) {
-          T acc = T(0);
-#pragma unroll
-          for (int j = 0; j < DVMAX; ++j)
-            if (j < deg) acc = add_rn(acc, mv[j].v[l]);  // increasing edge id (np.bincount order)
-          xn.v[l] = deg > 0 ? clip01(div_rn(sub_rn(acc, g.v[l]), T(deg))) : (g.v[l] < T(0) ? T(1) : T(0));
-        }
-        wst(x + rb + (long long)i * 32, xn);
-        continue;
-      }
 #pragma unroll
       for (int l = 0; l < VS; ++l) {
         const int state = stv.v[l];
-        if (state == kSlotRetiring) {
-          // Output statistics of the final iterate (make_output, :92-105); x stays.
-          const T xv = xn.v[l];
-          const bool h = xv > T(0.5);
-          if (p.x_out) p.x_out[fr[l] * p.ld_x + i] = xv;
-          if (p.hard_out) p.hard_out[fr[l] * p.ld_hard + i] = h;
-          wsum[l] += h;
-          if (!(vmin(fabs(xv), fabs(T(1) - xv)) <= T(1e-5))) nonint[l] = 1;
-        } else if (state == kSlotRunning || state == kSlotFresh) {
-          T acc = T(0);
-          if (state == kSlotFresh) {
-            const T gi = p.synth.kind != 0 ? static_cast<T>(synth_llr(p.synth, p.synth.trial0 + fr[l], i))
-                                            : p.gamma[fr[l] * p.ld_gamma + i];
-            g.v[l] = div_rn(gi, p.mu);
-          } else {
+        const bool fresh = state == kSlotFresh, ret = state == kSlotRetiring;
+        T acc = T(0);
 #pragma unroll
-            for (int j = 0; j < DVMAX; ++j)
-              if (j < deg) acc = add_rn(acc, mv[j].v[l]);  // increasing edge id (np.bincount order)
-          }
-          xn.v[l] = deg > 0 ? clip01(div_rn(sub_rn(acc, g.v[l]), T(deg))) : (g.v[l] < T(0) ? T(1) : T(0));
+        for (int j = 0; j < DVMAX; ++j)
+          if (j < deg) acc = add_rn(acc, mv[j].v[l]);  // increasing edge id (np.bincount order)
+        if (anyfresh) {
+          if (fresh) acc = T(0);  // z = lambda = 0 (AdmmState.initial)
+          g.v[l] = fresh ? div_rn(gf.v[l], p.mu) : g.v[l];
         }
+        T xv = deg > 0 ? clip01(div_rn(sub_rn(acc, g.v[l]), T(deg))) : (g.v[l] < T(0) ? T(1) : T(0));
+        if (anyret) {
+          const T xf = xo.v[l];  // final iterate of a retiring slot
+          const bool h = xf > T(0.5);
+          wsum[l] += (ret && h) ? 1 : 0;
+          nonint[l] |= (ret && !(vmin(fabs(xf), fabs(T(1) - xf)) <= T(1e-5))) ? 1 : 0;
+          if (ret) {
+            if (p.x_out) p.x_out[(long long)frv.v[l] * p.ld_x + i] = xf;
+            if (p.hard_out) p.hard_out[(long long)frv.v[l] * p.ld_hard + i] = h;
+            xv = xf;
+          }
+        }
+        xn.v[l] = xv;
       }
       if (anyupd) wst(x + rb + (long long)i * 32, xn);
       if (anyfresh) st_cs(gm + rb + (long long)i * 32, g);
@@ -492,7 +512,6 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
     if (anyret) {
 #pragma unroll
       for (int l = 0; l < VS; ++l) {
-        if (stv.v[l] != kSlotRetiring) continue;
         if (wsum[l]) atomicAdd(p.weight + s0 + l, wsum[l]);
         if (nonint[l]) atomicOr(p.nonint + s0 + l, 1);
       }
@@ -517,6 +536,9 @@ __device__ __forceinline__ void wide_store_z(WVec<T, 2 * VS>* zl, WVec<T, VS>* z
 
 // ---- phase C: fused z-update, projection, residuals, lambda-update, message
 // (admm_decoder.py:127-149, parity_polytope.py:352-421) ----
+// One code path for every slot state: FRESH slots start from z = lambda = 0,
+// only RUNNING/FRESH slots add to the residual partials, RETIRING slots add
+// the parity of their final hard decision (is_codeword, codes.py:145-154).
 template <typename T, int VS, int D, int DVMAX, bool REG, int NS>
 __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned char* ring, int* tslot, int tstride,
                                              const int* sflag, int n_ci) {
@@ -525,22 +547,21 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
   using V2 = WVec<T, 2 * VS>;
   using G = WideStage<T, VS, D, DVMAX>;
   constexpr int W = 32 * VS, CB = kWideCB, VB = G::VB, TB = wide_ct(D);
+  // fp32 keeps (z, message) per edge and recovers lambda/mu = z - message:
+  // 20 instead of 24 bytes of edge-state traffic per edge-update.  fp64 (the
+  // parity mode) keeps (z, lambda/mu) and writes the message separately.
+  constexpr bool ZM = sizeof(T) == 4;
   const int lane = threadIdx.x & 31;
   const long long E = p.n_edges, N = p.n_vars;
   const V* x = reinterpret_cast<const V*>(p.x);
-  // fp32 keeps (z, message) per edge and recovers lambda/mu = z - message:
-  // 20 instead of 24 bytes of edge state traffic per edge-update.  fp64 (the
-  // parity mode) keeps (z, lambda/mu) and writes the message separately.
-  constexpr bool ZM = sizeof(T) == 4;
   V2* zl = reinterpret_cast<V2*>(p.zl);
   V* zv = reinterpret_cast<V*>(p.zl);
   V* msg = reinterpret_cast<V*>(p.msg);
   const int ncb = p.ncb;
   const uint32_t ring_s = smem_u32(ring);
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t pol = l2_evict_first_policy(p.l2_evict_first);
-  ItemFeed<TB> feed{p.ctbl, p.ctr + 3, n_ci, ncb, gw, p.static_items ? (int)((gridDim.x * blockDim.x) >> 5) : 0,
-                    p.chunk};
+  ItemFeed<TB, VS> feed{p.ctbl, p.ctr + 3, n_ci, ncb, W, p.st, p.frame, gw,
+                        p.static_items ? (int)((gridDim.x * blockDim.x) >> 5) : 0};
   int ik = 0, iq = 0, ti = 0;
   int iid = feed.start(tslot);
 
@@ -550,7 +571,6 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
       const int stripe = tb[TB + 1], c = tb[TB + 2] * CB + iq;
       if ((sflag[stripe] & kStripeActive) && c < p.n_checks) {
         const uint32_t st = ring_s + (ti % NS) * G::bytes;
-        cp_async_vec<4 * VS>(st + lane * 4 * VS, p.st + stripe * W + lane * VS);
         const long long e0 = tb[D * CB + iq];
         const long long xb = (long long)stripe * N * 32 + lane, eb = (long long)stripe * E * 32 + lane;
 #pragma unroll
@@ -559,10 +579,10 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
           if (v >= 0) {
             cp_async_vec<VB>(st + G::CX + (k * 32 + lane) * VB, x + xb + (long long)v * 32);
             if constexpr (ZM) {
-              cp_async_vec_ef<VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zv + eb + (e0 + k) * 32, pol);
-              cp_async_vec_ef<VB>(st + G::CZ + (k * 32 + lane) * 2 * VB + VB, msg + eb + (e0 + k) * 32, pol);
+              cp_async_vec<VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zv + eb + (e0 + k) * 32);
+              cp_async_vec<VB>(st + G::CZ + (k * 32 + lane) * 2 * VB + VB, msg + eb + (e0 + k) * 32);
             } else {
-              cp_async_vec_ef<2 * VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zl + eb + (e0 + k) * 32, pol);
+              cp_async_vec<2 * VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zl + eb + (e0 + k) * 32);
             }
           }
         }
@@ -596,14 +616,10 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
     const int stripe = tb[TB + 1], cb = tb[TB + 2], c = cb * CB + cq;
     if (!(sflag[stripe] & kStripeActive) || c >= p.n_checks) continue;
     const unsigned char* st = ring + (t % NS) * G::bytes;
-    const VI stv = lds_vec<VI>(st + lane * 4 * VS);
-    bool anyupd = false, anyret = false, allrun = true;
+    const VI stv = *reinterpret_cast<const VI*>(tb + TB + 4 + lane * VS);
+    bool anyret = false;
 #pragma unroll
-    for (int l = 0; l < VS; ++l) {
-      allrun &= stv.v[l] == kSlotRunning;
-      anyupd |= stv.v[l] == kSlotRunning || stv.v[l] == kSlotFresh;
-      anyret |= stv.v[l] == kSlotRetiring;
-    }
+    for (int l = 0; l < VS; ++l) anyret |= stv.v[l] == kSlotRetiring;
     int d = REG ? D : 0;
     if constexpr (!REG) {
 #pragma unroll
@@ -612,126 +628,85 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
     const long long e0 = tb[D * CB + cq];
     const long long eb = (long long)stripe * E * 32 + lane;
     V gx[D];
+    V2 zlv[D];
 #pragma unroll
     for (int k = 0; k < D; ++k)
-      if (k < d) gx[k] = lds_vec<V>(st + G::CX + (k * 32 + lane) * VB);
-    if (anyret) {
-      // Syndrome of the final hard decision (is_codeword, codes.py:145-154).
-#pragma unroll
-      for (int k = 0; k < D; ++k)
-        if (k < d) {
-#pragma unroll
-          for (int l = 0; l < VS; ++l) odd[l] ^= gx[k].v[l] > T(0.5);
-        }
-    }
-    if (REG && allrun) {
-      // every slot of the thread running: the plain fused check update
-      V2 zlv[D];
-#pragma unroll
-      for (int k = 0; k < D; ++k) {
+      if (k < d) {
+        gx[k] = lds_vec<V>(st + G::CX + (k * 32 + lane) * VB);
         zlv[k] = lds_vec<V2>(st + G::CZ + (k * 32 + lane) * 2 * VB);
         if constexpr (ZM) {
 #pragma unroll
           for (int l = 0; l < VS; ++l) zlv[k].v[VS + l] = sub_rn(zlv[k].v[l], zlv[k].v[VS + l]);
         }
       }
+    if (anyret) {
 #pragma unroll
       for (int l = 0; l < VS; ++l) {
-        T w_[D], u[D], zn[D];
+        int par = 0;
 #pragma unroll
-        for (int k = 0; k < D; ++k) {
-          w_[k] = add_rn(mul_rn(p.rho, gx[k].v[l]), mul_rn(p.one_minus_rho, zlv[k].v[l]));
-          u[k] = add_rn(w_[k], zlv[k].v[VS + l]);  // scaled dual lambda/mu
-        }
+        for (int k = 0; k < D; ++k)
+          if (k < d) par ^= gx[k].v[l] > T(0.5);
+        odd[l] |= (stv.v[l] == kSlotRetiring) ? par : 0;
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < VS; ++l) {
+      const bool run = stv.v[l] == kSlotRunning;
+      const bool act = run || stv.v[l] == kSlotFresh;
+      T w_[D], u[D], zn[D], zo[D], lo[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const bool on = k < d;
+        zo[k] = run ? zlv[k].v[l] : T(0);
+        lo[k] = run ? zlv[k].v[VS + l] : T(0);  // scaled dual lambda/mu
+        const T g = on ? gx[k].v[l] : T(0);
+        w_[k] = add_rn(mul_rn(p.rho, g), mul_rn(p.one_minus_rho, zo[k]));
+        u[k] = on ? add_rn(w_[k], lo[k]) : -Num<T>::inf();
+      }
+      if constexpr (REG) {
         project_pp_fixed<T, D>(u, zn);
+      } else {
+        project_pp<T, D>(u, zn, d);
+      }
+      T pr = T(0), mo = T(0);
 #pragma unroll
-        for (int k = 0; k < D; ++k) {
+      for (int k = 0; k < D; ++k) {
+        if (k < d) {
           const T r1 = sub_rn(gx[k].v[l], zn[k]);
-          const T r2 = sub_rn(zn[k], zlv[k].v[l]);
-          primal[l] = add_rn(primal[l], mul_rn(r1, r1));
-          moved[l] = add_rn(moved[l], mul_rn(r2, r2));
-          const T lnew = add_rn(zlv[k].v[VS + l], sub_rn(w_[k], zn[k]));
+          const T r2 = sub_rn(zn[k], zo[k]);
+          pr = add_rn(pr, mul_rn(r1, r1));
+          mo = add_rn(mo, mul_rn(r2, r2));
+          const T lnew = add_rn(lo[k], sub_rn(w_[k], zn[k]));
           zlv[k].v[l] = zn[k];
           zlv[k].v[VS + l] = lnew;
           gx[k].v[l] = sub_rn(zn[k], lnew);  // message
         }
       }
+      primal[l] = act ? add_rn(primal[l], pr) : primal[l];
+      moved[l] = act ? add_rn(moved[l], mo) : moved[l];
+    }
 #pragma unroll
-      for (int k = 0; k < D; ++k) {
+    for (int k = 0; k < D; ++k)
+      if (k < d) {
         wide_store_z<T, VS, ZM>(zl, zv, eb + (e0 + k) * 32, zlv[k]);
         st_cs(msg + eb + (e0 + k) * 32, gx[k]);
       }
-    } else if (anyupd) {
-      V2 zlv[D];
-#pragma unroll
-      for (int k = 0; k < D; ++k)
-        if (k < d) {
-          zlv[k] = lds_vec<V2>(st + G::CZ + (k * 32 + lane) * 2 * VB);
-          if constexpr (ZM) {
-#pragma unroll
-            for (int l = 0; l < VS; ++l) zlv[k].v[VS + l] = sub_rn(zlv[k].v[l], zlv[k].v[VS + l]);
-          }
-        }
-#pragma unroll
-      for (int l = 0; l < VS; ++l) {
-        const bool run = stv.v[l] == kSlotRunning;
-        T w_[D], u[D], zn[D], zo[D], lo[D];
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-          const bool on = k < d;
-          zo[k] = (on && run) ? zlv[k].v[l] : T(0);
-          lo[k] = (on && run) ? zlv[k].v[VS + l] : T(0);  // scaled dual lambda/mu
-          const T g = on ? gx[k].v[l] : T(0);
-          w_[k] = add_rn(mul_rn(p.rho, g), mul_rn(p.one_minus_rho, zo[k]));
-          u[k] = on ? add_rn(w_[k], lo[k]) : -Num<T>::inf();
-        }
-        if constexpr (REG) {
-          project_pp_fixed<T, D>(u, zn);
-        } else {
-          project_pp<T, D>(u, zn, d);
-        }
-        const bool act = run || stv.v[l] == kSlotFresh;
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-          if (k < d) {
-            const T r1 = sub_rn(gx[k].v[l], zn[k]);
-            const T r2 = sub_rn(zn[k], zo[k]);
-            if (act) {
-              primal[l] = add_rn(primal[l], mul_rn(r1, r1));
-              moved[l] = add_rn(moved[l], mul_rn(r2, r2));
-            }
-            const T lnew = add_rn(lo[k], sub_rn(w_[k], zn[k]));
-            zlv[k].v[l] = zn[k];
-            zlv[k].v[VS + l] = lnew;
-            gx[k].v[l] = sub_rn(zn[k], lnew);  // message
-          }
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < D; ++k)
-        if (k < d) {
-          wide_store_z<T, VS, ZM>(zl, zv, eb + (e0 + k) * 32, zlv[k]);
-          st_cs(msg + eb + (e0 + k) * 32, gx[k]);
-        }
-    }
     if (cq == CB - 1 || c + 1 >= p.n_checks) {
       // End of the item: per-slot partials of its checks (fixed order).
-      if (anyupd) {
-        V* part = reinterpret_cast<V*>(p.part) + ((long long)stripe * ncb + cb) * 64 + lane;
-        V a, b;
+      V* part = reinterpret_cast<V*>(p.part) + ((long long)stripe * ncb + cb) * 64 + lane;
+      V a, b;
 #pragma unroll
-        for (int l = 0; l < VS; ++l) {
-          a.v[l] = primal[l];
-          b.v[l] = moved[l];
-        }
-        wst(part, a);
-        wst(part + 32, b);
+      for (int l = 0; l < VS; ++l) {
+        a.v[l] = primal[l];
+        b.v[l] = moved[l];
       }
+      wst(part, a);
+      wst(part + 32, b);
       if (anyret) {
         const int s0 = stripe * W + lane * VS;
 #pragma unroll
         for (int l = 0; l < VS; ++l)
-          if (stv.v[l] == kSlotRetiring && odd[l]) atomicOr(p.odd + s0 + l, 1);
+          if (odd[l]) atomicOr(p.odd + s0 + l, 1);
       }
 #pragma unroll
       for (int l = 0; l < VS; ++l) {
@@ -741,24 +716,6 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
     }
   }
   cp_wait<0>();
-}
-
-template <typename T>
-__device__ __forceinline__ void wide_refill(const WideParams<T>& p, int s) {
-  const int f = atomicAdd(p.ctr + 0, 1);
-  p.tcount[s] = 0;
-  p.weight[s] = 0;
-  p.nonint[s] = 0;
-  p.odd[s] = 0;
-  p.conv[s] = 0;
-  if (f < p.batch) {
-    p.frame[s] = f;
-    p.st[s] = kSlotFresh;
-  } else {
-    p.frame[s] = -1;
-    p.st[s] = kSlotEmpty;
-    atomicSub(p.ctr + 1, 1);
-  }
 }
 
 // ---- phase S: one warp per slot ----
@@ -774,7 +731,19 @@ __device__ __forceinline__ void wide_phase_s(const WideParams<T>& p, int s) {
       if (p.iters_out) p.iters_out[f] = p.tcount[s];
       if (p.flags_out) p.flags_out[f] = (p.conv[s] ? 1 : 0) | (p.nonint[s] ? 0 : 2) | (p.odd[s] ? 0 : 4);
       if (p.weight_out) p.weight_out[f] = p.weight[s];
-      wide_refill(p, s);
+      p.tcount[s] = 0;
+      p.weight[s] = 0;
+      p.nonint[s] = 0;
+      p.odd[s] = 0;
+      p.conv[s] = 0;
+      const int fn = p.fnext[s];
+      p.frame[s] = fn;
+      if (fn >= 0) {
+        p.st[s] = kSlotFresh;
+      } else {
+        p.st[s] = kSlotEmpty;
+        atomicSub(p.ctr + 1, 1);
+      }
     }
     return;
   }
@@ -782,7 +751,7 @@ __device__ __forceinline__ void wide_phase_s(const WideParams<T>& p, int s) {
   const int stripe = s / W, r = s % W;
   const T* part = p.part + (long long)stripe * p.ncb * 2 * W + r;
   T a = T(0), b = T(0);
-#pragma unroll 4
+#pragma unroll 8
   for (int q = lane; q < p.ncb; q += 32) {
     a = add_rn(a, part[(long long)q * 2 * W]);
     b = add_rn(b, part[(long long)q * 2 * W + W]);
@@ -796,6 +765,12 @@ __device__ __forceinline__ void wide_phase_s(const WideParams<T>& p, int s) {
     if (converged || t >= p.t_max) {
       p.conv[s] = converged;
       p.st[s] = kSlotRetiring;
+      // the slot's next frame, known one pass early so that its LLRs can be
+      // synthesised during the retiring pass
+      const int f = atomicAdd(p.ctr + 0, 1);
+      const int fn = f < p.batch ? f : -1;
+      p.fnext[s] = fn;
+      if (fn >= 0 && p.synth.kind != 0) p.slist[atomicAdd(p.ctr + 5, 1)] = s;
     } else {
       p.st[s] = kSlotRunning;
     }
@@ -807,7 +782,7 @@ __global__ void __launch_bounds__(kWideThreads, MINB) wide_decode_kernel(const W
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char wide_smem[];
-  constexpr int W = 32 * VS, TS = wide_tstride<D, DVMAX>();
+  constexpr int W = 32 * VS, TS = wide_tstride<D, DVMAX, VS>();
   int* sflag = reinterpret_cast<int*>(wide_smem);
   unsigned char* wbase = wide_smem + kWideMaxStripes * 4 + (threadIdx.x >> 5) * wide_warp_bytes<T, VS, D, DVMAX, NS>();
   int* tslot = reinterpret_cast<int*>(wbase);
@@ -817,15 +792,24 @@ __global__ void __launch_bounds__(kWideThreads, MINB) wide_decode_kernel(const W
   const int n_vi = n_vb * n_stripes, n_ci = p.ncb * n_stripes;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int n_gwarp = (gridDim.x * blockDim.x) >> 5;
+  const long long first = p.batch < p.S ? p.batch : p.S;
 
+  // Prologue: slot s takes frame s; synthesised LLRs of the first frames.
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    p.ctr[0] = 0;
-    p.ctr[1] = p.S;
-    p.ctr[2] = 0;
-    p.ctr[3] = 0;
+    p.ctr[0] = static_cast<int>(first);
+    p.ctr[1] = static_cast<int>(first);
+    for (int k = 2; k < 8; ++k) p.ctr[k] = 0;
   }
-  grid.sync();
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < p.S; s += gridDim.x * blockDim.x) wide_refill(p, s);
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < p.S; s += gridDim.x * blockDim.x) {
+    p.frame[s] = s < first ? s : -1;
+    p.st[s] = s < first ? kSlotFresh : kSlotEmpty;
+    p.tcount[s] = p.weight[s] = p.nonint[s] = p.odd[s] = p.conv[s] = 0;
+  }
+  if (p.synth.kind != 0) {
+    const long long n = first * p.n_vars;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x)
+      p.gfr[q] = static_cast<T>(synth_llr(p.synth, p.synth.trial0 + q / p.n_vars, static_cast<int>(q % p.n_vars)));
+  }
   grid.sync();
 
   const long long max_passes = ((long long)(p.batch + p.S - 1) / p.S + 1) * ((long long)p.t_max + 2) + 4;
@@ -836,22 +820,20 @@ __global__ void __launch_bounds__(kWideThreads, MINB) wide_decode_kernel(const W
     __syncthreads();
     for (int s = threadIdx.x * 4; s < p.S; s += blockDim.x * 4) {
       const int4 q = *reinterpret_cast<const int4*>(p.st + s);
-      const int a[4] = {q.x, q.y, q.z, q.w};
-      int f = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        f |= (a[j] != kSlotEmpty ? kStripeActive : 0) | (a[j] == kSlotRetiring ? kStripeRetiring : 0) |
-             (a[j] == kSlotFresh ? kStripeFresh : 0);
-      if (f) atomicOr_block(sflag + s / W, f);
+      if (q.x != kSlotEmpty || q.y != kSlotEmpty || q.z != kSlotEmpty || q.w != kSlotEmpty)
+        atomicOr_block(sflag + s / W, kStripeActive);
     }
     __syncthreads();
+    if (p.synth.kind != 0) wide_synth_items(p, *(volatile int*)(p.ctr + 5));
     wide_phase_v<T, VS, D, DVMAX, REG, NS>(p, ring, tslot, TS, sflag, n_vi, n_vb);
     grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.ctr[5] = 0;  // synthesis list of the next pass (read in phase V)
     wide_phase_c<T, VS, D, DVMAX, REG, NS>(p, ring, tslot, TS, sflag, n_ci);
     grid.sync();
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // item counters of the next pass (both phases are done)
       p.ctr[2] = 0;
       p.ctr[3] = 0;
+      p.ctr[4] = 0;
     }
     for (int s = gwarp; s < p.S; s += n_gwarp) wide_phase_s<T, VS>(p, s);
     grid.sync();
