@@ -77,6 +77,7 @@ struct WideParams {
   int* weight_out;
   int S, ncb;
   int static_items;  // debug: static round-robin work items instead of the atomic feed
+  int l2_evict_first;  // L2 evict-first policy on the rows streamed once per pass
   T* zl;
   T* msg;
   T* x;
@@ -226,10 +227,6 @@ __device__ __forceinline__ V lds_vec(const unsigned char* p) {
   return *reinterpret_cast<const V*>(p);
 }
 
-// Stripe flags, rebuilt in shared memory by every CTA at the start of a pass.
-enum : int { kStripeActive = 1 };
-constexpr int kWideMaxStripes = 256;
-
 // Stage geometry.  A stage holds one task: for a check task D x-rows and D
 // edge-state rows, for a variable task VBB variables x (DVMAX message rows,
 // gamma/mu, x, fresh LLR) -- each row 32 lanes x one vector.
@@ -257,7 +254,7 @@ struct WideStage {
 __host__ __device__ constexpr int wide_ct(int D) { return ((D + 1) * kWideCB + 31) / 32 * 32; }
 __host__ __device__ constexpr int wide_vt(int DV) { return (kWideVB * DV + 31) / 32 * 32; }
 
-// Table slot: [TB index ints][id, stripe, block, -][32 x VS states][32 x VS frames]
+// Table slot: [TB index ints][id, stripe, block, busy][32 x VS states][32 x VS frames]
 template <int D, int DVMAX, int VS>
 __host__ __device__ constexpr int wide_tstride() {
   return (wide_ct(D) > wide_vt(DVMAX) ? wide_ct(D) : wide_vt(DVMAX)) + 4 + 64 * VS;
@@ -274,7 +271,7 @@ struct ItemFeed {
   const int* frame;
   int stat_next, stat_step;  // static assignment (debug): stat_step > 0
   int id1;                   // next item (its table/states are in registers)
-  int raw2;                  // lane 0: atomic result for the item after (in flight)
+  int raw2, raw3;            // lane 0: atomic results for the two items after (in flight)
   int reg[NR];
   VI sreg, freg;
 
@@ -309,6 +306,11 @@ struct ItemFeed {
     }
     *reinterpret_cast<VI*>(slot + TB + 4 + lane * VS) = sreg;
     *reinterpret_cast<VI*>(slot + TB + 4 + 32 * VS + lane * VS) = freg;
+    bool act = false;
+#pragma unroll
+    for (int l = 0; l < VS; ++l) act |= sreg.v[l] != kSlotEmpty;
+    act = __any_sync(0xffffffffu, act);
+    if (lane == 0) slot[TB + 3] = act;  // any slot of the item's stripe lanes busy
     __syncwarp();
   }
   // First item: published into slot0; returns its id.
@@ -319,6 +321,7 @@ struct ItemFeed {
     publish(slot0, a);
     load(id1);
     raw2 = grab_raw();
+    raw3 = grab_raw();
     return a;
   }
   // Move to the next item: publish it into `slot`, prefetch the one after.
@@ -327,20 +330,20 @@ struct ItemFeed {
     publish(slot, cur);
     id1 = __shfl_sync(0xffffffffu, raw2, 0);
     load(id1);
-    raw2 = grab_raw();
+    raw2 = raw3;
+    raw3 = grab_raw();
     return cur;
   }
 };
 
-// Shared memory: stripe flags, then per warp two table slots and the ring of
-// NS stages.
+// Shared memory: per warp two table slots and the ring of NS stages.
 template <typename T, int VS, int D, int DVMAX, int NS>
 __host__ __device__ constexpr int wide_warp_bytes() {
   return 2 * 4 * wide_tstride<D, DVMAX, VS>() + NS * WideStage<T, VS, D, DVMAX>::bytes;
 }
 template <typename T, int VS, int D, int DVMAX, int NS>
 __host__ __device__ constexpr int wide_smem_bytes() {
-  return kWideMaxStripes * 4 + (kWideThreads / 32) * wide_warp_bytes<T, VS, D, DVMAX, NS>();
+  return (kWideThreads / 32) * wide_warp_bytes<T, VS, D, DVMAX, NS>();
 }
 
 // LLRs of the next frames of the slots retired in the last pass (in-kernel
@@ -372,7 +375,7 @@ __device__ __forceinline__ void wide_synth_items(const WideParams<T>& p, int nli
 // keeps x and accumulates the output statistics (make_output, :92-105).
 template <typename T, int VS, int D, int DVMAX, bool REG, int NS>
 __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned char* ring, int* tslot, int tstride,
-                                             const int* sflag, int n_vi, int n_vb) {
+                                             int n_vi, int n_vb) {
   using V = WVec<T, VS>;
   using VI = WVec<int, VS>;
   using G = WideStage<T, VS, D, DVMAX>;
@@ -385,6 +388,7 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
   V* gm = reinterpret_cast<V*>(p.gm);
   const uint32_t ring_s = smem_u32(ring);
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t pol = l2_evict_first_policy(p.l2_evict_first);
   ItemFeed<TB, VS> feed{p.vtbl, p.ctr + 2, n_vi, n_vb, W, p.st, p.frame, gw,
                         p.static_items ? (int)((gridDim.x * blockDim.x) >> 5) : 0};
   int ik = 0, iq = 0, ti = 0;
@@ -395,7 +399,7 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
       const int* tb = tslot + (ik & 1) * tstride;
       const int stripe = tb[TB + 1], vb = tb[TB + 2];
       const int i0 = vb * kWideVB + iq * VBB, i1 = min(p.n_vars, min((vb + 1) * kWideVB, i0 + VBB));
-      if ((sflag[stripe] & kStripeActive) && i0 < i1) {
+      if (tb[TB + 3] && i0 < i1) {
         const VI stv = *reinterpret_cast<const VI*>(tb + TB + 4 + lane * VS);
         const VI frv = *reinterpret_cast<const VI*>(tb + TB + 4 + 32 * VS + lane * VS);
         bool anyret = false;
@@ -411,9 +415,9 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
 #pragma unroll
             for (int j = 0; j < DVMAX; ++j) {
               const int e = tb[(iq * VBB + b) * DVMAX + j];
-              if (e >= 0) cp_async_vec<VB>(rowb + j * 32 * VB, msg + ((long long)stripe * E + e) * 32 + lane);
+              if (e >= 0) cp_async_vec_ef<VB>(rowb + j * 32 * VB, msg + ((long long)stripe * E + e) * 32 + lane, pol);
             }
-            cp_async_vec<VB>(rowb + DVMAX * 32 * VB, gm + rb + (long long)i * 32);
+            cp_async_vec_ef<VB>(rowb + DVMAX * 32 * VB, gm + rb + (long long)i * 32, pol);
             if (anyret) cp_async_vec<VB>(rowb + (DVMAX + 1) * 32 * VB, x + rb + (long long)i * 32);
 #pragma unroll
             for (int l = 0; l < VS; ++l) {
@@ -446,7 +450,7 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
     cp_wait<NS - 1>();
     const int stripe = tb[TB + 1], vb = tb[TB + 2];
     const int i0 = vb * kWideVB + cq * VBB, i1 = min(p.n_vars, min((vb + 1) * kWideVB, i0 + VBB));
-    if (!(sflag[stripe] & kStripeActive) || i0 >= i1) continue;
+    if (!tb[TB + 3] || i0 >= i1) continue;
     const unsigned char* st = ring + (t % NS) * G::bytes;
     const VI stv = *reinterpret_cast<const VI*>(tb + TB + 4 + lane * VS);
     const VI frv = *reinterpret_cast<const VI*>(tb + TB + 4 + 32 * VS + lane * VS);
@@ -541,7 +545,7 @@ __device__ __forceinline__ void wide_store_z(WVec<T, 2 * VS>* zl, WVec<T, VS>* z
 // the parity of their final hard decision (is_codeword, codes.py:145-154).
 template <typename T, int VS, int D, int DVMAX, bool REG, int NS>
 __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned char* ring, int* tslot, int tstride,
-                                             const int* sflag, int n_ci) {
+                                             int n_ci) {
   using V = WVec<T, VS>;
   using VI = WVec<int, VS>;
   using V2 = WVec<T, 2 * VS>;
@@ -560,6 +564,7 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
   const int ncb = p.ncb;
   const uint32_t ring_s = smem_u32(ring);
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t pol = l2_evict_first_policy(p.l2_evict_first);
   ItemFeed<TB, VS> feed{p.ctbl, p.ctr + 3, n_ci, ncb, W, p.st, p.frame, gw,
                         p.static_items ? (int)((gridDim.x * blockDim.x) >> 5) : 0};
   int ik = 0, iq = 0, ti = 0;
@@ -569,7 +574,7 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
     if (iid < n_ci) {
       const int* tb = tslot + (ik & 1) * tstride;
       const int stripe = tb[TB + 1], c = tb[TB + 2] * CB + iq;
-      if ((sflag[stripe] & kStripeActive) && c < p.n_checks) {
+      if (tb[TB + 3] && c < p.n_checks) {
         const uint32_t st = ring_s + (ti % NS) * G::bytes;
         const long long e0 = tb[D * CB + iq];
         const long long xb = (long long)stripe * N * 32 + lane, eb = (long long)stripe * E * 32 + lane;
@@ -579,10 +584,10 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
           if (v >= 0) {
             cp_async_vec<VB>(st + G::CX + (k * 32 + lane) * VB, x + xb + (long long)v * 32);
             if constexpr (ZM) {
-              cp_async_vec<VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zv + eb + (e0 + k) * 32);
-              cp_async_vec<VB>(st + G::CZ + (k * 32 + lane) * 2 * VB + VB, msg + eb + (e0 + k) * 32);
+              cp_async_vec_ef<VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zv + eb + (e0 + k) * 32, pol);
+              cp_async_vec_ef<VB>(st + G::CZ + (k * 32 + lane) * 2 * VB + VB, msg + eb + (e0 + k) * 32, pol);
             } else {
-              cp_async_vec<2 * VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zl + eb + (e0 + k) * 32);
+              cp_async_vec_ef<2 * VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zl + eb + (e0 + k) * 32, pol);
             }
           }
         }
@@ -614,7 +619,7 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
     issue_next();
     cp_wait<NS - 1>();
     const int stripe = tb[TB + 1], cb = tb[TB + 2], c = cb * CB + cq;
-    if (!(sflag[stripe] & kStripeActive) || c >= p.n_checks) continue;
+    if (!tb[TB + 3] || c >= p.n_checks) continue;
     const unsigned char* st = ring + (t % NS) * G::bytes;
     const VI stv = *reinterpret_cast<const VI*>(tb + TB + 4 + lane * VS);
     bool anyret = false;
@@ -783,8 +788,7 @@ __global__ void __launch_bounds__(kWideThreads, MINB) wide_decode_kernel(const W
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char wide_smem[];
   constexpr int W = 32 * VS, TS = wide_tstride<D, DVMAX, VS>();
-  int* sflag = reinterpret_cast<int*>(wide_smem);
-  unsigned char* wbase = wide_smem + kWideMaxStripes * 4 + (threadIdx.x >> 5) * wide_warp_bytes<T, VS, D, DVMAX, NS>();
+  unsigned char* wbase = wide_smem + (threadIdx.x >> 5) * wide_warp_bytes<T, VS, D, DVMAX, NS>();
   int* tslot = reinterpret_cast<int*>(wbase);
   unsigned char* ring = wbase + 2 * 4 * TS;
   const int n_stripes = p.S / W;
@@ -815,20 +819,11 @@ __global__ void __launch_bounds__(kWideThreads, MINB) wide_decode_kernel(const W
   const long long max_passes = ((long long)(p.batch + p.S - 1) / p.S + 1) * ((long long)p.t_max + 2) + 4;
   for (long long pass = 0; pass < max_passes; ++pass) {
     if (*(volatile int*)(p.ctr + 1) == 0) break;
-    // stripe flags of this pass (slot states only change in phase S)
-    for (int i = threadIdx.x; i < n_stripes; i += blockDim.x) sflag[i] = 0;
-    __syncthreads();
-    for (int s = threadIdx.x * 4; s < p.S; s += blockDim.x * 4) {
-      const int4 q = *reinterpret_cast<const int4*>(p.st + s);
-      if (q.x != kSlotEmpty || q.y != kSlotEmpty || q.z != kSlotEmpty || q.w != kSlotEmpty)
-        atomicOr_block(sflag + s / W, kStripeActive);
-    }
-    __syncthreads();
     if (p.synth.kind != 0) wide_synth_items(p, *(volatile int*)(p.ctr + 5));
-    wide_phase_v<T, VS, D, DVMAX, REG, NS>(p, ring, tslot, TS, sflag, n_vi, n_vb);
+    wide_phase_v<T, VS, D, DVMAX, REG, NS>(p, ring, tslot, TS, n_vi, n_vb);
     grid.sync();
     if (blockIdx.x == 0 && threadIdx.x == 0) p.ctr[5] = 0;  // synthesis list of the next pass (read in phase V)
-    wide_phase_c<T, VS, D, DVMAX, REG, NS>(p, ring, tslot, TS, sflag, n_ci);
+    wide_phase_c<T, VS, D, DVMAX, REG, NS>(p, ring, tslot, TS, n_ci);
     grid.sync();
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // item counters of the next pass (both phases are done)
       p.ctr[2] = 0;
