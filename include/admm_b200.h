@@ -158,6 +158,9 @@ int admm_project_batch(int dtype, int64_t m, int32_t d, const void* values, void
  * cycles8 (host, may be NULL) receives {variable phase, grid sync, check
  * phase, grid sync, slot phase, passes, 0, 0} accumulated so far. */
 int admm_phase_profile(int enable, uint64_t* cycles8);
+/* Same for the wide kernel (wide.cuh): cycles8 = {variable phase, grid sync,
+ * check phase, grid sync, slot phase, grid sync, passes, 0} of CTA 0. */
+int admm_wide_phase_profile(int enable, uint64_t* cycles8);
 
 /* Flooding sum-product BP on the same graph handle (the comparison baseline,
  * SURVEY.md 8f #4).  Replaces posterior_llrs / decode_bp

@@ -932,6 +932,12 @@ int admm_phase_profile(int enable, uint64_t* cycles8) {
   return ADMM_OK;
 }
 
+int admm_wide_phase_profile(int enable, uint64_t* cycles8) {
+  if (!admm::wide_phase_profile(enable, reinterpret_cast<unsigned long long*>(cycles8)))
+    return fail(ADMM_E_CUDA, "wide phase profile: CUDA error");
+  return ADMM_OK;
+}
+
 int admm_project_batch(int dtype, int64_t m, int32_t d, const void* values, void* out, void* stream) {
   if (dtype != ADMM_F32 && dtype != ADMM_F64) return fail(ADMM_E_ARG, "dtype must be ADMM_F32 or ADMM_F64");
   if (m < 0 || d < 1) return fail(ADMM_E_ARG, "project_batch expects an (m, d) array with d >= 1");

@@ -343,5 +343,6 @@ int launch_wide(const StreamGraphArgs& g, const ResidentFrameArgs& a, int S, voi
 
 // Defined in wide.cu.
 bool wide_lookup(int dtype, int D, int DVMAX, bool regular, WideLaunch* out);
+bool wide_phase_profile(int enable, unsigned long long* out8);
 
 }  // namespace admm

@@ -58,4 +58,17 @@ bool wide_lookup(int dtype, int D, int DVMAX, bool regular, WideLaunch* out) {
   return false;
 }
 
+bool wide_phase_profile(int enable, unsigned long long* out8) {
+  if (out8) {
+    if (cudaMemcpyFromSymbol(out8, g_wide_cycles, sizeof(unsigned long long) * 8) != cudaSuccess) return false;
+  }
+  if (enable >= 0) {
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const int on = enable > 0;
+    if (cudaMemcpyToSymbol(g_wide_cycles, z, sizeof(z)) != cudaSuccess) return false;
+    if (cudaMemcpyToSymbol(g_wide_prof, &on, sizeof(int)) != cudaSuccess) return false;
+  }
+  return true;
+}
+
 }  // namespace admm

@@ -782,6 +782,11 @@ __device__ __forceinline__ void wide_phase_s(const WideParams<T>& p, int s) {
   }
 }
 
+// Phase profiler (admm_wide_phase_profile): CTA 0, thread 0 accumulates
+// clock64() cycles: 0 phase V, 1 sync, 2 phase C, 3 sync, 4 phase S, 5 sync, 6 passes.
+__device__ unsigned long long g_wide_cycles[8];
+__device__ int g_wide_prof;
+
 template <typename T, int VS, int D, int DVMAX, bool REG, int NS, int MINB>
 __global__ void __launch_bounds__(kWideThreads, MINB) wide_decode_kernel(const WideParams<T> p) {
   namespace cg = cooperative_groups;
@@ -797,6 +802,7 @@ __global__ void __launch_bounds__(kWideThreads, MINB) wide_decode_kernel(const W
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int n_gwarp = (gridDim.x * blockDim.x) >> 5;
   const long long first = p.batch < p.S ? p.batch : p.S;
+  const bool prof = g_wide_prof && blockIdx.x == 0 && threadIdx.x == 0;
 
   // Prologue: slot s takes frame s; synthesised LLRs of the first frames.
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -819,19 +825,32 @@ __global__ void __launch_bounds__(kWideThreads, MINB) wide_decode_kernel(const W
   const long long max_passes = ((long long)(p.batch + p.S - 1) / p.S + 1) * ((long long)p.t_max + 2) + 4;
   for (long long pass = 0; pass < max_passes; ++pass) {
     if (*(volatile int*)(p.ctr + 1) == 0) break;
+    long long tp[7];
+    tp[0] = prof ? clock64() : 0;
     if (p.synth.kind != 0) wide_synth_items(p, *(volatile int*)(p.ctr + 5));
     wide_phase_v<T, VS, D, DVMAX, REG, NS>(p, ring, tslot, TS, n_vi, n_vb);
+    if (prof) tp[1] = clock64();
     grid.sync();
+    if (prof) tp[2] = clock64();
     if (blockIdx.x == 0 && threadIdx.x == 0) p.ctr[5] = 0;  // synthesis list of the next pass (read in phase V)
     wide_phase_c<T, VS, D, DVMAX, REG, NS>(p, ring, tslot, TS, n_ci);
+    if (prof) tp[3] = clock64();
     grid.sync();
+    if (prof) tp[4] = clock64();
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // item counters of the next pass (both phases are done)
       p.ctr[2] = 0;
       p.ctr[3] = 0;
       p.ctr[4] = 0;
     }
     for (int s = gwarp; s < p.S; s += n_gwarp) wide_phase_s<T, VS>(p, s);
+    if (prof) tp[5] = clock64();
     grid.sync();
+    if (prof) {
+      tp[6] = clock64();
+#pragma unroll
+      for (int k = 0; k < 6; ++k) g_wide_cycles[k] += tp[k + 1] - tp[k];
+      g_wide_cycles[6] += 1;
+    }
   }
 }
 
