@@ -319,6 +319,8 @@ WideParams<T> make_wide_params(const StreamGraphArgs& g, const ResidentFrameArgs
   p.gm = reinterpret_cast<T*>(base + L.gm);
   p.part = reinterpret_cast<T*>(base + L.part);
   p.gfr = a.synth.kind != 0 ? reinterpret_cast<T*>(base + L.gfr) : nullptr;
+  p.vpart = reinterpret_cast<int*>(base + L.vpart);
+  p.direct = (a.x_out == nullptr && a.hard_out == nullptr && std::getenv("ADMM_B200_WIDE_RETIRE_PASS") == nullptr) ? 1 : 0;
   int* ib = reinterpret_cast<int*>(base + L.ints);
   p.st = ib;
   p.tcount = ib + S;

@@ -84,6 +84,8 @@ struct WideParams {
   T* gm;
   T* part;
   T* gfr;    // [S][N] LLRs of the slots' next frames (in-kernel synthesis only)
+  int* vpart;  // [stripe][nvb][W] hard-decision weight | non-integral << 8 of x per variable block (every pass)
+  int direct;  // no per-variable outputs requested: retire without the retiring pass
   int* frame;  // [S] frame of the slot
   int* fnext;  // [S] frame that follows a retiring slot's frame (-1 = none)
   int* slist;  // [S] slots whose next frame's LLRs are synthesised in the coming pass
@@ -92,7 +94,7 @@ struct WideParams {
 };
 
 struct WideLayout {
-  size_t zl, msg, x, gm, part, gfr, ints, total;
+  size_t zl, msg, x, gm, part, gfr, vpart, ints, total;
   static size_t al(size_t b) { return (b + 255) & ~size_t(255); }
   WideLayout(size_t elem, long long E, long long N, long long ncb, long long S, bool synth) {
     size_t o = 0;
@@ -102,6 +104,7 @@ struct WideLayout {
     gm = o; o += al(elem * N * S);
     part = o; o += al(elem * 2 * ncb * S);
     gfr = o; o += synth ? al(elem * N * S) : 0;
+    vpart = o; o += al(sizeof(int) * ((N + kWideVB - 1) / kWideVB) * S);
     ints = o; o += al(sizeof(int) * (9 * S + 16));
     total = o;
   }
@@ -439,6 +442,9 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
     }
   };
 
+  int iw[VS], inon[VS];  // weight / non-integral of the item's new x, per slot (phase S retires from them)
+#pragma unroll
+  for (int l = 0; l < VS; ++l) iw[l] = inon[l] = 0;
 #pragma unroll
   for (int t = 0; t < NS - 1; ++t) issue_next();
   for (int t = 0;; ++t) {
@@ -497,6 +503,8 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
           g.v[l] = fresh ? div_rn(gf.v[l], p.mu) : g.v[l];
         }
         T xv = deg > 0 ? clip01(div_rn(sub_rn(acc, g.v[l]), T(deg))) : (g.v[l] < T(0) ? T(1) : T(0));
+        iw[l] += xv > T(0.5) ? 1 : 0;  // make_output (:92-105) of x_t, in case the slot stops now
+        inon[l] |= !(vmin(fabs(xv), fabs(T(1) - xv)) <= T(1e-5)) ? 1 : 0;
         if (anyret) {
           const T xf = xo.v[l];  // final iterate of a retiring slot
           const bool h = xf > T(0.5);
@@ -519,6 +527,16 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
         if (wsum[l]) atomicAdd(p.weight + s0 + l, wsum[l]);
         if (nonint[l]) atomicOr(p.nonint + s0 + l, 1);
       }
+    }
+    if (i1 == min(p.n_vars, (vb + 1) * kWideVB)) {  // last task of the item
+      if (p.direct) {
+        VI o;
+#pragma unroll
+        for (int l = 0; l < VS; ++l) o.v[l] = iw[l] | (inon[l] << 8);
+        *reinterpret_cast<VI*>(p.vpart + ((long long)stripe * n_vb + vb) * W + lane * VS) = o;
+      }
+#pragma unroll
+      for (int l = 0; l < VS; ++l) iw[l] = inon[l] = 0;
     }
   }
   cp_wait<0>();
@@ -644,14 +662,14 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
           for (int l = 0; l < VS; ++l) zlv[k].v[VS + l] = sub_rn(zlv[k].v[l], zlv[k].v[VS + l]);
         }
       }
-    if (anyret) {
+    {
 #pragma unroll
       for (int l = 0; l < VS; ++l) {
         int par = 0;
 #pragma unroll
         for (int k = 0; k < D; ++k)
           if (k < d) par ^= gx[k].v[l] > T(0.5);
-        odd[l] |= (stv.v[l] == kSlotRetiring) ? par : 0;
+        odd[l] |= par;
       }
     }
 #pragma unroll
@@ -703,7 +721,7 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
 #pragma unroll
       for (int l = 0; l < VS; ++l) {
         a.v[l] = primal[l];
-        b.v[l] = moved[l];
+        b.v[l] = odd[l] ? -moved[l] : moved[l];  // sign bit: an odd check in the block (is_codeword of x_t)
       }
       wst(part, a);
       wst(part + 32, b);
@@ -711,7 +729,7 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
         const int s0 = stripe * W + lane * VS;
 #pragma unroll
         for (int l = 0; l < VS; ++l)
-          if (odd[l]) atomicOr(p.odd + s0 + l, 1);
+          if (stv.v[l] == kSlotRetiring && odd[l]) atomicOr(p.odd + s0 + l, 1);
       }
 #pragma unroll
       for (int l = 0; l < VS; ++l) {
@@ -752,30 +770,70 @@ __device__ __forceinline__ void wide_phase_s(const WideParams<T>& p, int s) {
     }
     return;
   }
-  // Exact residual sums (admm_decoder.py:174-176), fixed order.
+  // Exact residual sums (admm_decoder.py:174-176), fixed order; the sign
+  // of a moved-partial flags an odd check of x_t in its block.
   const int stripe = s / W, r = s % W;
   const T* part = p.part + (long long)stripe * p.ncb * 2 * W + r;
   T a = T(0), b = T(0);
+  bool odd = false;
 #pragma unroll 8
   for (int q = lane; q < p.ncb; q += 32) {
+    const T mv = part[(long long)q * 2 * W + W];
     a = add_rn(a, part[(long long)q * 2 * W]);
-    b = add_rn(b, part[(long long)q * 2 * W + W]);
+    b = add_rn(b, fabs(mv));
+    odd |= signbit(mv);
   }
   a = warp_allsum(a);
   b = warp_allsum(b);
+  const bool converged = a < p.thr && b < p.thr;  // admm_decoder.py:169, 179 (strict)
+  const int t = __shfl_sync(0xffffffffu, lane == 0 ? p.tcount[s] : 0, 0) + 1;
+  const bool stop = converged || t >= p.t_max;
+  if (stop && state == kSlotRunning && p.direct) {
+    // Retire now: the outputs of x_t (make_output, :92-105; is_codeword,
+    // codes.py:145-154) were accumulated by phases V and C of this pass, and
+    // the next frame (popped when this one started) is ready.
+    const int n_vb = (p.n_vars + kWideVB - 1) / kWideVB;
+    const int* vp = p.vpart + (long long)stripe * n_vb * W + r;
+    int w = 0, nonint = 0;
+    for (int q = lane; q < n_vb; q += 32) {
+      const int v = vp[(long long)q * W];
+      w += v & 0xff;
+      nonint |= v >> 8;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    nonint = __any_sync(0xffffffffu, nonint != 0);
+    odd = __any_sync(0xffffffffu, odd);
+    if (lane == 0) {
+      const long long f = p.frame[s];
+      if (p.iters_out) p.iters_out[f] = t;
+      if (p.flags_out) p.flags_out[f] = (converged ? 1 : 0) | (nonint ? 0 : 2) | (odd ? 0 : 4);
+      if (p.weight_out) p.weight_out[f] = w;
+      p.tcount[s] = 0;
+      const int fn = p.fnext[s];
+      p.frame[s] = fn;
+      if (fn >= 0) {
+        p.st[s] = kSlotFresh;
+      } else {
+        p.st[s] = kSlotEmpty;
+        atomicSub(p.ctr + 1, 1);
+      }
+    }
+    return;
+  }
   if (lane == 0) {
-    const bool converged = a < p.thr && b < p.thr;  // admm_decoder.py:169, 179 (strict)
-    const int t = p.tcount[s] + 1;
     p.tcount[s] = t;
-    if (converged || t >= p.t_max) {
-      p.conv[s] = converged;
-      p.st[s] = kSlotRetiring;
-      // the slot's next frame, known one pass early so that its LLRs can be
-      // synthesised during the retiring pass
+    if (state == kSlotFresh) {
+      // The frame that follows this one, popped when this one starts so that
+      // (in-kernel synthesis) its LLRs are ready when this one retires.
       const int f = atomicAdd(p.ctr + 0, 1);
       const int fn = f < p.batch ? f : -1;
       p.fnext[s] = fn;
       if (fn >= 0 && p.synth.kind != 0) p.slist[atomicAdd(p.ctr + 5, 1)] = s;
+    }
+    if (stop) {
+      p.conv[s] = converged;
+      p.st[s] = kSlotRetiring;  // the next pass computes the outputs from x_t
     } else {
       p.st[s] = kSlotRunning;
     }

@@ -190,3 +190,25 @@ def test_wide_kernel_large_batch_matches_sharded(cuda_ok):
     same = w32.hard.eq(w64.hard).all(dim=1).float().mean().item()
     assert same >= 0.999
     assert abs(int(w32.iterations.sum()) - int(w64.iterations.sum())) <= 0.02 * int(w64.iterations.sum())
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_wide_direct_retirement_equals_retiring_pass(cuda_ok, dt):
+    """Without per-variable outputs the wide kernel retires a converged frame
+    in the pass that converged it, from the weight / integrality / syndrome
+    statistics of x_t accumulated every pass; with x or hard decisions
+    requested it spends a retiring pass.  Both give the same per-frame
+    results (iterations, flags, weight), on AWGN and on BSC frames."""
+    from paper_1204_0556_b200 import AdmmConfig, Awgn, Bsc, baseline_code, decode_synth
+
+    code = baseline_code("cfg5_n16384")
+    cfg = AdmmConfig(mu=5.0)
+    for k, ch in enumerate((Awgn(2.0, code.design_rate), Bsc(0.045))):
+        a = decode_synth(code, ch, cfg, seed=3, point=k, trial0=0, batch=2560, dtype=dt, engine="wide")
+        b = decode_synth(code, ch, cfg, seed=3, point=k, trial0=0, batch=2560, dtype=dt, engine="wide",
+                         want_hard=True)
+        assert a.info["kernel"] == 5 and b.info["kernel"] == 5
+        assert torch.equal(a.iterations, b.iterations)
+        assert torch.equal(a.flags, b.flags)
+        assert torch.equal(a.weight, b.weight)
+        assert torch.equal(b.weight, b.hard.to(torch.int32).sum(dim=1))
