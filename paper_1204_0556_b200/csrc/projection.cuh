@@ -145,6 +145,10 @@ __device__ __forceinline__ void bitonic_merge_asc(T (&s)[D]) {
   }
 }
 
+#ifndef ADMM_PROJ_FMA_MASK
+#define ADMM_PROJ_FMA_MASK 0
+#endif
+
 // Fixed-degree variant used by the regular-code kernels: d == D at compile
 // time, no padding, and branch-free -- a row that passes the facet test gets
 // beta = 0, and clip(u - 0 * f) is exactly the cube clip the reference
@@ -178,14 +182,24 @@ __device__ __forceinline__ void project_pp_fixed(const T (&u)[D], T (&z)[D]) {
   // Activation shifts in SORTED order: s = v_k - 1 on the +1 block (k <= r,
   // descending) then -v_k (ascending) -- a V-shaped sequence whatever r is,
   // so a bitonic merger sorts it.
-  const int r2 = r >> 1;
   T s[D];
+  if constexpr (sizeof(T) == 4 && ADMM_PROJ_FMA_MASK) {
+    // fp32 (throughput mode): the block mask as a float on the FMA pipe,
+    // m_k = [k <= r] = sat(r + 1 - k), and s_k = m_k (2 v_k - 1) - v_k, in
+    // place of integer compares and selects on the ALU pipe (the kernel is
+    // ALU-issue bound).  Same values up to the rounding of 2 v_k - 1.
+    const float rp1 = static_cast<float>(r + 1);
 #pragma unroll
-  for (int k = 0; k < D; ++k) s[k] = (((k + 1) >> 1) <= r2) ? sub_rn(v[k], T(1)) : -v[k];
+    for (int k = 0; k < D; ++k) {
+      const float m = __saturatef(rp1 - static_cast<float>(k));
+      s[k] = __fmaf_rn(m, __fmaf_rn(2.f, v[k], -1.f), -v[k]);
+    }
+  } else {
+    const int r2 = r >> 1;
+#pragma unroll
+    for (int k = 0; k < D; ++k) s[k] = (((k + 1) >> 1) <= r2) ? sub_rn(v[k], T(1)) : -v[k];
+  }
   bitonic_merge_asc<T, D>(s);
-  bool up[D];
-#pragma unroll
-  for (int k = 0; k < D; ++k) up[k] = u[k] >= v_top;
   T beta = beta_max, p = T(1);
 #pragma unroll
   for (int j = 0; j < D; ++j) {
@@ -193,8 +207,22 @@ __device__ __forceinline__ void project_pp_fixed(const T (&u)[D], T (&z)[D]) {
     beta = vmin(beta, mul_rn(p, T(1) / T(j + 1)));
   }
   beta = inside ? T(0) : beta;
+  if constexpr (sizeof(T) == 4) {
+    // z_k = clip(u_k -/+ beta): the sign of u_k - v_top (+0 on a tie: the
+    // +1 block) moved onto beta >= 0 with one bit operation.
 #pragma unroll
-  for (int k = 0; k < D; ++k) z[k] = clip01(up[k] ? sub_rn(u[k], beta) : add_rn(u[k], beta));
+    for (int k = 0; k < D; ++k) {
+      const float d = u[k] - v_top;
+      const float sb = __int_as_float(__float_as_int(beta) | (__float_as_int(d) & 0x80000000));
+      z[k] = __saturatef(u[k] - sb);
+    }
+  } else {
+    bool up[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) up[k] = u[k] >= v_top;
+#pragma unroll
+    for (int k = 0; k < D; ++k) z[k] = clip01(up[k] ? sub_rn(u[k], beta) : add_rn(u[k], beta));
+  }
 }
 
 }  // namespace admm
