@@ -661,7 +661,7 @@ int shard_slots(const admm_graph* g, int dtype, int64_t batch) {
 bool use_wide(const admm_graph* g, int dtype, int64_t batch) {
   if (g->kind != 3 || !g->wide_ok[dtype]) return false;
   if (g->engine_req == ADMM_ENGINE_WIDE) return true;
-  long long min_batch = 2048;
+  long long min_batch = 1024;  // measured crossover (cfg5 fp32): 512 frames sharded 111 G vs wide 82 G, 1024: 81 G vs 127 G
   if (const char* env = std::getenv("ADMM_B200_WIDE_MIN")) min_batch = std::atoll(env);
   return batch >= min_batch;
 }

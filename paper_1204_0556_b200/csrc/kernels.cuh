@@ -306,9 +306,6 @@ WideParams<T> make_wide_params(const StreamGraphArgs& g, const ResidentFrameArgs
   p.weight_out = a.weight_out;
   p.S = S;
   p.ncb = static_cast<int>(wide_ncb(g.n_checks));
-  p.static_items = std::getenv("ADMM_B200_WIDE_STATIC") != nullptr;
-  const char* ef = std::getenv("ADMM_B200_WIDE_L2EF");
-  p.l2_evict_first = ef ? std::atoi(ef) : 0;
 
   p.synth = a.synth;
   const WideLayout L(sizeof(T), g.n_edges, g.n_vars, p.ncb, S, a.synth.kind != 0);

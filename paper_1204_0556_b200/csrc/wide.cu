@@ -14,30 +14,13 @@ WideLaunch wide_entry() {
                     &launch_wide<T, VS, D, DV, REG, NS, MINB>, 0, 0, VS, wide_smem_bytes<T, VS, D, DV, NS>(), D, DV};
 }
 
-// Tuning variants of the BASELINE config-5 kernel (ADMM_B200_WIDE_VARIANT).
-inline int wide_variant() {
-  const char* env = std::getenv("ADMM_B200_WIDE_VARIANT");
-  return env ? std::atoi(env) : 0;
-}
-
 template <typename T, int DV>
 bool wide_lookup_dv(int D, bool regular, WideLaunch* out) {
   constexpr int VS = sizeof(T) == 4 ? 2 : 1;  // z/lambda of a thread's slots: one 16-byte access
   if constexpr (DV == 3) {
     if (!regular) return false;
     switch (D) {
-      case 6:
-        if constexpr (sizeof(T) == 4) {
-          switch (wide_variant()) {
-            case 1: *out = wide_entry<T, VS, 6, 3, true, 3, 1>(); return true;
-            case 2: *out = wide_entry<T, VS, 6, 3, true, 4, 1>(); return true;
-            case 3: *out = wide_entry<T, 4, 6, 3, true, 2, 1>(); return true;
-            case 4: *out = wide_entry<T, 1, 6, 3, true, 3, 2>(); return true;
-            default: break;
-          }
-        }
-        *out = wide_entry<T, VS, 6, 3, true>();
-        return true;
+      case 6: *out = wide_entry<T, VS, 6, 3, true>(); return true;
       case 13: *out = wide_entry<T, 1, 13, 3, true>(); return true;
       default: return false;
     }

@@ -4,37 +4,42 @@
 // The sharded engine (sharded.cuh) keeps z/lambda in shared memory and can
 // therefore hold only ~64 frame slots; its passes are short (~25 us) and
 // bound by L2 latency and grid syncs.  This engine instead streams the whole
-// state through HBM every pass over S = 2048-8192 slots, so each phase is a
+// state through HBM every pass over S = 1024-4096 slots, so each phase is a
 // long, fully parallel, bandwidth-bound sweep -- the two-kernel HBM schedule
 // of SURVEY.md 8d (28 B per edge-update in fp32):
 //
-//   phase V (variables)  read msg (DV per var) + gamma/mu, write x
-//   phase C (checks)     gather x (L2-resident, see below), read z/lambda,
-//                        write z/lambda and msg = z - lambda/mu
-//   phase S (slots)      exact stop rule, retirement, refill
+//   phase V (variables)  read messages (DV per variable) + gamma/mu, write x
+//                        (admm_decoder.py:108-124)
+//   phase C (checks)     gather x, read the edge state, fused z-update,
+//                        projection, residual partials, lambda-update; write
+//                        the edge state and the messages z - lambda/mu
+//                        (admm_decoder.py:127-149, parity_polytope.py:352-421)
+//   phase S (slots)      exact stop rule (:169, 174-181), retirement, refill
 //
-// Layout: slots are grouped in STRIPES of W = 32*VS consecutive slots, one
-// stripe per warp access; every array is stripe-major, then row (edge or
-// variable), then the stripe's 32 lanes x VS slots:
-//     zl  [stripe][E][32][2][VS]   z and lambda/mu of a lane: 2 adjacent vectors
-//     msg [stripe][E][32][VS]      x, gm [stripe][N][32][VS]
+// Layout: slots are grouped in STRIPES of W = 32*VS consecutive slots (VS = 2
+// fp32 / 1 fp64 slots per lane); every array is stripe-major, then row (edge
+// or variable), then the stripe's 32 lanes x VS slots:
+//     zl  [stripe][E][32][VS] z (fp32; the messages hold z - lambda/mu)
+//         [stripe][E][32][2][VS] z and lambda/mu (fp64)
+//     msg [stripe][E][32][VS]   x, gm [stripe][N][32][VS]
 //     part[stripe][ncb][2][32][VS] per-check-block residual partials
-// so a warp's access to one row is 32 lanes x 16 B = 512 B contiguous
-// (1 KB for z/lambda), each thread moving VS slots with one 128-bit access.
-// Within a stripe the rows of the checks of one work item are contiguous.
+// so a warp's access to one row is one contiguous 256-byte segment (512 for
+// the fp64 edge state); the rows of the checks of one work item are
+// contiguous.
 //
-// Work items are (stripe, block of rows), distributed round-robin over all
-// warps in stripe-major order, so at any moment the grid works on a few
-// stripes: their x rows (N x 512 B = 8 MB per stripe at n = 16384) stay in
-// L2 while the D-fold reuse of the x gathers happens.  No __syncthreads in
-// the phases; phases are separated by grid syncs of the cooperative kernel.
+// Work items are (stripe, block of rows), taken dynamically by warps in
+// stripe-major order (ItemFeed below), moved through a per-warp cp.async
+// ring of shared-memory stages.  No __syncthreads in the phases; phases are
+// separated by grid syncs of the cooperative kernel.
 //
-// Slot life (as in streaming.cuh): FRESH (z = lambda = 0 implicit) ->
-// RUNNING -> RETIRING (the next V/C pass computes the outputs from the final
-// x) -> next frame or EMPTY.  The stop rule is exact: the S phase sums the
-// per-block partials of every running slot in a fixed order (lane-strided
-// blocks + butterfly), so decisions are deterministic and independent of
-// the batch composition.
+// Slot life: FRESH (z = lambda = 0 implicit) -> RUNNING -> next frame, or
+// EMPTY.  Phase V accumulates the output statistics of every new x and phase
+// C the syndrome of its hard decision, so phase S retires a converged frame
+// in the pass that converged it; only when x or hard decisions are requested
+// does the slot spend a RETIRING pass writing them.  The stop rule is exact:
+// the S phase sums the per-block partials of every running slot in a fixed
+// order (lane-strided blocks + butterfly), so decisions are deterministic and
+// independent of the batch composition.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -76,8 +81,6 @@ struct WideParams {
   uint8_t* flags_out;
   int* weight_out;
   int S, ncb;
-  int static_items;  // debug: static round-robin work items instead of the atomic feed
-  int l2_evict_first;  // L2 evict-first policy on the rows streamed once per pass
   T* zl;
   T* msg;
   T* x;
@@ -115,30 +118,8 @@ __device__ __forceinline__ V wld(const V* p) { return *p; }
 template <typename V>
 __device__ __forceinline__ void wst(V* p, const V& v) { *p = v; }
 
-// Streaming accesses (ld/st.global.cs: evict-first in L1 and L2) for the
-// state that is touched once per pass -- z/lambda, messages, gamma/mu -- so
-// that L2 keeps the x rows of the stripes in flight for their D-fold reuse.
-template <typename V>
-__device__ __forceinline__ V ld_cs(const V* p) {
-  static_assert(sizeof(V) == 32 || sizeof(V) == 16 || sizeof(V) == 8 || sizeof(V) == 4, "vector size");
-  V r;
-  if constexpr (sizeof(V) == 32) {
-    const float4 t0 = __ldcs(reinterpret_cast<const float4*>(p));
-    const float4 t1 = __ldcs(reinterpret_cast<const float4*>(p) + 1);
-    memcpy(&r, &t0, 16);
-    memcpy(reinterpret_cast<char*>(&r) + 16, &t1, 16);
-  } else if constexpr (sizeof(V) == 16) {
-    const float4 t = __ldcs(reinterpret_cast<const float4*>(p));
-    memcpy(&r, &t, 16);
-  } else if constexpr (sizeof(V) == 8) {
-    const float2 t = __ldcs(reinterpret_cast<const float2*>(p));
-    memcpy(&r, &t, 8);
-  } else {
-    const float t = __ldcs(reinterpret_cast<const float*>(p));
-    memcpy(&r, &t, 4);
-  }
-  return r;
-}
+// Streaming stores (st.global.cs: evict-first) for the state written once
+// per pass and read back only in the next one: edge state, messages, gamma/mu.
 template <typename V>
 __device__ __forceinline__ void st_cs(V* p, const V& v) {
   if constexpr (sizeof(V) == 32) {
@@ -170,35 +151,6 @@ __device__ __forceinline__ void st_cs(V* p, const V& v) {
 // memory instead of registers.
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-// Same, with an L2 cache policy (evict_first for rows touched once per pass).
-__device__ __forceinline__ void cp_async16p(uint32_t dst, const void* src, uint64_t pol) {
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void cp_async8p(uint32_t dst, const void* src, uint64_t pol) {
-  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "l"(pol) : "memory");
-}
-__device__ __forceinline__ uint64_t l2_evict_first_policy(bool on) {
-  uint64_t pol;
-  if (on)
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  else
-    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-template <int BYTES>
-__device__ __forceinline__ void cp_async_vec_ef(uint32_t dst, const void* src, uint64_t pol) {
-  if constexpr (BYTES == 32) {
-    cp_async16p(dst, src, pol);
-    cp_async16p(dst + 16, static_cast<const char*>(src) + 16, pol);
-  } else if constexpr (BYTES == 16) {
-    cp_async16p(dst, src, pol);
-  } else if constexpr (BYTES == 8) {
-    cp_async8p(dst, src, pol);
-  } else {
-    static_assert(BYTES == 4, "vector size");
-    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "l"(pol) : "memory");
-  }
 }
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
@@ -272,20 +224,12 @@ struct ItemFeed {
   int n_items, nblk, W;
   const int* st;
   const int* frame;
-  int stat_next, stat_step;  // static assignment (debug): stat_step > 0
   int id1;                   // next item (its table/states are in registers)
   int raw2, raw3;            // lane 0: atomic results for the two items after (in flight)
   int reg[NR];
   VI sreg, freg;
 
-  __device__ __forceinline__ int grab_raw() {
-    if (stat_step > 0) {
-      const int v = stat_next;
-      stat_next += stat_step;
-      return v;
-    }
-    return (threadIdx.x & 31) == 0 ? atomicAdd(ctr, 1) : 0;
-  }
+  __device__ __forceinline__ int grab_raw() { return (threadIdx.x & 31) == 0 ? atomicAdd(ctr, 1) : 0; }
   __device__ __forceinline__ void load(int id) {
     if (id < n_items) {
       const int lane = threadIdx.x & 31;
@@ -390,10 +334,7 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
   V* x = reinterpret_cast<V*>(p.x);
   V* gm = reinterpret_cast<V*>(p.gm);
   const uint32_t ring_s = smem_u32(ring);
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t pol = l2_evict_first_policy(p.l2_evict_first);
-  ItemFeed<TB, VS> feed{p.vtbl, p.ctr + 2, n_vi, n_vb, W, p.st, p.frame, gw,
-                        p.static_items ? (int)((gridDim.x * blockDim.x) >> 5) : 0};
+  ItemFeed<TB, VS> feed{p.vtbl, p.ctr + 2, n_vi, n_vb, W, p.st, p.frame};
   int ik = 0, iq = 0, ti = 0;
   int iid = feed.start(tslot);
 
@@ -418,9 +359,9 @@ __device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned ch
 #pragma unroll
             for (int j = 0; j < DVMAX; ++j) {
               const int e = tb[(iq * VBB + b) * DVMAX + j];
-              if (e >= 0) cp_async_vec_ef<VB>(rowb + j * 32 * VB, msg + ((long long)stripe * E + e) * 32 + lane, pol);
+              if (e >= 0) cp_async_vec<VB>(rowb + j * 32 * VB, msg + ((long long)stripe * E + e) * 32 + lane);
             }
-            cp_async_vec_ef<VB>(rowb + DVMAX * 32 * VB, gm + rb + (long long)i * 32, pol);
+            cp_async_vec<VB>(rowb + DVMAX * 32 * VB, gm + rb + (long long)i * 32);
             if (anyret) cp_async_vec<VB>(rowb + (DVMAX + 1) * 32 * VB, x + rb + (long long)i * 32);
 #pragma unroll
             for (int l = 0; l < VS; ++l) {
@@ -581,10 +522,7 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
   V* msg = reinterpret_cast<V*>(p.msg);
   const int ncb = p.ncb;
   const uint32_t ring_s = smem_u32(ring);
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t pol = l2_evict_first_policy(p.l2_evict_first);
-  ItemFeed<TB, VS> feed{p.ctbl, p.ctr + 3, n_ci, ncb, W, p.st, p.frame, gw,
-                        p.static_items ? (int)((gridDim.x * blockDim.x) >> 5) : 0};
+  ItemFeed<TB, VS> feed{p.ctbl, p.ctr + 3, n_ci, ncb, W, p.st, p.frame};
   int ik = 0, iq = 0, ti = 0;
   int iid = feed.start(tslot);
 
@@ -602,10 +540,10 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
           if (v >= 0) {
             cp_async_vec<VB>(st + G::CX + (k * 32 + lane) * VB, x + xb + (long long)v * 32);
             if constexpr (ZM) {
-              cp_async_vec_ef<VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zv + eb + (e0 + k) * 32, pol);
-              cp_async_vec_ef<VB>(st + G::CZ + (k * 32 + lane) * 2 * VB + VB, msg + eb + (e0 + k) * 32, pol);
+              cp_async_vec<VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zv + eb + (e0 + k) * 32);
+              cp_async_vec<VB>(st + G::CZ + (k * 32 + lane) * 2 * VB + VB, msg + eb + (e0 + k) * 32);
             } else {
-              cp_async_vec_ef<2 * VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zl + eb + (e0 + k) * 32, pol);
+              cp_async_vec<2 * VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zl + eb + (e0 + k) * 32);
             }
           }
         }

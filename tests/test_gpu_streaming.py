@@ -177,7 +177,7 @@ def test_wide_kernel_large_batch_matches_sharded(cuda_ok):
     code = baseline_code("cfg5_n16384")
     cfg = AdmmConfig(mu=5.0)
     ch = Awgn(2.5, code.design_rate)
-    B = 2304  # > the 2048-frame switch, not a multiple of the 4096 slots
+    B = 2304  # > the 1024-frame switch, not a multiple of the 4096 slots
     w64 = decode_synth(code, ch, cfg, seed=1, point=1, trial0=0, batch=B, dtype=torch.float64, want_hard=True)
     assert w64.info["kernel"] == 5
     # the sharded kernel on a sub-batch (below the switch) of the same trials
