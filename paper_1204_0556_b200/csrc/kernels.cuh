@@ -327,8 +327,8 @@ WideParams<T> make_wide_params(const StreamGraphArgs& g, const ResidentFrameArgs
   p.odd = ib + 5 * S;
   p.frame = ib + 6 * S;
   p.fnext = ib + 7 * S;
-  p.slist = ib + 8 * S;
-  p.ctr = ib + 9 * S;
+  p.slist = ib + 8 * S;  // two lists of S
+  p.ctr = ib + 10 * S;
   return p;
 }
 

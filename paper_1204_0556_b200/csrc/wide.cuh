@@ -108,7 +108,7 @@ struct WideLayout {
     part = o; o += al(elem * 2 * ncb * S);
     gfr = o; o += synth ? al(elem * N * S) : 0;
     vpart = o; o += al(sizeof(int) * ((N + kWideVB - 1) / kWideVB) * S);
-    ints = o; o += al(sizeof(int) * (9 * S + 16));
+    ints = o; o += al(sizeof(int) * (10 * S + 16));
     total = o;
   }
 };
@@ -197,46 +197,98 @@ struct WideStage {
 };
 
 // ---- work items ----
-// Items are (stripe, block of kWideVB variables) in phase V and (stripe,
-// block of kWideCB checks) in phase C, numbered stripe-major.  Warps take
-// them dynamically from a global counter (ctr[2] / ctr[3]): a static split
-// left a quarter of the SM time waiting at the grid syncs.  For the item
-// after the current one the feed prefetches (into registers) the block's
-// precomputed index table (wide_ct / wide_vt ints, one coalesced access per
-// lane) and the lane's slot states and frames, and publishes them to the
-// warp's shared-memory table slot when the item starts: no copy issue and
-// no compute step ever waits on a dependent index or state load.
+// The stripes form two groups, G0 and G1, half a pass out of phase: one
+// STEP runs the variable phase of one group together with the check phase of
+// the other, so the latency-bound variable work (random message-row gathers)
+// and the bandwidth-bound check work share the SMs and HBM instead of
+// alternating; a pass is two steps, each followed by the slot phase of the
+// group whose check phase just finished.
+//
+// Within a step, items are (stripe, block of kWideVB variables) of the V
+// group and (stripe, block of kWideCB checks) of the C group, numbered
+// stripe-major and interleaved V, C, V, C, ...  Warps take them dynamically
+// from a global counter (a static split left a quarter of the SM time
+// waiting at the grid syncs).  For the item after the current one the feed
+// prefetches (into registers) the block's precomputed index table (wide_ct /
+// wide_vt ints, one coalesced access per lane) and the lane's slot states and
+// frames, and publishes them to the warp's shared-memory table slot when the
+// item starts: no copy issue and no compute step ever waits on a dependent
+// index or state load.
 __host__ __device__ constexpr int wide_ct(int D) { return ((D + 1) * kWideCB + 31) / 32 * 32; }
 __host__ __device__ constexpr int wide_vt(int DV) { return (kWideVB * DV + 31) / 32 * 32; }
-
-// Table slot: [TB index ints][id, stripe, block, busy][32 x VS states][32 x VS frames]
+template <int D, int DVMAX>
+__host__ __device__ constexpr int wide_tbmax() {
+  return wide_ct(D) > wide_vt(DVMAX) ? wide_ct(D) : wide_vt(DVMAX);
+}
+// Table slot: [TBM index ints][id, stripe, block, busy, kind, -, -, -][32 x VS states][32 x VS frames]
 template <int D, int DVMAX, int VS>
 __host__ __device__ constexpr int wide_tstride() {
-  return (wide_ct(D) > wide_vt(DVMAX) ? wide_ct(D) : wide_vt(DVMAX)) + 4 + 64 * VS;
+  return wide_tbmax<D, DVMAX>() + 8 + 64 * VS;
 }
+enum : int { kItemV = 0, kItemC = 1 };
 
-template <int TB, int VS>
+// The items of one step: nv variable items of stripes [vs0, vs0 + nvs) and
+// nc check items of stripes [cs0, cs0 + ncs).
+struct WideStep {
+  int vs0, nvs, cs0, ncs;
+  int n_vb, ncb;
+  int nv, nc, m, total;
+  __device__ __forceinline__ WideStep(int vs0_, int nvs_, int cs0_, int ncs_, int n_vb_, int ncb_)
+      : vs0(vs0_), nvs(nvs_), cs0(cs0_), ncs(ncs_), n_vb(n_vb_), ncb(ncb_) {
+    nv = nvs * n_vb;
+    nc = ncs * ncb;
+    m = nv < nc ? nv : nc;
+    total = nv + nc;
+  }
+  // item k -> kind, stripe, block
+  __device__ __forceinline__ void decode(int k, int& kind, int& stripe, int& block) const {
+    int idx;
+    if (k < 2 * m) {
+      kind = k & 1;
+      idx = k >> 1;
+    } else {
+      kind = nv > nc ? kItemV : kItemC;
+      idx = k - m;
+    }
+    if (kind == kItemV) {
+      stripe = vs0 + idx / n_vb;
+      block = idx % n_vb;
+    } else {
+      stripe = cs0 + idx / ncb;
+      block = idx % ncb;
+    }
+  }
+};
+
+template <int TBV, int TBC, int VS>
 struct ItemFeed {
-  static constexpr int NR = TB / 32;
+  static constexpr int TBM = TBV > TBC ? TBV : TBC;
+  static constexpr int NR = TBM / 32;
   using VI = WVec<int, VS>;
-  const int* tbl;  // [n_blocks][TB]
+  const int* vtbl;  // [n_vb][TBV]
+  const int* ctbl;  // [ncb][TBC]
   int* ctr;
-  int n_items, nblk, W;
+  const WideStep* stp;
+  int W;
   const int* st;
   const int* frame;
-  int id1;                   // next item (its table/states are in registers)
-  int raw2, raw3;            // lane 0: atomic results for the two items after (in flight)
+  int id1;         // next item (its table/states are in registers)
+  int raw2, raw3;  // lane 0: atomic results for the two items after (in flight)
+  int kind1, stripe1, block1;
   int reg[NR];
   VI sreg, freg;
 
   __device__ __forceinline__ int grab_raw() { return (threadIdx.x & 31) == 0 ? atomicAdd(ctr, 1) : 0; }
   __device__ __forceinline__ void load(int id) {
-    if (id < n_items) {
+    if (id < stp->total) {
       const int lane = threadIdx.x & 31;
-      const int* t = tbl + (long long)(id % nblk) * TB + lane;
+      stp->decode(id, kind1, stripe1, block1);
+      const int tb = kind1 == kItemV ? TBV : TBC;
+      const int* t = (kind1 == kItemV ? vtbl : ctbl) + (long long)block1 * tb + lane;
 #pragma unroll
-      for (int r = 0; r < NR; ++r) reg[r] = __ldg(t + r * 32);
-      const int s0 = (id / nblk) * W + lane * VS;
+      for (int r = 0; r < NR; ++r)
+        if (r * 32 < tb) reg[r] = __ldg(t + r * 32);
+      const int s0 = stripe1 * W + lane * VS;
       sreg = *reinterpret_cast<const VI*>(st + s0);
       freg = *reinterpret_cast<const VI*>(frame + s0);
     }
@@ -246,18 +298,19 @@ struct ItemFeed {
     __syncwarp();  // every lane is done reading the slot's previous contents
 #pragma unroll
     for (int r = 0; r < NR; ++r) slot[r * 32 + lane] = reg[r];
-    if (lane == 0) {
-      slot[TB] = id;
-      slot[TB + 1] = id / nblk;  // stripe
-      slot[TB + 2] = id % nblk;  // block within the stripe
-    }
-    *reinterpret_cast<VI*>(slot + TB + 4 + lane * VS) = sreg;
-    *reinterpret_cast<VI*>(slot + TB + 4 + 32 * VS + lane * VS) = freg;
     bool act = false;
 #pragma unroll
     for (int l = 0; l < VS; ++l) act |= sreg.v[l] != kSlotEmpty;
     act = __any_sync(0xffffffffu, act);
-    if (lane == 0) slot[TB + 3] = act;  // any slot of the item's stripe lanes busy
+    if (lane == 0) {
+      slot[TBM] = id;
+      slot[TBM + 1] = stripe1;
+      slot[TBM + 2] = block1;
+      slot[TBM + 3] = act;  // any slot of the item's stripe lanes busy
+      slot[TBM + 4] = kind1;
+    }
+    *reinterpret_cast<VI*>(slot + TBM + 8 + lane * VS) = sreg;
+    *reinterpret_cast<VI*>(slot + TBM + 8 + 32 * VS + lane * VS) = freg;
     __syncwarp();
   }
   // First item: published into slot0; returns its id.
@@ -293,194 +346,27 @@ __host__ __device__ constexpr int wide_smem_bytes() {
   return (kWideThreads / 32) * wide_warp_bytes<T, VS, D, DVMAX, NS>();
 }
 
-// LLRs of the next frames of the slots retired in the last pass (in-kernel
-// synthesis): written slot-major, one lane per variable, while the slots
-// spend their retiring pass, so the first x-update of the new frame reads
-// them like a stored LLR vector instead of running Philox + Box-Muller on a
-// few lanes of every warp.
+// LLRs of the next frames of slots that started a frame in the last slot
+// phase (in-kernel synthesis): written slot-major, one lane per variable,
+// while the current frame runs, so the first x-update of the next frame
+// reads them like a stored LLR vector instead of running Philox +
+// Box-Muller on a few lanes of every warp.
 constexpr int kWideSynthChunk = 2048;
 
 template <typename T>
-__device__ __forceinline__ void wide_synth_items(const WideParams<T>& p, int nlist) {
+__device__ __forceinline__ void wide_synth_items(const WideParams<T>& p, const int* list, int nlist, int* grab) {
   const int lane = threadIdx.x & 31;
   const int nch = (p.n_vars + kWideSynthChunk - 1) / kWideSynthChunk;
   const int n = nlist * nch;
   for (;;) {
-    const int q = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(p.ctr + 4, 1) : 0, 0);
+    const int q = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(grab, 1) : 0, 0);
     if (q >= n) break;
-    const int s = p.slist[q / nch], c = q % nch;
+    const int s = list[q / nch], c = q % nch;
     const int f = p.fnext[s];
     const int i1 = min(p.n_vars, (c + 1) * kWideSynthChunk);
     for (int i = c * kWideSynthChunk + lane; i < i1; i += 32)
       p.gfr[(long long)s * p.n_vars + i] = static_cast<T>(synth_llr(p.synth, p.synth.trial0 + f, i));
   }
-}
-
-// ---- phase V: x = clip((sum msg - gamma/mu) / deg) (admm_decoder.py:108-124) ----
-// One code path for every slot state (per-lane selects): a FRESH slot sums no
-// messages and takes gamma/mu from its frame's LLR vector; a RETIRING slot
-// keeps x and accumulates the output statistics (make_output, :92-105).
-template <typename T, int VS, int D, int DVMAX, bool REG, int NS>
-__device__ __forceinline__ void wide_phase_v(const WideParams<T>& p, unsigned char* ring, int* tslot, int tstride,
-                                             int n_vi, int n_vb) {
-  using V = WVec<T, VS>;
-  using VI = WVec<int, VS>;
-  using G = WideStage<T, VS, D, DVMAX>;
-  constexpr int W = 32 * VS, VBB = G::VBB, TPI = (kWideVB + VBB - 1) / VBB, VB = G::VB, TB = wide_vt(DVMAX);
-  constexpr int ES = static_cast<int>(sizeof(T));
-  const int lane = threadIdx.x & 31;
-  const long long E = p.n_edges, N = p.n_vars;
-  const V* msg = reinterpret_cast<const V*>(p.msg);
-  V* x = reinterpret_cast<V*>(p.x);
-  V* gm = reinterpret_cast<V*>(p.gm);
-  const uint32_t ring_s = smem_u32(ring);
-  ItemFeed<TB, VS> feed{p.vtbl, p.ctr + 2, n_vi, n_vb, W, p.st, p.frame};
-  int ik = 0, iq = 0, ti = 0;
-  int iid = feed.start(tslot);
-
-  auto issue_next = [&]() {
-    if (iid < n_vi) {
-      const int* tb = tslot + (ik & 1) * tstride;
-      const int stripe = tb[TB + 1], vb = tb[TB + 2];
-      const int i0 = vb * kWideVB + iq * VBB, i1 = min(p.n_vars, min((vb + 1) * kWideVB, i0 + VBB));
-      if (tb[TB + 3] && i0 < i1) {
-        const VI stv = *reinterpret_cast<const VI*>(tb + TB + 4 + lane * VS);
-        const VI frv = *reinterpret_cast<const VI*>(tb + TB + 4 + 32 * VS + lane * VS);
-        bool anyret = false;
-#pragma unroll
-        for (int l = 0; l < VS; ++l) anyret |= stv.v[l] == kSlotRetiring;
-        const uint32_t st = ring_s + (ti % NS) * G::bytes;
-        const long long rb = (long long)stripe * N * 32 + lane;
-#pragma unroll
-        for (int b = 0; b < VBB; ++b) {
-          const int i = i0 + b;
-          if (i < i1) {
-            const uint32_t rowb = st + b * G::VROWS * 32 * VB + lane * VB;
-#pragma unroll
-            for (int j = 0; j < DVMAX; ++j) {
-              const int e = tb[(iq * VBB + b) * DVMAX + j];
-              if (e >= 0) cp_async_vec<VB>(rowb + j * 32 * VB, msg + ((long long)stripe * E + e) * 32 + lane);
-            }
-            cp_async_vec<VB>(rowb + DVMAX * 32 * VB, gm + rb + (long long)i * 32);
-            if (anyret) cp_async_vec<VB>(rowb + (DVMAX + 1) * 32 * VB, x + rb + (long long)i * 32);
-#pragma unroll
-            for (int l = 0; l < VS; ++l) {
-              if (stv.v[l] != kSlotFresh) continue;
-              const T* src = p.synth.kind != 0 ? p.gfr + (long long)(stripe * W + lane * VS + l) * N + i
-                                               : p.gamma + (long long)frv.v[l] * p.ld_gamma + i;
-              cp_async_vec<ES>(rowb + (DVMAX + 2) * 32 * VB + l * ES, src);
-            }
-          }
-        }
-      }
-    }
-    cp_commit();
-    ++ti;
-    if (++iq == TPI) {
-      iq = 0;
-      ++ik;
-      iid = feed.advance(tslot + (ik & 1) * tstride);
-    }
-  };
-
-  int iw[VS], inon[VS];  // weight / non-integral of the item's new x, per slot (phase S retires from them)
-#pragma unroll
-  for (int l = 0; l < VS; ++l) iw[l] = inon[l] = 0;
-#pragma unroll
-  for (int t = 0; t < NS - 1; ++t) issue_next();
-  for (int t = 0;; ++t) {
-    const int ck = t / TPI, cq = t % TPI;
-    const int* tb = tslot + (ck & 1) * tstride;
-    const int cid = tb[TB];
-    if (cid >= n_vi) break;
-    issue_next();
-    cp_wait<NS - 1>();
-    const int stripe = tb[TB + 1], vb = tb[TB + 2];
-    const int i0 = vb * kWideVB + cq * VBB, i1 = min(p.n_vars, min((vb + 1) * kWideVB, i0 + VBB));
-    if (!tb[TB + 3] || i0 >= i1) continue;
-    const unsigned char* st = ring + (t % NS) * G::bytes;
-    const VI stv = *reinterpret_cast<const VI*>(tb + TB + 4 + lane * VS);
-    const VI frv = *reinterpret_cast<const VI*>(tb + TB + 4 + 32 * VS + lane * VS);
-    const int s0 = stripe * W + lane * VS;
-    bool anyupd = false, anyfresh = false, anyret = false;
-#pragma unroll
-    for (int l = 0; l < VS; ++l) {
-      anyupd |= stv.v[l] != kSlotEmpty;
-      anyfresh |= stv.v[l] == kSlotFresh;
-      anyret |= stv.v[l] == kSlotRetiring;
-    }
-    int wsum[VS], nonint[VS];
-#pragma unroll
-    for (int l = 0; l < VS; ++l) wsum[l] = nonint[l] = 0;
-    const long long rb = (long long)stripe * N * 32 + lane;
-#pragma unroll
-    for (int b = 0; b < VBB; ++b) {
-      const int i = i0 + b;
-      if (i >= i1) break;
-      const unsigned char* rowb = st + b * G::VROWS * 32 * VB + lane * VB;
-      int deg = 0;
-      V mv[DVMAX];
-#pragma unroll
-      for (int j = 0; j < DVMAX; ++j) {
-        const bool on = REG || tb[(cq * VBB + b) * DVMAX + j] >= 0;
-        deg += on;
-        if (on) mv[j] = lds_vec<V>(rowb + j * 32 * VB);
-      }
-      V g = lds_vec<V>(rowb + DVMAX * 32 * VB);
-      V xo, gf;
-      if (anyret) xo = lds_vec<V>(rowb + (DVMAX + 1) * 32 * VB);
-      if (anyfresh) gf = lds_vec<V>(rowb + (DVMAX + 2) * 32 * VB);
-      V xn;
-#pragma unroll
-      for (int l = 0; l < VS; ++l) {
-        const int state = stv.v[l];
-        const bool fresh = state == kSlotFresh, ret = state == kSlotRetiring;
-        T acc = T(0);
-#pragma unroll
-        for (int j = 0; j < DVMAX; ++j)
-          if (j < deg) acc = add_rn(acc, mv[j].v[l]);  // increasing edge id (np.bincount order)
-        if (anyfresh) {
-          if (fresh) acc = T(0);  // z = lambda = 0 (AdmmState.initial)
-          g.v[l] = fresh ? div_rn(gf.v[l], p.mu) : g.v[l];
-        }
-        T xv = deg > 0 ? clip01(div_rn(sub_rn(acc, g.v[l]), T(deg))) : (g.v[l] < T(0) ? T(1) : T(0));
-        iw[l] += xv > T(0.5) ? 1 : 0;  // make_output (:92-105) of x_t, in case the slot stops now
-        inon[l] |= !(vmin(fabs(xv), fabs(T(1) - xv)) <= T(1e-5)) ? 1 : 0;
-        if (anyret) {
-          const T xf = xo.v[l];  // final iterate of a retiring slot
-          const bool h = xf > T(0.5);
-          wsum[l] += (ret && h) ? 1 : 0;
-          nonint[l] |= (ret && !(vmin(fabs(xf), fabs(T(1) - xf)) <= T(1e-5))) ? 1 : 0;
-          if (ret) {
-            if (p.x_out) p.x_out[(long long)frv.v[l] * p.ld_x + i] = xf;
-            if (p.hard_out) p.hard_out[(long long)frv.v[l] * p.ld_hard + i] = h;
-            xv = xf;
-          }
-        }
-        xn.v[l] = xv;
-      }
-      if (anyupd) wst(x + rb + (long long)i * 32, xn);
-      if (anyfresh) st_cs(gm + rb + (long long)i * 32, g);
-    }
-    if (anyret) {
-#pragma unroll
-      for (int l = 0; l < VS; ++l) {
-        if (wsum[l]) atomicAdd(p.weight + s0 + l, wsum[l]);
-        if (nonint[l]) atomicOr(p.nonint + s0 + l, 1);
-      }
-    }
-    if (i1 == min(p.n_vars, (vb + 1) * kWideVB)) {  // last task of the item
-      if (p.direct) {
-        VI o;
-#pragma unroll
-        for (int l = 0; l < VS; ++l) o.v[l] = iw[l] | (inon[l] << 8);
-        *reinterpret_cast<VI*>(p.vpart + ((long long)stripe * n_vb + vb) * W + lane * VS) = o;
-      }
-#pragma unroll
-      for (int l = 0; l < VS; ++l) iw[l] = inon[l] = 0;
-    }
-  }
-  cp_wait<0>();
 }
 
 // Edge-state store of phase C: (z, lambda/mu) pairs, or z alone (ZM).
@@ -497,53 +383,100 @@ __device__ __forceinline__ void wide_store_z(WVec<T, 2 * VS>* zl, WVec<T, VS>* z
   }
 }
 
-// ---- phase C: fused z-update, projection, residuals, lambda-update, message
-// (admm_decoder.py:127-149, parity_polytope.py:352-421) ----
-// One code path for every slot state: FRESH slots start from z = lambda = 0,
-// only RUNNING/FRESH slots add to the residual partials, RETIRING slots add
-// the parity of their final hard decision (is_codeword, codes.py:145-154).
+// ---- one step: phase V of one stripe group, phase C of the other ----
+//
+// phase V: x = clip((sum msg - gamma/mu) / deg) (admm_decoder.py:108-124).
+// One code path for every slot state (per-lane selects): a FRESH slot sums no
+// messages and takes gamma/mu from its frame's LLR vector; a RETIRING slot
+// keeps x and accumulates the output statistics (make_output, :92-105).
+//
+// phase C: fused z-update, projection, residuals, lambda-update, message
+// (admm_decoder.py:127-149, parity_polytope.py:352-421).  FRESH slots start
+// from z = lambda = 0, only RUNNING/FRESH slots add to the residual partials,
+// every slot adds the parity of its hard decision (is_codeword,
+// codes.py:145-154) to the block's syndrome flag.
 template <typename T, int VS, int D, int DVMAX, bool REG, int NS>
-__device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned char* ring, int* tslot, int tstride,
-                                             int n_ci) {
+__device__ __forceinline__ void wide_step(const WideParams<T>& p, unsigned char* ring, int* tslot, int tstride,
+                                          const WideStep& sp, int* ctr_items) {
   using V = WVec<T, VS>;
   using VI = WVec<int, VS>;
   using V2 = WVec<T, 2 * VS>;
   using G = WideStage<T, VS, D, DVMAX>;
-  constexpr int W = 32 * VS, CB = kWideCB, VB = G::VB, TB = wide_ct(D);
+  constexpr int W = 32 * VS, VBB = G::VBB, VB = G::VB, CB = kWideCB;
+  constexpr int TPIV = (kWideVB + VBB - 1) / VBB;
+  constexpr int TBV = wide_vt(DVMAX), TBC = wide_ct(D), TBM = wide_tbmax<D, DVMAX>();
+  constexpr int ES = static_cast<int>(sizeof(T));
   // fp32 keeps (z, message) per edge and recovers lambda/mu = z - message:
   // 20 instead of 24 bytes of edge-state traffic per edge-update.  fp64 (the
   // parity mode) keeps (z, lambda/mu) and writes the message separately.
   constexpr bool ZM = sizeof(T) == 4;
+  static_assert(NS - 1 < TPIV && NS - 1 < CB, "stage ring deeper than an item");
   const int lane = threadIdx.x & 31;
   const long long E = p.n_edges, N = p.n_vars;
-  const V* x = reinterpret_cast<const V*>(p.x);
+  V* x = reinterpret_cast<V*>(p.x);
+  V* gm = reinterpret_cast<V*>(p.gm);
   V2* zl = reinterpret_cast<V2*>(p.zl);
   V* zv = reinterpret_cast<V*>(p.zl);
   V* msg = reinterpret_cast<V*>(p.msg);
-  const int ncb = p.ncb;
+  const int n_vb = sp.n_vb, ncb = sp.ncb, n_items = sp.total;
   const uint32_t ring_s = smem_u32(ring);
-  ItemFeed<TB, VS> feed{p.ctbl, p.ctr + 3, n_ci, ncb, W, p.st, p.frame};
+  ItemFeed<TBV, TBC, VS> feed{p.vtbl, p.ctbl, ctr_items, &sp, W, p.st, p.frame};
   int ik = 0, iq = 0, ti = 0;
   int iid = feed.start(tslot);
 
   auto issue_next = [&]() {
-    if (iid < n_ci) {
-      const int* tb = tslot + (ik & 1) * tstride;
-      const int stripe = tb[TB + 1], c = tb[TB + 2] * CB + iq;
-      if (tb[TB + 3] && c < p.n_checks) {
-        const uint32_t st = ring_s + (ti % NS) * G::bytes;
-        const long long e0 = tb[D * CB + iq];
-        const long long xb = (long long)stripe * N * 32 + lane, eb = (long long)stripe * E * 32 + lane;
+    const int* tb = tslot + (ik & 1) * tstride;
+    const int kind = tb[TBM + 4];
+    if (iid < n_items) {
+      const int stripe = tb[TBM + 1], blk = tb[TBM + 2];
+      const uint32_t st = ring_s + (ti % NS) * G::bytes;
+      if (kind == kItemV) {
+        const int i0 = blk * kWideVB + iq * VBB, i1 = min(p.n_vars, min((blk + 1) * kWideVB, i0 + VBB));
+        if (tb[TBM + 3] && i0 < i1) {
+          const VI stv = *reinterpret_cast<const VI*>(tb + TBM + 8 + lane * VS);
+          const VI frv = *reinterpret_cast<const VI*>(tb + TBM + 8 + 32 * VS + lane * VS);
+          bool anyret = false;
 #pragma unroll
-        for (int k = 0; k < D; ++k) {
-          const int v = tb[k * CB + iq];
-          if (v >= 0) {
-            cp_async_vec<VB>(st + G::CX + (k * 32 + lane) * VB, x + xb + (long long)v * 32);
-            if constexpr (ZM) {
-              cp_async_vec<VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zv + eb + (e0 + k) * 32);
-              cp_async_vec<VB>(st + G::CZ + (k * 32 + lane) * 2 * VB + VB, msg + eb + (e0 + k) * 32);
-            } else {
-              cp_async_vec<2 * VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zl + eb + (e0 + k) * 32);
+          for (int l = 0; l < VS; ++l) anyret |= stv.v[l] == kSlotRetiring;
+          const long long rb = (long long)stripe * N * 32 + lane;
+#pragma unroll
+          for (int b = 0; b < VBB; ++b) {
+            const int i = i0 + b;
+            if (i < i1) {
+              const uint32_t rowb = st + b * G::VROWS * 32 * VB + lane * VB;
+#pragma unroll
+              for (int j = 0; j < DVMAX; ++j) {
+                const int e = tb[(iq * VBB + b) * DVMAX + j];
+                if (e >= 0) cp_async_vec<VB>(rowb + j * 32 * VB, msg + ((long long)stripe * E + e) * 32 + lane);
+              }
+              cp_async_vec<VB>(rowb + DVMAX * 32 * VB, gm + rb + (long long)i * 32);
+              if (anyret) cp_async_vec<VB>(rowb + (DVMAX + 1) * 32 * VB, x + rb + (long long)i * 32);
+#pragma unroll
+              for (int l = 0; l < VS; ++l) {
+                if (stv.v[l] != kSlotFresh) continue;
+                const T* src = p.synth.kind != 0 ? p.gfr + (long long)(stripe * W + lane * VS + l) * N + i
+                                                 : p.gamma + (long long)frv.v[l] * p.ld_gamma + i;
+                cp_async_vec<ES>(rowb + (DVMAX + 2) * 32 * VB + l * ES, src);
+              }
+            }
+          }
+        }
+      } else {
+        const int c = blk * CB + iq;
+        if (tb[TBM + 3] && c < p.n_checks) {
+          const long long e0 = tb[D * CB + iq];
+          const long long xb = (long long)stripe * N * 32 + lane, eb = (long long)stripe * E * 32 + lane;
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            const int v = tb[k * CB + iq];
+            if (v >= 0) {
+              cp_async_vec<VB>(st + G::CX + (k * 32 + lane) * VB, x + xb + (long long)v * 32);
+              if constexpr (ZM) {
+                cp_async_vec<VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zv + eb + (e0 + k) * 32);
+                cp_async_vec<VB>(st + G::CZ + (k * 32 + lane) * 2 * VB + VB, msg + eb + (e0 + k) * 32);
+              } else {
+                cp_async_vec<2 * VB>(st + G::CZ + (k * 32 + lane) * 2 * VB, zl + eb + (e0 + k) * 32);
+              }
             }
           }
         }
@@ -551,56 +484,150 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
     }
     cp_commit();
     ++ti;
-    if (++iq == CB) {
+    if (++iq == (kind == kItemV ? TPIV : CB)) {
       iq = 0;
       ++ik;
       iid = feed.advance(tslot + (ik & 1) * tstride);
     }
   };
 
+  // per-item accumulators (phase V: weight / non-integral of the new x;
+  // phase C: residual partials and the syndrome flag), flushed at item ends
+  int iw[VS], inon[VS], odd[VS];
   T primal[VS], moved[VS];
-  int odd[VS];
 #pragma unroll
   for (int l = 0; l < VS; ++l) {
+    iw[l] = inon[l] = odd[l] = 0;
     primal[l] = moved[l] = T(0);
-    odd[l] = 0;
   }
 #pragma unroll
   for (int t = 0; t < NS - 1; ++t) issue_next();
+  int ck = 0, cq = 0;
   for (int t = 0;; ++t) {
-    const int ck = t / CB, cq = t % CB;
     const int* tb = tslot + (ck & 1) * tstride;
-    const int cid = tb[TB];
-    if (cid >= n_ci) break;
+    const int cid = tb[TBM];
+    if (cid >= n_items) break;
+    const int kind = tb[TBM + 4];
+    const int cqt = cq;
+    if (++cq == (kind == kItemV ? TPIV : CB)) {
+      cq = 0;
+      ++ck;
+    }
     issue_next();
     cp_wait<NS - 1>();
-    const int stripe = tb[TB + 1], cb = tb[TB + 2], c = cb * CB + cq;
-    if (!tb[TB + 3] || c >= p.n_checks) continue;
+    const int stripe = tb[TBM + 1], blk = tb[TBM + 2];
+    if (!tb[TBM + 3]) continue;  // every slot of the stripe empty
     const unsigned char* st = ring + (t % NS) * G::bytes;
-    const VI stv = *reinterpret_cast<const VI*>(tb + TB + 4 + lane * VS);
-    bool anyret = false;
+    const VI stv = *reinterpret_cast<const VI*>(tb + TBM + 8 + lane * VS);
+    const int s0 = stripe * W + lane * VS;
+    if (kind == kItemV) {
+      // ---------------- phase V task: VBB variables ----------------
+      const int i0 = blk * kWideVB + cqt * VBB, i1 = min(p.n_vars, min((blk + 1) * kWideVB, i0 + VBB));
+      if (i0 >= i1) continue;
+      const VI frv = *reinterpret_cast<const VI*>(tb + TBM + 8 + 32 * VS + lane * VS);
+      bool anyupd = false, anyfresh = false, anyret = false;
 #pragma unroll
-    for (int l = 0; l < VS; ++l) anyret |= stv.v[l] == kSlotRetiring;
-    int d = REG ? D : 0;
-    if constexpr (!REG) {
+      for (int l = 0; l < VS; ++l) {
+        anyupd |= stv.v[l] != kSlotEmpty;
+        anyfresh |= stv.v[l] == kSlotFresh;
+        anyret |= stv.v[l] == kSlotRetiring;
+      }
+      int wsum[VS], nonint[VS];
 #pragma unroll
-      for (int k = 0; k < D; ++k) d += tb[k * CB + cq] >= 0;
-    }
-    const long long e0 = tb[D * CB + cq];
-    const long long eb = (long long)stripe * E * 32 + lane;
-    V gx[D];
-    V2 zlv[D];
+      for (int l = 0; l < VS; ++l) wsum[l] = nonint[l] = 0;
+      const long long rb = (long long)stripe * N * 32 + lane;
 #pragma unroll
-    for (int k = 0; k < D; ++k)
-      if (k < d) {
-        gx[k] = lds_vec<V>(st + G::CX + (k * 32 + lane) * VB);
-        zlv[k] = lds_vec<V2>(st + G::CZ + (k * 32 + lane) * 2 * VB);
-        if constexpr (ZM) {
+      for (int b = 0; b < VBB; ++b) {
+        const int i = i0 + b;
+        if (i >= i1) break;
+        const unsigned char* rowb = st + b * G::VROWS * 32 * VB + lane * VB;
+        int deg = 0;
+        V mv[DVMAX];
 #pragma unroll
-          for (int l = 0; l < VS; ++l) zlv[k].v[VS + l] = sub_rn(zlv[k].v[l], zlv[k].v[VS + l]);
+        for (int j = 0; j < DVMAX; ++j) {
+          const bool on = REG || tb[(cqt * VBB + b) * DVMAX + j] >= 0;
+          deg += on;
+          if (on) mv[j] = lds_vec<V>(rowb + j * 32 * VB);
+        }
+        V g = lds_vec<V>(rowb + DVMAX * 32 * VB);
+        V xo, gf;
+        if (anyret) xo = lds_vec<V>(rowb + (DVMAX + 1) * 32 * VB);
+        if (anyfresh) gf = lds_vec<V>(rowb + (DVMAX + 2) * 32 * VB);
+        V xn;
+#pragma unroll
+        for (int l = 0; l < VS; ++l) {
+          const int state = stv.v[l];
+          const bool fresh = state == kSlotFresh, ret = state == kSlotRetiring;
+          T acc = T(0);
+#pragma unroll
+          for (int j = 0; j < DVMAX; ++j)
+            if (j < deg) acc = add_rn(acc, mv[j].v[l]);  // increasing edge id (np.bincount order)
+          if (anyfresh) {
+            if (fresh) acc = T(0);  // z = lambda = 0 (AdmmState.initial)
+            g.v[l] = fresh ? div_rn(gf.v[l], p.mu) : g.v[l];
+          }
+          T xv = deg > 0 ? clip01(div_rn(sub_rn(acc, g.v[l]), T(deg))) : (g.v[l] < T(0) ? T(1) : T(0));
+          iw[l] += xv > T(0.5) ? 1 : 0;  // make_output (:92-105) of x_t, in case the slot stops now
+          inon[l] |= !(vmin(fabs(xv), fabs(T(1) - xv)) <= T(1e-5)) ? 1 : 0;
+          if (anyret) {
+            const T xf = xo.v[l];  // final iterate of a retiring slot
+            const bool h = xf > T(0.5);
+            wsum[l] += (ret && h) ? 1 : 0;
+            nonint[l] |= (ret && !(vmin(fabs(xf), fabs(T(1) - xf)) <= T(1e-5))) ? 1 : 0;
+            if (ret) {
+              if (p.x_out) p.x_out[(long long)frv.v[l] * p.ld_x + i] = xf;
+              if (p.hard_out) p.hard_out[(long long)frv.v[l] * p.ld_hard + i] = h;
+              xv = xf;
+            }
+          }
+          xn.v[l] = xv;
+        }
+        if (anyupd) wst(x + rb + (long long)i * 32, xn);
+        if (anyfresh) st_cs(gm + rb + (long long)i * 32, g);
+      }
+      if (anyret) {
+#pragma unroll
+        for (int l = 0; l < VS; ++l) {
+          if (wsum[l]) atomicAdd(p.weight + s0 + l, wsum[l]);
+          if (nonint[l]) atomicOr(p.nonint + s0 + l, 1);
         }
       }
-    {
+      if (i1 == min(p.n_vars, (blk + 1) * kWideVB)) {  // last task of the item
+        if (p.direct) {
+          VI o;
+#pragma unroll
+          for (int l = 0; l < VS; ++l) o.v[l] = iw[l] | (inon[l] << 8);
+          *reinterpret_cast<VI*>(p.vpart + ((long long)stripe * n_vb + blk) * W + lane * VS) = o;
+        }
+#pragma unroll
+        for (int l = 0; l < VS; ++l) iw[l] = inon[l] = 0;
+      }
+    } else {
+      // ---------------- phase C task: one check ----------------
+      const int c = blk * CB + cqt;
+      if (c >= p.n_checks) continue;
+      bool anyret = false;
+#pragma unroll
+      for (int l = 0; l < VS; ++l) anyret |= stv.v[l] == kSlotRetiring;
+      int d = REG ? D : 0;
+      if constexpr (!REG) {
+#pragma unroll
+        for (int k = 0; k < D; ++k) d += tb[k * CB + cqt] >= 0;
+      }
+      const long long e0 = tb[D * CB + cqt];
+      const long long eb = (long long)stripe * E * 32 + lane;
+      V gx[D];
+      V2 zlv[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k)
+        if (k < d) {
+          gx[k] = lds_vec<V>(st + G::CX + (k * 32 + lane) * VB);
+          zlv[k] = lds_vec<V2>(st + G::CZ + (k * 32 + lane) * 2 * VB);
+          if constexpr (ZM) {
+#pragma unroll
+            for (int l = 0; l < VS; ++l) zlv[k].v[VS + l] = sub_rn(zlv[k].v[l], zlv[k].v[VS + l]);
+          }
+        }
 #pragma unroll
       for (int l = 0; l < VS; ++l) {
         int par = 0;
@@ -609,70 +636,69 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
           if (k < d) par ^= gx[k].v[l] > T(0.5);
         odd[l] |= par;
       }
-    }
 #pragma unroll
-    for (int l = 0; l < VS; ++l) {
-      const bool run = stv.v[l] == kSlotRunning;
-      const bool act = run || stv.v[l] == kSlotFresh;
-      T w_[D], u[D], zn[D], zo[D], lo[D];
+      for (int l = 0; l < VS; ++l) {
+        const bool run = stv.v[l] == kSlotRunning;
+        const bool act = run || stv.v[l] == kSlotFresh;
+        T w_[D], u[D], zn[D], zo[D], lo[D];
 #pragma unroll
-      for (int k = 0; k < D; ++k) {
-        const bool on = k < d;
-        zo[k] = run ? zlv[k].v[l] : T(0);
-        lo[k] = run ? zlv[k].v[VS + l] : T(0);  // scaled dual lambda/mu
-        const T g = on ? gx[k].v[l] : T(0);
-        w_[k] = add_rn(mul_rn(p.rho, g), mul_rn(p.one_minus_rho, zo[k]));
-        u[k] = on ? add_rn(w_[k], lo[k]) : -Num<T>::inf();
-      }
-      if constexpr (REG) {
-        project_pp_fixed<T, D>(u, zn);
-      } else {
-        project_pp<T, D>(u, zn, d);
-      }
-      T pr = T(0), mo = T(0);
-#pragma unroll
-      for (int k = 0; k < D; ++k) {
-        if (k < d) {
-          const T r1 = sub_rn(gx[k].v[l], zn[k]);
-          const T r2 = sub_rn(zn[k], zo[k]);
-          pr = add_rn(pr, mul_rn(r1, r1));
-          mo = add_rn(mo, mul_rn(r2, r2));
-          const T lnew = add_rn(lo[k], sub_rn(w_[k], zn[k]));
-          zlv[k].v[l] = zn[k];
-          zlv[k].v[VS + l] = lnew;
-          gx[k].v[l] = sub_rn(zn[k], lnew);  // message
+        for (int k = 0; k < D; ++k) {
+          const bool on = k < d;
+          zo[k] = run ? zlv[k].v[l] : T(0);
+          lo[k] = run ? zlv[k].v[VS + l] : T(0);  // scaled dual lambda/mu
+          const T g = on ? gx[k].v[l] : T(0);
+          w_[k] = add_rn(mul_rn(p.rho, g), mul_rn(p.one_minus_rho, zo[k]));
+          u[k] = on ? add_rn(w_[k], lo[k]) : -Num<T>::inf();
         }
-      }
-      primal[l] = act ? add_rn(primal[l], pr) : primal[l];
-      moved[l] = act ? add_rn(moved[l], mo) : moved[l];
-    }
+        if constexpr (REG) {
+          project_pp_fixed<T, D>(u, zn);
+        } else {
+          project_pp<T, D>(u, zn, d);
+        }
+        T pr = T(0), mo = T(0);
 #pragma unroll
-    for (int k = 0; k < D; ++k)
-      if (k < d) {
-        wide_store_z<T, VS, ZM>(zl, zv, eb + (e0 + k) * 32, zlv[k]);
-        st_cs(msg + eb + (e0 + k) * 32, gx[k]);
-      }
-    if (cq == CB - 1 || c + 1 >= p.n_checks) {
-      // End of the item: per-slot partials of its checks (fixed order).
-      V* part = reinterpret_cast<V*>(p.part) + ((long long)stripe * ncb + cb) * 64 + lane;
-      V a, b;
-#pragma unroll
-      for (int l = 0; l < VS; ++l) {
-        a.v[l] = primal[l];
-        b.v[l] = odd[l] ? -moved[l] : moved[l];  // sign bit: an odd check in the block (is_codeword of x_t)
-      }
-      wst(part, a);
-      wst(part + 32, b);
-      if (anyret) {
-        const int s0 = stripe * W + lane * VS;
-#pragma unroll
-        for (int l = 0; l < VS; ++l)
-          if (stv.v[l] == kSlotRetiring && odd[l]) atomicOr(p.odd + s0 + l, 1);
+        for (int k = 0; k < D; ++k) {
+          if (k < d) {
+            const T r1 = sub_rn(gx[k].v[l], zn[k]);
+            const T r2 = sub_rn(zn[k], zo[k]);
+            pr = add_rn(pr, mul_rn(r1, r1));
+            mo = add_rn(mo, mul_rn(r2, r2));
+            const T lnew = add_rn(lo[k], sub_rn(w_[k], zn[k]));
+            zlv[k].v[l] = zn[k];
+            zlv[k].v[VS + l] = lnew;
+            gx[k].v[l] = sub_rn(zn[k], lnew);  // message
+          }
+        }
+        primal[l] = act ? add_rn(primal[l], pr) : primal[l];
+        moved[l] = act ? add_rn(moved[l], mo) : moved[l];
       }
 #pragma unroll
-      for (int l = 0; l < VS; ++l) {
-        primal[l] = moved[l] = T(0);
-        odd[l] = 0;
+      for (int k = 0; k < D; ++k)
+        if (k < d) {
+          wide_store_z<T, VS, ZM>(zl, zv, eb + (e0 + k) * 32, zlv[k]);
+          st_cs(msg + eb + (e0 + k) * 32, gx[k]);
+        }
+      if (cqt == CB - 1 || c + 1 >= p.n_checks) {
+        // End of the item: per-slot partials of its checks (fixed order).
+        V* part = reinterpret_cast<V*>(p.part) + ((long long)stripe * ncb + blk) * 64 + lane;
+        V a, b;
+#pragma unroll
+        for (int l = 0; l < VS; ++l) {
+          a.v[l] = primal[l];
+          b.v[l] = odd[l] ? -moved[l] : moved[l];  // sign bit: an odd check in the block (is_codeword of x_t)
+        }
+        wst(part, a);
+        wst(part + 32, b);
+        if (anyret) {
+#pragma unroll
+          for (int l = 0; l < VS; ++l)
+            if (stv.v[l] == kSlotRetiring && odd[l]) atomicOr(p.odd + s0 + l, 1);
+        }
+#pragma unroll
+        for (int l = 0; l < VS; ++l) {
+          primal[l] = moved[l] = T(0);
+          odd[l] = 0;
+        }
       }
     }
   }
@@ -681,7 +707,7 @@ __device__ __forceinline__ void wide_phase_c(const WideParams<T>& p, unsigned ch
 
 // ---- phase S: one warp per slot ----
 template <typename T, int VS>
-__device__ __forceinline__ void wide_phase_s(const WideParams<T>& p, int s) {
+__device__ __forceinline__ void wide_phase_s(const WideParams<T>& p, int s, int* list, int* nlist) {
   constexpr int W = 32 * VS;
   const int lane = threadIdx.x & 31;
   const int state = __shfl_sync(0xffffffffu, lane == 0 ? p.st[s] : 0, 0);
@@ -767,7 +793,7 @@ __device__ __forceinline__ void wide_phase_s(const WideParams<T>& p, int s) {
       const int f = atomicAdd(p.ctr + 0, 1);
       const int fn = f < p.batch ? f : -1;
       p.fnext[s] = fn;
-      if (fn >= 0 && p.synth.kind != 0) p.slist[atomicAdd(p.ctr + 5, 1)] = s;
+      if (fn >= 0 && p.synth.kind != 0) list[atomicAdd(nlist, 1)] = s;
     }
     if (stop) {
       p.conv[s] = converged;
@@ -779,10 +805,14 @@ __device__ __forceinline__ void wide_phase_s(const WideParams<T>& p, int s) {
 }
 
 // Phase profiler (admm_wide_phase_profile): CTA 0, thread 0 accumulates
-// clock64() cycles: 0 phase V, 1 sync, 2 phase C, 3 sync, 4 phase S, 5 sync, 6 passes.
+// clock64() cycles: 0 step A, 1 sync, 2 slot phase G1 + sync, 3 step B,
+// 4 sync, 5 slot phase G0 + sync, 6 passes.
 __device__ unsigned long long g_wide_cycles[8];
 __device__ int g_wide_prof;
 
+// ctr: [0] frame queue, [1] busy slots, [2] / [3] work items of step A / B,
+// [4] / [6] synthesis items of step A / B, [5] / [7] synthesis list lengths
+// (list A filled by slot phase G0 for step A, list B by slot phase G1).
 template <typename T, int VS, int D, int DVMAX, bool REG, int NS, int MINB>
 __global__ void __launch_bounds__(kWideThreads, MINB) wide_decode_kernel(const WideParams<T> p) {
   namespace cg = cooperative_groups;
@@ -793,15 +823,18 @@ __global__ void __launch_bounds__(kWideThreads, MINB) wide_decode_kernel(const W
   int* tslot = reinterpret_cast<int*>(wbase);
   unsigned char* ring = wbase + 2 * 4 * TS;
   const int n_stripes = p.S / W;
+  const int h = (n_stripes + 1) / 2;  // group G0 = stripes [0, h), G1 = [h, n_stripes)
   const int n_vb = (p.n_vars + kWideVB - 1) / kWideVB;
-  const int n_vi = n_vb * n_stripes, n_ci = p.ncb * n_stripes;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int n_gwarp = (gridDim.x * blockDim.x) >> 5;
   const long long first = p.batch < p.S ? p.batch : p.S;
   const bool prof = g_wide_prof && blockIdx.x == 0 && threadIdx.x == 0;
+  int* list_a = p.slist;
+  int* list_b = p.slist + p.S;
+  const bool root = blockIdx.x == 0 && threadIdx.x == 0;
 
   // Prologue: slot s takes frame s; synthesised LLRs of the first frames.
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (root) {
     p.ctr[0] = static_cast<int>(first);
     p.ctr[1] = static_cast<int>(first);
     for (int k = 2; k < 8; ++k) p.ctr[k] = 0;
@@ -823,23 +856,41 @@ __global__ void __launch_bounds__(kWideThreads, MINB) wide_decode_kernel(const W
     if (*(volatile int*)(p.ctr + 1) == 0) break;
     long long tp[7];
     tp[0] = prof ? clock64() : 0;
-    if (p.synth.kind != 0) wide_synth_items(p, *(volatile int*)(p.ctr + 5));
-    wide_phase_v<T, VS, D, DVMAX, REG, NS>(p, ring, tslot, TS, n_vi, n_vb);
+    // step A: phase V of G0, phase C of G1 (G1 has no x yet in the first pass)
+    if (p.synth.kind != 0) wide_synth_items(p, list_a, *(volatile int*)(p.ctr + 5), p.ctr + 4);
+    {
+      const WideStep sa(0, h, h, pass == 0 ? 0 : n_stripes - h, n_vb, p.ncb);
+      wide_step<T, VS, D, DVMAX, REG, NS>(p, ring, tslot, TS, sa, p.ctr + 2);
+    }
     if (prof) tp[1] = clock64();
     grid.sync();
     if (prof) tp[2] = clock64();
-    if (blockIdx.x == 0 && threadIdx.x == 0) p.ctr[5] = 0;  // synthesis list of the next pass (read in phase V)
-    wide_phase_c<T, VS, D, DVMAX, REG, NS>(p, ring, tslot, TS, n_ci);
-    if (prof) tp[3] = clock64();
-    grid.sync();
-    if (prof) tp[4] = clock64();
-    if (blockIdx.x == 0 && threadIdx.x == 0) {  // item counters of the next pass (both phases are done)
-      p.ctr[2] = 0;
+    // slot phase of G1; reset the counters step B will use and list A
+    if (root) {
       p.ctr[3] = 0;
-      p.ctr[4] = 0;
+      p.ctr[6] = 0;
+      p.ctr[5] = 0;
     }
-    for (int s = gwarp; s < p.S; s += n_gwarp) wide_phase_s<T, VS>(p, s);
+    if (pass > 0)
+      for (int s = h * W + gwarp; s < p.S; s += n_gwarp) wide_phase_s<T, VS>(p, s, list_b, p.ctr + 7);
+    grid.sync();
+    if (prof) tp[3] = clock64();
+    // step B: phase C of G0, phase V of G1
+    if (p.synth.kind != 0) wide_synth_items(p, list_b, *(volatile int*)(p.ctr + 7), p.ctr + 6);
+    {
+      const WideStep sb(h, n_stripes - h, 0, h, n_vb, p.ncb);
+      wide_step<T, VS, D, DVMAX, REG, NS>(p, ring, tslot, TS, sb, p.ctr + 3);
+    }
+    if (prof) tp[4] = clock64();
+    grid.sync();
     if (prof) tp[5] = clock64();
+    // slot phase of G0; reset the counters step A will use and list B
+    if (root) {
+      p.ctr[2] = 0;
+      p.ctr[4] = 0;
+      p.ctr[7] = 0;
+    }
+    for (int s = gwarp; s < h * W; s += n_gwarp) wide_phase_s<T, VS>(p, s, list_a, p.ctr + 5);
     grid.sync();
     if (prof) {
       tp[6] = clock64();

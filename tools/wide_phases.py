@@ -28,7 +28,7 @@ _lib.check(lib.admm_wide_phase_profile(0, out))
 ms = e0.elapsed_time(e1)
 eu = int(r.iterations.sum()) * code.n_edges
 passes = out[6]
-names = ["V", "sync", "C", "sync", "S", "sync"]
+names = ["stepA(V:G0+C:G1)", "sync", "slotsG1+sync", "stepB(C:G0+V:G1)", "sync", "slotsG0+sync"]
 tot = sum(out[:6])
 print(f"B={B} {ms:.1f} ms  {eu / ms / 1e6:.1f} G eu/s  passes={passes}  us/pass={1e3 * ms / max(passes, 1):.1f}")
 print("  ".join(f"{n}={100 * out[k] / tot:.1f}%" for k, n in enumerate(names)))
