@@ -425,6 +425,7 @@ __device__ __forceinline__ void wide_step(const WideParams<T>& p, unsigned char*
   int iid = feed.start(tslot);
 
   auto issue_next = [&]() {
+    __syncwarp();
     const int* tb = tslot + (ik & 1) * tstride;
     const int kind = tb[TBM + 4];
     if (iid < n_items) {

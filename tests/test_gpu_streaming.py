@@ -212,3 +212,28 @@ def test_wide_direct_retirement_equals_retiring_pass(cuda_ok, dt):
         assert torch.equal(a.flags, b.flags)
         assert torch.equal(a.weight, b.weight)
         assert torch.equal(b.weight, b.hard.to(torch.int32).sum(dim=1))
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_wide_device_llrs_match_sharded(cuda_ok, dt):
+    """decode_batch on device LLRs (the fresh-slot LLRs come from the caller's
+    array, not the synthesis buffer) on the wide kernel at a batch that fills
+    several stripes of both stripe groups: iteration counts equal the sharded
+    kernel's frame by frame, with and without per-variable outputs, and x
+    after a fixed iteration count agrees to rounding."""
+    from paper_1204_0556_b200 import AdmmConfig, Awgn, baseline_code, decode_batch, synth_llr
+
+    code = baseline_code("cfg5_n16384")
+    B = 2304
+    g = synth_llr(code.n_vars, Awgn(2.5, code.design_rate), seed=5, point=0, trial0=0, batch=B, dtype=dt)
+    cfg = AdmmConfig(mu=5.0)
+    ref = torch.cat([decode_batch(g[lo:lo + 256], code, cfg, dtype=dt, want_x=False, engine="streaming").iterations
+                     for lo in range(0, B, 256)])
+    for want_x in (False, True):
+        w = decode_batch(g, code, cfg, dtype=dt, want_x=want_x, engine="wide")
+        assert w.info["kernel"] == 5
+        assert torch.equal(w.iterations, ref)
+    fixed = AdmmConfig(mu=5.0, epsilon=1e-300, t_max=3)
+    w = decode_batch(g, code, fixed, dtype=dt, engine="wide")
+    r = torch.cat([decode_batch(g[lo:lo + 256], code, fixed, dtype=dt, engine="streaming").x for lo in range(0, B, 256)])
+    assert (w.x - r).abs().max().item() <= (1e-5 if dt == torch.float32 else 1e-12)
