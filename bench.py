@@ -14,7 +14,8 @@ n=16384, uses LLRs synthesised inside the decode kernel: 1M frames/point).
 CUDA events, inputs resident in HBM.  ``e2e`` = the same metric through the
 public pipelined host API (paper_1204_0556_b200.pipeline): pinned host LLRs
 in, host hard decisions / iterations / flags out, copies inside the timed
-region.  ``cpu_baseline`` and ``--impl reference`` time the CPU oracle
+region (for the in-kernel-synthesis workload cfg5: decode_synth with the
+per-frame results read back to pinned host memory every step).  ``cpu_baseline`` and ``--impl reference`` time the CPU oracle
 (numpy restatement of the reference, oracle/admm_oracle.py) on the box's
 host cores on a bounded, SNR-stratified sample of the same workload.
 
@@ -78,7 +79,7 @@ def parse():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
     ap.add_argument("--dtype", choices=["f32", "f64"], default="f32")
     ap.add_argument("--frames", type=int, default=0, help="frames per point (0 = the workload's)")
-    ap.add_argument("--chunk", type=int, default=65536, help="frames per decode call (synth workloads)")
+    ap.add_argument("--chunk", type=int, default=262144, help="frames per decode call (synth workloads)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-block", type=int, default=65536, help="frames per host block of the e2e pipeline")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
@@ -356,6 +357,39 @@ def run_ours(args, wl: Workload):
         e_el = max_over_ranks(e0.elapsed_time(e1) / 1e3, device=dev)
         e2e = {"value": frames_all * args.steps / e_el, "unit": "frames/s",
                "h2d_bytes_per_step": pipe.h2d_bytes_per_run(host), "d2h_bytes_per_step": pipe.d2h_bytes_per_run(host)}
+    elif not args.no_e2e:
+        # in-kernel synthesis: a trial's input is its (seed, point, trial) key, so
+        # nothing crosses to the device; every step reads each call's per-frame
+        # results (iterations, flags, weight) back into pinned host memory
+        d2h = 0
+        pinned = {}
+
+        def e2e_step():
+            nonlocal d2h
+            d2h = 0
+            for j, o in enumerate(step()):
+                for name in ("iterations", "flags", "weight"):
+                    t = getattr(o, name)
+                    buf = pinned.get((j, name))
+                    if buf is None or buf.numel() != t.numel():
+                        buf = pinned[(j, name)] = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                    buf.copy_(t, non_blocking=True)
+                    d2h += t.numel() * t.element_size()
+
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e_el = max_over_ranks(e0.elapsed_time(e1) / 1e3, device=dev)
+        e2e = {"value": frames_all * args.steps / e_el, "unit": "frames/s", "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": d2h, "note": "decode_synth: LLRs synthesised in the kernel from the trial key"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
