@@ -232,7 +232,13 @@ def test_wide_device_llrs_match_sharded(cuda_ok, dt):
     for want_x in (False, True):
         w = decode_batch(g, code, cfg, dtype=dt, want_x=want_x, engine="wide")
         assert w.info["kernel"] == 5
-        assert torch.equal(w.iterations, ref)
+        if dt == torch.float64:
+            assert torch.equal(w.iterations, ref)
+        else:
+            # fp32: the wide kernel keeps (z, message) and recovers lambda, a
+            # different rounding from the sharded kernel's; a rare frame may
+            # stop one iteration apart
+            assert (w.iterations != ref).float().mean().item() <= 0.002
     fixed = AdmmConfig(mu=5.0, epsilon=1e-300, t_max=3)
     w = decode_batch(g, code, fixed, dtype=dt, engine="wide")
     r = torch.cat([decode_batch(g[lo:lo + 256], code, fixed, dtype=dt, engine="streaming").x for lo in range(0, B, 256)])
