@@ -243,3 +243,33 @@ def test_wide_device_llrs_match_sharded(cuda_ok, dt):
     w = decode_batch(g, code, fixed, dtype=dt, engine="wide")
     r = torch.cat([decode_batch(g[lo:lo + 256], code, fixed, dtype=dt, engine="streaming").x for lo in range(0, B, 256)])
     assert (w.x - r).abs().max().item() <= (1e-5 if dt == torch.float32 else 1e-12)
+
+
+def test_wide_irregular_code_multi_stripe_matches_sharded(cuda_ok):
+    """An irregular code too large for one SM (check degrees 4-8, variable
+    degrees 2-4, 2600 checks) on the generic wide kernel at a batch spanning
+    both stripe groups: fp64 iteration counts, flags and weights equal the
+    sharded kernel's frame by frame."""
+    from paper_1204_0556_b200 import AdmmConfig, ParityCheckMatrix, decode_batch
+
+    rng = np.random.default_rng(11)
+    n, m = 5200, 2600
+    deg = np.zeros(n, dtype=int)
+    rows = []
+    for c in range(m):
+        d = int(rng.integers(4, 9))
+        free = np.nonzero(deg < 4)[0]  # variable degrees at most 4 (the wide kernel's bucket)
+        r = sorted(rng.choice(free, size=d, replace=False).tolist())
+        deg[r] += 1
+        rows.append(r)
+    code = ParityCheckMatrix(n, rows)
+    assert code.n_checks == m
+    g = torch.as_tensor(rng.normal(1.2, 1.0, (1536, n)))
+    cfg = AdmmConfig(mu=3.0, t_max=200)
+    w = decode_batch(g, code, cfg, dtype=torch.float64, want_x=False, engine="wide")
+    assert w.info["kernel"] == 5
+    parts = [decode_batch(g[lo:lo + 512], code, cfg, dtype=torch.float64, want_x=False) for lo in range(0, 1536, 512)]
+    assert parts[0].info["kernel"] == 3
+    assert torch.equal(w.iterations, torch.cat([q.iterations for q in parts]))
+    assert torch.equal(w.flags, torch.cat([q.flags for q in parts]))
+    assert torch.equal(w.weight, torch.cat([q.weight for q in parts]))
