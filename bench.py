@@ -332,6 +332,12 @@ def run_ours(args, wl: Workload):
             traffic = None if bpf is None else bpf * F  # ncu DRAM bytes per frame x frames per launch
         except Exception:
             traffic = None
+    elif tpath.exists() and wl.name == "cfg5" and info.get("kernel") == 5:
+        try:  # wide kernel: ncu DRAM bytes per edge-update x edge-updates per launch
+            bpe_ncu = json.loads(tpath.read_text()).get(f"bytes_per_edge_update_wide_{args.dtype}")
+            traffic = None if bpe_ncu is None else bpe_ncu * edge_updates / n_launch
+        except Exception:
+            traffic = None
     kernel = {1: "resident_decode_kernel", 2: "resident_regular_kernel", 3: "sharded_decode_kernel",
               4: "cluster_decode_kernel", 5: "wide_decode_kernel"}.get(info.get("kernel", info.get("engine")), "?")
 
