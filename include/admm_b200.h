@@ -50,7 +50,7 @@ enum admm_status {
 enum admm_engine {
   ADMM_ENGINE_AUTO = 0,      /* resident if the code fits one SM, else streaming */
   ADMM_ENGINE_RESIDENT = 1,  /* one CTA per frame, state on chip (fails if it does not fit) */
-  ADMM_ENGINE_STREAMING = 3, /* batch-interleaved L2-resident state, cooperative kernel */
+  ADMM_ENGINE_STREAMING = 3, /* codes beyond one SM: sharded kernel (small batches), wide HBM kernel (>= 1024 frames) */
   ADMM_ENGINE_CLUSTER = 4,   /* one thread-block cluster per frame, DSMEM gathers (regular codes) */
   ADMM_ENGINE_WIDE = 5       /* streaming placement, wide HBM-streaming kernel for every batch size */
 };

@@ -115,7 +115,10 @@ def device_graph(code, device=None, engine: str = "auto") -> DeviceGraph:
     """The (cached) device-resident graph of ``code`` on ``device``.
 
     ``engine``: "auto" (resident when the code fits one SM, else streaming),
-    "resident" or "streaming" (csrc/streaming.cuh)."""
+    "resident", "streaming" (codes beyond one SM: the sharded kernel below
+    1024 frames per call, the wide HBM-streaming kernel from there on --
+    csrc/sharded.cuh, csrc/wide.cuh), "wide" (the wide kernel for every
+    batch) or "cluster" (csrc/cluster_resident.cuh)."""
     code = as_code(code)
     dev = torch.device(device if device is not None else "cuda")
     idx = dev.index if dev.index is not None else torch.cuda.current_device()
