@@ -427,9 +427,12 @@ def run_ours(args, wl: Workload):
                          "bytes_model": f"{bpe} B per edge-update (two-kernel HBM schedule, SURVEY 8d) x "
                                         f"{edge_updates // n_launch} edge-updates per launch",
                          "kernel": kernel, "avg_launch_ms": launch_s * 1e3,
-                         "note": "resident engines keep the edge state on chip, so the HBM-model bytes are never "
-                                 "moved and frac > 1 is expected; `traffic` is ncu DRAM bytes per launch; the real "
-                                 "bound is SM instruction issue / latency (DESIGN.md 3.6)"},
+                         "note": ("the wide kernel streams the whole decoder state through HBM every pass: the HBM "
+                                  "model is its real bound; `traffic` is ncu DRAM bytes per launch (DESIGN.md 3.3)"
+                                  if kernel == "wide_decode_kernel" else
+                                  "resident engines keep the edge state on chip, so the HBM-model bytes are never "
+                                  "moved and frac > 1 is expected; `traffic` is ncu DRAM bytes per launch; the real "
+                                  "bound is SM instruction issue / latency (DESIGN.md 3.6)")},
             "gpu_launches": args.steps * n_launch,
             "clocks": clk,
             "e2e": e2e,
