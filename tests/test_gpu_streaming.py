@@ -245,15 +245,16 @@ def test_wide_device_llrs_match_sharded(cuda_ok, dt):
     assert (w.x - r).abs().max().item() <= (1e-5 if dt == torch.float32 else 1e-12)
 
 
-def test_wide_irregular_code_multi_stripe_matches_sharded(cuda_ok):
+@pytest.mark.parametrize("n,m,batch", [(5200, 2600, 1536), (5203, 2601, 1100)])
+def test_wide_irregular_code_multi_stripe_matches_sharded(cuda_ok, n, m, batch):
     """An irregular code too large for one SM (check degrees 4-8, variable
-    degrees 2-4, 2600 checks) on the generic wide kernel at a batch spanning
-    both stripe groups: fp64 iteration counts, flags and weights equal the
-    sharded kernel's frame by frame."""
+    degrees up to 4, some of degree 0) on the generic wide kernel at a batch
+    spanning both stripe groups -- also with partial variable / check blocks
+    and a partial last stripe: fp64 iteration counts, flags and weights equal
+    the sharded kernel's frame by frame."""
     from paper_1204_0556_b200 import AdmmConfig, ParityCheckMatrix, decode_batch
 
     rng = np.random.default_rng(11)
-    n, m = 5200, 2600
     deg = np.zeros(n, dtype=int)
     rows = []
     for c in range(m):
@@ -264,11 +265,11 @@ def test_wide_irregular_code_multi_stripe_matches_sharded(cuda_ok):
         rows.append(r)
     code = ParityCheckMatrix(n, rows)
     assert code.n_checks == m
-    g = torch.as_tensor(rng.normal(1.2, 1.0, (1536, n)))
+    g = torch.as_tensor(rng.normal(1.2, 1.0, (batch, n)))
     cfg = AdmmConfig(mu=3.0, t_max=200)
     w = decode_batch(g, code, cfg, dtype=torch.float64, want_x=False, engine="wide")
     assert w.info["kernel"] == 5
-    parts = [decode_batch(g[lo:lo + 512], code, cfg, dtype=torch.float64, want_x=False) for lo in range(0, 1536, 512)]
+    parts = [decode_batch(g[lo:lo + 512], code, cfg, dtype=torch.float64, want_x=False) for lo in range(0, batch, 512)]
     assert parts[0].info["kernel"] == 3
     assert torch.equal(w.iterations, torch.cat([q.iterations for q in parts]))
     assert torch.equal(w.flags, torch.cat([q.flags for q in parts]))
