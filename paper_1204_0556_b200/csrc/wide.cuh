@@ -377,9 +377,9 @@ __device__ __forceinline__ void wide_store_z(WVec<T, 2 * VS>* zl, WVec<T, VS>* z
     WVec<T, VS> z;
 #pragma unroll
     for (int l = 0; l < VS; ++l) z.v[l] = v.v[l];
-    st_cs(zv + row, z);
+    wst(zv + row, z);
   } else {
-    st_cs(zl + row, v);
+    wst(zl + row, v);
   }
 }
 
@@ -677,7 +677,7 @@ __device__ __forceinline__ void wide_step(const WideParams<T>& p, unsigned char*
       for (int k = 0; k < D; ++k)
         if (k < d) {
           wide_store_z<T, VS, ZM>(zl, zv, eb + (e0 + k) * 32, zlv[k]);
-          st_cs(msg + eb + (e0 + k) * 32, gx[k]);
+          wst(msg + eb + (e0 + k) * 32, gx[k]);
         }
       if (cqt == CB - 1 || c + 1 >= p.n_checks) {
         // End of the item: per-slot partials of its checks (fixed order).
