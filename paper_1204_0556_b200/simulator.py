@@ -159,9 +159,28 @@ def _decode_wave(code, channel, cfg, sent, seed, point, trials: range, *, frames
             res = decode_bp_batch(gam, code, cfg, dtype=dtype, device=device, want_beliefs=False, want_x=False,
                                   validate=False)
         else:
+            # All-zero codeword: the bit errors are the hard-decision weight and
+            # cost_sent = 0, so no per-variable output is needed (the wide
+            # kernel then retires frames without a retiring pass); the rare
+            # certified error words get their hard decisions and LLRs from a
+            # re-decode of those trials (a trial's result does not depend on
+            # its batch).
             res = decode_synth(code, channel, cfg, seed=seed, point=point, trial0=trials.start, batch=B,
-                               dtype=dtype, device=device, want_hard=True, engine=engine)
-            gam = None
+                               dtype=dtype, device=device, want_hard=False, engine=engine)
+            bit_err = res.weight.to(torch.int64)
+            word_err = bit_err > 0
+            ml = torch.zeros(B, dtype=torch.bool, device=bit_err.device)
+            for k in (word_err & res.codeword).nonzero().flatten().tolist():
+                t = trials.start + k
+                one = decode_synth(code, channel, cfg, seed=seed, point=point, trial0=t, batch=1, dtype=dtype,
+                                   device=device, want_hard=True, engine=engine)
+                g1 = synth_llr(code.n_vars, channel, seed=seed, point=point, trial0=t, batch=1,
+                               dtype=torch.float64, device=device)
+                ml[k] = bool((g1[0] * one.hard[0].to(torch.float64)).sum() < 0)  # cost_est < cost_sent = 0
+            out = (word_err.cpu().numpy(), bit_err.cpu().numpy(), res.iterations.cpu().numpy().astype(np.int64),
+                   ml.cpu().numpy())
+            dt = time.perf_counter() - t0
+            return out[0], out[1], out[2], np.full(B, dt / max(B, 1)), out[3]
     elif frames == "reference":
         gam_np = np.empty((B, code.n_vars))
         for k, t in enumerate(trials):

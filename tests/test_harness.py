@@ -70,3 +70,30 @@ def test_device_frames_statistically_match(cuda_ok):
     # device frames are a pure function of (seed, point, trial): batch-size invariant
     c = run_point(code, ch, dec, n_trials=20000, seed=5, frames="device", dtype=torch.float32, batch_size=777)
     assert stats_to_csv([b], timing=False) == stats_to_csv([c], timing=False)
+
+
+@pytest.mark.gpu
+def test_device_frames_fast_accounting_equals_full(cuda_ok):
+    """The device-frame path counts bit errors from the kernel's weights and
+    resolves ML accounting only for certified error words; the per-trial
+    records equal a full computation from the hard decisions and LLRs of every
+    trial (BSC near the LP threshold, so certified errors occur)."""
+    from paper_1204_0556_b200 import AdmmConfig, Bsc, baseline_code, decode_synth, synth_llr
+    from paper_1204_0556_b200.simulator import _decode_wave
+
+    code = baseline_code("cfg1_n96")
+    cfg = AdmmConfig(mu=5.0)
+    ch = Bsc(0.09)
+    sent = np.zeros(code.n_vars, dtype=np.uint8)
+    we, be, it, _, ml = _decode_wave(code, ch, cfg, sent, 3, 1, range(0, 3000), frames="device",
+                                     dtype=torch.float64, device="cuda", engine="auto")
+    full = decode_synth(code, ch, cfg, seed=3, point=1, trial0=0, batch=3000, dtype=torch.float64, want_hard=True)
+    gam = synth_llr(code.n_vars, ch, seed=3, point=1, trial0=0, batch=3000, dtype=torch.float64)
+    hard = full.hard.to(torch.float64)
+    be_full = full.hard.to(torch.int64).sum(dim=1)
+    ml_full = (be_full > 0) & full.codeword & ((gam * hard).sum(dim=1) < 0)
+    assert np.array_equal(be, be_full.cpu().numpy())
+    assert np.array_equal(we, (be_full > 0).cpu().numpy())
+    assert np.array_equal(it, full.iterations.cpu().numpy().astype(np.int64))
+    assert np.array_equal(ml, ml_full.cpu().numpy())
+    assert int(ml_full.sum()) > 0 or int(((be_full > 0) & full.codeword).sum()) > 0
