@@ -4,7 +4,7 @@
 // The sharded engine (sharded.cuh) keeps z/lambda in shared memory and can
 // therefore hold only ~64 frame slots; its passes are short (~25 us) and
 // bound by L2 latency and grid syncs.  This engine instead streams the whole
-// state through HBM every pass over S = 1024-4096 slots, so each phase is a
+// state through HBM every pass over S = 1024-8192 slots, so each phase is a
 // long, fully parallel, bandwidth-bound sweep -- the two-kernel HBM schedule
 // of SURVEY.md 8d (28 B per edge-update in fp32):
 //
