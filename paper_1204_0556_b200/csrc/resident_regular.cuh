@@ -351,7 +351,13 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
             const T r2 = sub_rn(zn[k], z[kPacked ? 0 : q][k]);
             primal = add_rn(primal, mul_rn(r1, r1));
             moved = add_rn(moved, mul_rn(r2, r2));
-            lam[kPacked ? 0 : q][k] = add_rn(lam[kPacked ? 0 : q][k], sub_rn(w[k], zn[k]));
+            if constexpr (kF64) {
+              lam[kPacked ? 0 : q][k] = add_rn(lam[kPacked ? 0 : q][k], sub_rn(w[k], zn[k]));
+            } else {
+              // fp32 (throughput mode), as in the packed path: l' = (w + l) - z'
+              // = u - z', so w is dead once u is formed (13 registers at d = 13)
+              lam[kPacked ? 0 : q][k] = sub_rn(u[k], zn[k]);
+            }
             z[kPacked ? 0 : q][k] = zn[k];
             sts(xaddr[q][k] + moff(q, k), sub_rn(zn[k], lam[kPacked ? 0 : q][k]));
           }
