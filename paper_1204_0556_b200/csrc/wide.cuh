@@ -664,7 +664,9 @@ __device__ __forceinline__ void wide_step(const WideParams<T>& p, unsigned char*
             const T r2 = sub_rn(zn[k], zo[k]);
             pr = add_rn(pr, mul_rn(r1, r1));
             mo = add_rn(mo, mul_rn(r2, r2));
-            const T lnew = add_rn(lo[k], sub_rn(w_[k], zn[k]));
+            // fp32 (throughput mode): l' = (w + l) - z' = u - z' as in the
+            // resident kernels; fp64 keeps the reference's expression tree
+            const T lnew = ZM ? sub_rn(u[k], zn[k]) : add_rn(lo[k], sub_rn(w_[k], zn[k]));
             zlv[k].v[l] = zn[k];
             zlv[k].v[VS + l] = lnew;
             gx[k].v[l] = sub_rn(zn[k], lnew);  // message
