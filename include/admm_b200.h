@@ -51,7 +51,7 @@ enum admm_engine {
   ADMM_ENGINE_AUTO = 0,      /* resident if the code fits one SM, else streaming */
   ADMM_ENGINE_RESIDENT = 1,  /* one CTA per frame, state on chip (fails if it does not fit) */
   ADMM_ENGINE_STREAMING = 3, /* codes beyond one SM: sharded kernel (small batches), wide HBM kernel (>= 1024 frames) */
-  ADMM_ENGINE_CLUSTER = 4,   /* one thread-block cluster per frame, DSMEM gathers (regular codes) */
+  ADMM_ENGINE_CLUSTER = 4,   /* reserved (no cluster engine in this build: graph creation fails) */
   ADMM_ENGINE_WIDE = 5       /* streaming placement, wide HBM-streaming kernel for every batch size */
 };
 
@@ -60,7 +60,7 @@ enum admm_kernel {
   ADMM_KERNEL_RESIDENT = 1,  /* generic resident (one CTA per frame)              */
   ADMM_KERNEL_REGULAR = 2,   /* regular-code resident                              */
   ADMM_KERNEL_SHARDED = 3,   /* sharded / L2 streaming (codes beyond one SM)       */
-  ADMM_KERNEL_CLUSTER = 4,   /* cluster resident                                   */
+  ADMM_KERNEL_CLUSTER = 4,   /* reserved                                           */
   ADMM_KERNEL_WIDE = 5       /* wide HBM streaming (large batches beyond one SM)   */
 };
 
@@ -69,15 +69,15 @@ typedef struct admm_graph admm_graph;
 typedef struct admm_graph_info {
   int32_t n_vars, n_checks, n_edges;
   int32_t max_check_degree, max_var_degree;
-  int32_t engine;           /* 1 resident generic, 2 resident regular, 3 streaming, 4 cluster */
+  int32_t engine;           /* 1 resident generic, 2 resident regular, 3 streaming */
   int32_t degree_bucket;    /* D: compiled check-degree bucket   */
   int32_t checks_per_thread;
   int32_t threads_per_cta;
-  int32_t ctas_per_sm_f32, ctas_per_sm_f64; /* engine 4: active clusters per GPU */
+  int32_t ctas_per_sm_f32, ctas_per_sm_f64;
   int32_t smem_bytes_f32, smem_bytes_f64;
   int32_t regs_f32, regs_f64;
   int32_t num_sms;
-  int32_t cluster_size;     /* CTAs per cluster (engine 4), else 0 */
+  int32_t cluster_size;     /* CTAs per cluster (0: one CTA per frame or streaming) */
   double layout_cost_before, layout_cost_after; /* bank-conflict cost of the relabeling (engine 2) */
 } admm_graph_info;
 
@@ -179,6 +179,30 @@ int admm_bp_decode_batch(const admm_graph* g, int dtype, int64_t batch, const vo
                          int64_t ld_beliefs, void* x_out, int64_t ld_x, uint8_t* hard_out, int64_t ld_hard,
                          int32_t* iters_out, uint8_t* flags_out, int32_t* weight_out, void* workspace,
                          size_t workspace_bytes, void* stream);
+
+/* Step API: the reference's AdmmState driven by hand (admm_decoder.py:47-149,
+ * tests/test_admm.py:147-168, 208-240), batched.  All arrays are DEVICE
+ * arrays in the reference's edge order (codes.py:91-99), one frame per row:
+ * edge arrays [batch][ld_edge], variable arrays [batch][ld].  In fp64 the
+ * x- and lambda-updates are bit-identical to the reference's expressions
+ * (true IEEE division); the z-update differs only inside the projection.
+ *   admm_x_update      x_update (:108-124): x = clip((sum_e (z - lam/mu) - gamma/mu) / deg, 0, 1),
+ *                      deg-0 variables take gamma < 0
+ *   admm_z_update      z_update (:127-141): w = rho x[edge_var] + (1 - rho) z_old,
+ *                      z_out = project(w + lam / mu) per check; w_out (may be NULL) receives w
+ *   admm_lambda_update lambda_update (:144-149): lam_out = lam + mu (w - z) (lam_out may alias lam) */
+int admm_x_update(const admm_graph* g, int dtype, int64_t batch, const void* z, const void* lam, int64_t ld_edge,
+                  const void* gamma, int64_t ld_gamma, double mu, void* x_out, int64_t ld_x, void* stream);
+int admm_z_update(const admm_graph* g, int dtype, int64_t batch, const void* x, int64_t ld_x, const void* z_old,
+                  const void* lam, int64_t ld_edge, double mu, double rho, void* z_out, void* w_out, void* stream);
+int admm_lambda_update(const admm_graph* g, int dtype, int64_t batch, const void* lam, const void* w, const void* z,
+                       int64_t ld_edge, double mu, void* lam_out, void* stream);
+
+/* Row-wise membership test of the parity polytope within `tol`.  Replaces
+ * membership (parity_polytope.py:69-91): values [m][d] device array,
+ * 1 <= d <= 32; out[m] uint8 (1 = inside). */
+int admm_membership_batch(int dtype, int64_t m, int32_t d, const void* values, double tol, uint8_t* out,
+                          void* stream);
 
 const char* admm_last_error(void);
 int admm_version(void);

@@ -137,6 +137,29 @@ def project_rows(values) -> np.ndarray:
     return out
 
 
+def membership(u, tol: float = PARITY_TOL) -> bool:
+    """Parity-polytope membership within ``tol`` (parity_polytope.py:69-91):
+    unit-cube test; r = even floor of the clipped l1 norm snapped up by
+    PARITY_TOL (:62-64); two-slice weight alpha = clip((2 + r - s)/2, 0, 1);
+    no upper slice when r + 2 > d unless alpha = 1; then every descending
+    prefix sum must stay below alpha min(q, r) + (1 - alpha) min(q, r + 2)."""
+    u = np.asarray(u, dtype=float)
+    if u.ndim != 1 or u.size == 0:
+        raise ValueError("membership expects a non-empty 1-D vector")
+    d = u.size
+    if np.any(u < -tol) or np.any(u > 1.0 + tol):
+        return False
+    s = min(max(float(u.sum()), 0.0), float(d))
+    r = 2 * math.floor((s + PARITY_TOL) / 2.0)
+    alpha = min(max((2.0 + r - s) / 2.0, 0.0), 1.0)
+    if r + 2 > d and alpha < 1.0 - tol:
+        return False
+    prefix = np.cumsum(-np.sort(-u))
+    q = np.arange(1, d + 1)
+    bound = alpha * np.minimum(q, r) + (1.0 - alpha) * np.minimum(q, r + 2)
+    return bool(np.all(prefix <= bound + tol))
+
+
 # ---------------------------------------------------------------------------
 # ADMM updates (admm_decoder.py:108-149) and the decode loop (:152-182)
 # ---------------------------------------------------------------------------

@@ -19,9 +19,9 @@ ADMM_F64 = 1
 ADMM_FLAG_CONVERGED = 1
 ADMM_FLAG_INTEGRAL = 2
 ADMM_FLAG_CODEWORD = 4
-ENGINES = {"auto": 0, "resident": 1, "streaming": 3, "cluster": 4, "wide": 5}
+ENGINES = {"auto": 0, "resident": 1, "streaming": 3, "wide": 5}
 #: Kernel ids of admm_decode_kernel (enum admm_kernel).
-KERNELS = {1: "resident", 2: "regular", 3: "sharded", 4: "cluster", 5: "wide"}
+KERNELS = {1: "resident", 2: "regular", 3: "sharded", 5: "wide"}
 
 #: Every symbol the public header declares (checked by the CPU test-suite).
 EXPORTED = (
@@ -40,6 +40,10 @@ EXPORTED = (
     "admm_phase_profile",
     "admm_wide_phase_profile",
     "admm_bp_decode_batch",
+    "admm_x_update",
+    "admm_z_update",
+    "admm_lambda_update",
+    "admm_membership_batch",
 )
 
 
@@ -121,6 +125,14 @@ def load() -> ctypes.CDLL:
         P, I64, P, I64, P, I64, P, P, P, P, SZ, P,
     ]
     lib.admm_bp_decode_batch.restype = ctypes.c_int
+    lib.admm_x_update.argtypes = [P, ctypes.c_int, I64, P, P, I64, P, I64, D, P, I64, P]
+    lib.admm_x_update.restype = ctypes.c_int
+    lib.admm_z_update.argtypes = [P, ctypes.c_int, I64, P, I64, P, P, I64, D, D, P, P, P]
+    lib.admm_z_update.restype = ctypes.c_int
+    lib.admm_lambda_update.argtypes = [P, ctypes.c_int, I64, P, P, P, I64, D, P, P]
+    lib.admm_lambda_update.restype = ctypes.c_int
+    lib.admm_membership_batch.argtypes = [ctypes.c_int, I64, I32, P, D, P, P]
+    lib.admm_membership_batch.restype = ctypes.c_int
     _lib = lib
     return lib
 

@@ -3,7 +3,12 @@
 Mirror of ``polylp.admm_decoder`` (/root/reference/pkg/src/polylp/admm_decoder.py):
 
 * :class:`AdmmConfig` -- same fields, defaults and validation (:27-44);
-* :class:`DecodeOutput` and the ``STATUS_*`` strings (:23-24, :74-89);
+* :class:`DecodeOutput` and the ``STATUS_*`` strings (:23-24, :74-89),
+  :func:`make_output` (:92-105);
+* :class:`AdmmState` and the step functions :func:`x_update`,
+  :func:`z_update`, :func:`lambda_update` (:47-71, :108-149) -- the same
+  state object driven by hand, each step one batched sm_100a kernel
+  (csrc/steps.cu);
 * :func:`decode` ``(gamma, code, config) -> DecodeOutput`` -- same
   arguments, errors and output convention (:152-182), computed in fp64 on the
   GPU (the parity mode);
@@ -65,6 +70,134 @@ class DecodeOutput:
     ml_certificate: bool
 
 
+def make_output(x, status: str, iterations: int, code) -> DecodeOutput:
+    """Hard decision, integrality and ML certificate of a final iterate
+    (admm_decoder.py:92-105); host arrays, as the reference."""
+    from .codes import is_codeword
+
+    x = np.asarray(x, dtype=float)
+    hard = (x > 0.5).astype(np.uint8)
+    integral = bool(np.all(np.minimum(np.abs(x), np.abs(1.0 - x)) <= INTEGRALITY_TOL))
+    cert = integral and is_codeword(as_code(code), hard)
+    return DecodeOutput(x=x, status=status, integral=integral, iterations=iterations, hard_decision=hard,
+                        ml_certificate=cert)
+
+
+@dataclass
+class AdmmState:
+    """Iterates of a decode (admm_decoder.py:47-71): variables ``x`` (N),
+    replicas ``z``, duals ``lam``, previous replicas ``z_prev`` and the
+    over-relaxed mixture ``w`` (E, edge-flat in check order; the slice of
+    check j is ``code.check_slice(j)``).
+
+    As in the reference the fields are host numpy arrays of one frame; the
+    step functions then run in fp64.  They may also be CUDA tensors, one
+    frame ([N] / [E]) or a batch ([B, N] / [B, E]), float32 or float64:
+    the steps then stay on the device in that dtype.
+    """
+
+    x: NDArray[np.float64] | torch.Tensor
+    z: NDArray[np.float64] | torch.Tensor
+    lam: NDArray[np.float64] | torch.Tensor
+    z_prev: NDArray[np.float64] | torch.Tensor
+    w: NDArray[np.float64] | torch.Tensor = field(default_factory=lambda: np.empty(0))
+    iterations: int = 0
+
+    @classmethod
+    def initial(cls, code, *, batch: int | None = None, dtype=None, device=None) -> "AdmmState":
+        """Zero state (admm_decoder.py:63-71).  With ``device`` (or ``batch``)
+        the state is a CUDA tensor state of ``batch`` frames."""
+        code = as_code(code)
+        e = code.n_edges
+        if device is None and batch is None:
+            return cls(x=np.zeros(code.n_vars), z=np.zeros(e), lam=np.zeros(e), z_prev=np.zeros(e))
+        dev = torch.device(device if device is not None else "cuda")
+        tdt = torch.float64 if dtype is None or _dtype_code(dtype) == _lib.ADMM_F64 else torch.float32
+        shp = (() if batch is None else (int(batch),))
+        zeros = lambda n: torch.zeros(shp + (n,), dtype=tdt, device=dev)  # noqa: E731
+        return cls(x=zeros(code.n_vars), z=zeros(e), lam=zeros(e), z_prev=zeros(e), w=zeros(e))
+
+
+class _StepIO:
+    """Host <-> device marshalling of one step: numpy in -> fp64 CUDA rows ->
+    numpy out, or CUDA tensors in -> CUDA tensors out (same dtype/shape)."""
+
+    def __init__(self, state: AdmmState, code):
+        self.code = as_code(code)
+        ref = state.z
+        self.host = not (isinstance(ref, torch.Tensor) and ref.is_cuda)
+        if self.host:
+            self.dev = torch.device("cuda", torch.cuda.current_device())
+            self.tdt = torch.float64
+            self.batched = np.ndim(ref) == 2
+        else:
+            self.dev = ref.device
+            self.tdt = ref.dtype
+            self.batched = ref.ndim == 2
+        self.dt_code = _dtype_code(self.tdt)
+        self.dg = device_graph(self.code, self.dev)
+        self.stream = torch.cuda.current_stream(self.dev)
+
+    def rows(self, a, n: int) -> torch.Tensor:
+        t = torch.as_tensor(a).to(device=self.dev, dtype=self.tdt)
+        if t.shape[-1] != n:
+            raise ValueError(f"expected trailing dimension {n}, got {tuple(t.shape)}")
+        return t.reshape(-1, n).contiguous()
+
+    def out(self, t: torch.Tensor):
+        t = t if self.batched else t[0]
+        return t.cpu().numpy() if self.host else t
+
+
+def x_update(state: AdmmState, code, gamma, config: AdmmConfig):
+    """Average the dual-adjusted replicas, step against the LLRs, clamp
+    (admm_decoder.py:108-124): one sm_100a kernel (admm_x_update)."""
+    io = _StepIO(state, code)
+    N, E = io.code.n_vars, io.code.n_edges
+    z, lam, g = io.rows(state.z, E), io.rows(state.lam, E), io.rows(gamma, N)
+    B = z.shape[0]
+    if g.shape[0] != B:
+        g = g.expand(B, N).contiguous()
+    x = torch.empty((B, N), dtype=io.tdt, device=io.dev)
+    _lib.check(_lib.load().admm_x_update(io.dg.handle, io.dt_code, B, z.data_ptr(), lam.data_ptr(), E, g.data_ptr(),
+                                         N, float(config.mu), x.data_ptr(), N, io.stream.cuda_stream))
+    state.x = io.out(x)
+    return state.x
+
+
+def z_update(state: AdmmState, code, config: AdmmConfig):
+    """Project each check's over-relaxed replica target onto the parity
+    polytope (admm_decoder.py:127-141): one kernel (admm_z_update).
+    Sets ``z_prev``, ``w`` and ``z`` as the reference does."""
+    io = _StepIO(state, code)
+    N, E = io.code.n_vars, io.code.n_edges
+    x, z, lam = io.rows(state.x, N), io.rows(state.z, E), io.rows(state.lam, E)
+    B = z.shape[0]
+    z_new = torch.empty((B, E), dtype=io.tdt, device=io.dev)
+    w = torch.empty((B, E), dtype=io.tdt, device=io.dev)
+    _lib.check(_lib.load().admm_z_update(io.dg.handle, io.dt_code, B, x.data_ptr(), N, z.data_ptr(), lam.data_ptr(),
+                                         E, float(config.mu), float(config.rho), z_new.data_ptr(), w.data_ptr(),
+                                         io.stream.cuda_stream))
+    state.z_prev = state.z
+    state.w = io.out(w)
+    state.z = io.out(z_new)
+    return state.z
+
+
+def lambda_update(state: AdmmState, code, config: AdmmConfig):
+    """Dual step against the residual of the same mixture the replicas saw
+    (admm_decoder.py:144-149): one kernel (admm_lambda_update)."""
+    io = _StepIO(state, code)
+    E = io.code.n_edges
+    lam, w, z = io.rows(state.lam, E), io.rows(state.w, E), io.rows(state.z, E)
+    B = lam.shape[0]
+    out = torch.empty((B, E), dtype=io.tdt, device=io.dev)
+    _lib.check(_lib.load().admm_lambda_update(io.dg.handle, io.dt_code, B, lam.data_ptr(), w.data_ptr(), z.data_ptr(),
+                                              E, float(config.mu), out.data_ptr(), io.stream.cuda_stream))
+    state.lam = io.out(out)
+    return state.lam
+
+
 # ---------------------------------------------------------------------------
 # Device graph
 # ---------------------------------------------------------------------------
@@ -118,7 +251,7 @@ def device_graph(code, device=None, engine: str = "auto") -> DeviceGraph:
     "resident", "streaming" (codes beyond one SM: the sharded kernel below
     1024 frames per call, the wide HBM-streaming kernel from there on --
     csrc/sharded.cuh, csrc/wide.cuh), "wide" (the wide kernel for every
-    batch) or "cluster" (csrc/cluster_resident.cuh)."""
+    batch)."""
     code = as_code(code)
     dev = torch.device(device if device is not None else "cuda")
     idx = dev.index if dev.index is not None else torch.cuda.current_device()
@@ -245,35 +378,50 @@ def decode_batch(
         g = g.unsqueeze(0)
     if g.ndim != 2 or g.shape[1] != code.n_vars:
         raise ValueError(f"expected a [B, {code.n_vars}] block of LLR vectors")
-    g = g.to(device=dev, dtype=tdt, non_blocking=True)
-    if not g.is_contiguous() or (g.shape[0] > 1 and g.stride(0) != g.shape[1]):
-        g = g.contiguous()
-    if validate and not bool(torch.isfinite(g).all()):
-        raise ValueError("LLR vector must be finite")
-    B, N, E = g.shape[0], code.n_vars, code.n_edges
-    dg = device_graph(code, dev, engine)
-    code_dt = _dtype_code(tdt)
-    iters = torch.empty(B, dtype=torch.int32, device=dev)
-    flags = torch.empty(B, dtype=torch.uint8, device=dev)
-    weight = torch.empty(B, dtype=torch.int32, device=dev)
-    x = torch.empty((B, N), dtype=tdt, device=dev) if want_x else None
-    hard = torch.empty((B, N), dtype=torch.uint8, device=dev) if want_hard else None
-    zi = li = None
     if z0 is not None or lam0 is not None:
         if z0 is None or lam0 is None:
             raise ValueError("z0 and lam0 go together")
-        zi = torch.as_tensor(z0).to(device=dev, dtype=tdt).reshape(B, E).contiguous()
-        li = torch.as_tensor(lam0).to(device=dev, dtype=tdt).reshape(B, E).contiguous()
-    zo = torch.empty((B, E), dtype=tdt, device=dev) if want_state else None
-    lo = torch.empty((B, E), dtype=tdt, device=dev) if want_state else None
-    ws_bytes = dg.workspace_bytes(code_dt, B)
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
-    launch(dg, code_dt, g, config, iters, flags, weight, x=x, hard=hard, z0=zi, lam0=li, z_out=zo,
-           lam_out=lo, workspace=ws, stream=st)
-    # keep inputs alive until the kernel has consumed them
+    B, N, E = g.shape[0], code.n_vars, code.n_edges
+    dg = device_graph(code, dev, engine)
+    code_dt = _dtype_code(tdt)
+    # Everything below is enqueued on `st`: the conversions, the allocations
+    # (the caching allocator then ties the buffers to `st`) and the kernel.
+    # `st` first waits for the caller's current stream, which produced the
+    # inputs; a caller-side input tensor read on a side stream is recorded
+    # on it so its memory is not reused before the kernel has read it.
+    cur = torch.cuda.current_stream(dev)
+    st = stream if stream is not None else cur
+    if st != cur:
+        st.wait_stream(cur)
+        for t in (g, z0, lam0):
+            if isinstance(t, torch.Tensor) and t.is_cuda:
+                t.record_stream(st)
+    with torch.cuda.stream(st):
+        g = g.to(device=dev, dtype=tdt, non_blocking=True)
+        if not g.is_contiguous() or (g.shape[0] > 1 and g.stride(0) != g.shape[1]):
+            g = g.contiguous()
+        if validate and not bool(torch.isfinite(g).all()):
+            raise ValueError("LLR vector must be finite")
+        iters = torch.empty(B, dtype=torch.int32, device=dev)
+        flags = torch.empty(B, dtype=torch.uint8, device=dev)
+        weight = torch.empty(B, dtype=torch.int32, device=dev)
+        x = torch.empty((B, N), dtype=tdt, device=dev) if want_x else None
+        hard = torch.empty((B, N), dtype=torch.uint8, device=dev) if want_hard else None
+        zi = li = None
+        if z0 is not None:
+            zi = torch.as_tensor(z0).to(device=dev, dtype=tdt).reshape(B, E).contiguous()
+            li = torch.as_tensor(lam0).to(device=dev, dtype=tdt).reshape(B, E).contiguous()
+        zo = torch.empty((B, E), dtype=tdt, device=dev) if want_state else None
+        lo = torch.empty((B, E), dtype=tdt, device=dev) if want_state else None
+        ws_bytes = dg.workspace_bytes(code_dt, B)
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        launch(dg, code_dt, g, config, iters, flags, weight, x=x, hard=hard, z0=zi, lam0=li, z_out=zo,
+               lam_out=lo, workspace=ws, stream=st)
     res = BatchResult(iterations=iters, flags=flags, weight=weight, x=x, hard=hard, z=zo, lam=lo,
                       info=dg.call_info(code_dt, B))
+    # the temporaries were allocated on `st`, so the allocator reuses their
+    # memory only for work ordered after the kernel; the reference keeps the
+    # host-side objects alive for the caller's convenience
     res._keepalive = (g, zi, li, ws)  # type: ignore[attr-defined]
     return res
 
@@ -310,6 +458,15 @@ def run_iterations(gamma, code, config: AdmmConfig, iterations: int, z0=None, la
     E = code.n_edges
     z0 = np.zeros(E) if z0 is None else np.asarray(z0, dtype=float)
     lam0 = np.zeros(E) if lam0 is None else np.asarray(lam0, dtype=float)
+    if device_graph(code).info["engine"] == 3:
+        # codes beyond one SM: the streaming engines keep their state in their
+        # own layouts, so the iterations run as step kernels (csrc/steps.cu)
+        st = AdmmState(x=np.zeros(code.n_vars), z=z0.copy(), lam=lam0.copy(), z_prev=z0.copy())
+        for _ in range(int(iterations)):
+            x_update(st, code, g[0], cfg)
+            z_update(st, code, cfg)
+            lambda_update(st, code, cfg)
+        return st.x, st.z, st.lam
     res = decode_batch(g, code, cfg, dtype=torch.float64, z0=z0[None], lam0=lam0[None], want_state=True)
     torch.cuda.current_stream().synchronize()
     return (res.x[0].cpu().numpy(), res.z[0].cpu().numpy(), res.lam[0].cpu().numpy())
@@ -335,9 +492,10 @@ def synth_llr(n_vars: int, channel, *, seed: int, point: int, trial0: int, batch
     :func:`decode_synth` decodes.  All-zero codeword."""
     dev = torch.device(device if device is not None else "cuda")
     tdt = torch.float64 if _dtype_code(dtype) == _lib.ADMM_F64 else torch.float32
-    out = torch.empty((batch, n_vars), dtype=tdt, device=dev)
-    ch = _channel_struct(channel)
     st = stream if stream is not None else torch.cuda.current_stream(dev)
+    with torch.cuda.stream(st):
+        out = torch.empty((batch, n_vars), dtype=tdt, device=dev)
+    ch = _channel_struct(channel)
     _lib.check(_lib.load().admm_synth_llr(_dtype_code(tdt), batch, n_vars, ctypes.byref(ch), int(seed) & (2**64 - 1),
                                           int(point), int(trial0), out.data_ptr(), n_vars, st.cuda_stream))
     return out
@@ -356,15 +514,16 @@ def decode_synth(code, channel, config: AdmmConfig = AdmmConfig(), *, seed: int,
     dg = device_graph(code, dev, engine)
     code_dt = _dtype_code(tdt)
     B, N = int(batch), code.n_vars
-    iters = torch.empty(B, dtype=torch.int32, device=dev)
-    flags = torch.empty(B, dtype=torch.uint8, device=dev)
-    weight = torch.empty(B, dtype=torch.int32, device=dev)
-    x = torch.empty((B, N), dtype=tdt, device=dev) if want_x else None
-    hard = torch.empty((B, N), dtype=torch.uint8, device=dev) if want_hard else None
-    ws_bytes = dg.workspace_bytes(code_dt, B)
-    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
-    ch = _channel_struct(channel)
     st = stream if stream is not None else torch.cuda.current_stream(dev)
+    with torch.cuda.stream(st):  # allocations tied to the stream the kernel runs on
+        iters = torch.empty(B, dtype=torch.int32, device=dev)
+        flags = torch.empty(B, dtype=torch.uint8, device=dev)
+        weight = torch.empty(B, dtype=torch.int32, device=dev)
+        x = torch.empty((B, N), dtype=tdt, device=dev) if want_x else None
+        hard = torch.empty((B, N), dtype=torch.uint8, device=dev) if want_hard else None
+        ws_bytes = dg.workspace_bytes(code_dt, B)
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    ch = _channel_struct(channel)
     if B > 0:
         _lib.check(_lib.load().admm_decode_synth(
             dg.handle, code_dt, B, ctypes.byref(ch), int(seed) & (2**64 - 1), int(point), int(trial0),

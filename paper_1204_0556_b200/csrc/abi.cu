@@ -12,6 +12,7 @@
 
 #include "../../include/admm_b200.h"
 #include "bp_launch.h"
+#include "steps.h"
 #include "kernels.cuh"
 #include "layout.h"
 
@@ -28,6 +29,30 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(ADMM_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
+// Makes `dev` current for the scope of an entry point and restores the
+// caller's current device on every return path.
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev_) != cudaSuccess) prev_ = -1;
+    err_ = prev_ == dev ? cudaSuccess : cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev_ >= 0 && changed()) cudaSetDevice(prev_);
+  }
+  cudaError_t error() const { return err_; }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+
+ private:
+  bool changed() const {
+    int cur = -1;
+    return cudaGetDevice(&cur) == cudaSuccess && cur != prev_;
+  }
+  int prev_ = -1;
+  cudaError_t err_ = cudaSuccess;
+};
+
 #define ADMM_CUDA(call)                                  \
   do {                                                   \
     cudaError_t _e = (call);                             \
@@ -41,9 +66,8 @@ struct admm_graph {
   int n_vars = 0, n_checks = 0, n_edges = 0;
   int dmax = 0, dvmax_actual = 0;
   int D = 0, DVMAX = 0, CPT = 0, NT = 0, m_pad = 0, VPT = 0;
-  int kind = 0;  // 1 = generic resident, 2 = regular resident, 3 = streaming, 4 = cluster resident
-  int C = 0, MC = 0, NC = 0;
-  admm::ClusterLaunch claunch[2];
+  int kind = 0;  // 1 = generic resident, 2 = regular resident, 3 = streaming
+  int C = 0;
   int l2_bytes = 0;
   admm::StreamLaunch slaunch[2];
   admm::ShardLaunch shlaunch[2];
@@ -62,6 +86,7 @@ struct admm_graph {
   uint16_t* var_pos = nullptr;
   uint8_t* var_deg = nullptr;
   int* edge_base = nullptr;
+  int* check_ptr_d = nullptr;   // [n_checks + 1] (step API, steps.cu)
   int* var_edge = nullptr;
   int* var_orig = nullptr;      // relabeled regular layout (kind 2)
   int* edge_ref = nullptr;
@@ -165,10 +190,10 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
     delete g;
     return fail(ADMM_E_UNSUPPORTED, "check degree > 32 or variable degree > 8 is not supported");
   }
-  cudaError_t ce = cudaSetDevice(device);
-  if (ce != cudaSuccess) {
+  DeviceGuard guard(device);
+  if (guard.error() != cudaSuccess) {
     delete g;
-    return cuda_fail(ce, "cudaSetDevice");
+    return cuda_fail(guard.error(), "cudaSetDevice");
   }
   cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device);
   int smem_optin = 0;
@@ -273,73 +298,6 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
         g->VPT = vpt;
         placed = true;
       }
-    }
-  }
-  if (!placed && regular && engine == ADMM_ENGINE_CLUSTER) {  // opt-in: DSMEM gathers measured slower than streaming
-    // Cluster-resident engine: one cluster of C CTAs per frame, DSMEM gathers.
-    // Prefer one check per thread (the most warps per SM), then the smallest cluster.
-    const int c_env = std::getenv("ADMM_B200_CLUSTER") ? std::atoi(std::getenv("ADMM_B200_CLUSTER")) : 0;
-    for (int cpt : {1, 2}) {
-      if (placed) break;
-      for (int C : {2, 4, 8, 16}) {
-      if (placed) break;
-      if (c_env && C != c_env) continue;
-      const int MC = (n_checks + C - 1) / C, NC = (n_vars + C - 1) / C;
-      if (MC < 32 && C > 2) continue;
-      {
-        const int nt = ((MC + cpt - 1) / cpt + 31) / 32 * 32;
-        if (nt > 512) continue;
-        const int need = (NC + nt - 1) / nt;
-        bool ok = true;
-        admm::ClusterLaunch Ls[2];
-        for (int dt = 0; dt < 2 && ok; ++dt) {
-          admm::ClusterLaunch L{};
-          int vpt = 0;
-          if (!admm::cluster_lookup(dt, dmax, dvmax, cpt, need, &vpt, &L)) { ok = false; break; }
-          const int smem = admm::cluster_smem_bytes(dt ? 8 : 4, dmax, nt * cpt, NC);
-          if (smem > smem_optin) { ok = false; break; }
-          cudaFuncAttributes fa{};
-          if (cudaFuncGetAttributes(&fa, L.fn) != cudaSuccess) { ok = false; break; }
-          if (fa.numRegs * nt > 65536) { ok = false; break; }
-          ensure_smem(L.fn, smem);
-          if (C > 8) cudaFuncSetAttribute(L.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-          cudaLaunchConfig_t cfg{};
-          cfg.gridDim = dim3(C);
-          cfg.blockDim = dim3(nt);
-          cfg.dynamicSmemBytes = smem;
-          cudaLaunchAttribute attr[1];
-          attr[0].id = cudaLaunchAttributeClusterDimension;
-          attr[0].val.clusterDim.x = C;
-          attr[0].val.clusterDim.y = 1;
-          attr[0].val.clusterDim.z = 1;
-          cfg.attrs = attr;
-          cfg.numAttrs = 1;
-          int clusters = 0;
-          if (cudaOccupancyMaxActiveClusters(&clusters, L.fn, &cfg) != cudaSuccess || clusters < 1) {
-            cudaGetLastError();
-            ok = false;
-            break;
-          }
-          L.clusters = clusters;
-          L.regs = fa.numRegs;
-          L.smem = smem;
-          Ls[dt] = L;
-          g->VPT = vpt;
-        }
-        if (!ok) continue;
-        g->claunch[0] = Ls[0];
-        g->claunch[1] = Ls[1];
-        g->kind = 4;
-        g->C = C;
-        g->MC = MC;
-        g->NC = NC;
-        g->CPT = cpt;
-        g->NT = nt;
-        g->m_pad = (n_checks + 31) / 32 * 32;
-        placed = true;
-        break;
-      }
-    }
     }
   }
   if (!placed && (engine == ADMM_ENGINE_AUTO || engine == ADMM_ENGINE_STREAMING || engine == ADMM_ENGINE_WIDE)) {
@@ -478,6 +436,7 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
   cudaError_t e2 = up((void**)&g->var_pos, var_pos.data(), var_pos.size() * sizeof(uint16_t));
   cudaError_t e3 = up((void**)&g->var_deg, var_deg.data(), var_deg.size());
   cudaError_t e4 = up((void**)&g->edge_base, edge_base.data(), edge_base.size() * sizeof(int));
+  if (e4 == cudaSuccess) e4 = up((void**)&g->check_ptr_d, check_ptr, (size_t)(n_checks + 1) * sizeof(int));
   cudaError_t e5 = up((void**)&g->var_edge, var_edge.data(), var_edge.size() * sizeof(int));
   if (e5 == cudaSuccess && !wct.empty()) e5 = up((void**)&g->wctbl, wct.data(), wct.size() * sizeof(int));
   if (e5 == cudaSuccess && !wvt.empty()) e5 = up((void**)&g->wvtbl, wvt.data(), wvt.size() * sizeof(int));
@@ -589,11 +548,12 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
 
 int admm_graph_destroy(admm_graph* g) {
   if (!g) return ADMM_OK;
-  cudaSetDevice(g->device);
+  DeviceGuard guard(g->device);
   cudaFree(g->chk_var);
   cudaFree(g->var_pos);
   cudaFree(g->var_deg);
   cudaFree(g->edge_base);
+  cudaFree(g->check_ptr_d);
   cudaFree(g->var_edge);
   cudaFree(g->wctbl);
   cudaFree(g->wvtbl);
@@ -621,13 +581,13 @@ int admm_graph_get_info(const admm_graph* g, admm_graph_info* info) {
   info->degree_bucket = g->D;
   info->checks_per_thread = g->CPT;
   info->threads_per_cta = g->NT;
-  const bool st = g->kind == 3, cl = g->kind == 4;
-  info->ctas_per_sm_f32 = st ? g->slaunch[0].occupancy : cl ? g->claunch[0].clusters : g->launch[0].occupancy;
-  info->ctas_per_sm_f64 = st ? g->slaunch[1].occupancy : cl ? g->claunch[1].clusters : g->launch[1].occupancy;
-  info->smem_bytes_f32 = st ? 0 : cl ? g->claunch[0].smem : g->launch[0].smem;
-  info->smem_bytes_f64 = st ? 0 : cl ? g->claunch[1].smem : g->launch[1].smem;
-  info->regs_f32 = st ? g->slaunch[0].regs : cl ? g->claunch[0].regs : g->launch[0].regs;
-  info->regs_f64 = st ? g->slaunch[1].regs : cl ? g->claunch[1].regs : g->launch[1].regs;
+  const bool st = g->kind == 3;
+  info->ctas_per_sm_f32 = st ? g->slaunch[0].occupancy : g->launch[0].occupancy;
+  info->ctas_per_sm_f64 = st ? g->slaunch[1].occupancy : g->launch[1].occupancy;
+  info->smem_bytes_f32 = st ? 0 : g->launch[0].smem;
+  info->smem_bytes_f64 = st ? 0 : g->launch[1].smem;
+  info->regs_f32 = st ? g->slaunch[0].regs : g->launch[0].regs;
+  info->regs_f64 = st ? g->slaunch[1].regs : g->launch[1].regs;
   info->cluster_size = g->C;
   info->layout_cost_before = g->layout_cost[0];
   info->layout_cost_after = g->layout_cost[1];
@@ -776,7 +736,8 @@ int decode_impl(const admm_graph* g, int dtype, int64_t batch, const void* gamma
     return fail(ADMM_E_WORKSPACE, "workspace too small");
   if (batch > (1ll << 31) - 1024) return fail(ADMM_E_ARG, "batch too large for one call");
 
-  ADMM_CUDA(cudaSetDevice(g->device));
+  DeviceGuard guard(g->device);
+  ADMM_CUDA(guard.error());
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (g->kind == 3) {
     if (z_in || z_out) return fail(ADMM_E_UNSUPPORTED, "state input/output is not supported by the streaming engine");
@@ -814,21 +775,6 @@ int decode_impl(const admm_graph* g, int dtype, int64_t batch, const void* gamma
     return ADMM_OK;
   }
   ADMM_CUDA(cudaMemsetAsync(workspace, 0, sizeof(int), st));
-  if (g->kind == 4) {
-    if (z_in || z_out) return fail(ADMM_E_UNSUPPORTED, "state input/output is not supported by the cluster engine");
-    const admm::ClusterLaunch& CL = g->claunch[dtype];
-    const double thr = epsilon * epsilon * (double)g->n_edges;
-    const long long clusters = std::min<long long>(batch, CL.clusters);
-    admm::ResidentGraphArgs ga{g->n_vars, g->n_checks, g->m_pad, g->chk_var, g->var_pos, g->var_deg,
-                               g->edge_base, g->var_edge, nullptr, nullptr, nullptr};
-    admm::ResidentFrameArgs fa{batch, gamma, ld_gamma, mu, rho, thr, t_max, nullptr, nullptr, 0,
-                               x_out, ld_x, hard_out, ld_hard, iters_out, flags_out, weight_out,
-                               nullptr, nullptr, reinterpret_cast<int*>(workspace), synth};
-    const int rc = CL.launch(ga, fa, (int)clusters, g->C, g->MC, g->NC, g->NT, CL.smem, st);
-    if (rc != 0) return cuda_fail((cudaError_t)rc, "cudaLaunchKernelEx(cluster)");
-    ADMM_CUDA(cudaGetLastError());
-    return ADMM_OK;
-  }
   const admm::ResidentLaunch& L = g->launch[dtype];
   const long long grid = std::min<long long>(batch, (long long)L.occupancy * g->num_sms);
   const double thr = epsilon * epsilon * (double)g->n_edges;  // admm_decoder.py:169
@@ -845,8 +791,8 @@ int decode_impl(const admm_graph* g, int dtype, int64_t batch, const void* gamma
   admm::ResidentFrameArgs fa{batch, gamma, ld_gamma, mu, rho, thr, t_max, z_in, lam_in, ld_edge,
                              x_out, ld_x, hard_out, ld_hard, iters_out, flags_out, weight_out,
                              z_out, lam_out, reinterpret_cast<int*>(workspace), synth};
-  L.launch(ga, fa, (int)grid, g->NT, L.smem, st);
-  ADMM_CUDA(cudaGetLastError());
+  const cudaError_t le = L.launch(ga, fa, (int)grid, g->NT, L.smem, st);
+  if (le != cudaSuccess) return cuda_fail(le, "resident kernel launch");
   return ADMM_OK;
 }
 
@@ -912,7 +858,8 @@ int admm_bp_decode_batch(const admm_graph* g, int dtype, int64_t batch, const vo
   if (!workspace || workspace_bytes < 16) return fail(ADMM_E_WORKSPACE, "workspace too small (16 bytes)");
   if (!g->bp_ok[dtype]) return fail(ADMM_E_UNSUPPORTED, "BP: the graph does not fit one SM");
   if (batch > (1ll << 31) - 1024) return fail(ADMM_E_ARG, "batch too large for one call");
-  ADMM_CUDA(cudaSetDevice(g->device));
+  DeviceGuard guard(g->device);
+  ADMM_CUDA(guard.error());
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   ADMM_CUDA(cudaMemsetAsync(workspace, 0, sizeof(int), st));
   const admm::BpLaunch& L = g->bp_launch[dtype];
@@ -921,8 +868,8 @@ int admm_bp_decode_batch(const admm_graph* g, int dtype, int64_t batch, const vo
   admm::BpFrameArgs fa{batch, gamma, ld_gamma, llr_clip, t_max, early_stop ? 1 : 0, beliefs_out, ld_beliefs,
                        x_out, ld_x, hard_out, ld_hard, iters_out, flags_out, weight_out,
                        reinterpret_cast<int*>(workspace), admm::SynthParams{}};
-  L.launch(ga, fa, (int)grid, g->bp_nt, L.smem, st);
-  ADMM_CUDA(cudaGetLastError());
+  const cudaError_t le = L.launch(ga, fa, (int)grid, g->bp_nt, L.smem, st);
+  if (le != cudaSuccess) return cuda_fail(le, "BP kernel launch");
   return ADMM_OK;
 }
 
@@ -947,6 +894,88 @@ int admm_project_batch(int dtype, int64_t m, int32_t d, const void* values, void
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (!admm::launch_project(dtype, pick_bucket(d), m, d, values, out, st))
     return fail(ADMM_E_UNSUPPORTED, "no projection kernel for this degree");
+  ADMM_CUDA(cudaGetLastError());
+  return ADMM_OK;
+}
+
+// ---- step API (steps.cu): x_update / z_update / lambda_update, membership ----
+
+namespace {
+
+admm::StepGraph step_graph(const admm_graph* g) {
+  return admm::StepGraph{g->n_vars, g->n_checks, g->m_pad, g->D, g->dvmax_actual, g->chk_var_ref, g->check_ptr_d,
+                         g->var_edge, g->var_deg};
+}
+
+int step_args(const admm_graph* g, int dtype, int64_t batch, int64_t ld_edge) {
+  if (!g) return fail(ADMM_E_ARG, "null graph");
+  if (dtype != ADMM_F32 && dtype != ADMM_F64) return fail(ADMM_E_ARG, "dtype must be ADMM_F32 or ADMM_F64");
+  if (batch < 0) return fail(ADMM_E_ARG, "batch must be non-negative");
+  if (ld_edge < g->n_edges) return fail(ADMM_E_ARG, "ld_edge < n_edges");
+  return ADMM_OK;
+}
+
+}  // namespace
+
+int admm_x_update(const admm_graph* g, int dtype, int64_t batch, const void* z, const void* lam, int64_t ld_edge,
+                  const void* gamma, int64_t ld_gamma, double mu, void* x_out, int64_t ld_x, void* stream) {
+  if (const int rc = step_args(g, dtype, batch, ld_edge)) return rc;
+  if (ld_gamma < g->n_vars || ld_x < g->n_vars) return fail(ADMM_E_ARG, "ld_gamma / ld_x < n_vars");
+  if (!(mu > 0)) return fail(ADMM_E_ARG, "mu must be positive");
+  if (batch == 0) return ADMM_OK;
+  if (!z || !lam || !gamma || !x_out) return fail(ADMM_E_ARG, "null pointer argument");
+  DeviceGuard guard(g->device);
+  ADMM_CUDA(guard.error());
+  cudaGetLastError();
+  admm::launch_x_update(dtype, step_graph(g), batch, z, lam, ld_edge, gamma, ld_gamma, mu, x_out, ld_x,
+                        reinterpret_cast<cudaStream_t>(stream));
+  ADMM_CUDA(cudaGetLastError());
+  return ADMM_OK;
+}
+
+int admm_z_update(const admm_graph* g, int dtype, int64_t batch, const void* x, int64_t ld_x, const void* z_old,
+                  const void* lam, int64_t ld_edge, double mu, double rho, void* z_out, void* w_out, void* stream) {
+  if (const int rc = step_args(g, dtype, batch, ld_edge)) return rc;
+  if (ld_x < g->n_vars) return fail(ADMM_E_ARG, "ld_x < n_vars");
+  if (!(mu > 0)) return fail(ADMM_E_ARG, "mu must be positive");
+  if (!(rho >= 1.0 && rho < 2.0)) return fail(ADMM_E_ARG, "rho must be in [1, 2)");
+  if (batch == 0) return ADMM_OK;
+  if (!x || !z_old || !lam || !z_out) return fail(ADMM_E_ARG, "null pointer argument");
+  DeviceGuard guard(g->device);
+  ADMM_CUDA(guard.error());
+  cudaGetLastError();
+  if (!admm::launch_z_update(dtype, step_graph(g), batch, x, ld_x, z_old, lam, ld_edge, mu, rho, z_out, w_out,
+                             reinterpret_cast<cudaStream_t>(stream)))
+    return fail(ADMM_E_UNSUPPORTED, "no z-update kernel for this check-degree bucket");
+  ADMM_CUDA(cudaGetLastError());
+  return ADMM_OK;
+}
+
+int admm_lambda_update(const admm_graph* g, int dtype, int64_t batch, const void* lam, const void* w, const void* z,
+                       int64_t ld_edge, double mu, void* lam_out, void* stream) {
+  if (const int rc = step_args(g, dtype, batch, ld_edge)) return rc;
+  if (batch == 0) return ADMM_OK;
+  if (!lam || !w || !z || !lam_out) return fail(ADMM_E_ARG, "null pointer argument");
+  DeviceGuard guard(g->device);
+  ADMM_CUDA(guard.error());
+  cudaGetLastError();
+  admm::launch_lambda_update(dtype, batch, g->n_edges, lam, w, z, ld_edge, mu, lam_out,
+                             reinterpret_cast<cudaStream_t>(stream));
+  ADMM_CUDA(cudaGetLastError());
+  return ADMM_OK;
+}
+
+int admm_membership_batch(int dtype, int64_t m, int32_t d, const void* values, double tol, uint8_t* out,
+                          void* stream) {
+  if (dtype != ADMM_F32 && dtype != ADMM_F64) return fail(ADMM_E_ARG, "dtype must be ADMM_F32 or ADMM_F64");
+  if (m < 0 || d < 1) return fail(ADMM_E_ARG, "membership expects a non-empty 1-D vector per row");
+  if (d > 32) return fail(ADMM_E_UNSUPPORTED, "membership supports d <= 32");
+  if (!(tol >= 0)) return fail(ADMM_E_ARG, "tol must be non-negative");
+  if (m == 0) return ADMM_OK;
+  if (!values || !out) return fail(ADMM_E_ARG, "null pointer argument");
+  cudaGetLastError();
+  if (!admm::launch_membership(dtype, pick_bucket(d), m, d, values, tol, out, reinterpret_cast<cudaStream_t>(stream)))
+    return fail(ADMM_E_UNSUPPORTED, "no membership kernel for this degree");
   ADMM_CUDA(cudaGetLastError());
   return ADMM_OK;
 }

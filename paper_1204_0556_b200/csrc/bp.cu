@@ -6,7 +6,7 @@
 namespace admm {
 
 template <typename T, int D, int CPT, int DVMAX>
-void bp_launch_t(const BpGraphArgs& g, const BpFrameArgs& a, int grid, int nt, int smem, cudaStream_t st) {
+cudaError_t bp_launch_t(const BpGraphArgs& g, const BpFrameArgs& a, int grid, int nt, int smem, cudaStream_t st) {
   BpParams<T> p;
   p.n_vars = g.n_vars;
   p.n_checks = g.n_checks;
@@ -34,6 +34,7 @@ void bp_launch_t(const BpGraphArgs& g, const BpFrameArgs& a, int grid, int nt, i
   p.queue = a.queue;
   p.synth = a.synth;
   bp_decode_kernel<T, D, CPT, DVMAX><<<grid, nt, smem, st>>>(p);
+  return cudaGetLastError();
 }
 
 template <typename T, int D, int CPT, int DVMAX>

@@ -35,7 +35,8 @@ struct BpFrameArgs {
   SynthParams synth;
 };
 
-using BpLaunchFn = void (*)(const BpGraphArgs&, const BpFrameArgs&, int grid, int nt, int smem, cudaStream_t st);
+using BpLaunchFn = cudaError_t (*)(const BpGraphArgs&, const BpFrameArgs&, int grid, int nt, int smem,
+                                   cudaStream_t st);
 
 struct BpLaunch {
   const void* fn;

@@ -4,13 +4,13 @@
 
 #include <cuda_runtime.h>
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <stdint.h>
 
 #include "resident.cuh"
 #include "resident_regular.cuh"
 #include "streaming.cuh"
-#include "cluster_resident.cuh"
 #include "sharded.cuh"
 #include "wide.cuh"
 
@@ -51,8 +51,8 @@ struct ResidentFrameArgs {
   SynthParams synth;
 };
 
-using ResidentLaunchFn = void (*)(const ResidentGraphArgs&, const ResidentFrameArgs&, int grid, int nt,
-                                  int smem, cudaStream_t st);
+using ResidentLaunchFn = cudaError_t (*)(const ResidentGraphArgs&, const ResidentFrameArgs&, int grid, int nt,
+                                         int smem, cudaStream_t st);
 
 struct ResidentLaunch {
   const void* fn;
@@ -63,6 +63,19 @@ struct ResidentLaunch {
   bool gm_smem;  // LLR steps in shared memory (regular_gm_smem)
   int zs_cpt;    // > 0: edge state in shared memory for this many checks per thread
 };
+
+// The stop-rule threshold in T, rounded toward +inf: a partial sum >= it is
+// >= the fp64 threshold (early-out tests stay exact in fp32 mode).
+template <typename T>
+inline T thr_round_up(double thr) {
+  if constexpr (sizeof(T) == 8) {
+    return thr;
+  } else {
+    float f = static_cast<float>(thr);
+    if (static_cast<double>(f) < thr) f = std::nextafter(f, INFINITY);
+    return f;
+  }
+}
 
 template <typename T>
 ResidentParams<T> make_params(const ResidentGraphArgs& g, const ResidentFrameArgs& a) {
@@ -84,7 +97,8 @@ ResidentParams<T> make_params(const ResidentGraphArgs& g, const ResidentFrameArg
   p.inv_mu = T(1.0 / a.mu);
   p.rho = T(a.rho);
   p.one_minus_rho = T(1.0 - a.rho);
-  p.thr = T(a.thr);
+  p.thr = thr_round_up<T>(a.thr);
+  p.thr_d = a.thr;
   p.t_max = a.t_max;
   p.z_in = static_cast<const T*>(a.z_in);
   p.lam_in = static_cast<const T*>(a.lam_in);
@@ -104,16 +118,18 @@ ResidentParams<T> make_params(const ResidentGraphArgs& g, const ResidentFrameArg
 }
 
 template <typename T, int D, int CPT, int DVMAX>
-void launch_resident(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int grid, int nt, int smem,
-                     cudaStream_t st) {
+cudaError_t launch_resident(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int grid, int nt, int smem,
+                            cudaStream_t st) {
   resident_decode_kernel<T, D, CPT, DVMAX><<<grid, nt, smem, st>>>(make_params<T>(g, a));
+  return cudaGetLastError();
 }
 
 template <typename T, int D, int DV, int CPT, int VPT, int MINB, int MAXT, bool COL, int NPC, int NTC, bool ZS>
-void launch_regular(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int grid, int nt, int smem,
-                    cudaStream_t st) {
+cudaError_t launch_regular(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int grid, int nt, int smem,
+                           cudaStream_t st) {
   resident_regular_kernel<T, D, DV, CPT, VPT, MINB, MAXT, COL, NPC, NTC, ZS><<<grid, nt, smem, st>>>(
       make_params<T>(g, a), g.var_edge_int ? g.var_edge_int : g.var_edge);
+  return cudaGetLastError();
 }
 
 // Regular-code variants: (D, DV, CPT, VPT).  `variant` enumerates the
@@ -170,7 +186,8 @@ StreamParams<T> make_stream_params(const StreamGraphArgs& g, const ResidentFrame
   p.inv_mu = T(1.0 / a.mu);
   p.rho = T(a.rho);
   p.one_minus_rho = T(1.0 - a.rho);
-  p.thr = T(a.thr);
+  p.thr = thr_round_up<T>(a.thr);
+  p.thr_d = a.thr;
   p.t_max = a.t_max;
   p.x_out = static_cast<T*>(a.x_out);
   p.ld_x = a.ld_x;
@@ -232,36 +249,6 @@ bool phase_profile(int enable, unsigned long long* out8);
 
 bool stream_lookup(int dtype, int D, int DVMAX, bool regular, StreamLaunch* out);
 
-// ---- cluster-resident engine ----
-struct ClusterLaunch {
-  const void* fn;
-  int (*launch)(const ResidentGraphArgs&, const ResidentFrameArgs&, int clusters, int C, int MC, int NC, int nt,
-                int smem, cudaStream_t st);
-  int clusters, regs, smem;
-};
-
-template <typename T, int D, int DV, int CPT, int VPT>
-int launch_cluster(const ResidentGraphArgs& g, const ResidentFrameArgs& a, int clusters, int C, int MC, int NC, int nt,
-                   int smem, cudaStream_t st) {
-  const ResidentParams<T> p = make_params<T>(g, a);
-  const int* ve = g.var_edge;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(clusters * C);
-  cfg.blockDim = dim3(nt);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return (int)cudaLaunchKernelEx(&cfg, cluster_decode_kernel<T, D, DV, CPT, VPT>, p, ve, MC, NC);
-}
-
-bool cluster_lookup(int dtype, int D, int DV, int CPT, int VPT_min, int* VPT, ClusterLaunch* out);
-
 // Defined in project.cu.
 bool launch_project(int dtype, int D, long long m, int d, const void* in, void* out, cudaStream_t st);
 void launch_synth(int dtype, long long batch, int n, const SynthParams& s, void* out, long long ld, cudaStream_t st);
@@ -295,7 +282,8 @@ WideParams<T> make_wide_params(const StreamGraphArgs& g, const ResidentFrameArgs
   p.mu = T(a.mu);
   p.rho = T(a.rho);
   p.one_minus_rho = T(1.0 - a.rho);
-  p.thr = T(a.thr);
+  p.thr = thr_round_up<T>(a.thr);
+  p.thr_d = a.thr;
   p.t_max = a.t_max;
   p.x_out = static_cast<T*>(a.x_out);
   p.ld_x = a.ld_x;

@@ -47,7 +47,11 @@ struct ResidentParams {
   const T* gamma;
   long long ld_gamma;
   // parameters
+  // thr_d = eps^2 E (admm_decoder.py:169) in fp64: the exact stop-rule sums
+  // are accumulated and compared in fp64 in both modes.  thr is its T value
+  // rounded UP, so a per-thread partial >= thr implies partial >= thr_d.
   T mu, inv_mu, rho, one_minus_rho, thr;
+  double thr_d;
   int t_max;
   // optional initial state (reference edge order), null = zeros
   const T* z_in;
@@ -103,7 +107,7 @@ struct ResidentSmem {
     pos = align16(ideg + elem * n_vars);
     deg = align16(pos + 2 * dvmax * n_vars);
     red = align16(deg + n_vars);
-    total = align16(red + elem * 2 * 32 + 16);
+    total = align16(red + 8 * 2 * 32 + 16);  // fp64 reduction slots
   }
 };
 
@@ -119,8 +123,8 @@ __global__ void __launch_bounds__(512) resident_decode_kernel(const ResidentPara
   T* ideg = reinterpret_cast<T*>(smem_raw + L.ideg);
   Pos* spos = reinterpret_cast<Pos*>(smem_raw + L.pos);
   uint8_t* sdeg = reinterpret_cast<uint8_t*>(smem_raw + L.deg);
-  T* red = reinterpret_cast<T*>(smem_raw + L.red);
-  int* s_frame = reinterpret_cast<int*>(smem_raw + L.red + sizeof(T) * 64);
+  double* red = reinterpret_cast<double*>(smem_raw + L.red);
+  int* s_frame = reinterpret_cast<int*>(smem_raw + L.red + sizeof(double) * 64);
   int* s_weight = s_frame + 1;
 
   const int tid = threadIdx.x, NT = blockDim.x;
@@ -229,19 +233,19 @@ __global__ void __launch_bounds__(512) resident_decode_kernel(const ResidentPara
           }
         }
       }
-      // ---- stop rule (admm_decoder.py:169,174-181) ----
-      primal = warp_allsum(primal);
-      moved = warp_allsum(moved);
+      // ---- stop rule (admm_decoder.py:169,174-181): fp64 accumulation ----
+      const double pa = warp_allsum(static_cast<double>(primal));
+      const double pb = warp_allsum(static_cast<double>(moved));
       if (lane == 0) {
-        red[2 * warp] = primal;
-        red[2 * warp + 1] = moved;
+        red[2 * warp] = pa;
+        red[2 * warp + 1] = pb;
       }
       __syncthreads();
-      T a = lane < nwarps ? red[2 * lane] : T(0);
-      T b = lane < nwarps ? red[2 * lane + 1] : T(0);
+      double a = lane < nwarps ? red[2 * lane] : 0.0;
+      double b = lane < nwarps ? red[2 * lane + 1] : 0.0;
       a = warp_allsum(a);
       b = warp_allsum(b);
-      if (a < p.thr && b < p.thr) {
+      if (a < p.thr_d && b < p.thr_d) {
         converged = true;
         break;
       }

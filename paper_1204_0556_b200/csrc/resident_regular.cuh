@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
   // live in shared memory after the messages, read as pairs next to them --
   // four fewer registers (+1.5 % at 4 CTAs/SM; -3 % at one CTA per SM).
   constexpr bool kGmSmem = regular_gm_smem(COL, MINB, ZS);
-  T* red = msg + kRows * NP + (kGmSmem ? NP : 0);
+  double* red = reinterpret_cast<double*>(msg + kRows * NP + (kGmSmem ? NP : 0));  // 8-byte aligned: NP % 32 == 0
   int* s_int = reinterpret_cast<int*>(red + 64);  // [0] frame, [1] weight
   const uint32_t msg_a = smem_u32(msg), xs_a = smem_u32(xs);
   constexpr uint32_t ES = sizeof(T);
@@ -365,19 +365,21 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
       }
       }
       // ---- stop rule (admm_decoder.py:169,174-181) ----
+      // (p.thr is eps^2 E rounded up to T: a partial >= thr is >= the fp64
+      // threshold; the exact sums below are accumulated in fp64)
       if (__syncthreads_or(primal >= p.thr || moved >= p.thr)) continue;
-      primal = warp_allsum(primal);
-      moved = warp_allsum(moved);
+      const double pa = warp_allsum(static_cast<double>(primal));
+      const double pb = warp_allsum(static_cast<double>(moved));
       if (lane == 0) {
-        red[2 * warp] = primal;
-        red[2 * warp + 1] = moved;
+        red[2 * warp] = pa;
+        red[2 * warp + 1] = pb;
       }
       __syncthreads();
-      T a = lane < nwarps ? red[2 * lane] : T(0);
-      T b = lane < nwarps ? red[2 * lane + 1] : T(0);
+      double a = lane < nwarps ? red[2 * lane] : 0.0;
+      double b = lane < nwarps ? red[2 * lane + 1] : 0.0;
       a = warp_allsum(a);
       b = warp_allsum(b);
-      if (a < p.thr && b < p.thr) {
+      if (a < p.thr_d && b < p.thr_d) {
         converged = true;
         break;
       }
@@ -431,12 +433,12 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
   }
 }
 
-// Shared memory of the regular kernel (bytes): x[Npad] | msg[rows][Npad] | red | ints,
+// Shared memory of the regular kernel (bytes): x[Npad] | msg[rows][Npad] | red (64 fp64) | ints,
 // rows = D (slot layout) or DV (colored layout).
 inline int regular_smem_bytes(int elem, int D, int DV, int n_vars, bool col, bool gm_smem, int nt, int vpt,
                               int np_fixed = 0, int zs_cpt = 0) {
   const int np = np_fixed ? np_fixed : regular_np(n_vars, col, nt, vpt);
-  return zs_cpt * (D / 2) * nt * 16 + elem * (np + (col ? DV : D) * np + (gm_smem ? np : 0) + 64) + 16;
+  return zs_cpt * (D / 2) * nt * 16 + elem * (np + (col ? DV : D) * np + (gm_smem ? np : 0)) + 8 * 64 + 16;
 }
 
 }  // namespace admm

@@ -365,14 +365,14 @@ __global__ void __launch_bounds__(ShardThreads<T>::value, 1) sharded_decode_kern
       const int state = st_s[q];
       int conv = 0;
       if ((state == kSlotFresh || state == kSlotRunning) && dec_s[q] == 0) {
-        T a = T(0), bb = T(0);
+        double a = 0.0, bb = 0.0;  // per-CTA partials accumulated in fp64
         for (int r = lane; r < G; r += 32) {
-          a = add_rn(a, p.part[((long long)r * S + q) * 2]);
-          bb = add_rn(bb, p.part[((long long)r * S + q) * 2 + 1]);
+          a += static_cast<double>(p.part[((long long)r * S + q) * 2]);
+          bb += static_cast<double>(p.part[((long long)r * S + q) * 2 + 1]);
         }
         a = warp_allsum(a);
         bb = warp_allsum(bb);
-        conv = a < p.thr && bb < p.thr;
+        conv = a < p.thr_d && bb < p.thr_d;
       }
       __syncwarp();
       if (lane == 0) dec_s[q] = conv;

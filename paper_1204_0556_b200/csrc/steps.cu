@@ -1,0 +1,223 @@
+// The reference's step API and polytope membership as batched kernels.
+//
+//   x_update      admm_decoder.py:108-124  one thread per (frame, variable)
+//   z_update      admm_decoder.py:127-141  one thread per (frame, check)
+//   lambda_update admm_decoder.py:144-149  one thread per (frame, edge)
+//   membership    parity_polytope.py:69-91 one thread per row
+//
+// These are the level-3 plug-point of the reference (AdmmState driven by
+// hand, tests/test_admm.py:147-168, 208-240) and the state I/O of every
+// engine (the fused decode kernels keep their state on chip or in their own
+// layouts).  State arrays are [batch][ld] in the reference's edge order
+// (codes.py:91-99).  In fp64 every expression follows the reference's numpy
+// expression tree operation by operation, with true IEEE division: x_update
+// and lambda_update are bit-identical to the reference; z_update differs only
+// inside the projection (a different, exact algorithm; ~1e-16).
+#include <cuda_runtime.h>
+
+#include "projection.cuh"
+#include "steps.h"
+
+namespace admm {
+
+namespace {
+
+__device__ __forceinline__ float div_ieee(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_ieee(double a, double b) { return __ddiv_rn(a, b); }
+
+template <typename T>
+__global__ void __launch_bounds__(256) x_update_kernel(StepGraph g, long long batch, const T* __restrict__ z,
+                                                       const T* __restrict__ lam, long long ld_edge,
+                                                       const T* __restrict__ gamma, long long ld_gamma, T mu,
+                                                       T* __restrict__ x, long long ld_x) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= batch * g.n_vars) return;
+  const long long f = idx / g.n_vars;
+  const int v = static_cast<int>(idx - f * g.n_vars);
+  const int deg = g.var_deg[v];
+  const T gv = gamma[f * ld_gamma + v];
+  T out;
+  if (deg == 0) {
+    out = gv < T(0) ? T(1) : T(0);  // unconstrained variable: minimiser of its cost (:119-122)
+  } else {
+    // np.bincount accumulates the weights in edge order from 0.0 (:116)
+    T acc = T(0);
+    for (int j = 0; j < deg; ++j) {
+      const long long e = f * ld_edge + g.var_edge[(long long)v * g.dv_stride + j];
+      acc = add_rn(acc, sub_rn(z[e], div_ieee(lam[e], mu)));  // adj = z - lam / mu (:115)
+    }
+    out = clip01(div_ieee(sub_rn(acc, div_ieee(gv, mu)), T(deg)));  // (:118)
+  }
+  x[f * ld_x + v] = out;
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(256) z_update_kernel(StepGraph g, long long batch, const T* __restrict__ x,
+                                                       long long ld_x, const T* __restrict__ z_old,
+                                                       const T* __restrict__ lam, long long ld_edge, T mu, T rho,
+                                                       T one_minus_rho, T* __restrict__ z_new,
+                                                       T* __restrict__ w_out) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= batch * g.n_checks) return;
+  const long long f = idx / g.n_checks;
+  const int c = static_cast<int>(idx - f * g.n_checks);
+  const long long e0 = f * ld_edge + g.check_ptr[c];
+  const int d = g.check_ptr[c + 1] - g.check_ptr[c];
+  T u[D], w[D], zn[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if (k < d) {
+      const T gx = x[f * ld_x + g.chk_var[(long long)k * g.m_pad + c]];  // x[edge_var] (:131)
+      w[k] = add_rn(mul_rn(rho, gx), mul_rn(one_minus_rho, z_old[e0 + k]));  // (:132)
+      u[k] = add_rn(w[k], div_ieee(lam[e0 + k], mu));                          // (:133)
+    } else {
+      w[k] = T(0);
+      u[k] = -Num<T>::inf();
+    }
+  }
+  project_pp<T, D>(u, zn, d);  // project_batch per degree group (:134-137)
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if (k < d) {
+      z_new[e0 + k] = zn[k];
+      if (w_out) w_out[e0 + k] = w[k];
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) lambda_update_kernel(long long batch, int n_edges, const T* __restrict__ lam,
+                                                            const T* __restrict__ w, const T* __restrict__ z,
+                                                            long long ld_edge, T mu, T* __restrict__ lam_out) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= batch * n_edges) return;
+  const long long f = idx / n_edges;
+  const long long e = f * ld_edge + (idx - f * n_edges);
+  lam_out[e] = add_rn(lam[e], mul_rn(mu, sub_rn(w[e], z[e])));  // lam + mu (w - z) (:148)
+}
+
+// membership (parity_polytope.py:69-91): cube test, r = even floor of the
+// clipped l1 norm snapped by PARITY_TOL, two-slice weight alpha, and the
+// majorisation test of the descending prefix sums against
+// alpha min(q, r) + (1 - alpha) min(q, r + 2).
+template <typename T, int D>
+__global__ void __launch_bounds__(256) membership_kernel(long long m, int d, const T* __restrict__ in, T tol,
+                                                         uint8_t* __restrict__ out) {
+  const long long row = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (row >= m) return;
+  T v[D], a[D];
+  bool cube = true;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    a[k] = (k < d) ? in[row * d + k] : T(0);
+    v[k] = (k < d) ? a[k] : -Num<T>::inf();
+    if (k < d) cube &= !(a[k] < -tol) && !(a[k] > T(1) + tol);
+  }
+  if (!cube) {
+    out[row] = 0;
+    return;
+  }
+  const T s = vmin(vmax(numpy_rowsum<T, D>(a, d), T(0)), T(d));  // float(u.sum()) in numpy's order
+  const T snapped = add_rn(s, T(1e-9));  // _snapped_parity: even_floor(s + PARITY_TOL) (:62-64)
+  const int r = 2 * static_cast<int>(floor(snapped * T(0.5)));
+  const T alpha = vmin(vmax(mul_rn(sub_rn(add_rn(T(2), T(r)), s), T(0.5)), T(0)), T(1));  // (2 + r - s) / 2
+  if (r + 2 > d && alpha < T(1) - tol) {
+    out[row] = 0;
+    return;
+  }
+  SortNet<D>::desc(v);
+  T prefix = T(0);
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if (k < d) {
+      prefix = add_rn(prefix, v[k]);
+      const int q = k + 1;
+      const T b = add_rn(mul_rn(alpha, T(q < r ? q : r)), mul_rn(sub_rn(T(1), alpha), T(q < r + 2 ? q : r + 2)));
+      ok &= prefix <= add_rn(b, tol);
+    }
+  }
+  out[row] = ok ? 1 : 0;
+}
+
+inline long long blocks(long long n) { return (n + 255) / 256; }
+
+template <typename T>
+bool z_update_t(const StepGraph& g, long long batch, const void* x, long long ld_x, const void* z_old,
+                const void* lam, long long ld_edge, double mu, double rho, void* z_new, void* w_out,
+                cudaStream_t st) {
+  const long long n = batch * g.n_checks;
+  auto go = [&](auto kern) {
+    kern<<<blocks(n), 256, 0, st>>>(g, batch, static_cast<const T*>(x), ld_x, static_cast<const T*>(z_old),
+                                    static_cast<const T*>(lam), ld_edge, T(mu), T(rho), T(1.0 - rho),
+                                    static_cast<T*>(z_new), static_cast<T*>(w_out));
+  };
+  switch (g.D) {
+    case 4: go(z_update_kernel<T, 4>); return true;
+    case 6: go(z_update_kernel<T, 6>); return true;
+    case 8: go(z_update_kernel<T, 8>); return true;
+    case 13: go(z_update_kernel<T, 13>); return true;
+    case 16: go(z_update_kernel<T, 16>); return true;
+    case 32: go(z_update_kernel<T, 32>); return true;
+  }
+  return false;
+}
+
+template <typename T>
+bool membership_t(int D, long long m, int d, const void* in, double tol, uint8_t* out, cudaStream_t st) {
+  auto go = [&](auto kern) { kern<<<blocks(m), 256, 0, st>>>(m, d, static_cast<const T*>(in), T(tol), out); };
+  switch (D) {
+    case 4: go(membership_kernel<T, 4>); return true;
+    case 6: go(membership_kernel<T, 6>); return true;
+    case 8: go(membership_kernel<T, 8>); return true;
+    case 13: go(membership_kernel<T, 13>); return true;
+    case 16: go(membership_kernel<T, 16>); return true;
+    case 32: go(membership_kernel<T, 32>); return true;
+  }
+  return false;
+}
+
+}  // namespace
+
+void launch_x_update(int dtype, const StepGraph& g, long long batch, const void* z, const void* lam,
+                     long long ld_edge, const void* gamma, long long ld_gamma, double mu, void* x, long long ld_x,
+                     cudaStream_t st) {
+  const long long n = batch * g.n_vars;
+  if (dtype)
+    x_update_kernel<double><<<blocks(n), 256, 0, st>>>(g, batch, static_cast<const double*>(z),
+                                                       static_cast<const double*>(lam), ld_edge,
+                                                       static_cast<const double*>(gamma), ld_gamma, mu,
+                                                       static_cast<double*>(x), ld_x);
+  else
+    x_update_kernel<float><<<blocks(n), 256, 0, st>>>(g, batch, static_cast<const float*>(z),
+                                                      static_cast<const float*>(lam), ld_edge,
+                                                      static_cast<const float*>(gamma), ld_gamma, float(mu),
+                                                      static_cast<float*>(x), ld_x);
+}
+
+bool launch_z_update(int dtype, const StepGraph& g, long long batch, const void* x, long long ld_x,
+                     const void* z_old, const void* lam, long long ld_edge, double mu, double rho, void* z_new,
+                     void* w_out, cudaStream_t st) {
+  return dtype ? z_update_t<double>(g, batch, x, ld_x, z_old, lam, ld_edge, mu, rho, z_new, w_out, st)
+               : z_update_t<float>(g, batch, x, ld_x, z_old, lam, ld_edge, mu, rho, z_new, w_out, st);
+}
+
+void launch_lambda_update(int dtype, long long batch, int n_edges, const void* lam, const void* w, const void* z,
+                          long long ld_edge, double mu, void* lam_out, cudaStream_t st) {
+  const long long n = batch * n_edges;
+  if (dtype)
+    lambda_update_kernel<double><<<blocks(n), 256, 0, st>>>(
+        batch, n_edges, static_cast<const double*>(lam), static_cast<const double*>(w),
+        static_cast<const double*>(z), ld_edge, mu, static_cast<double*>(lam_out));
+  else
+    lambda_update_kernel<float><<<blocks(n), 256, 0, st>>>(
+        batch, n_edges, static_cast<const float*>(lam), static_cast<const float*>(w), static_cast<const float*>(z),
+        ld_edge, float(mu), static_cast<float*>(lam_out));
+}
+
+bool launch_membership(int dtype, int D, long long m, int d, const void* in, double tol, uint8_t* out,
+                       cudaStream_t st) {
+  return dtype ? membership_t<double>(D, m, d, in, tol, out, st) : membership_t<float>(D, m, d, in, tol, out, st);
+}
+
+}  // namespace admm

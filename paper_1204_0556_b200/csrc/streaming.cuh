@@ -51,7 +51,8 @@ struct StreamParams {
   long long batch;
   const T* gamma;
   long long ld_gamma;
-  T mu, inv_mu, rho, one_minus_rho, thr;
+  T mu, inv_mu, rho, one_minus_rho, thr;  // thr: eps^2 E rounded up to T (early-out tests)
+  double thr_d;                            // eps^2 E: the exact sums are fp64
   int t_max;
   // outputs
   T* x_out;
@@ -300,14 +301,14 @@ __device__ __forceinline__ void stream_phase_s(const StreamParams<T>& p, int s, 
   if (nc == 0) {
     // Exact residual sums (admm_decoder.py:174-176), fixed reduction tree.
     const long long S = p.S;
-    T a = T(0), b = T(0);
+    double a = 0.0, b = 0.0;  // per-block partials accumulated in fp64
     for (int q = lane; q < n_cblk; q += 32) {
-      a = add_rn(a, p.part[((long long)q * S + s) * 2]);
-      b = add_rn(b, p.part[((long long)q * S + s) * 2 + 1]);
+      a += static_cast<double>(p.part[((long long)q * S + s) * 2]);
+      b += static_cast<double>(p.part[((long long)q * S + s) * 2 + 1]);
     }
     a = warp_allsum(a);
     b = warp_allsum(b);
-    converged = a < p.thr && b < p.thr;
+    converged = a < p.thr_d && b < p.thr_d;
   }
   if (lane == 0) {
     const int t = p.tcount[s] + 1;

@@ -71,7 +71,8 @@ struct WideParams {
   long long batch;
   const T* gamma;
   long long ld_gamma;
-  T mu, rho, one_minus_rho, thr;
+  T mu, rho, one_minus_rho, thr;  // thr: eps^2 E rounded up to T (early-out tests)
+  double thr_d;                    // eps^2 E: the exact sums are fp64
   int t_max;
   T* x_out;
   long long ld_x;
@@ -741,18 +742,19 @@ __device__ __forceinline__ void wide_phase_s(const WideParams<T>& p, int s, int*
   // of a moved-partial flags an odd check of x_t in its block.
   const int stripe = s / W, r = s % W;
   const T* part = p.part + (long long)stripe * p.ncb * 2 * W + r;
-  T a = T(0), b = T(0);
+  // Per-item partials (8 checks) are T; they are accumulated in fp64.
+  double a = 0.0, b = 0.0;
   bool odd = false;
 #pragma unroll 8
   for (int q = lane; q < p.ncb; q += 32) {
     const T mv = part[(long long)q * 2 * W + W];
-    a = add_rn(a, part[(long long)q * 2 * W]);
-    b = add_rn(b, fabs(mv));
+    a += static_cast<double>(part[(long long)q * 2 * W]);
+    b += static_cast<double>(fabs(mv));
     odd |= signbit(mv);
   }
   a = warp_allsum(a);
   b = warp_allsum(b);
-  const bool converged = a < p.thr && b < p.thr;  // admm_decoder.py:169, 179 (strict)
+  const bool converged = a < p.thr_d && b < p.thr_d;  // admm_decoder.py:169, 179 (strict)
   const int t = __shfl_sync(0xffffffffu, lane == 0 ? p.tcount[s] : 0, 0) + 1;
   const bool stop = converged || t >= p.t_max;
   if (stop && state == kSlotRunning && p.direct) {

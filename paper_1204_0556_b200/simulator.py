@@ -170,10 +170,14 @@ def _decode_wave(code, channel, cfg, sent, seed, point, trials: range, *, frames
             bit_err = res.weight.to(torch.int64)
             word_err = bit_err > 0
             ml = torch.zeros(B, dtype=torch.bool, device=bit_err.device)
+            # re-decode on the kernel that decoded the wave (a frame's result is
+            # independent of its batch and slot on one kernel, but the kernels
+            # round differently in fp32; batch 1 would otherwise pick the sharded one)
+            eng1 = "wide" if res.info.get("kernel") == 5 else engine
             for k in (word_err & res.codeword).nonzero().flatten().tolist():
                 t = trials.start + k
                 one = decode_synth(code, channel, cfg, seed=seed, point=point, trial0=t, batch=1, dtype=dtype,
-                                   device=device, want_hard=True, engine=engine)
+                                   device=device, want_hard=True, engine=eng1)
                 g1 = synth_llr(code.n_vars, channel, seed=seed, point=point, trial0=t, batch=1,
                                dtype=torch.float64, device=device)
                 ml[k] = bool((g1[0] * one.hard[0].to(torch.float64)).sum() < 0)  # cost_est < cost_sent = 0

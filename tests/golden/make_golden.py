@@ -29,6 +29,22 @@ harness.npz        reference sweep()/run_point() CSV (timing=False) on the confi
 steps.npz          single-iteration state dumps (x, z, lam) after 1, 2, 3
                    iterations for one config-1 frame (x_update / z_update /
                    lambda_update driven directly, as test_admm.py:151-160).
+sweep_*.npz        sweep END POINTS of the BASELINE workloads (round 2): for each
+                   (config, channel point) 1000 frames (256 for config 5)
+                   trial_gamma(seed=1, point=k, trial=t), AdmmConfig(mu=5.0):
+                   iterations, status, integral, certificate, packed hard
+                   decisions, x of the first frames.  Points: cfg2 1.5 / 3.0 dB,
+                   cfg3 1.5 / 2.0 / 3.0 dB, cfg4 3.5 / 5.0 dB, cfg5 BSC 0.04 /
+                   AWGN 2.5 dB.  Decoded over a process pool (`sweep`).
+conformance.npz    the reference's decode properties and acceptance criteria
+                   5-7 as data (`conformance`): Hamming one-flip LP values and
+                   ML words (test_admm.py:116-135), the codebook certificate
+                   case (:170-184), LP value of the objective case (:186-197),
+                   the feasibility case's final z (:147-168), criterion 5/6
+                   iteration counts and the criterion 7 WERs
+                   (test_acceptance.py:186-262).
+membership.npz     membership() on adversarial rows d = 1..10 (inside, outside,
+                   boundary, projected points) (parity_polytope.py:69-91).
 bp.npz             the reference's BP (bp_decoder.py): config-1 code at 2.5 dB,
                    200 frames with the default BpConfig (beliefs, iterations,
                    found, decode_bp x / integral / status), 16 frames for a
@@ -234,6 +250,184 @@ def bp_fixture():
           int(rec["c2_found"].sum()), "iters", rec["c2_iterations"])
 
 
+# ---------------------------------------------------------------------------
+# Round 2: sweep end points, conformance properties, membership
+# ---------------------------------------------------------------------------
+SWEEP_POINTS = [
+    # (fixture name, baseline code, channel, channel parameter, point index, frames, frames with x)
+    ("sweep_cfg2_1p5.npz", "cfg2_n1008", "awgn", 1.5, 0, 1000, 16),
+    ("sweep_cfg2_3p0.npz", "cfg2_n1008", "awgn", 3.0, 6, 1000, 16),
+    ("sweep_cfg3_1p5.npz", "cfg3_n2640", "awgn", 1.5, 3, 1000, 16),
+    ("sweep_cfg3_2p0.npz", "cfg3_n2640", "awgn", 2.0, 0, 1000, 16),
+    ("sweep_cfg3_3p0.npz", "cfg3_n2640", "awgn", 3.0, 2, 1000, 16),
+    ("sweep_cfg4_3p5.npz", "cfg4_n1040", "awgn", 3.5, 0, 1000, 16),
+    ("sweep_cfg4_5p0.npz", "cfg4_n1040", "awgn", 5.0, 3, 1000, 16),
+    ("sweep_cfg5_bsc.npz", "cfg5_n16384", "bsc", 0.04, 0, 256, 8),
+    ("sweep_cfg5_awgn.npz", "cfg5_n16384", "awgn", 2.5, 1, 256, 8),
+]
+
+
+def _channel(code, kind, val):
+    return polylp.Bsc(val) if kind == "bsc" else polylp.Awgn(val, code.design_rate)
+
+
+def _sweep_chunk(args):
+    n_vars, checks, kind, val, point, trials, n_x = args
+    rc = polylp.ParityCheckMatrix(n_vars, [np.asarray(c) for c in checks])
+    ch = _channel(rc, kind, val)
+    cfg = AdmmConfig(mu=5.0)
+    out = []
+    for t in trials:
+        rng = np.random.default_rng(np.random.SeedSequence(entropy=1, spawn_key=(point, t)))
+        g = polylp.llr(polylp.transmit(np.zeros(n_vars, dtype=np.uint8), ch, rng), ch)
+        o = decode(g, rc, cfg)
+        out.append((t, o.iterations, o.status == polylp.STATUS_CONVERGED, o.integral, o.ml_certificate,
+                    np.packbits(o.hard_decision), o.x if t < n_x else None))
+    return out
+
+
+def sweep_fixtures(only=None, workers=8):
+    from multiprocessing import Pool
+
+    for name, key, kind, val, point, frames, n_x in SWEEP_POINTS:
+        if only and name not in only:
+            continue
+        code = baseline_code(key)
+        checks = [np.asarray(c) for c in code.check_neighborhoods]
+        # small chunks first-come: the slow (T_max) frames spread over the pool
+        jobs = [(code.n_vars, checks, kind, val, point, range(lo, min(lo + 8, frames)), n_x)
+                for lo in range(0, frames, 8)]
+        with Pool(workers) as pool:
+            recs = sorted(r for part in pool.imap_unordered(_sweep_chunk, jobs) for r in part)
+        assert [r[0] for r in recs] == list(range(frames))
+        ptr, ev = pack_checks(code)
+        np.savez_compressed(
+            OUT / name, code=key, n_vars=code.n_vars, check_ptr=ptr, edge_var=ev, channel=kind, param=val,
+            point=point, seed=1, mu=5.0, epsilon=1e-5, t_max=1000, rho=1.9,
+            iterations=np.array([r[1] for r in recs], np.int32), converged=np.array([r[2] for r in recs], np.uint8),
+            integral=np.array([r[3] for r in recs], np.uint8), certificate=np.array([r[4] for r in recs], np.uint8),
+            hard=np.stack([r[5] for r in recs]), x=np.stack([r[6] for r in recs[:n_x]]))
+        it = np.array([r[1] for r in recs])
+        we = sum(int(np.unpackbits(r[5]).any()) for r in recs)
+        print(name, "mean iters", it.mean(), "at T_max", int((it == 1000).sum()), "word errors", we, flush=True)
+
+
+def conformance_fixture():
+    """The reference's decode properties and acceptance criteria 5-7 as data
+    (the GPU box has no /root/reference)."""
+    from polylp import Bsc, DecoderRef, gen_regular_ldpc, is_codeword, llr, run_point
+    from polylp.admm_decoder import AdmmState, lambda_update, x_update, z_update
+
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    import oracles  # noqa: E402  (the reference's own test oracles)
+
+    rec = {}
+    # Hamming one-flip cases (test_admm.py:116-135)
+    ham = oracles.hamming_7_4()
+    book = oracles.codebook(ham.to_dense())
+    rec["ham_checks"] = np.concatenate([np.asarray(c) for c in ham.check_neighborhoods])
+    rec["ham_check_len"] = np.array([len(c) for c in ham.check_neighborhoods])
+    gam, lpv, ml, xs = [], [], [], []
+    for flip in [None, 0, 1, 2, 3, 4, 5, 6]:
+        y = np.zeros(7, dtype=np.uint8)
+        if flip is not None:
+            y[flip] = 1
+        g = llr(y, Bsc(0.05))
+        gam.append(g)
+        lpv.append(oracles.fundamental_lp(g, ham)[0])
+        ml.append(book[np.argmin(book @ g)])
+        xs.append(decode(g, ham).x)
+    rec.update(ham_gamma=np.array(gam), ham_lp=np.array(lpv), ham_ml=np.array(ml), ham_x=np.array(xs),
+               ham_var_deg=np.asarray(ham.var_degrees))
+    # ML certificate against the codebook (test_admm.py:170-184)
+    c16 = gen_regular_ldpc(16, 3, 6, seed=9)
+    book16 = oracles.codebook(c16.to_dense())
+    rng = np.random.default_rng(2)
+    g16 = []
+    for _ in range(200):
+        y = (rng.random(16) < 0.05).astype(np.uint8)
+        g16.append(llr(y, Bsc(0.05)))
+    g16 = np.array(g16)
+    o16 = [decode(g, c16) for g in g16]
+    rec.update(c16_book=book16, c16_gamma=g16, c16_best=(g16 @ book16.T).min(axis=1),
+               c16_iterations=np.array([o.iterations for o in o16]),
+               c16_cert=np.array([o.integral and is_codeword(c16, o.hard_decision) for o in o16]))
+    # objective approaches the LP value (test_admm.py:186-197)
+    c24 = gen_regular_ldpc(24, 3, 6, seed=3)
+    g24 = np.random.default_rng(5).normal(0.4, 1.0, 24)
+    rec.update(lp24_gamma=g24, lp24_value=oracles.fundamental_lp(g24, c24)[0],
+               lp24_x100=decode(g24, c24, AdmmConfig(epsilon=1e-14, t_max=100, rho=1.0)).x,
+               lp24_x1000=decode(g24, c24, AdmmConfig(epsilon=1e-14, t_max=1000, rho=1.0)).x)
+    # feasibility at convergence (test_admm.py:147-168): final z, lambda of the reference
+    c48 = gen_regular_ldpc(48, 3, 6, seed=4)
+    g48 = np.random.default_rng(1).normal(0.8, 1.0, 48)
+    cfg = AdmmConfig()
+    st = AdmmState.initial(c48)
+    thr = cfg.epsilon ** 2 * c48.n_edges
+    for t in range(cfg.t_max):
+        x_update(st, c48, g48, cfg)
+        z_update(st, c48, cfg)
+        gx = st.x[c48.edge_var]
+        primal = float(((gx - st.z) ** 2).sum())
+        moved = float(((st.z - st.z_prev) ** 2).sum())
+        lambda_update(st, c48, cfg)
+        if primal < thr and moved < thr:
+            break
+    rec.update(feas_gamma=g48, feas_iterations=t + 1, feas_z=st.z, feas_x=st.x)
+    # acceptance criteria 5 and 6 (test_acceptance.py:186-223): per-trial iterations
+    c96 = gen_regular_ldpc(96, 3, 6, seed=5)
+
+    def tg(code, ch, seed, point, trial):
+        r = np.random.default_rng(np.random.SeedSequence(entropy=seed, spawn_key=(point, trial)))
+        return llr(polylp.transmit(np.zeros(code.n_vars, dtype=np.uint8), ch, r), ch)
+
+    it5, w5 = [], []
+    for t in range(2000):
+        o = decode(tg(c96, Bsc(0.02), 105, 0, t), c96, AdmmConfig())
+        it5.append(o.iterations)
+        w5.append(int(o.hard_decision.sum()))
+    it6 = {1.0: [], 1.9: []}
+    for t in range(1000):
+        g = tg(c96, Bsc(0.02), 106, 0, t)
+        for rho in it6:
+            it6[rho].append(decode(g, c96, AdmmConfig(rho=rho)).iterations)
+    rec.update(crit5_iterations=np.array(it5), crit5_weight=np.array(w5), crit6_iter_rho1=np.array(it6[1.0]),
+               crit6_iter_rho19=np.array(it6[1.9]))
+    # criterion 7 (test_acceptance.py:226-262): WER and trials of the four runs
+    c7 = {}
+    for tag, cfg7, pt in (("mu3", AdmmConfig(mu=3.0), 0), ("mu7", AdmmConfig(mu=7.0), 0),
+                          ("eps4", AdmmConfig(epsilon=1e-4), 1), ("eps6", AdmmConfig(epsilon=1e-6), 1)):
+        s = run_point(c96, Bsc(0.03), DecoderRef("admm", cfg7), n_trials=5000, seed=107, point_index=pt, workers=8)
+        c7[f"crit7_{tag}_word_errors"] = s.word_errors
+        c7[f"crit7_{tag}_bit_errors"] = s.bit_errors
+        c7[f"crit7_{tag}_trials"] = s.trials
+    rec.update(c7)
+    for name, c in (("c16", c16), ("c24", c24), ("c48", c48), ("c96", c96)):
+        ptr, ev = pack_checks(c)
+        rec[f"{name}_check_ptr"], rec[f"{name}_edge_var"], rec[f"{name}_n_vars"] = ptr, ev, c.n_vars
+    np.savez_compressed(OUT / "conformance.npz", **rec)
+    print("conformance: crit5 frac<200", float((np.array(it5)[np.array(w5) == 0] < 200).mean()),
+          "crit6 ratio", sum(it6[1.9]) / sum(it6[1.0]), c7)
+
+
+def membership_fixture():
+    from polylp.parity_polytope import membership
+
+    rng = np.random.default_rng(424242)
+    rec = {}
+    for d in range(1, 11):
+        rows = [rng.uniform(-0.2, 1.2, size=(200, d)),                       # mostly outside
+                project_batch(rng.uniform(-1.0, 2.0, size=(200, d))),        # on the boundary / inside
+                0.5 * project_batch(rng.uniform(-1.0, 2.0, size=(100, d))) + 0.25,  # interior mixes
+                rng.integers(0, 2, size=(60, d)).astype(float),              # vertices, odd ones outside
+                np.round(rng.uniform(0, 1, size=(60, d)) * 4) / 4]
+        rows = np.concatenate(rows)
+        rec[f"in_d{d}"] = rows
+        rec[f"out_d{d}"] = np.array([membership(u) for u in rows])
+        rec[f"out7_d{d}"] = np.array([membership(u, 1e-7) for u in rows])
+    np.savez_compressed(OUT / "membership.npz", **rec)
+
+
 def main():
     projection_fixture()
     c1 = baseline_code("cfg1_n96")
@@ -252,6 +446,12 @@ def main_bp():
 if __name__ == "__main__":
     if sys.argv[1:] == ["bp"]:
         main_bp()
+    elif sys.argv[1:2] == ["sweep"]:
+        sweep_fixtures(set(sys.argv[2:]) or None)
+    elif sys.argv[1:] == ["conformance"]:
+        conformance_fixture()
+    elif sys.argv[1:] == ["membership"]:
+        membership_fixture()
     else:
         main()
         bp_fixture()

@@ -1,0 +1,111 @@
+"""Decoder parity at the END POINTS of every BASELINE sweep, against the
+reference's own outputs (tests/golden/sweep_*.npz, written by
+tests/golden/make_golden.py from /root/reference; see its header).
+
+Frames are the reference harness's trials (trial_gamma(seed=1, point=k,
+trial=t), simulator.py:169-173), regenerated bit-identically on the host.
+
+* fp64 (parity mode): identical iteration counts, status, integrality,
+  certificate and hard decisions on every frame; x within 1e-9 on the
+  frames the fixture stores (BASELINE north_star).
+* fp32 (throughput mode): >= 99.9 % of frames with identical hard
+  decisions; frame-error and bit-error counts within 2 standard errors
+  (the two-sample binomial tolerance of the reference's acceptance suite,
+  tests/test_acceptance.py:242-244).
+
+Config 5 runs on every engine a call can reach at n = 16384: the sharded
+kernel (batches below 1024 frames) and the wide HBM-streaming kernel.
+"""
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN, load_golden
+
+pytestmark = pytest.mark.gpu
+
+FIXTURES = sorted(p.name for p in Path(GOLDEN).glob("sweep_*.npz"))
+_CACHE = {}
+
+
+def _case(name):
+    if name not in _CACHE:
+        from paper_1204_0556_b200 import AdmmConfig, Awgn, Bsc, baseline_code, trial_gammas
+
+        f = load_golden(name)
+        code = baseline_code(str(f["code"]))
+        assert np.array_equal(code.check_ptr, f["check_ptr"]) and np.array_equal(code.edge_var, f["edge_var"])
+        ch = Bsc(float(f["param"])) if str(f["channel"]) == "bsc" else Awgn(float(f["param"]), code.design_rate)
+        F = len(f["iterations"])
+        gam = trial_gammas(code.n_vars, ch, int(f["seed"]), int(f["point"]), range(F))
+        cfg = AdmmConfig(mu=float(f["mu"]), epsilon=float(f["epsilon"]), t_max=int(f["t_max"]), rho=float(f["rho"]))
+        want = np.unpackbits(f["hard"], axis=1)[:, : code.n_vars]
+        _CACHE[name] = (f, code, gam, cfg, want)
+    return _CACHE[name]
+
+
+def _engines(name):
+    return ["auto", "wide"] if "cfg5" in name else ["auto"]
+
+
+def _decode(name, dtype, engine):
+    from paper_1204_0556_b200 import decode_batch
+
+    f, code, gam, cfg, _ = _case(name)
+    res = decode_batch(gam, code, cfg, dtype=dtype, want_hard=True, engine=engine)
+    torch.cuda.synchronize()
+    return res
+
+
+def test_fixtures_present():
+    assert len(FIXTURES) == 9, FIXTURES
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+@pytest.mark.parametrize("engine", ["auto", "wide"])
+def test_f64_sweep_endpoint_matches_reference(cuda_ok, name, engine):
+    if engine not in _engines(name):
+        pytest.skip("one engine for codes that fit one SM")
+    f, code, gam, cfg, want = _case(name)
+    res = _decode(name, torch.float64, engine)
+    it = res.iterations.cpu().numpy()
+    fl = res.flags.cpu().numpy()
+    hard = res.hard.cpu().numpy()
+    assert np.array_equal(it, f["iterations"]), int((it != f["iterations"]).sum())
+    assert np.array_equal((fl & 1) != 0, f["converged"] != 0)
+    assert np.array_equal((fl & 2) != 0, f["integral"] != 0)
+    assert np.array_equal(((fl & 2) != 0) & ((fl & 4) != 0), f["certificate"] != 0)
+    assert np.array_equal(hard, want), int((hard != want).any(axis=1).sum())
+    assert np.array_equal(res.weight.cpu().numpy(), want.sum(1))
+    nx = len(f["x"])
+    assert np.abs(res.x[:nx].cpu().numpy() - f["x"]).max() <= 1e-9
+
+
+def _two_se(a, b, n):
+    """2 standard errors of the difference of two binomial proportions."""
+    return 2.0 * np.sqrt(a * (1 - a) / n + b * (1 - b) / n)
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+@pytest.mark.parametrize("engine", ["auto", "wide"])
+def test_f32_sweep_endpoint_statistics(cuda_ok, name, engine):
+    """fp32: >= 99.9 % identical hard decisions; FER and BER within 2 s.e."""
+    if engine not in _engines(name):
+        pytest.skip("one engine for codes that fit one SM")
+    f, code, gam, cfg, want = _case(name)
+    res = _decode(name, torch.float32, engine)
+    hard = res.hard.cpu().numpy()
+    F, N = hard.shape
+    same = (hard == want).all(axis=1)
+    # >= 99.9 % identical (at 256 frames per config-5 point: every frame)
+    assert same.mean() >= 0.999, f"{int((~same).sum())} of {F} frames differ"
+    fe32, fe64 = (hard.any(1)).mean(), (want.any(1)).mean()
+    assert abs(fe32 - fe64) <= _two_se(fe32, fe64, F) + 1e-12, (fe32, fe64)
+    be32, be64 = hard.sum() / (F * N), want.sum() / (F * N)
+    assert abs(be32 - be64) <= _two_se(be32, be64, F * N) + 1e-12, (be32, be64)
+    assert np.array_equal(res.weight.cpu().numpy(), hard.sum(1))
+    # fp32 iteration counts track the reference's (non-converged frames stop at T_max in both)
+    it = res.iterations.cpu().numpy()
+    assert np.abs(it.astype(np.int64) - f["iterations"]).sum() <= 0.02 * f["iterations"].sum()

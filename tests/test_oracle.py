@@ -118,3 +118,40 @@ def test_params_validation():
     for kw in ({"mu": 0.0}, {"rho": 2.0}, {"epsilon": -1.0}, {"t_max": 0}):
         with pytest.raises(ValueError):
             O.Params(**kw)
+
+
+@pytest.mark.parametrize("d", range(1, 11))
+def test_membership_matches_reference_golden(d):
+    """membership() restatement (parity_polytope.py:69-91) against the
+    reference's answers on inside / outside / boundary rows, two tolerances."""
+    f = load_golden("membership.npz")
+    rows = f[f"in_d{d}"]
+    assert np.array_equal([O.membership(u) for u in rows], f[f"out_d{d}"])
+    assert np.array_equal([O.membership(u, 1e-7) for u in rows], f[f"out7_d{d}"])
+    assert f[f"out_d{d}"].any() and not f[f"out_d{d}"].all()  # both outcomes exercised
+
+
+def test_membership_rejects_empty():
+    with pytest.raises(ValueError):
+        O.membership(np.zeros(0))
+
+
+@pytest.mark.parametrize("name", ["sweep_cfg2_3p0.npz", "sweep_cfg4_5p0.npz", "sweep_cfg5_bsc.npz"])
+def test_oracle_reproduces_sweep_endpoint_golden(name):
+    """The round-2 sweep fixtures (reference outputs) against the oracle on
+    their first frames: same frame recipe, iterations, hard decisions, x."""
+    f = load_golden(name)
+    g = graph_of(f)
+    n = g.n_vars
+    p = O.Params(mu=float(f["mu"]), epsilon=float(f["epsilon"]), t_max=int(f["t_max"]), rho=float(f["rho"]))
+    rate = 1.0 - g.n_checks / n
+    want = np.unpackbits(f["hard"], axis=1)[:, :n]
+    for t in range(2 if "cfg5" in name else 4):
+        if str(f["channel"]) == "bsc":
+            gam = O.trial_gamma_bsc(n, float(f["param"]), int(f["seed"]), int(f["point"]), t)
+        else:
+            gam = O.trial_gamma_awgn(n, float(f["param"]), rate, int(f["seed"]), int(f["point"]), t)
+        r = O.decode(gam, g, p)
+        assert r.iterations == f["iterations"][t]
+        assert np.array_equal(r.hard_decision, want[t])
+        assert np.array_equal(r.x, f["x"][t])
