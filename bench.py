@@ -1,26 +1,31 @@
 """Benchmark of the sm_100a ADMM-LP decoder on the BASELINE.json workloads.
 
-Default (what the driver runs): BASELINE config 2 -- the (3,6) n=1008
-girth-6 code, all-zero codeword over BPSK/AWGN at Eb/N0 = 1.5, 1.75, ...,
-3.0 dB (7 points), 65536 frames per point, mu=5, eps=1e-5, T_max=1000,
-rho=1.9 (the reference default), fp32.  One STEP = decoding the whole
-workload once (458,752 frames per GPU).  Inputs are seeded synthetic LLRs
-generated on the device before timing (1.85 GB fp32 per step, far larger
-than the 126 MB L2, so no L2 flush is needed between steps).
-``--workload cfg1|cfg3|cfg4|cfg5`` selects the other BASELINE configs (cfg5,
-n=16384, uses LLRs synthesised inside the decode kernel: 1M frames/point).
+Default (what the driver runs): BASELINE config 5, the metric's
+"1/2/4/8 B200" case -- the (3,6) n=16384 girth-6 code, all-zero codeword,
+BSC p=0.04 and BPSK/AWGN 2.5 dB, 1,048,576 frames per point SHARDED over
+the GPUs (strong scaling), mu=5, eps=1e-5, T_max=1000, rho=1.9 (the
+reference default), fp32.  One STEP = decoding both points once (2,097,152
+frames over all GPUs).
 
-``value`` = decoded frames/s of the whole job (all ranks), device-timed with
-CUDA events, inputs resident in HBM.  ``e2e`` = the same metric through the
-public pipelined host API (paper_1204_0556_b200.pipeline): pinned host LLRs
-in, host hard decisions / iterations / flags out, copies inside the timed
-region (for the in-kernel-synthesis workload cfg5: decode_synth with the
-per-frame results read back to pinned host memory every step).  ``cpu_baseline`` and ``--impl reference`` time the CPU oracle
-(numpy restatement of the reference, oracle/admm_oracle.py) on the box's
-host cores on a bounded, SNR-stratified sample of the same workload.
+``value`` = decoded frames/s of the whole job, device-timed with CUDA events
+(max over ranks).  The frames' LLRs are synthesised inside the decode kernel
+from (seed, point, trial) (Philox; csrc/synth.cuh), so no input is read at
+all.  ``e2e`` = the same metric through the public host API
+(paper_1204_0556_b200.pipeline.HostPipeline): pinned host fp32 LLR blocks
+copied in, per-frame iterations / flags / weights copied out, H2D,
+decode and D2H overlapped on three streams; the host LLRs are a pool of
+distinct frames per point (synth_llr of the point's first trials, staged
+once before timing) that the blocks cycle through -- every step copies
+all 2 x 1M frames' LLRs (h2d_bytes_per_step).  ``cpu_baseline`` and
+``--impl reference`` time the CPU oracle (numpy restatement of the reference,
+oracle/admm_oracle.py) on the box's host cores on a bounded sample.
 
-Multi-GPU (torchrun): weak scaling for cfg1-4 (every rank decodes its own
-frames), strong scaling for cfg5 (1M frames/point sharded over the ranks);
+``--workload cfg1..cfg4`` run the other BASELINE configs (weak scaling: every
+rank decodes its own frames, device-resident LLRs).
+
+Multi-GPU: ``--gpus N`` without a launcher re-launches itself under
+torch.distributed.run with N ranks (NCCL); under torchrun the world size
+must equal --gpus.  Frames are independent: rank r decodes its shard, and
 one NCCL all-reduce of int64 counters merges the statistics.
 """
 
@@ -76,14 +81,18 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg5")
     ap.add_argument("--dtype", choices=["f32", "f64"], default="f32")
     ap.add_argument("--frames", type=int, default=0, help="frames per point (0 = the workload's)")
     ap.add_argument("--chunk", type=int, default=262144, help="frames per decode call (synth workloads)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-block", type=int, default=65536, help="frames per host block of the e2e pipeline")
+    ap.add_argument("--e2e-pool", type=int, default=131072,
+                    help="distinct host LLR frames per point of the e2e leg of synthesised workloads")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--cpu-frames", type=int, default=0, help="oracle frames per point (0 = auto)")
+    ap.add_argument("--stub", action="store_true",
+                    help="CPU rehearsal of the launcher and rank logic: gloo, a stub decoder, no GPU (tests)")
     return ap.parse_args()
 
 
@@ -216,7 +225,70 @@ def run_reference(args, wl: Workload):
 
 
 def metric_name(wl: Workload) -> str:
-    return "decoded frames/s (ADMM-LP, config 2 sweep)" if wl.name == "cfg2" else f"decoded frames/s (ADMM-LP, {wl.name})"
+    return {
+        "cfg1": "decoded frames/s (ADMM-LP, config 1: n=96, AWGN 3.0 dB)",
+        "cfg2": "decoded frames/s (ADMM-LP, config 2 sweep: n=1008, AWGN 1.5-3.0 dB)",
+        "cfg3": "decoded frames/s (ADMM-LP, config 3: n=2640, AWGN 2.0/2.5/3.0 dB)",
+        "cfg4": "decoded frames/s (ADMM-LP, config 4: (3,13) n=1040, AWGN 3.5-5.0 dB)",
+        "cfg5": "decoded frames/s (ADMM-LP, config 5: n=16384, BSC 0.04 + AWGN 2.5 dB, 1M frames/point)",
+    }[wl.name]
+
+
+KERNEL_NAMES = {1: "resident_decode_kernel", 2: "resident_regular_kernel", 3: "sharded_decode_kernel",
+                4: "cluster_decode_kernel", 5: "wide_decode_kernel"}
+
+
+def load_peaks():
+    peak_path = ROOT / "MEASURED_PEAKS.json"
+    if peak_path.exists():
+        d = json.loads(peak_path.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", float(d.get("sm_max_mhz", 1965.0))
+    return 7700.0, "fallback (B200_PROFILING.md nominal HBM3e)", 1965.0
+
+
+def roofline(args, wl, kernel_id: int, edge_updates_per_launch: float, launch_s: float, sm_mhz, num_sms: int):
+    """Roofline of the dominant kernel, per launch.
+
+    * HBM-streaming kernels (wide): ALGORITHMIC bytes = 28 B (fp32) / 56 B
+      (fp64) per edge-update (6s + 3s/d_v) x edge-updates per
+      launch / launch time, against the measured copy bandwidth.
+    * On-chip kernels (resident, cluster): the edge state never touches
+      HBM, so the binding resource is instruction issue: warp-instructions
+      per launch (ncu inst_executed per edge-update of the same launch shape,
+      profiles/traffic.json, x edge-updates per launch) / launch time,
+      against 4 issue slots x SMs x the SM clock under load.
+    ``traffic`` = ncu dram__bytes_read.sum + dram__bytes_write.sum per launch
+    (profiles/traffic.json, same launch shape), null when not captured."""
+    hbm_peak, hbm_src, max_mhz = load_peaks()
+    name = KERNEL_NAMES.get(kernel_id, "?")
+    tr = {}
+    tpath = ROOT / "profiles" / "traffic.json"
+    key = f"{wl.name}_{args.dtype}_{name}"
+    if tpath.exists():
+        tr = json.loads(tpath.read_text()).get("launch_shapes", {}).get(key, {})
+    traffic = None
+    if tr.get("dram_bytes_per_edge_update") is not None:
+        traffic = tr["dram_bytes_per_edge_update"] * edge_updates_per_launch
+    if kernel_id == 5:
+        bpe = BYTES_PER_EDGE_UPDATE[args.dtype]
+        achieved = bpe * edge_updates_per_launch / launch_s / 1e9
+        return {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "traffic": traffic, "peak_source": hbm_src, "kernel": name, "avg_launch_ms": launch_s * 1e3,
+                "bytes_model": f"{bpe} B per edge-update (SURVEY 8d: 6s + 3s/d_v) x {edge_updates_per_launch:.4g} "
+                               f"edge-updates per launch", "traffic_source": tr.get("source")}
+    clk = float(sm_mhz or max_mhz)
+    peak = 4.0 * num_sms * clk * 1e6 / 1e9  # G warp-instructions/s
+    wipe = tr.get("warp_inst_per_edge_update")
+    achieved = None if wipe is None else wipe * edge_updates_per_launch / launch_s / 1e9
+    return {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "G warp-inst/s",
+            "frac": None if achieved is None else achieved / peak, "traffic": traffic,
+            "peak_source": f"4 issue slots x {num_sms} SMs x {clk:.0f} MHz (SM clock under load)",
+            "kernel": name, "avg_launch_ms": launch_s * 1e3,
+            "inst_model": None if wipe is None else f"{wipe:.4g} warp-instructions per edge-update (ncu "
+                                                    f"inst_executed, same launch shape) x {edge_updates_per_launch:.4g}",
+            "hbm_model_frac": BYTES_PER_EDGE_UPDATE[args.dtype] * edge_updates_per_launch / launch_s / 1e9 / hbm_peak,
+            "traffic_source": tr.get("source"),
+            "note": "on-chip engine: the HBM model's bytes are never moved (hbm_model_frac > 1 is expected)"}
 
 
 # ---------------------------------------------------------------------------
@@ -226,13 +298,15 @@ def run_ours(args, wl: Workload):
     import torch
     import torch.distributed as dist
 
-    from paper_1204_0556_b200 import AdmmConfig, baseline_code, decode_batch, decode_synth
+    from paper_1204_0556_b200 import AdmmConfig, baseline_code, decode_batch, decode_synth, synth_llr
     from paper_1204_0556_b200.channels import awgn_gammas_device, bsc_gammas_device
     from paper_1204_0556_b200.distributed import (allreduce_counters, counters_as_dict, counters_from_results,
                                                   max_over_ranks, shard)
     from paper_1204_0556_b200.pipeline import HostPipeline
 
     rank, world, local = dist_env()
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} ranks")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -256,9 +330,10 @@ def run_ours(args, wl: Workload):
                 gam.append(awgn_gammas_device(F, code.n_vars, pt[1], code.design_rate, seed=seed, device=dev,
                                               dtype=tdt))
         frames_local = F * len(wl.points)
+        mine = None
 
         def step(collect=False):
-            return [decode_batch(g, code, cfg, dtype=tdt, want_x=True, want_hard=collect, validate=False,
+            return [decode_batch(g, code, cfg, dtype=tdt, want_x=False, want_hard=collect, validate=False,
                                  stream=stream) for g in gam]
     else:
         mine = shard(F, rank, world) if wl.scaling == "strong" else range(rank * F, (rank + 1) * F)
@@ -316,39 +391,40 @@ def run_ours(args, wl: Workload):
         dist.all_reduce(totals)
     frames_all, eu_all = int(totals[0]), int(totals[1])
     value = frames_all * args.steps / elapsed
+    kernel_id = info.get("kernel", info.get("engine"))
+    roof = roofline(args, wl, kernel_id, edge_updates / n_launch, launch_s, clk.get("sm_mhz"), info["num_sms"])
 
-    # roofline of the dominant kernel (one decode kernel per launch)
-    peak_path = ROOT / "MEASURED_PEAKS.json"
-    peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
-    if peak_path.exists():
-        peak, peak_src = float(json.loads(peak_path.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-    bpe = BYTES_PER_EDGE_UPDATE[args.dtype]
-    achieved = bpe * edge_updates / n_launch / launch_s / 1e9
-    traffic = None
-    tpath = ROOT / "profiles" / "traffic.json"
-    if tpath.exists() and wl.name == "cfg2":
-        try:
-            bpf = json.loads(tpath.read_text()).get(f"bytes_per_frame_{args.dtype}")
-            traffic = None if bpf is None else bpf * F  # ncu DRAM bytes per frame x frames per launch
-        except Exception:
-            traffic = None
-    elif tpath.exists() and wl.name == "cfg5" and info.get("kernel") == 5:
-        try:  # wide kernel: ncu DRAM bytes per edge-update x edge-updates per launch
-            bpe_ncu = json.loads(tpath.read_text()).get(f"bytes_per_edge_update_wide_{args.dtype}")
-            traffic = None if bpe_ncu is None else bpe_ncu * edge_updates / n_launch
-        except Exception:
-            traffic = None
-    kernel = {1: "resident_decode_kernel", 2: "resident_regular_kernel", 3: "sharded_decode_kernel",
-              4: "cluster_decode_kernel", 5: "wide_decode_kernel"}.get(info.get("kernel", info.get("engine")), "?")
-
-    # e2e through the pipelined host API (memory workloads)
+    # e2e through the pipelined host API: pinned host LLRs in, per-frame
+    # results (iterations, flags, weights) out
     e2e = None
-    if not args.no_e2e and gam is not None:
-        # host blocks of --e2e-block frames: a short pipeline fill (first H2D)
-        # and drain (last D2H) per step
-        blk = min(F, args.e2e_block)
-        pipe = HostPipeline(code, cfg, dtype=tdt, device=dev, max_batch=blk, reuse_outputs=True)
-        host = [h for g in gam for h in g.cpu().pin_memory().split(blk)]
+    if not args.no_e2e:
+        blk = min(args.e2e_block, frames_local // len(wl.points))
+        # outputs as in the device-timed leg: per-frame iterations, flags and
+        # Hamming weight (the harness's TrialStats inputs; hard decisions on request)
+        pipe = HostPipeline(code, cfg, dtype=tdt, device=dev, max_batch=blk, want_hard=False, reuse_outputs=True)
+        if gam is not None:
+            host = [h for g in gam for h in g.cpu().pin_memory().split(blk)]
+            pool_note = "device-generated LLRs of the timed workload, staged in pinned host memory"
+        else:
+            # a pool of distinct frames per point (the point's first trials of this
+            # rank's shard), staged once in pinned host memory; the blocks of a
+            # step cycle through it so that every step copies the LLRs of all of
+            # the rank's frames
+            P = max(blk, min(args.e2e_pool, len(mine)) // blk * blk)
+            host = []
+            for k, ch in enumerate(chans):
+                pool = torch.empty((P, code.n_vars), dtype=tdt, pin_memory=True)
+                for lo in range(0, P, blk):
+                    pool[lo:lo + blk].copy_(synth_llr(code.n_vars, ch, seed=1, point=k, trial0=mine.start + lo,
+                                                      batch=blk, dtype=tdt, device=dev))
+                blocks = list(pool.split(blk))
+                n_blk = -(-len(mine) // blk)
+                for j in range(n_blk):
+                    b = blocks[j % len(blocks)]
+                    rest = len(mine) - j * blk
+                    host.append(b if rest >= blk else b[:rest])
+            pool_note = (f"host pool of {P} distinct frames per point ({P * code.n_vars * (4 if args.dtype == 'f32' else 8) / 2**30:.1f} "
+                         f"GiB pinned), blocks of {blk} frames cycled to cover the rank's {len(mine)} frames per point")
         pipe.run(host)  # warm-up: allocates the pinned result buffers reused by the timed runs
         torch.cuda.synchronize(dev)
         if world > 1:
@@ -361,41 +437,14 @@ def run_ours(args, wl: Workload):
         e1.record(stream)
         torch.cuda.synchronize(dev)
         e_el = max_over_ranks(e0.elapsed_time(e1) / 1e3, device=dev)
-        e2e = {"value": frames_all * args.steps / e_el, "unit": "frames/s",
-               "h2d_bytes_per_step": pipe.h2d_bytes_per_run(host), "d2h_bytes_per_step": pipe.d2h_bytes_per_run(host)}
-    elif not args.no_e2e:
-        # in-kernel synthesis: a trial's input is its (seed, point, trial) key, so
-        # nothing crosses to the device; every step reads each call's per-frame
-        # results (iterations, flags, weight) back into pinned host memory
-        d2h = 0
-        pinned = {}
-
-        def e2e_step():
-            nonlocal d2h
-            d2h = 0
-            for j, o in enumerate(step()):
-                for name in ("iterations", "flags", "weight"):
-                    t = getattr(o, name)
-                    buf = pinned.get((j, name))
-                    if buf is None or buf.numel() != t.numel():
-                        buf = pinned[(j, name)] = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-                    buf.copy_(t, non_blocking=True)
-                    d2h += t.numel() * t.element_size()
-
-        e2e_step()
-        torch.cuda.synchronize(dev)
+        nb = torch.tensor([pipe.h2d_bytes_per_run(host), pipe.d2h_bytes_per_run(host)], dtype=torch.int64, device=dev)
         if world > 1:
-            dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        e_el = max_over_ranks(e0.elapsed_time(e1) / 1e3, device=dev)
-        e2e = {"value": frames_all * args.steps / e_el, "unit": "frames/s", "h2d_bytes_per_step": 0,
-               "d2h_bytes_per_step": d2h, "note": "decode_synth: LLRs synthesised in the kernel from the trial key"}
+            dist.all_reduce(nb)
+        e2e = {"value": frames_all * args.steps / e_el, "unit": "frames/s",
+               "h2d_bytes_per_step": int(nb[0]), "d2h_bytes_per_step": int(nb[1]),
+               "api": "paper_1204_0556_b200.pipeline.HostPipeline.run (decode_batch on three streams)",
+               "inputs": pool_note, "block_frames": blk}
+        del pipe, host
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -403,8 +452,8 @@ def run_ours(args, wl: Workload):
         fpp = args.cpu_frames or auto_cpu_frames(wl, code, workers)
         dt, nf, eu = cpu_sample(wl, code, fpp, workers)
         cpu = {"value": nf / dt, "unit": "frames/s", "cores": workers, "kind": "port", "edge_updates_per_s": eu / dt,
-               "sample": f"{fpp} frames per channel point x {len(wl.points)} points (SNR-stratified sample of the "
-                         f"same workload), oracle/admm_oracle.py over {workers} processes, {cpu_model()}"}
+               "sample": f"{fpp} frames per channel point x {len(wl.points)} points (the same workload's channel "
+                         f"points, numpy-seeded trials), oracle/admm_oracle.py over {workers} processes, {cpu_model()}"}
 
     if rank == 0:
         line = {
@@ -413,26 +462,16 @@ def run_ours(args, wl: Workload):
             "scaling": wl.scaling, "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic (seeded device LLRs, all-zero codeword)" if gam is not None
             else "synthetic (in-kernel Philox LLRs keyed by seed/point/trial, all-zero codeword)",
-            "config": {"workload": wl.text + f" ({F} frames/point{'/GPU' if wl.scaling == 'weak' else ''}; "
+            "config": {"workload": wl.text + f" ({F} frames/point{'/GPU' if wl.scaling == 'weak' else ' over all GPUs'}; "
                                              "mu=5, eps=1e-5, T_max=1000, rho=1.9)",
                        "frames_per_step_per_gpu": frames_local, "parallelism": f"frame-shard x{world}",
                        "l2": "inputs >> 126 MB L2 per step (no flush needed)" if gam is not None
-                       else "no LLR input (synthesised in the decode kernel)",
+                       else "no LLR input (synthesised in the decode kernel); decoder state >> 126 MB L2",
                        "engine": info},
             "edge_updates_per_s": eu_all * args.steps / elapsed,
             "mean_iterations": iters_sum / frames_local,
             "stats_one_step_all_ranks": cnt,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "peak_source": peak_src,
-                         "bytes_model": f"{bpe} B per edge-update (two-kernel HBM schedule, SURVEY 8d) x "
-                                        f"{edge_updates // n_launch} edge-updates per launch",
-                         "kernel": kernel, "avg_launch_ms": launch_s * 1e3,
-                         "note": ("the wide kernel streams the whole decoder state through HBM every pass: the HBM "
-                                  "model is its real bound; `traffic` is ncu DRAM bytes per launch (DESIGN.md 3.3)"
-                                  if kernel == "wide_decode_kernel" else
-                                  "resident engines keep the edge state on chip, so the HBM-model bytes are never "
-                                  "moved and frac > 1 is expected; `traffic` is ncu DRAM bytes per launch; the real "
-                                  "bound is SM instruction issue / latency (DESIGN.md 3.6)")},
+            "roofline": roof,
             "gpu_launches": args.steps * n_launch,
             "clocks": clk,
             "e2e": e2e,
@@ -443,11 +482,65 @@ def run_ours(args, wl: Workload):
         dist.destroy_process_group()
 
 
+def run_stub(args, wl: Workload):
+    """The multi-rank logic of run_ours without a GPU: same sharding,
+    counter all-reduce and max-over-ranks timing, over gloo, with a stub
+    decoder whose per-trial results are a pure function of the trial index
+    (so the merged counters must not depend on the rank count)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1204_0556_b200.distributed import (allreduce_counters, counters_as_dict, counters_from_results,
+                                                  max_over_ranks, shard)
+
+    rank, world, _ = dist_env()
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} ranks")
+    if world > 1:
+        dist.init_process_group("gloo")
+    F = args.frames or wl.frames
+    mine = shard(F, rank, world) if wl.scaling == "strong" else range(rank * F, (rank + 1) * F)
+    t0 = time.perf_counter()
+    cnt = torch.zeros(8, dtype=torch.int64)
+    for k in range(len(wl.points)):
+        t = torch.arange(mine.start, mine.stop, dtype=torch.int64)
+        it = (t * 7 + k) % 23 + 1
+        w = torch.where(t % 5 == k, t % 4, torch.zeros_like(t))
+        conv = it < 20
+        cnt += counters_from_results(it, w, conv, conv, torch.zeros(len(t), dtype=torch.float64), 49152)
+    cnt = counters_as_dict(allreduce_counters(cnt))
+    elapsed = max_over_ranks(time.perf_counter() - t0)
+    if rank == 0:
+        print(json.dumps({"stub": True, "n_gpus": world, "frames": cnt["trials"], "counters": cnt,
+                          "elapsed_max_s": elapsed, "scaling": wl.scaling}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def relaunch(args) -> int:
+    """`--gpus N` without a launcher: re-run this script under
+    torch.distributed.run with N ranks on this node (one per GPU)."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
     wl = WORKLOADS[args.workload]
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(relaunch(args))
     if args.impl == "reference":
         run_reference(args, wl)
+    elif args.stub:
+        run_stub(args, wl)
     else:
         run_ours(args, wl)
 
