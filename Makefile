@@ -5,7 +5,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-r
 SRC_DIR := paper_1204_0556_b200/csrc
 BUILD := build
 LIB := paper_1204_0556_b200/libadmm_b200.so
-OBJS := $(BUILD)/abi.o $(BUILD)/resident_f32.o $(BUILD)/resident_f64.o $(BUILD)/project.o $(BUILD)/streaming.o $(BUILD)/steps.o $(BUILD)/bp.o $(BUILD)/wide.o
+OBJS := $(BUILD)/abi.o $(BUILD)/resident_f32.o $(BUILD)/resident_f64.o $(BUILD)/project.o $(BUILD)/streaming.o $(BUILD)/steps.o $(BUILD)/cluster.o $(BUILD)/bp.o $(BUILD)/wide.o
 HDRS := $(wildcard $(SRC_DIR)/*.cuh) $(wildcard $(SRC_DIR)/*.h) include/admm_b200.h
 
 all: $(LIB)

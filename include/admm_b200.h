@@ -48,10 +48,10 @@ enum admm_status {
 
 /* Engine selection for admm_graph_create_ex. */
 enum admm_engine {
-  ADMM_ENGINE_AUTO = 0,      /* resident if the code fits one SM, else streaming */
+  ADMM_ENGINE_AUTO = 0,      /* resident if the code fits one SM, else streaming placement (cluster engine for fp32) */
   ADMM_ENGINE_RESIDENT = 1,  /* one CTA per frame, state on chip (fails if it does not fit) */
   ADMM_ENGINE_STREAMING = 3, /* codes beyond one SM: sharded kernel (small batches), wide HBM kernel (>= 1024 frames) */
-  ADMM_ENGINE_CLUSTER = 4,   /* reserved (no cluster engine in this build: graph creation fails) */
+  ADMM_ENGINE_CLUSTER = 4,   /* streaming placement + the cluster engine required (fp32 calls run on it) */
   ADMM_ENGINE_WIDE = 5       /* streaming placement, wide HBM-streaming kernel for every batch size */
 };
 
@@ -60,7 +60,7 @@ enum admm_kernel {
   ADMM_KERNEL_RESIDENT = 1,  /* generic resident (one CTA per frame)              */
   ADMM_KERNEL_REGULAR = 2,   /* regular-code resident                              */
   ADMM_KERNEL_SHARDED = 3,   /* sharded / L2 streaming (codes beyond one SM)       */
-  ADMM_KERNEL_CLUSTER = 4,   /* reserved                                           */
+  ADMM_KERNEL_CLUSTER = 4,   /* cluster engine: one 4-CTA cluster per frame, fp32  */
   ADMM_KERNEL_WIDE = 5       /* wide HBM streaming (large batches beyond one SM)   */
 };
 
@@ -77,8 +77,11 @@ typedef struct admm_graph_info {
   int32_t smem_bytes_f32, smem_bytes_f64;
   int32_t regs_f32, regs_f64;
   int32_t num_sms;
-  int32_t cluster_size;     /* CTAs per cluster (0: one CTA per frame or streaming) */
+  int32_t cluster_size;     /* CTAs per cluster of the cluster engine (0: not placed) */
   double layout_cost_before, layout_cost_after; /* bank-conflict cost of the relabeling (engine 2) */
+  int32_t cluster_active;   /* clusters resident per GPU (cluster engine) */
+  int32_t cluster_threads, cluster_smem, cluster_regs;
+  int64_t cluster_exchange; /* DSMEM values exchanged per iteration and frame (ghost x + messages) */
 } admm_graph_info;
 
 /* Build the device-resident Tanner graph.  Replaces the edge-array views of

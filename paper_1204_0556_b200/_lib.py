@@ -19,9 +19,9 @@ ADMM_F64 = 1
 ADMM_FLAG_CONVERGED = 1
 ADMM_FLAG_INTEGRAL = 2
 ADMM_FLAG_CODEWORD = 4
-ENGINES = {"auto": 0, "resident": 1, "streaming": 3, "wide": 5}
+ENGINES = {"auto": 0, "resident": 1, "streaming": 3, "cluster": 4, "wide": 5}
 #: Kernel ids of admm_decode_kernel (enum admm_kernel).
-KERNELS = {1: "resident", 2: "regular", 3: "sharded", 5: "wide"}
+KERNELS = {1: "resident", 2: "regular", 3: "sharded", 4: "cluster", 5: "wide"}
 
 #: Every symbol the public header declares (checked by the CPU test-suite).
 EXPORTED = (
@@ -65,6 +65,8 @@ class GraphInfo(ctypes.Structure):
         ("regs_f32", ctypes.c_int32), ("regs_f64", ctypes.c_int32),
         ("num_sms", ctypes.c_int32), ("cluster_size", ctypes.c_int32),
         ("layout_cost_before", ctypes.c_double), ("layout_cost_after", ctypes.c_double),
+        ("cluster_active", ctypes.c_int32), ("cluster_threads", ctypes.c_int32), ("cluster_smem", ctypes.c_int32),
+        ("cluster_regs", ctypes.c_int32), ("cluster_exchange", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

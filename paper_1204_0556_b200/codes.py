@@ -25,6 +25,8 @@ What is new here:
 
 from __future__ import annotations
 
+import functools
+
 from functools import cached_property
 
 import numpy as np
@@ -470,6 +472,9 @@ BASELINE_CODES = {
 }
 
 
+@functools.lru_cache(maxsize=None)
 def baseline_code(name: str, seed: int = 0) -> ParityCheckMatrix:
+    """The BASELINE code `name` (cached: a ParityCheckMatrix is immutable, and
+    its device graphs are cached on it)."""
     n, dv, dc, g6 = BASELINE_CODES[name]
     return make_ldpc(n, dv, dc, seed, girth6=g6)

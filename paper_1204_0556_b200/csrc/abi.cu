@@ -12,6 +12,9 @@
 
 #include "../../include/admm_b200.h"
 #include "bp_launch.h"
+#include "cluster_launch.h"
+#include "cluster_layout.h"
+#include "cluster.cuh"
 #include "steps.h"
 #include "kernels.cuh"
 #include "layout.h"
@@ -74,6 +77,18 @@ struct admm_graph {
   bool shard_ok[2] = {false, false};
   admm::WideLaunch wlaunch[2];
   bool wide_ok[2] = {false, false};
+  // cluster engine (cluster.cuh, fp32): one 4-CTA cluster per frame
+  bool cluster_ok = false;
+  int cl_nt = 0, cl_smem = 0, cl_clusters = 0, cl_regs = 0;
+  int cl_NPL = 0, cl_NIN = 0, cl_NXS = 0, cl_NMS = 0, cl_MC = 0, cl_NO = 0;
+  int cl_n_xs[admm::kClusterMax] = {}, cl_n_ms[admm::kClusterMax] = {}, cl_n_in[admm::kClusterMax] = {};
+  long long cl_exchange = 0;
+  int* cl_chk_slot = nullptr;
+  int* cl_chk_orig = nullptr;
+  int* cl_own_var = nullptr;
+  uint32_t* cl_xsend = nullptr;
+  uint32_t* cl_msend = nullptr;
+  uint16_t* cl_scatter = nullptr;
   int* wctbl = nullptr;  // wide engine index tables (wide.cuh)
   int* wvtbl = nullptr;
   int engine_req = 0;
@@ -300,7 +315,8 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
       }
     }
   }
-  if (!placed && (engine == ADMM_ENGINE_AUTO || engine == ADMM_ENGINE_STREAMING || engine == ADMM_ENGINE_WIDE)) {
+  if (!placed && (engine == ADMM_ENGINE_AUTO || engine == ADMM_ENGINE_STREAMING || engine == ADMM_ENGINE_WIDE ||
+                  engine == ADMM_ENGINE_CLUSTER)) {
     // Streaming engine: batch-interleaved state in global memory (L2-resident).
     bool ok = true;
     for (int dt = 0; dt < 2 && ok; ++dt) {
@@ -365,6 +381,76 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
       if (engine == ADMM_ENGINE_WIDE && !g->wide_ok[0] && !g->wide_ok[1]) {
         delete g;
         return fail(ADMM_E_UNSUPPORTED, "no wide streaming kernel for this graph");
+      }
+      // Cluster engine (fp32): one 4-CTA cluster per frame, state on chip.
+      if ((engine == ADMM_ENGINE_AUTO || engine == ADMM_ENGINE_CLUSTER) && regular && dmax == 6 && dvmax == 3 &&
+          std::getenv("ADMM_B200_NO_CLUSTER") == nullptr) {
+        const int C = 4, CPT = 2, VPT = 4;
+        const int nt = ((n_checks + C - 1) / C + CPT - 1) / CPT;
+        const int NT = (nt + 31) / 32 * 32;
+        if (admm::cluster_supported(6, 3, C, CPT, VPT) && NT <= 1024 && n_vars <= C * NT * VPT) {
+          long long pm = 20000000, bm = 20000000;
+          if (const char* e = std::getenv("ADMM_B200_CLUSTER_MOVES")) pm = bm = std::atoll(e);
+          const admm::ClusterLayout CL =
+              admm::build_cluster_layout(rows, n_vars, 6, 3, C, NT, CPT, VPT, pm, bm, 4242);
+          if (dbg)
+            std::fprintf(stderr, "[admm] cluster layout ok=%d %s NPL=%d NIN=%d ghosts=%lld bank %.0f->%.0f\n", (int)CL.ok,
+                         CL.error.c_str(), CL.NPL, CL.NIN, CL.ghost_total, CL.bank_cost_before, CL.bank_cost_after);
+          if (CL.ok) {
+            const int smem = admm::cluster_smem_bytes(CL.NPL, 3, CL.NIN, CL.NXS, CL.NMS);
+            int clusters = 0, regs = 0;
+            if (smem <= smem_optin && admm::cluster_query(NT, smem, &clusters, &regs) == cudaSuccess && clusters > 0) {
+              // packed exchange tables: src | dst << 15 | rank << 30
+              std::vector<uint32_t> xs((size_t)C * CL.NXS, 0), ms((size_t)C * CL.NMS, 0);
+              for (int p = 0; p < C; ++p) {
+                for (int r = 0; r < C; ++r)
+                  for (int i = CL.xs_start[p * (C + 1) + r]; i < CL.xs_start[p * (C + 1) + r + 1]; ++i) {
+                    const uint32_t dst = CL.gbase[r * C + p] + (i - CL.xs_start[p * (C + 1) + r]);
+                    xs[(size_t)p * CL.NXS + i] = CL.xsend[(size_t)p * CL.NXS + i] | (dst << 15) | ((uint32_t)r << 30);
+                  }
+                for (int o = 0; o < C; ++o)
+                  for (int i = CL.ms_start[p * (C + 1) + o]; i < CL.ms_start[p * (C + 1) + o + 1]; ++i) {
+                    const uint32_t dst = CL.ibase[o * C + p] + (i - CL.ms_start[p * (C + 1) + o]);
+                    ms[(size_t)p * CL.NMS + i] = CL.msend[(size_t)p * CL.NMS + i] | (dst << 15) | ((uint32_t)o << 30);
+                  }
+                g->cl_n_xs[p] = CL.xs_start[p * (C + 1) + C];
+                g->cl_n_ms[p] = CL.ms_start[p * (C + 1) + C];
+                g->cl_n_in[p] = CL.n_in[p];
+              }
+              auto upc = [&](void** dst, const void* src, size_t bytes) -> bool {
+                if (cudaMalloc(dst, bytes) != cudaSuccess) return false;
+                return cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
+              };
+              const bool up_ok =
+                  upc((void**)&g->cl_chk_slot, CL.chk_slot.data(), CL.chk_slot.size() * sizeof(int)) &&
+                  upc((void**)&g->cl_chk_orig, CL.chk_orig.data(), CL.chk_orig.size() * sizeof(int)) &&
+                  upc((void**)&g->cl_own_var, CL.own_var.data(), CL.own_var.size() * sizeof(int)) &&
+                  upc((void**)&g->cl_xsend, xs.data(), xs.size() * sizeof(uint32_t)) &&
+                  upc((void**)&g->cl_msend, ms.data(), ms.size() * sizeof(uint32_t)) &&
+                  upc((void**)&g->cl_scatter, CL.scatter.data(), CL.scatter.size() * sizeof(uint16_t));
+              if (up_ok) {
+                g->cluster_ok = true;
+                g->C = C;
+                g->cl_nt = NT;
+                g->cl_smem = smem;
+                g->cl_clusters = clusters;
+                g->cl_regs = regs;
+                g->cl_NPL = CL.NPL;
+                g->cl_NIN = CL.NIN;
+                g->cl_NXS = CL.NXS;
+                g->cl_NMS = CL.NMS;
+                g->cl_MC = CL.MC;
+                g->cl_NO = CL.NO;
+                g->cl_exchange = CL.ghost_total + CL.inbox_total;
+              }
+            }
+          }
+          cudaGetLastError();
+        }
+      }
+      if (engine == ADMM_ENGINE_CLUSTER && !g->cluster_ok) {
+        admm_graph_destroy(g);
+        return fail(ADMM_E_UNSUPPORTED, "no cluster engine for this graph ((3,6)-regular codes beyond one SM)");
       }
       g->kind = 3;
       g->CPT = 1;
@@ -556,6 +642,12 @@ int admm_graph_destroy(admm_graph* g) {
   cudaFree(g->check_ptr_d);
   cudaFree(g->var_edge);
   cudaFree(g->wctbl);
+  cudaFree(g->cl_chk_slot);
+  cudaFree(g->cl_chk_orig);
+  cudaFree(g->cl_own_var);
+  cudaFree(g->cl_xsend);
+  cudaFree(g->cl_msend);
+  cudaFree(g->cl_scatter);
   cudaFree(g->wvtbl);
   cudaFree(g->var_orig);
   cudaFree(g->edge_ref);
@@ -588,7 +680,12 @@ int admm_graph_get_info(const admm_graph* g, admm_graph_info* info) {
   info->smem_bytes_f64 = st ? 0 : g->launch[1].smem;
   info->regs_f32 = st ? g->slaunch[0].regs : g->launch[0].regs;
   info->regs_f64 = st ? g->slaunch[1].regs : g->launch[1].regs;
-  info->cluster_size = g->C;
+  info->cluster_size = g->cluster_ok ? g->C : 0;
+  info->cluster_active = g->cl_clusters;
+  info->cluster_threads = g->cl_nt;
+  info->cluster_smem = g->cl_smem;
+  info->cluster_regs = g->cl_regs;
+  info->cluster_exchange = g->cl_exchange;
   info->layout_cost_before = g->layout_cost[0];
   info->layout_cost_after = g->layout_cost[1];
   info->num_sms = g->num_sms;
@@ -626,6 +723,13 @@ bool use_wide(const admm_graph* g, int dtype, int64_t batch) {
   return batch >= min_batch;
 }
 
+// Cluster engine for this call?  fp32 on graphs that placed it, unless the
+// caller forced the streaming kernels.
+bool use_cluster(const admm_graph* g, int dtype, int64_t /*batch*/) {
+  if (g->kind != 3 || !g->cluster_ok || dtype != ADMM_F32) return false;
+  return g->engine_req == ADMM_ENGINE_AUTO || g->engine_req == ADMM_ENGINE_CLUSTER;
+}
+
 // Slots of the wide kernel: a multiple of the stripe width, up to 8192
 // (ADMM_B200_WIDE_SLOTS overrides), no more than the batch needs.
 int wide_slots(const admm_graph* g, int dtype, int64_t batch) {
@@ -658,6 +762,7 @@ int stream_slots(const admm_graph* g, int dtype, int64_t batch) {
 int admm_decode_kernel(const admm_graph* g, int dtype, int64_t batch) {
   if (!g) return fail(ADMM_E_ARG, "null graph");
   if (dtype != ADMM_F32 && dtype != ADMM_F64) return fail(ADMM_E_ARG, "dtype must be ADMM_F32 or ADMM_F64");
+  if (g->kind == 3 && use_cluster(g, dtype, batch)) return ADMM_KERNEL_CLUSTER;
   if (g->kind == 3 && use_wide(g, dtype, batch)) return ADMM_KERNEL_WIDE;
   return g->kind;
 }
@@ -666,6 +771,7 @@ size_t admm_workspace_bytes(const admm_graph* g, int dtype, int64_t batch) {
   if (!g) return 0;
   if (g->kind == 3) {
     if (dtype < 0 || dtype > 1) return 0;
+    if (use_cluster(g, dtype, batch)) return 256;  // the frame queue counter (padded)
     if (use_wide(g, dtype, batch)) {
       const int S = wide_slots(g, dtype, batch);
       // upper bound: the synthesis buffer is only laid out for admm_decode_synth
@@ -739,6 +845,55 @@ int decode_impl(const admm_graph* g, int dtype, int64_t batch, const void* gamma
   DeviceGuard guard(g->device);
   ADMM_CUDA(guard.error());
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (g->kind == 3 && g->engine_req == ADMM_ENGINE_CLUSTER && dtype != ADMM_F32)
+    return fail(ADMM_E_UNSUPPORTED, "the cluster engine is fp32 only (fp64 runs on the streaming engine)");
+  if (g->kind == 3 && use_cluster(g, dtype, batch)) {
+    if (z_in || z_out) return fail(ADMM_E_UNSUPPORTED, "state input/output is not supported by the cluster engine");
+    ADMM_CUDA(cudaMemsetAsync(workspace, 0, sizeof(int), st));
+    admm::ClusterParams cp{};
+    cp.chk_slot = g->cl_chk_slot;
+    cp.chk_orig = g->cl_chk_orig;
+    cp.own_var = g->cl_own_var;
+    cp.xsend = g->cl_xsend;
+    cp.msend = g->cl_msend;
+    cp.scatter = g->cl_scatter;
+    cp.NPL = g->cl_NPL;
+    cp.NIN = g->cl_NIN;
+    cp.NXS = g->cl_NXS;
+    cp.NMS = g->cl_NMS;
+    cp.MC = g->cl_MC;
+    cp.NO = g->cl_NO;
+    for (int r = 0; r < admm::kClusterMax; ++r) {
+      cp.n_xs[r] = g->cl_n_xs[r];
+      cp.n_ms[r] = g->cl_n_ms[r];
+      cp.n_in[r] = g->cl_n_in[r];
+    }
+    cp.n_vars = g->n_vars;
+    cp.n_checks = g->n_checks;
+    cp.batch = batch;
+    cp.gamma = static_cast<const float*>(gamma);
+    cp.ld_gamma = ld_gamma;
+    cp.mu = static_cast<float>(mu);
+    cp.rho = static_cast<float>(rho);
+    cp.one_minus_rho = static_cast<float>(1.0 - rho);
+    const double thr = epsilon * epsilon * (double)g->n_edges;  // admm_decoder.py:169
+    cp.thr = admm::thr_round_up<float>(thr);
+    cp.thr_d = thr;
+    cp.t_max = t_max;
+    cp.x_out = static_cast<float*>(x_out);
+    cp.ld_x = ld_x;
+    cp.hard_out = hard_out;
+    cp.ld_hard = ld_hard;
+    cp.iters_out = iters_out;
+    cp.flags_out = flags_out;
+    cp.weight_out = weight_out;
+    cp.queue = reinterpret_cast<int*>(workspace);
+    cp.synth = synth;
+    const int clusters = (int)std::min<long long>(batch, g->cl_clusters);
+    const cudaError_t le = admm::cluster_launch(cp, clusters, g->cl_nt, g->cl_smem, st);
+    if (le != cudaSuccess) return cuda_fail(le, "cluster kernel launch");
+    return ADMM_OK;
+  }
   if (g->kind == 3) {
     if (z_in || z_out) return fail(ADMM_E_UNSUPPORTED, "state input/output is not supported by the streaming engine");
     const double thr = epsilon * epsilon * (double)g->n_edges;  // admm_decoder.py:169

@@ -1,0 +1,362 @@
+// Cluster engine: one thread-block CLUSTER of C CTAs decodes one frame of a
+// code too large for one SM (BASELINE config 5, n = 16384: C = 4 CTAs of
+// 1024 threads, one per SM), with every byte of the frame's decoder state on
+// chip.  fp32 (throughput mode) only; fp64 stays on the streaming engines.
+//
+// Layout (cluster_layout.h): CTA p owns M/C checks and N/C variables; the
+// variables its checks touch but other CTAs own are GHOSTS with local slots.
+// Per CTA and iteration, exactly the resident kernel's work
+// (resident_regular.cuh, colored layout, packed fp32 pairs) plus two
+// table-driven exchanges over DSMEM, each a warp-coalesced copy into
+// CONSECUTIVE words of the destination (~20-25 B/cycle; scattered 4-byte
+// remote accesses cost ~2.6 cycles each, tools/micro/dsmem.cu):
+//
+//   scatter-in  inbox -> message rows of own variables        (local)
+//   variable    x = clip((sum_j msg_j - gamma/mu) / DV) of own variables
+//   x-send      own x -> ghost slots of the CTAs holding them  (DSMEM)
+//   -- cluster barrier A --
+//   check       gather x (own + ghost slots), project, dual update, message
+//               to msg[color][slot(v)] (own rows, or ghost rows)
+//   msg-send    ghost-row messages -> owners' inboxes            (DSMEM)
+//               stop-rule header {flag, exact sums} -> every CTA
+//   -- cluster barrier B --
+//   decision    every thread reads the C headers: uniform, deterministic
+//
+// Stop rule (admm_decoder.py:169,174-181): each CTA forms its partials as the
+// resident kernel does; when no partial reaches eps^2 E it also forms the
+// CTA's exact sums in fp64; the frame converged iff every CTA's flag is clear
+// and the fp64 sum of the C CTA sums (rank order) is below the threshold.
+// Frames are pulled from a global queue by CTA 0 and broadcast to the
+// cluster; the outputs (make_output, is_codeword) are reduced into CTA 0.
+#pragma once
+
+#include "resident_regular.cuh"
+#include "synth.cuh"
+
+namespace admm {
+
+constexpr int kClusterMax = 4;
+
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cl_mapa(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cl_st(uint32_t a, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void cl_st_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void cl_st_f64(uint32_t a, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void cl_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+
+struct ClusterParams {
+  // graph (cluster_layout.h), per-part arrays flattened [C][...]
+  const int* chk_slot;   // [C][D][MC]
+  const int* chk_orig;   // [C][MC] original check (-1: idle slot)
+  const int* own_var;    // [C][NO]
+  const uint32_t* xsend; // [C][NXS] src slot | dst word << 15 | dst rank << 30
+  const uint32_t* msend; // [C][NMS] src word | dst inbox index << 15 | dst rank << 30
+  const uint16_t* scatter;  // [C][NIN] message-row word of inbox entry i
+  int NPL, NIN, NXS, NMS, MC, NO;
+  int n_xs[kClusterMax], n_ms[kClusterMax], n_in[kClusterMax];
+  int n_vars, n_checks;
+  // frames
+  long long batch;
+  const float* gamma;
+  long long ld_gamma;
+  float mu, rho, one_minus_rho, thr;  // thr: eps^2 E rounded up to fp32 (early-out)
+  double thr_d;                       // eps^2 E
+  int t_max;
+  float* x_out;
+  long long ld_x;
+  uint8_t* hard_out;
+  long long ld_hard;
+  int* iters_out;
+  uint8_t* flags_out;
+  int* weight_out;
+  int* queue;
+  SynthParams synth;
+};
+
+// Shared memory (bytes): X | MSG[DV] | GM (each NPL fp32) | inbox[NIN] fp32 |
+// xsend[NXS] u32 | msend[NMS] u32 | scatter[NIN] u16 | header | misc.
+struct ClusterSmem {
+  int x, inbox, xs, ms, sc, hdr, misc, total;
+  __host__ __device__ ClusterSmem(int NPL, int DV, int NIN, int NXS, int NMS) {
+    x = 0;
+    inbox = 4 * NPL * (DV + 2);
+    xs = inbox + 4 * NIN;
+    ms = xs + 4 * NXS;
+    sc = ms + 4 * NMS;
+    hdr = (sc + 2 * NIN + 15) & ~15;   // [kClusterMax] {double primal, double moved}, then int flags
+    misc = hdr + kClusterMax * 16 + 16;  // ints: frame, weight, nonint, odd, ... + per-CTA output slots
+    total = misc + 4 * (8 + 3 * kClusterMax) + 64 * 8;  // + fp64 block-reduction slots
+  }
+};
+
+template <int D, int DV, int CPT, int VPT, int C>
+__global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(1024, 1) cluster_decode_kernel(const ClusterParams p) {
+  static_assert(D % DV == 0 && D % 2 == 0 && VPT % 2 == 0, "cluster engine: colored fp32 layout");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int NPL = p.NPL;
+  const ClusterSmem L(NPL, DV, p.NIN, p.NXS, p.NMS);
+  const uint32_t rank = cl_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NT = blockDim.x, nwarps = NT >> 5;
+  const uint32_t base_a = smem_u32(smem_raw);
+  const uint32_t xs_a = base_a + L.x;          // X[NPL]; MSG[j] at +4 NPL (j + 1); GM at +4 NPL (DV + 1)
+  const uint32_t inbox_a = base_a + L.inbox;
+  const uint32_t mstride = 4u * NPL, moff0 = mstride, gmoff = mstride * (DV + 1);
+  double* hsum = reinterpret_cast<double*>(smem_raw + L.hdr);             // [C][2]
+  int* hflag = reinterpret_cast<int*>(smem_raw + L.hdr + kClusterMax * 16);  // [C]
+  int* misc = reinterpret_cast<int*>(smem_raw + L.misc);                  // [0] frame [1] weight
+  int* outslot = misc + 8;                                                // [C][3] integral, weight, odd
+  double* red = reinterpret_cast<double*>(smem_raw + L.misc + 4 * (8 + 3 * kClusterMax));
+
+  // ---- per-part tables into shared memory (once per CTA) ----
+  {
+    const uint32_t* gx = p.xsend + static_cast<size_t>(rank) * p.NXS;
+    const uint32_t* gms = p.msend + static_cast<size_t>(rank) * p.NMS;
+    const uint16_t* gsc = p.scatter + static_cast<size_t>(rank) * p.NIN;
+    uint32_t* sx = reinterpret_cast<uint32_t*>(smem_raw + L.xs);
+    uint32_t* sm = reinterpret_cast<uint32_t*>(smem_raw + L.ms);
+    uint16_t* ss = reinterpret_cast<uint16_t*>(smem_raw + L.sc);
+    for (int i = tid; i < p.NXS; i += NT) sx[i] = __ldg(gx + i);
+    for (int i = tid; i < p.NMS; i += NT) sm[i] = __ldg(gms + i);
+    for (int i = tid; i < p.NIN; i += NT) ss[i] = __ldg(gsc + i);
+  }
+  const int n_xs = p.n_xs[rank], n_ms = p.n_ms[rank], n_in = p.n_in[rank];
+
+  // ---- per-thread graph registers ----
+  uint32_t xaddr[CPT][D];
+  bool cact[CPT];
+#pragma unroll
+  for (int q = 0; q < CPT; ++q) {
+    const int lc = tid + q * NT;
+    cact[q] = __ldg(p.chk_orig + static_cast<size_t>(rank) * p.MC + lc) >= 0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const int s = __ldg(p.chk_slot + (static_cast<size_t>(rank) * D + k) * p.MC + lc);
+      xaddr[q][k] = xs_a + 4u * s;
+    }
+  }
+  uint32_t xst[VPT];
+  int vorig[VPT];
+#pragma unroll
+  for (int q = 0; q < VPT; ++q) {
+    const int i = 2 * tid + 2 * NT * (q >> 1) + (q & 1);
+    xst[q] = xs_a + 4u * i;
+    vorig[q] = __ldg(p.own_var + static_cast<size_t>(rank) * p.NO + i);
+  }
+  const float2 rho2 = make_float2(p.rho, p.rho), omr2 = make_float2(p.one_minus_rho, p.one_minus_rho);
+  float2 zp[CPT][D / 2], lp[CPT][D / 2];
+
+  // zero the whole local slot space once (ghost / spare slots hold finite values)
+  for (int i = tid; i < NPL * (DV + 2); i += NT) sts(xs_a + 4u * i, 0.f);
+  __syncthreads();
+  cl_barrier();  // every CTA of the cluster is running before any DSMEM access
+
+  for (;;) {
+    if (rank == 0 && tid == 0) {
+      const int f = atomicAdd(p.queue, 1);
+      for (uint32_t r = 0; r < C; ++r) cl_st_u32(cl_mapa(smem_u32(misc), r), static_cast<uint32_t>(f));
+    }
+    cl_barrier();
+    const long long f = static_cast<int>(*reinterpret_cast<volatile int*>(misc));
+    if (f >= p.batch) break;
+
+    // ---- frame setup: gamma/mu of own variables, zero messages and state ----
+#pragma unroll
+    for (int q = 0; q < VPT; ++q) {
+      const float g = vorig[q] >= 0 ? __fdividef(frame_llr<float>(p, f, vorig[q]), p.mu) : 0.f;
+      sts(xst[q] + gmoff, g);
+#pragma unroll
+      for (int j = 0; j < DV; ++j) sts(xst[q] + moff0 + j * mstride, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < CPT; ++q)
+#pragma unroll
+      for (int j = 0; j < D / 2; ++j) {
+        zp[q][j] = make_float2(0.f, 0.f);
+        lp[q][j] = make_float2(0.f, 0.f);
+      }
+    if (tid == 0) misc[1] = 0;
+    __syncthreads();
+
+    int t = 0;
+    bool converged = false;
+    for (;;) {
+      ++t;
+      if (t > 1) {
+        // scatter-in: messages of own variables computed by other CTAs
+        const uint16_t* ss = reinterpret_cast<const uint16_t*>(smem_raw + L.sc);
+        for (int i = tid; i < n_in; i += NT) sts(xs_a + 4u * ss[i], lds(inbox_a + 4u * i, 0.f));
+        __syncthreads();
+      }
+      // ---- x-update of own variables (pairs, color order; admm_decoder.py:108-124) ----
+#pragma unroll
+      for (int h = 0; h < VPT / 2; ++h) {
+        const uint32_t a = xst[2 * h];
+        float2 acc = lds2(a + moff0);
+#pragma unroll
+        for (int j = 1; j < DV; ++j) acc = __fadd2_rn(acc, lds2(a + moff0 + j * mstride));
+        const float2 num = fsub2_rn(acc, lds2(a + gmoff));
+        sts2(a, make_float2(clip01(num.x * (1.f / DV)), clip01(num.y * (1.f / DV))));
+      }
+      __syncthreads();
+      // ---- x-send: own x -> ghost slots of the other CTAs (coalesced per warp) ----
+      {
+        const uint32_t* sx = reinterpret_cast<const uint32_t*>(smem_raw + L.xs);
+        for (int i = tid; i < n_xs; i += NT) {
+          const uint32_t u = sx[i];
+          const float v = lds(xs_a + 4u * (u & 0x7fffu), 0.f);
+          cl_st(cl_mapa(xs_a + 4u * ((u >> 15) & 0x7fffu), u >> 30), v);
+        }
+      }
+      cl_barrier();  // A: ghost x visible; every CTA done with its message rows
+
+      // ---- fused z-update, projection, residuals, dual update (packed fp32) ----
+      float2 pr2 = make_float2(0.f, 0.f), mv2 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) {
+        float2 gx2[D / 2], u2[D / 2];
+#pragma unroll
+        for (int j = 0; j < D / 2; ++j)
+          gx2[j] = make_float2(lds(xaddr[q][2 * j], 0.f), lds(xaddr[q][2 * j + 1], 0.f));
+        float u[D], zn[D];
+#pragma unroll
+        for (int j = 0; j < D / 2; ++j) {
+          u2[j] = __fadd2_rn(__ffma2_rn(rho2, gx2[j], __fmul2_rn(omr2, zp[q][j])), lp[q][j]);
+          u[2 * j] = u2[j].x;
+          u[2 * j + 1] = u2[j].y;
+        }
+        project_pp_fixed<float, D>(u, zn);
+#pragma unroll
+        for (int j = 0; j < D / 2; ++j) {
+          const float2 zn2 = make_float2(zn[2 * j], zn[2 * j + 1]);
+          const float2 r1 = fsub2_rn(gx2[j], zn2);
+          const float2 r2 = fsub2_rn(zn2, zp[q][j]);
+          if (cact[q]) {
+            pr2 = __ffma2_rn(r1, r1, pr2);
+            mv2 = __ffma2_rn(r2, r2, mv2);
+          }
+          const float2 ln = fsub2_rn(u2[j], zn2);  // l' = (w + l) - z' = u - z'
+          const float2 m2 = fsub2_rn(zn2, ln);
+          lp[q][j] = ln;
+          zp[q][j] = zn2;
+          sts(xaddr[q][2 * j] + moff0 + ((2 * j) % DV) * mstride, m2.x);
+          sts(xaddr[q][2 * j + 1] + moff0 + ((2 * j + 1) % DV) * mstride, m2.y);
+        }
+      }
+      const float primal = pr2.x + pr2.y, moved = mv2.x + mv2.y;
+      const int nc = __syncthreads_or(primal >= p.thr || moved >= p.thr);
+      double sa = 0.0, sb = 0.0;
+      if (!nc) {  // exact CTA sums in fp64 (rare: only near convergence)
+        const double wa = warp_allsum(static_cast<double>(primal));
+        const double wb = warp_allsum(static_cast<double>(moved));
+        if (lane == 0) {
+          red[2 * warp] = wa;
+          red[2 * warp + 1] = wb;
+        }
+        __syncthreads();
+        double a = lane < nwarps ? red[2 * lane] : 0.0;
+        double b = lane < nwarps ? red[2 * lane + 1] : 0.0;
+        sa = warp_allsum(a);
+        sb = warp_allsum(b);
+      }
+      // ---- msg-send: ghost-row messages -> owners' inboxes; stop-rule header ----
+      {
+        const uint32_t* sm = reinterpret_cast<const uint32_t*>(smem_raw + L.ms);
+        for (int i = tid; i < n_ms; i += NT) {
+          const uint32_t u = sm[i];
+          const float v = lds(xs_a + 4u * (u & 0x7fffu), 0.f);
+          cl_st(cl_mapa(inbox_a + 4u * ((u >> 15) & 0x7fffu), u >> 30), v);
+        }
+      }
+      if (tid < C) {
+        const uint32_t r = tid;
+        cl_st_f64(cl_mapa(smem_u32(hsum + 2 * rank), r), sa);
+        cl_st_f64(cl_mapa(smem_u32(hsum + 2 * rank + 1), r), sb);
+        cl_st_u32(cl_mapa(smem_u32(hflag + rank), r), static_cast<uint32_t>(nc));
+      }
+      cl_barrier();  // B: inboxes and headers visible
+      bool anync = false;
+      double A = 0.0, B = 0.0;
+#pragma unroll
+      for (int r = 0; r < C; ++r) {
+        anync |= hflag[r] != 0;
+        A += hsum[2 * r];
+        B += hsum[2 * r + 1];
+      }
+      if (!anync && A < p.thr_d && B < p.thr_d) {
+        converged = true;
+        break;
+      }
+      if (t >= p.t_max) break;
+    }
+
+    // ---- outputs (make_output, admm_decoder.py:92-105; is_codeword, codes.py:145-154) ----
+    bool integral = true;
+    int ones = 0;
+#pragma unroll
+    for (int q = 0; q < VPT; ++q) {
+      if (vorig[q] >= 0) {
+        const float xv = lds(xst[q], 0.f);
+        const bool h = xv > 0.5f;
+        ones += h;
+        integral &= fminf(fabsf(xv), fabsf(1.f - xv)) <= 1e-5f;
+        if (p.x_out) p.x_out[f * p.ld_x + vorig[q]] = xv;
+        if (p.hard_out) p.hard_out[f * p.ld_hard + vorig[q]] = h;
+      }
+    }
+    bool odd = false;
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) {
+      int par = 0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) par ^= (lds(xaddr[q][k], 0.f) > 0.5f);
+      odd |= cact[q] && par;
+    }
+    ones = __reduce_add_sync(0xffffffffu, ones);
+    if (lane == 0 && ones) atomicAdd(misc + 1, ones);
+    const int all_integral = __syncthreads_and(integral);
+    const int any_odd = __syncthreads_or(odd);
+    if (tid == 0) {
+      const uint32_t o = cl_mapa(smem_u32(outslot + 3 * rank), 0);
+      cl_st_u32(o, static_cast<uint32_t>(all_integral));
+      cl_st_u32(o + 4, static_cast<uint32_t>(misc[1]));
+      cl_st_u32(o + 8, static_cast<uint32_t>(any_odd));
+    }
+    cl_barrier();
+    if (rank == 0 && tid == 0) {
+      int integ = 1, wt = 0, oddc = 0;
+      for (int r = 0; r < C; ++r) {
+        integ &= outslot[3 * r] != 0;
+        wt += outslot[3 * r + 1];
+        oddc |= outslot[3 * r + 2];
+      }
+      if (p.iters_out) p.iters_out[f] = t;
+      if (p.flags_out)
+        p.flags_out[f] = (converged ? kFlagConverged : 0) | (integ ? kFlagIntegral : 0) | (oddc ? 0 : kFlagCodeword);
+      if (p.weight_out) p.weight_out[f] = wt;
+    }
+  }
+}
+
+}  // namespace admm

@@ -1,0 +1,18 @@
+// Host-side interface of the cluster engine (cluster.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace admm {
+
+struct ClusterParams;
+
+// Compiled shapes: D = 6, DV = 3, C = 4 CTAs per cluster, 2 checks and 4
+// variables per thread (config 5 and other (3,6) codes beyond one SM).
+bool cluster_supported(int D, int DV, int C, int CPT, int VPT);
+int cluster_smem_bytes(int NPL, int DV, int NIN, int NXS, int NMS);
+// Active clusters per GPU for `nt` threads per CTA and `smem` bytes (0 = does not fit).
+cudaError_t cluster_query(int nt, int smem, int* clusters, int* regs);
+cudaError_t cluster_launch(const ClusterParams& p, int clusters, int nt, int smem, cudaStream_t st);
+
+}  // namespace admm
