@@ -164,6 +164,10 @@ int admm_phase_profile(int enable, uint64_t* cycles8);
 /* Same for the wide kernel (wide.cuh): cycles8 = {variable phase, grid sync,
  * check phase, grid sync, slot phase, grid sync, passes, 0} of CTA 0. */
 int admm_wide_phase_profile(int enable, uint64_t* cycles8);
+/* Same for the cluster engine (cluster.cuh): cycles8 = {scatter-in, variable
+ * phase, x-send, cluster barrier A, check phase, msg-send, barrier B +
+ * decision, iterations} of thread 0 of CTA 0. */
+int admm_cluster_phase_profile(int enable, uint64_t* cycles8);
 
 /* Flooding sum-product BP on the same graph handle (the comparison baseline,
  * SURVEY.md 8f #4).  Replaces posterior_llrs / decode_bp

@@ -39,6 +39,7 @@ EXPORTED = (
     "admm_project_batch",
     "admm_phase_profile",
     "admm_wide_phase_profile",
+    "admm_cluster_phase_profile",
     "admm_bp_decode_batch",
     "admm_x_update",
     "admm_z_update",
@@ -120,6 +121,8 @@ def load() -> ctypes.CDLL:
     lib.admm_phase_profile.restype = ctypes.c_int
     lib.admm_wide_phase_profile.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]
     lib.admm_wide_phase_profile.restype = ctypes.c_int
+    lib.admm_cluster_phase_profile.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]
+    lib.admm_cluster_phase_profile.restype = ctypes.c_int
     lib.admm_project_batch.argtypes = [ctypes.c_int, I64, I32, P, P, P]
     lib.admm_project_batch.restype = ctypes.c_int
     lib.admm_bp_decode_batch.argtypes = [

@@ -385,7 +385,9 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
       // Cluster engine (fp32): one 4-CTA cluster per frame, state on chip.
       if ((engine == ADMM_ENGINE_AUTO || engine == ADMM_ENGINE_CLUSTER) && regular && dmax == 6 && dvmax == 3 &&
           std::getenv("ADMM_B200_NO_CLUSTER") == nullptr) {
-        const int C = 4, CPT = 2, VPT = 4;
+        int C = 4;
+        if (const char* e = std::getenv("ADMM_B200_CLUSTER")) C = std::atoi(e);
+        const int CPT = 2, VPT = 4;
         const int nt = ((n_checks + C - 1) / C + CPT - 1) / CPT;
         const int NT = (nt + 31) / 32 * 32;
         if (admm::cluster_supported(6, 3, C, CPT, VPT) && NT <= 1024 && n_vars <= C * NT * VPT) {
@@ -399,19 +401,21 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
           if (CL.ok) {
             const int smem = admm::cluster_smem_bytes(CL.NPL, 3, CL.NIN, CL.NXS, CL.NMS);
             int clusters = 0, regs = 0;
-            if (smem <= smem_optin && admm::cluster_query(NT, smem, &clusters, &regs) == cudaSuccess && clusters > 0) {
+            const bool fits = smem <= smem_optin && CL.NO <= 8192 && (3 + 1) * CL.NPL < 65536 && CL.NPL < 65536 &&
+                              CL.NIN < 8192;  // xs_pack / ms_pack fields
+            if (fits && admm::cluster_query(C, NT, smem, &clusters, &regs) == cudaSuccess && clusters > 0) {
               // packed exchange tables: src | dst << 15 | rank << 30
               std::vector<uint32_t> xs((size_t)C * CL.NXS, 0), ms((size_t)C * CL.NMS, 0);
               for (int p = 0; p < C; ++p) {
                 for (int r = 0; r < C; ++r)
                   for (int i = CL.xs_start[p * (C + 1) + r]; i < CL.xs_start[p * (C + 1) + r + 1]; ++i) {
                     const uint32_t dst = CL.gbase[r * C + p] + (i - CL.xs_start[p * (C + 1) + r]);
-                    xs[(size_t)p * CL.NXS + i] = CL.xsend[(size_t)p * CL.NXS + i] | (dst << 15) | ((uint32_t)r << 30);
+                    xs[(size_t)p * CL.NXS + i] = admm::xs_pack(CL.xsend[(size_t)p * CL.NXS + i], dst, (uint32_t)r);
                   }
                 for (int o = 0; o < C; ++o)
                   for (int i = CL.ms_start[p * (C + 1) + o]; i < CL.ms_start[p * (C + 1) + o + 1]; ++i) {
                     const uint32_t dst = CL.ibase[o * C + p] + (i - CL.ms_start[p * (C + 1) + o]);
-                    ms[(size_t)p * CL.NMS + i] = CL.msend[(size_t)p * CL.NMS + i] | (dst << 15) | ((uint32_t)o << 30);
+                    ms[(size_t)p * CL.NMS + i] = admm::ms_pack(CL.msend[(size_t)p * CL.NMS + i], dst, (uint32_t)o);
                   }
                 g->cl_n_xs[p] = CL.xs_start[p * (C + 1) + C];
                 g->cl_n_ms[p] = CL.ms_start[p * (C + 1) + C];
@@ -890,7 +894,7 @@ int decode_impl(const admm_graph* g, int dtype, int64_t batch, const void* gamma
     cp.queue = reinterpret_cast<int*>(workspace);
     cp.synth = synth;
     const int clusters = (int)std::min<long long>(batch, g->cl_clusters);
-    const cudaError_t le = admm::cluster_launch(cp, clusters, g->cl_nt, g->cl_smem, st);
+    const cudaError_t le = admm::cluster_launch(g->C, cp, clusters, g->cl_nt, g->cl_smem, st);
     if (le != cudaSuccess) return cuda_fail(le, "cluster kernel launch");
     return ADMM_OK;
   }
@@ -1037,6 +1041,12 @@ int admm_phase_profile(int enable, uint64_t* cycles8) {
 int admm_wide_phase_profile(int enable, uint64_t* cycles8) {
   if (!admm::wide_phase_profile(enable, reinterpret_cast<unsigned long long*>(cycles8)))
     return fail(ADMM_E_CUDA, "wide phase profile: CUDA error");
+  return ADMM_OK;
+}
+
+int admm_cluster_phase_profile(int enable, uint64_t* cycles8) {
+  if (!admm::cluster_phase_profile(enable, reinterpret_cast<unsigned long long*>(cycles8)))
+    return fail(ADMM_E_CUDA, "cluster phase profile: CUDA error");
   return ADMM_OK;
 }
 

@@ -35,7 +35,13 @@
 
 namespace admm {
 
-constexpr int kClusterMax = 4;
+constexpr int kClusterMax = 8;
+
+// Packed exchange-table entries (cluster_layout.h / abi.cu):
+//   x-send   own slot (13 bits) | ghost slot in the destination (16) << 13 | rank (3) << 29
+//   msg-send message word (16)  | inbox index in the destination (13) << 16 | rank (3) << 29
+__host__ __device__ constexpr uint32_t xs_pack(uint32_t src, uint32_t dst, uint32_t r) { return src | dst << 13 | r << 29; }
+__host__ __device__ constexpr uint32_t ms_pack(uint32_t src, uint32_t dst, uint32_t r) { return src | dst << 16 | r << 29; }
 
 __device__ __forceinline__ uint32_t cl_rank() {
   uint32_t r;
@@ -70,8 +76,8 @@ struct ClusterParams {
   const int* chk_slot;   // [C][D][MC]
   const int* chk_orig;   // [C][MC] original check (-1: idle slot)
   const int* own_var;    // [C][NO]
-  const uint32_t* xsend; // [C][NXS] src slot | dst word << 15 | dst rank << 30
-  const uint32_t* msend; // [C][NMS] src word | dst inbox index << 15 | dst rank << 30
+  const uint32_t* xsend; // [C][NXS] xs_pack(own slot, ghost slot, rank)
+  const uint32_t* msend; // [C][NMS] ms_pack(message word, inbox index, rank)
   const uint16_t* scatter;  // [C][NIN] message-row word of inbox entry i
   int NPL, NIN, NXS, NMS, MC, NO;
   int n_xs[kClusterMax], n_ms[kClusterMax], n_in[kClusterMax];
@@ -110,7 +116,12 @@ struct ClusterSmem {
   }
 };
 
-template <int D, int DV, int CPT, int VPT, int C>
+// Phase profiler (admm_cluster_phase_profile; the PROF instantiation): thread
+// 0 of CTA 0 accumulates clock64() per phase: {scatter-in, variable, x-send,
+// barrier A, check, msg-send, barrier B + decision, iterations}.
+__device__ unsigned long long g_cl_cycles[8];
+
+template <int D, int DV, int CPT, int VPT, int C, bool PROF = false>
 __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(1024, 1) cluster_decode_kernel(const ClusterParams p) {
   static_assert(D % DV == 0 && D % 2 == 0 && VPT % 2 == 0, "cluster engine: colored fp32 layout");
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -166,6 +177,15 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(1024, 1) cluster_dec
   }
   const float2 rho2 = make_float2(p.rho, p.rho), omr2 = make_float2(p.one_minus_rho, p.one_minus_rho);
   float2 zp[CPT][D / 2], lp[CPT][D / 2];
+  const bool prof = PROF && blockIdx.x == 0 && tid == 0;
+  long long tp = 0;
+  auto phase = [&](int k) {
+    if (prof) {
+      const long long t2 = clock64();
+      g_cl_cycles[k] += t2 - tp;
+      tp = t2;
+    }
+  };
 
   // zero the whole local slot space once (ghost / spare slots hold finite values)
   for (int i = tid; i < NPL * (DV + 2); i += NT) sts(xs_a + 4u * i, 0.f);
@@ -201,14 +221,17 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(1024, 1) cluster_dec
 
     int t = 0;
     bool converged = false;
+    if (prof) tp = clock64();
     for (;;) {
       ++t;
+      if (prof) g_cl_cycles[7]++;
       if (t > 1) {
         // scatter-in: messages of own variables computed by other CTAs
         const uint16_t* ss = reinterpret_cast<const uint16_t*>(smem_raw + L.sc);
         for (int i = tid; i < n_in; i += NT) sts(xs_a + 4u * ss[i], lds(inbox_a + 4u * i, 0.f));
         __syncthreads();
       }
+      phase(0);
       // ---- x-update of own variables (pairs, color order; admm_decoder.py:108-124) ----
 #pragma unroll
       for (int h = 0; h < VPT / 2; ++h) {
@@ -220,16 +243,19 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(1024, 1) cluster_dec
         sts2(a, make_float2(clip01(num.x * (1.f / DV)), clip01(num.y * (1.f / DV))));
       }
       __syncthreads();
+      phase(1);
       // ---- x-send: own x -> ghost slots of the other CTAs (coalesced per warp) ----
       {
         const uint32_t* sx = reinterpret_cast<const uint32_t*>(smem_raw + L.xs);
         for (int i = tid; i < n_xs; i += NT) {
           const uint32_t u = sx[i];
-          const float v = lds(xs_a + 4u * (u & 0x7fffu), 0.f);
-          cl_st(cl_mapa(xs_a + 4u * ((u >> 15) & 0x7fffu), u >> 30), v);
+          const float v = lds(xs_a + 4u * (u & 0x1fffu), 0.f);
+          cl_st(cl_mapa(xs_a + 4u * ((u >> 13) & 0xffffu), u >> 29), v);
         }
       }
+      phase(2);
       cl_barrier();  // A: ghost x visible; every CTA done with its message rows
+      phase(3);
 
       // ---- fused z-update, projection, residuals, dual update (packed fp32) ----
       float2 pr2 = make_float2(0.f, 0.f), mv2 = make_float2(0.f, 0.f);
@@ -280,13 +306,14 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(1024, 1) cluster_dec
         sa = warp_allsum(a);
         sb = warp_allsum(b);
       }
+      phase(4);
       // ---- msg-send: ghost-row messages -> owners' inboxes; stop-rule header ----
       {
         const uint32_t* sm = reinterpret_cast<const uint32_t*>(smem_raw + L.ms);
         for (int i = tid; i < n_ms; i += NT) {
           const uint32_t u = sm[i];
-          const float v = lds(xs_a + 4u * (u & 0x7fffu), 0.f);
-          cl_st(cl_mapa(inbox_a + 4u * ((u >> 15) & 0x7fffu), u >> 30), v);
+          const float v = lds(xs_a + 4u * (u & 0xffffu), 0.f);
+          cl_st(cl_mapa(inbox_a + 4u * ((u >> 16) & 0x1fffu), u >> 29), v);
         }
       }
       if (tid < C) {
@@ -295,6 +322,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(1024, 1) cluster_dec
         cl_st_f64(cl_mapa(smem_u32(hsum + 2 * rank + 1), r), sb);
         cl_st_u32(cl_mapa(smem_u32(hflag + rank), r), static_cast<uint32_t>(nc));
       }
+      phase(5);
       cl_barrier();  // B: inboxes and headers visible
       bool anync = false;
       double A = 0.0, B = 0.0;
@@ -304,6 +332,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(1024, 1) cluster_dec
         A += hsum[2 * r];
         B += hsum[2 * r + 1];
       }
+      phase(6);
       if (!anync && A < p.thr_d && B < p.thr_d) {
         converged = true;
         break;

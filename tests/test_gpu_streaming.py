@@ -274,3 +274,40 @@ def test_wide_irregular_code_multi_stripe_matches_sharded(cuda_ok, n, m, batch):
     assert torch.equal(w.iterations, torch.cat([q.iterations for q in parts]))
     assert torch.equal(w.flags, torch.cat([q.flags for q in parts]))
     assert torch.equal(w.weight, torch.cat([q.weight for q in parts]))
+
+
+def test_cluster_engine_matches_wide_and_synthesis(cuda_ok):
+    """Cluster engine (fp32, csrc/cluster.cuh) on config 5: identical
+    decisions and iteration counts to the wide HBM kernel on the same
+    synthesised frames (both fp32, same arithmetic per edge), in-kernel
+    synthesis == materialised LLRs, and batch-split invariance."""
+    from paper_1204_0556_b200 import AdmmConfig, Awgn, Bsc, baseline_code, decode_batch, decode_synth, synth_llr
+
+    code = baseline_code("cfg5_n16384")
+    cfg = AdmmConfig(mu=5.0)
+    for k, ch in enumerate((Bsc(0.04), Awgn(2.5, code.design_rate), Awgn(1.5, code.design_rate))):
+        a = decode_synth(code, ch, cfg, seed=3, point=k, trial0=50, batch=300, want_hard=True, engine="cluster")
+        assert a.info["kernel_name"] == "cluster"
+        w = decode_synth(code, ch, cfg, seed=3, point=k, trial0=50, batch=300, want_hard=True, engine="wide")
+        same = (a.hard == w.hard).all(dim=1).float().mean().item()
+        assert same >= 0.99, same
+        assert (a.iterations - w.iterations).abs().float().mean().item() <= 0.05 * max(1.0, w.iterations.float().mean().item())
+        g = synth_llr(code.n_vars, ch, seed=3, point=k, trial0=50, batch=300, dtype=torch.float32)
+        b = decode_batch(g, code, cfg, dtype=torch.float32, want_hard=True, engine="cluster")
+        assert torch.equal(a.hard, b.hard) and torch.equal(a.iterations, b.iterations)
+        assert torch.equal(a.flags, b.flags) and torch.equal(a.weight, b.weight)
+        c1 = decode_synth(code, ch, cfg, seed=3, point=k, trial0=50, batch=17, engine="cluster")
+        assert torch.equal(c1.iterations, a.iterations[:17])
+
+
+def test_cluster_engine_rejects_fp64_and_state_io(cuda_ok):
+    from paper_1204_0556_b200 import AdmmConfig, baseline_code, decode_batch
+
+    code = baseline_code("cfg5_n16384")
+    g = np.full((2, code.n_vars), 3.0)
+    with pytest.raises(RuntimeError):
+        decode_batch(g, code, AdmmConfig(), dtype=torch.float64, engine="cluster")
+    with pytest.raises(RuntimeError):
+        decode_batch(g, code, AdmmConfig(), dtype=torch.float32, want_state=True, engine="cluster")
+    r = decode_batch(g, code, AdmmConfig(), dtype=torch.float64)  # auto: fp64 on the streaming engine
+    assert r.info["kernel_name"] in ("sharded", "wide") and bool(r.converged.all())

@@ -13,8 +13,10 @@ trial=t), simulator.py:169-173), regenerated bit-identically on the host.
   (the two-sample binomial tolerance of the reference's acceptance suite,
   tests/test_acceptance.py:242-244).
 
-Config 5 runs on every engine a call can reach at n = 16384: the sharded
-kernel (batches below 1024 frames) and the wide HBM-streaming kernel.
+Config 5 runs on every engine a call can reach at n = 16384: the cluster
+engine (fp32 default; one 4-CTA cluster per frame), the sharded kernel
+(fp64 below 1024 frames, or engine="streaming") and the wide HBM-streaming
+kernel.
 """
 from pathlib import Path
 
@@ -46,8 +48,13 @@ def _case(name):
     return _CACHE[name]
 
 
-def _engines(name):
-    return ["auto", "wide"] if "cfg5" in name else ["auto"]
+ENGINES = ["auto", "streaming", "wide", "cluster"]
+
+
+def _engines(name, dtype):
+    if "cfg5" not in name:
+        return ["auto"]
+    return ENGINES if dtype == torch.float32 else ["auto", "streaming", "wide"]  # the cluster engine is fp32 only
 
 
 def _decode(name, dtype, engine):
@@ -64,9 +71,9 @@ def test_fixtures_present():
 
 
 @pytest.mark.parametrize("name", FIXTURES)
-@pytest.mark.parametrize("engine", ["auto", "wide"])
+@pytest.mark.parametrize("engine", ENGINES)
 def test_f64_sweep_endpoint_matches_reference(cuda_ok, name, engine):
-    if engine not in _engines(name):
+    if engine not in _engines(name, torch.float64):
         pytest.skip("one engine for codes that fit one SM")
     f, code, gam, cfg, want = _case(name)
     res = _decode(name, torch.float64, engine)
@@ -89,13 +96,18 @@ def _two_se(a, b, n):
 
 
 @pytest.mark.parametrize("name", FIXTURES)
-@pytest.mark.parametrize("engine", ["auto", "wide"])
+@pytest.mark.parametrize("engine", ENGINES)
 def test_f32_sweep_endpoint_statistics(cuda_ok, name, engine):
     """fp32: >= 99.9 % identical hard decisions; FER and BER within 2 s.e."""
-    if engine not in _engines(name):
+    if engine not in _engines(name, torch.float32):
         pytest.skip("one engine for codes that fit one SM")
     f, code, gam, cfg, want = _case(name)
     res = _decode(name, torch.float32, engine)
+    want_kernel = {"cluster": "cluster", "wide": "wide", "streaming": "sharded"}.get(engine)
+    if "cfg5" in name and want_kernel:
+        assert res.info["kernel_name"] == want_kernel
+    if "cfg5" in name and engine == "auto":
+        assert res.info["kernel_name"] == "cluster"  # fp32 default beyond one SM
     hard = res.hard.cpu().numpy()
     F, N = hard.shape
     same = (hard == want).all(axis=1)

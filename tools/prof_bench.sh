@@ -13,5 +13,5 @@ python tools/prof_launch.py --workload $WL ${PFR:+--frames $PFR} > $OUT/launch.j
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv \
   python bench.py --workload $WL --frames ${LFR:-16384} --chunk ${LFR:-16384} --steps 1 --warmup 3 --no-e2e --no-cpu \
   > $OUT/ncu_launches.log 2>&1; echo "ncu launches exit $?"
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:$KRE -c 1 -o $OUT/full \
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:$KRE --launch-skip ${NCU_SKIP:-0} -c 1 -o $OUT/full \
   python tools/prof_launch.py --workload $WL ${PFR:+--frames $PFR} > $OUT/ncu_full.log 2>&1; echo "ncu full exit $?"
