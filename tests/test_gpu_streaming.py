@@ -157,7 +157,7 @@ def test_phase_profiler_counts_passes(cuda_ok):
     lib = _lib.load()
     code = baseline_code("cfg5_n16384")
     _lib.check(lib.admm_phase_profile(1, None))
-    r = decode_synth(code, Bsc(0.04), AdmmConfig(mu=5.0), seed=3, batch=64, dtype=torch.float32)
+    r = decode_synth(code, Bsc(0.04), AdmmConfig(mu=5.0), seed=3, batch=64, dtype=torch.float32, engine="streaming")
     torch.cuda.synchronize()
     out = (ctypes.c_uint64 * 8)()
     _lib.check(lib.admm_phase_profile(0, out))
