@@ -388,9 +388,9 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
         int C = 4;
         if (const char* e = std::getenv("ADMM_B200_CLUSTER")) C = std::atoi(e);
         const int CPT = 2, VPT = 4;
-        const int nt = ((n_checks + C - 1) / C + CPT - 1) / CPT;
-        const int NT = (nt + 31) / 32 * 32;
-        if (admm::cluster_supported(6, 3, C, CPT, VPT) && NT <= 1024 && n_vars <= C * NT * VPT) {
+        const int NT = 4096 / std::max(C, 1);  // compiled CTA size (cluster.cu)
+        const int nt_need = ((n_checks + C - 1) / C + CPT - 1) / CPT;
+        if (admm::cluster_supported(6, 3, C, CPT, VPT) && nt_need <= NT && n_vars <= C * NT * VPT) {
           long long pm = 20000000, bm = 20000000;
           if (const char* e = std::getenv("ADMM_B200_CLUSTER_MOVES")) pm = bm = std::atoll(e);
           const admm::ClusterLayout CL =

@@ -2,16 +2,34 @@
 #include "cluster.cuh"
 #include "cluster_launch.h"
 
+#include <cstdlib>
+
 namespace admm {
 
 namespace {
 
 constexpr int kD = 6, kDV = 3, kCPT = 2, kVPT = 4;
 bool g_prof = false;  // launch the profiling instantiation
+const bool g_spread = std::getenv("ADMM_B200_CLUSTER_SPREAD") != nullptr;
 
-const void* kernel_fn(int C) {
-  if (C == 8) return reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, 8>);
-  return reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, 4>);
+// Instantiations: C = 4 CTAs of 1024 threads (one per SM), C = 8 of 512 (two per SM).
+template <int C, bool PROF>
+const void* fn_of() {
+  return reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, C, 4096 / C, PROF>);
+}
+
+const void* kernel_fn(int C) { return C == 8 ? fn_of<8, false>() : fn_of<4, false>(); }
+
+void set_smem_all(int C, int smem) {
+  const void* fns[2];
+  if (C == 8) {
+    fns[0] = reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, 8, 512, false>);
+    fns[1] = reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, 8, 512, true>);
+  } else {
+    fns[0] = reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, 4, 1024, false>);
+    fns[1] = reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, 4, 1024, true>);
+  }
+  for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
 }  // namespace
@@ -22,13 +40,19 @@ bool cluster_supported(int D, int DV, int C, int CPT, int VPT) {
 
 int cluster_smem_bytes(int NPL, int DV, int NIN, int NXS, int NMS) { return ClusterSmem(NPL, DV, NIN, NXS, NMS).total; }
 
+// Spread the CTAs of a cluster over distinct SMs (two CTAs of DIFFERENT
+// clusters then share an SM at C = 8, so one hides the other's barriers).
+cudaLaunchAttributeValue spread_value() {
+  cudaLaunchAttributeValue v{};
+  v.clusterSchedulingPolicyPreference = cudaClusterSchedulingPolicySpread;
+  return v;
+}
+
 cudaError_t cluster_query(int C, int nt, int smem, int* clusters, int* regs) {
   const void* fn = kernel_fn(C);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  for (const void* pf : {reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, 4, true>),
-                         reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, 8, true>)})
-    cudaFuncSetAttribute(pf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  set_smem_all(C, smem);
   cudaFuncAttributes fa{};
   e = cudaFuncGetAttributes(&fa, fn);
   if (e != cudaSuccess) return e;
@@ -41,26 +65,42 @@ cudaError_t cluster_query(int C, int nt, int smem, int* clusters, int* regs) {
   cfg.gridDim = dim3(C * 64);
   cfg.blockDim = dim3(nt);
   cfg.dynamicSmemBytes = smem;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+  attr[1].val = spread_value();
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = g_spread ? 2 : 1;
   return cudaOccupancyMaxActiveClusters(clusters, fn, &cfg);
 }
 
+template <int C, int NT, bool PROF>
+cudaError_t launch_t(const ClusterParams& p, int clusters, int smem, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(clusters * C);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  int na = 0;
+  if (g_spread) {
+    attr[0].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+    attr[0].val = spread_value();
+    na = 1;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, cluster_decode_kernel<kD, kDV, kCPT, kVPT, C, NT, PROF>, p);
+}
+
 cudaError_t cluster_launch(int C, const ClusterParams& p, int clusters, int nt, int smem, cudaStream_t st) {
-  if (C == 8 && g_prof)
-    cluster_decode_kernel<kD, kDV, kCPT, kVPT, 8, true><<<clusters * 8, nt, smem, st>>>(p);
-  else if (C == 8)
-    cluster_decode_kernel<kD, kDV, kCPT, kVPT, 8><<<clusters * 8, nt, smem, st>>>(p);
-  else if (g_prof)
-    cluster_decode_kernel<kD, kDV, kCPT, kVPT, 4, true><<<clusters * 4, nt, smem, st>>>(p);
-  else
-    cluster_decode_kernel<kD, kDV, kCPT, kVPT, 4><<<clusters * 4, nt, smem, st>>>(p);
-  return cudaGetLastError();
+  if (nt != 4096 / C) return cudaErrorInvalidConfiguration;  // compiled CTA sizes
+  cudaGetLastError();
+  if (C == 8) return g_prof ? launch_t<8, 512, true>(p, clusters, smem, st) : launch_t<8, 512, false>(p, clusters, smem, st);
+  return g_prof ? launch_t<4, 1024, true>(p, clusters, smem, st) : launch_t<4, 1024, false>(p, clusters, smem, st);
 }
 
 bool cluster_phase_profile(int enable, unsigned long long* out8) {

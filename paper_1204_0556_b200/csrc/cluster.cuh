@@ -121,23 +121,21 @@ struct ClusterSmem {
 // barrier A, check, msg-send, barrier B + decision, iterations}.
 __device__ unsigned long long g_cl_cycles[8];
 
-template <int D, int DV, int CPT, int VPT, int C, bool PROF = false>
-__global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(1024, 1) cluster_decode_kernel(const ClusterParams p) {
+template <int D, int DV, int CPT, int VPT, int C, int NT, bool PROF = false>
+__global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) cluster_decode_kernel(const ClusterParams p) {
   static_assert(D % DV == 0 && D % 2 == 0 && VPT % 2 == 0, "cluster engine: colored fp32 layout");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int NPL = p.NPL;
   const ClusterSmem L(NPL, DV, p.NIN, p.NXS, p.NMS);
   const uint32_t rank = cl_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int NT = blockDim.x, nwarps = NT >> 5;
-  const uint32_t base_a = smem_u32(smem_raw);
-  const uint32_t xs_a = base_a + L.x;          // X[NPL]; MSG[j] at +4 NPL (j + 1); GM at +4 NPL (DV + 1)
-  const uint32_t inbox_a = base_a + L.inbox;
-  const uint32_t mstride = 4u * NPL, moff0 = mstride, gmoff = mstride * (DV + 1);
-  double* hsum = reinterpret_cast<double*>(smem_raw + L.hdr);             // [C][2]
+  constexpr int nwarps = NT / 32;
+  const uint32_t xs_a = smem_u32(smem_raw) + L.x;  // X[NPL]; MSG[j] at +4 NPL (j + 1); GM at +4 NPL (DV + 1)
+  const uint32_t mstride = 4u * NPL;
+  double* hsum = reinterpret_cast<double*>(smem_raw + L.hdr);                // [C][2]
   int* hflag = reinterpret_cast<int*>(smem_raw + L.hdr + kClusterMax * 16);  // [C]
-  int* misc = reinterpret_cast<int*>(smem_raw + L.misc);                  // [0] frame [1] weight
-  int* outslot = misc + 8;                                                // [C][3] integral, weight, odd
+  int* misc = reinterpret_cast<int*>(smem_raw + L.misc);                     // [0] frame [1] weight
+  int* outslot = misc + 8;                                                   // [C][3] integral, weight, odd
   double* red = reinterpret_cast<double*>(smem_raw + L.misc + 4 * (8 + 3 * kClusterMax));
 
   // ---- per-part tables into shared memory (once per CTA) ----
@@ -152,29 +150,27 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(1024, 1) cluster_dec
     for (int i = tid; i < p.NMS; i += NT) sm[i] = __ldg(gms + i);
     for (int i = tid; i < p.NIN; i += NT) ss[i] = __ldg(gsc + i);
   }
-  const int n_xs = p.n_xs[rank], n_ms = p.n_ms[rank], n_in = p.n_in[rank];
 
-  // ---- per-thread graph registers ----
+  // ---- per-thread graph registers: checks lc = tid + q NT, own variable
+  // pairs (2 tid + 2 NT h, +1) ----
   uint32_t xaddr[CPT][D];
-  bool cact[CPT];
+  uint32_t cmask = 0;  // bit q: check q active
 #pragma unroll
   for (int q = 0; q < CPT; ++q) {
     const int lc = tid + q * NT;
-    cact[q] = __ldg(p.chk_orig + static_cast<size_t>(rank) * p.MC + lc) >= 0;
+    if (__ldg(p.chk_orig + static_cast<size_t>(rank) * p.MC + lc) >= 0) cmask |= 1u << q;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       const int s = __ldg(p.chk_slot + (static_cast<size_t>(rank) * D + k) * p.MC + lc);
       xaddr[q][k] = xs_a + 4u * s;
     }
   }
-  uint32_t xst[VPT];
-  int vorig[VPT];
-#pragma unroll
-  for (int q = 0; q < VPT; ++q) {
-    const int i = 2 * tid + 2 * NT * (q >> 1) + (q & 1);
-    xst[q] = xs_a + 4u * i;
-    vorig[q] = __ldg(p.own_var + static_cast<size_t>(rank) * p.NO + i);
-  }
+  // own slots: xst(q) = xs0 + 4 (2 NT (q >> 1) + (q & 1)) (compile-time offsets)
+  const uint32_t xs0 = xs_a + 8u * tid;
+  const int* own_var = p.own_var + static_cast<size_t>(rank) * p.NO;
+  auto xst = [&](int q) -> uint32_t { return xs0 + 4u * (2 * NT * (q >> 1) + (q & 1)); };
+  auto vorig = [&](int q) -> int { return __ldg(own_var + 2 * tid + 2 * NT * (q >> 1) + (q & 1)); };
+
   const float2 rho2 = make_float2(p.rho, p.rho), omr2 = make_float2(p.one_minus_rho, p.one_minus_rho);
   float2 zp[CPT][D / 2], lp[CPT][D / 2];
   const bool prof = PROF && blockIdx.x == 0 && tid == 0;
@@ -184,6 +180,48 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(1024, 1) cluster_dec
       const long long t2 = clock64();
       g_cl_cycles[k] += t2 - tp;
       tp = t2;
+    }
+  };
+
+  // x-update of own pair h (admm_decoder.py:108-124; colors summed in order)
+  auto var_pair = [&](int h) {
+    const uint32_t a = xst(2 * h);
+    float2 acc = lds2(a + mstride);
+#pragma unroll
+    for (int j = 1; j < DV; ++j) acc = __fadd2_rn(acc, lds2(a + mstride * (j + 1)));
+    const float2 num = fsub2_rn(acc, lds2(a + mstride * (DV + 1)));
+    sts2(a, make_float2(clip01(num.x * (1.f / DV)), clip01(num.y * (1.f / DV))));
+  };
+  // fused z-update, projection, residuals, dual update of check q (packed fp32)
+  float2 pr2, mv2;
+  auto check = [&](int q) {
+    float2 gx2[D / 2], u2[D / 2];
+#pragma unroll
+    for (int j = 0; j < D / 2; ++j) gx2[j] = make_float2(lds(xaddr[q][2 * j], 0.f), lds(xaddr[q][2 * j + 1], 0.f));
+    float u[D], zn[D];
+#pragma unroll
+    for (int j = 0; j < D / 2; ++j) {
+      u2[j] = __fadd2_rn(__ffma2_rn(rho2, gx2[j], __fmul2_rn(omr2, zp[q][j])), lp[q][j]);
+      u[2 * j] = u2[j].x;
+      u[2 * j + 1] = u2[j].y;
+    }
+    project_pp_fixed<float, D>(u, zn);
+    const bool act = (cmask >> q) & 1u;
+#pragma unroll
+    for (int j = 0; j < D / 2; ++j) {
+      const float2 zn2 = make_float2(zn[2 * j], zn[2 * j + 1]);
+      const float2 r1 = fsub2_rn(gx2[j], zn2);
+      const float2 r2 = fsub2_rn(zn2, zp[q][j]);
+      if (act) {
+        pr2 = __ffma2_rn(r1, r1, pr2);
+        mv2 = __ffma2_rn(r2, r2, mv2);
+      }
+      const float2 ln = fsub2_rn(u2[j], zn2);  // l' = (w + l) - z' = u - z'
+      const float2 m2 = fsub2_rn(zn2, ln);
+      lp[q][j] = ln;
+      zp[q][j] = zn2;
+      sts(xaddr[q][2 * j] + mstride * (1 + (2 * j) % DV), m2.x);
+      sts(xaddr[q][2 * j + 1] + mstride * (1 + (2 * j + 1) % DV), m2.y);
     }
   };
 
@@ -204,10 +242,11 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(1024, 1) cluster_dec
     // ---- frame setup: gamma/mu of own variables, zero messages and state ----
 #pragma unroll
     for (int q = 0; q < VPT; ++q) {
-      const float g = vorig[q] >= 0 ? __fdividef(frame_llr<float>(p, f, vorig[q]), p.mu) : 0.f;
-      sts(xst[q] + gmoff, g);
+      const int v = vorig(q);
+      const float g = v >= 0 ? __fdividef(frame_llr<float>(p, f, v), p.mu) : 0.f;
+      sts(xst(q) + mstride * (DV + 1), g);
 #pragma unroll
-      for (int j = 0; j < DV; ++j) sts(xst[q] + moff0 + j * mstride, 0.f);
+      for (int j = 0; j < DV; ++j) sts(xst(q) + mstride * (j + 1), 0.f);
     }
 #pragma unroll
     for (int q = 0; q < CPT; ++q)
@@ -228,68 +267,34 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(1024, 1) cluster_dec
       if (t > 1) {
         // scatter-in: messages of own variables computed by other CTAs
         const uint16_t* ss = reinterpret_cast<const uint16_t*>(smem_raw + L.sc);
-        for (int i = tid; i < n_in; i += NT) sts(xs_a + 4u * ss[i], lds(inbox_a + 4u * i, 0.f));
+        const uint32_t inbox_a = smem_u32(smem_raw) + L.inbox;
+        for (int i = tid; i < p.n_in[rank]; i += NT) sts(xs_a + 4u * ss[i], lds(inbox_a + 4u * i, 0.f));
         __syncthreads();
       }
       phase(0);
-      // ---- x-update of own variables (pairs, color order; admm_decoder.py:108-124) ----
+      // ---- x-update of the own variables ----
 #pragma unroll
-      for (int h = 0; h < VPT / 2; ++h) {
-        const uint32_t a = xst[2 * h];
-        float2 acc = lds2(a + moff0);
-#pragma unroll
-        for (int j = 1; j < DV; ++j) acc = __fadd2_rn(acc, lds2(a + moff0 + j * mstride));
-        const float2 num = fsub2_rn(acc, lds2(a + gmoff));
-        sts2(a, make_float2(clip01(num.x * (1.f / DV)), clip01(num.y * (1.f / DV))));
-      }
+      for (int h = 0; h < VPT / 2; ++h)
+        var_pair(h);
       __syncthreads();
       phase(1);
       // ---- x-send: own x -> ghost slots of the other CTAs (coalesced per warp) ----
       {
         const uint32_t* sx = reinterpret_cast<const uint32_t*>(smem_raw + L.xs);
-        for (int i = tid; i < n_xs; i += NT) {
+        for (int i = tid; i < p.n_xs[rank]; i += NT) {
           const uint32_t u = sx[i];
           const float v = lds(xs_a + 4u * (u & 0x1fffu), 0.f);
           cl_st(cl_mapa(xs_a + 4u * ((u >> 13) & 0xffffu), u >> 29), v);
         }
       }
+      pr2 = make_float2(0.f, 0.f);
+      mv2 = make_float2(0.f, 0.f);
       phase(2);
       cl_barrier();  // A: ghost x visible; every CTA done with its message rows
       phase(3);
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) check(q);
 
-      // ---- fused z-update, projection, residuals, dual update (packed fp32) ----
-      float2 pr2 = make_float2(0.f, 0.f), mv2 = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int q = 0; q < CPT; ++q) {
-        float2 gx2[D / 2], u2[D / 2];
-#pragma unroll
-        for (int j = 0; j < D / 2; ++j)
-          gx2[j] = make_float2(lds(xaddr[q][2 * j], 0.f), lds(xaddr[q][2 * j + 1], 0.f));
-        float u[D], zn[D];
-#pragma unroll
-        for (int j = 0; j < D / 2; ++j) {
-          u2[j] = __fadd2_rn(__ffma2_rn(rho2, gx2[j], __fmul2_rn(omr2, zp[q][j])), lp[q][j]);
-          u[2 * j] = u2[j].x;
-          u[2 * j + 1] = u2[j].y;
-        }
-        project_pp_fixed<float, D>(u, zn);
-#pragma unroll
-        for (int j = 0; j < D / 2; ++j) {
-          const float2 zn2 = make_float2(zn[2 * j], zn[2 * j + 1]);
-          const float2 r1 = fsub2_rn(gx2[j], zn2);
-          const float2 r2 = fsub2_rn(zn2, zp[q][j]);
-          if (cact[q]) {
-            pr2 = __ffma2_rn(r1, r1, pr2);
-            mv2 = __ffma2_rn(r2, r2, mv2);
-          }
-          const float2 ln = fsub2_rn(u2[j], zn2);  // l' = (w + l) - z' = u - z'
-          const float2 m2 = fsub2_rn(zn2, ln);
-          lp[q][j] = ln;
-          zp[q][j] = zn2;
-          sts(xaddr[q][2 * j] + moff0 + ((2 * j) % DV) * mstride, m2.x);
-          sts(xaddr[q][2 * j + 1] + moff0 + ((2 * j + 1) % DV) * mstride, m2.y);
-        }
-      }
       const float primal = pr2.x + pr2.y, moved = mv2.x + mv2.y;
       const int nc = __syncthreads_or(primal >= p.thr || moved >= p.thr);
       double sa = 0.0, sb = 0.0;
@@ -301,8 +306,8 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(1024, 1) cluster_dec
           red[2 * warp + 1] = wb;
         }
         __syncthreads();
-        double a = lane < nwarps ? red[2 * lane] : 0.0;
-        double b = lane < nwarps ? red[2 * lane + 1] : 0.0;
+        const double a = lane < nwarps ? red[2 * lane] : 0.0;
+        const double b = lane < nwarps ? red[2 * lane + 1] : 0.0;
         sa = warp_allsum(a);
         sb = warp_allsum(b);
       }
@@ -310,7 +315,8 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(1024, 1) cluster_dec
       // ---- msg-send: ghost-row messages -> owners' inboxes; stop-rule header ----
       {
         const uint32_t* sm = reinterpret_cast<const uint32_t*>(smem_raw + L.ms);
-        for (int i = tid; i < n_ms; i += NT) {
+        const uint32_t inbox_a = smem_u32(smem_raw) + L.inbox;
+        for (int i = tid; i < p.n_ms[rank]; i += NT) {
           const uint32_t u = sm[i];
           const float v = lds(xs_a + 4u * (u & 0xffffu), 0.f);
           cl_st(cl_mapa(inbox_a + 4u * ((u >> 16) & 0x1fffu), u >> 29), v);
@@ -345,13 +351,14 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(1024, 1) cluster_dec
     int ones = 0;
 #pragma unroll
     for (int q = 0; q < VPT; ++q) {
-      if (vorig[q] >= 0) {
-        const float xv = lds(xst[q], 0.f);
+      const int v = vorig(q);
+      if (v >= 0) {
+        const float xv = lds(xst(q), 0.f);
         const bool h = xv > 0.5f;
         ones += h;
         integral &= fminf(fabsf(xv), fabsf(1.f - xv)) <= 1e-5f;
-        if (p.x_out) p.x_out[f * p.ld_x + vorig[q]] = xv;
-        if (p.hard_out) p.hard_out[f * p.ld_hard + vorig[q]] = h;
+        if (p.x_out) p.x_out[f * p.ld_x + v] = xv;
+        if (p.hard_out) p.hard_out[f * p.ld_hard + v] = h;
       }
     }
     bool odd = false;
@@ -360,7 +367,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(1024, 1) cluster_dec
       int par = 0;
 #pragma unroll
       for (int k = 0; k < D; ++k) par ^= (lds(xaddr[q][k], 0.f) > 0.5f);
-      odd |= cact[q] && par;
+      odd |= ((cmask >> q) & 1u) && par;
     }
     ones = __reduce_add_sync(0xffffffffu, ones);
     if (lane == 0 && ones) atomicAdd(misc + 1, ones);

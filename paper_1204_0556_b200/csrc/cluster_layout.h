@@ -188,6 +188,9 @@ struct ClusterLayout {
   std::vector<int> ms_start;        // [C][C+1] msend range of part p for destination o
   std::vector<int> ibase;           // [C][C] ibase[o][p]: first inbox entry of part o filled by part p
   std::vector<int> n_in;            // [C] inbox entries of part p
+  std::vector<int> nb;              // [C] own slots [0, nb) hold the boundary variables; the kernel
+                                    // updates the pairs starting below nb first
+  std::vector<int> nic;             // [C] local check slots [0, nic) hold the interior checks
   std::vector<uint16_t> xsend;      // [C][NXS] own slots whose x goes to ghosts (grouped by destination)
   std::vector<uint16_t> msend;      // [C][NMS] word offsets (j+1)*NPL + ghost slot (grouped by destination)
   std::vector<uint16_t> scatter;    // [C][NIN] word offsets (j+1)*NPL + own slot of the inbox entries
@@ -265,16 +268,50 @@ inline ClusterLayout build_cluster_layout(const std::vector<std::vector<int>>& r
       L.error = "cluster engine: variable ownership does not balance";
       return L;
     }
-  // Local checks of each part, in original order.
+  // A variable is BOUNDARY if it has edges in more than one part (its x is
+  // shipped to ghosts, its owner receives messages); a check is INTERIOR if
+  // none of its variables is a ghost in its part.  Boundary own variables take
+  // the first own slots [0, nb) (nb even: variable pairs), interior checks the
+  // first local check slots [0, nic): the kernel updates boundary variables
+  // first, ships their x, and overlaps the cluster barrier with the interior
+  // variables and checks (cluster.cuh).  (nb may be odd: the pair straddling
+// it is updated with the boundary pairs.)
+  std::vector<char> boundary(n_vars, 0);
+  for (int v = 0; v < n_vars; ++v) {
+    int lam = 0;
+    for (int p = 0; p < C; ++p) lam += cnt[static_cast<size_t>(v) * C + p] > 0;
+    boundary[v] = lam > 1;
+  }
   std::vector<std::vector<int>> pchecks(C);
-  for (int c = 0; c < M; ++c) pchecks[pc[c]].push_back(c);
-  // Own slots: owned variables in index order (the bank annealer permutes them).
+  L.nic.assign(C, 0);
+  for (int pass = 0; pass < 2; ++pass)
+    for (int c = 0; c < M; ++c) {
+      bool interior = true;
+      for (int v : rows[c]) interior &= owner[v] == pc[c];
+      if (interior == (pass == 0)) {
+        pchecks[pc[c]].push_back(c);
+        L.nic[pc[c]] += interior;
+      }
+    }
+  // Own slots: boundary then interior owned variables, in index order (the
+  // bank annealer permutes them inside each class).
   std::vector<std::vector<int>> slot_var(C);  // [p][slot] -> variable (-1 dummy / spare)
   std::vector<std::vector<int>> ghosts_of(C * C);  // [r][o] ghost variables of part r owned by o
+  L.nb.assign(C, 0);
   for (int p = 0; p < C; ++p) slot_var[p].assign(L.NO, -1);
   {
     std::vector<int> fill(C, 0);
-    for (int v = 0; v < n_vars; ++v) slot_var[owner[v]][fill[owner[v]]++] = v;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int v = 0; v < n_vars; ++v)
+        if (boundary[v] == (pass == 0)) slot_var[owner[v]][fill[owner[v]]++] = v;
+      if (pass == 0)
+        for (int p = 0; p < C; ++p) L.nb[p] = fill[p];
+    }
+    for (int p = 0; p < C; ++p)
+      if (fill[p] > L.NO) {
+        L.error = "cluster engine: own slots overflow";
+        return L;
+      }
     for (int v = 0; v < n_vars; ++v)
       for (int r = 0; r < C; ++r)
         if (r != owner[v] && cnt[static_cast<size_t>(v) * C + r] > 0) ghosts_of[r * C + owner[v]].push_back(v);
@@ -361,6 +398,7 @@ inline ClusterLayout build_cluster_layout(const std::vector<std::vector<int>>& r
         if (kind == 0) {
           s1 = static_cast<int>(rng() % L.NO);
           s2 = static_cast<int>(rng() % L.NO);
+          if ((s1 < L.nb[p]) != (s2 < L.nb[p])) continue;  // keep the boundary / interior classes
         } else {
           const int o = static_cast<int>(rng() % C);
           const int n = static_cast<int>(ghosts_of[p * C + o].size());
