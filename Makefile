@@ -20,7 +20,21 @@ $(LIB): $(OBJS)
 $(SRC_DIR)/sortnet.cuh: tools/gen_sortnet.py
 	python tools/gen_sortnet.py
 
-clean:
-	rm -rf $(BUILD) $(LIB)
+# Checked build: bounds checks, asserts and barrier jitter (common.cuh ADMM_CHECKED).
+#   make checked; ADMM_B200_LIB=$(CHECKED_LIB) python -m pytest tests -m gpu
+CHECKED_LIB := paper_1204_0556_b200/libadmm_b200_checked.so
+CHECKED_OBJS := $(patsubst $(BUILD)/%,build_checked/%,$(OBJS))
 
-.PHONY: all clean
+checked: $(CHECKED_LIB)
+
+build_checked/%.o: $(SRC_DIR)/%.cu $(HDRS)
+	@mkdir -p build_checked
+	$(NVCC) $(NVFLAGS) -DADMM_CHECKED -c $< -o $@ > build_checked/$*.ptxas.log 2>&1 || (cat build_checked/$*.ptxas.log; exit 1)
+
+$(CHECKED_LIB): $(CHECKED_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(CHECKED_OBJS) -lcudart
+
+clean:
+	rm -rf $(BUILD) build_checked $(LIB) $(CHECKED_LIB)
+
+.PHONY: all clean checked

@@ -53,6 +53,14 @@ __device__ __forceinline__ uint32_t cl_mapa(uint32_t a, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
   return r;
 }
+// DSMEM address of local shared address `a` in CTA `rank` (checked build:
+// `a` inside the shared window, rank inside the cluster).
+template <int C>
+__device__ __forceinline__ uint32_t cl_addr(uint32_t a, uint32_t rank, uint32_t bytes = 4) {
+  ADMM_CHECK_SMEM(a, bytes);
+  ADMM_ASSERT(rank < static_cast<uint32_t>(C));
+  return cl_mapa(a, rank);
+}
 __device__ __forceinline__ void cl_st(uint32_t a, float v) {
   asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
 }
@@ -233,7 +241,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
   for (;;) {
     if (rank == 0 && tid == 0) {
       const int f = atomicAdd(p.queue, 1);
-      for (uint32_t r = 0; r < C; ++r) cl_st_u32(cl_mapa(smem_u32(misc), r), static_cast<uint32_t>(f));
+      for (uint32_t r = 0; r < C; ++r) cl_st_u32(cl_addr<C>(smem_u32(misc), r), static_cast<uint32_t>(f));
     }
     cl_barrier();
     const long long f = static_cast<int>(*reinterpret_cast<volatile int*>(misc));
@@ -269,6 +277,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
         const uint16_t* ss = reinterpret_cast<const uint16_t*>(smem_raw + L.sc);
         const uint32_t inbox_a = smem_u32(smem_raw) + L.inbox;
         for (int i = tid; i < p.n_in[rank]; i += NT) sts(xs_a + 4u * ss[i], lds(inbox_a + 4u * i, 0.f));
+        ADMM_JITTER();
         __syncthreads();
       }
       phase(0);
@@ -276,6 +285,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
 #pragma unroll
       for (int h = 0; h < VPT / 2; ++h)
         var_pair(h);
+      ADMM_JITTER();
       __syncthreads();
       phase(1);
       // ---- x-send: own x -> ghost slots of the other CTAs (coalesced per warp) ----
@@ -284,18 +294,20 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
         for (int i = tid; i < p.n_xs[rank]; i += NT) {
           const uint32_t u = sx[i];
           const float v = lds(xs_a + 4u * (u & 0x1fffu), 0.f);
-          cl_st(cl_mapa(xs_a + 4u * ((u >> 13) & 0xffffu), u >> 29), v);
+          cl_st(cl_addr<C>(xs_a + 4u * ((u >> 13) & 0xffffu), u >> 29), v);
         }
       }
       pr2 = make_float2(0.f, 0.f);
       mv2 = make_float2(0.f, 0.f);
       phase(2);
+      ADMM_JITTER();
       cl_barrier();  // A: ghost x visible; every CTA done with its message rows
       phase(3);
 #pragma unroll
       for (int q = 0; q < CPT; ++q) check(q);
 
       const float primal = pr2.x + pr2.y, moved = mv2.x + mv2.y;
+      ADMM_JITTER();
       const int nc = __syncthreads_or(primal >= p.thr || moved >= p.thr);
       double sa = 0.0, sb = 0.0;
       if (!nc) {  // exact CTA sums in fp64 (rare: only near convergence)
@@ -319,16 +331,17 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
         for (int i = tid; i < p.n_ms[rank]; i += NT) {
           const uint32_t u = sm[i];
           const float v = lds(xs_a + 4u * (u & 0xffffu), 0.f);
-          cl_st(cl_mapa(inbox_a + 4u * ((u >> 16) & 0x1fffu), u >> 29), v);
+          cl_st(cl_addr<C>(inbox_a + 4u * ((u >> 16) & 0x1fffu), u >> 29), v);
         }
       }
       if (tid < C) {
         const uint32_t r = tid;
-        cl_st_f64(cl_mapa(smem_u32(hsum + 2 * rank), r), sa);
-        cl_st_f64(cl_mapa(smem_u32(hsum + 2 * rank + 1), r), sb);
-        cl_st_u32(cl_mapa(smem_u32(hflag + rank), r), static_cast<uint32_t>(nc));
+        cl_st_f64(cl_addr<C>(smem_u32(hsum + 2 * rank), r, 8), sa);
+        cl_st_f64(cl_addr<C>(smem_u32(hsum + 2 * rank + 1), r, 8), sb);
+        cl_st_u32(cl_addr<C>(smem_u32(hflag + rank), r), static_cast<uint32_t>(nc));
       }
       phase(5);
+      ADMM_JITTER();
       cl_barrier();  // B: inboxes and headers visible
       bool anync = false;
       double A = 0.0, B = 0.0;
@@ -357,6 +370,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
         const bool h = xv > 0.5f;
         ones += h;
         integral &= fminf(fabsf(xv), fabsf(1.f - xv)) <= 1e-5f;
+        ADMM_ASSERT(v < p.n_vars && f < p.batch);
         if (p.x_out) p.x_out[f * p.ld_x + v] = xv;
         if (p.hard_out) p.hard_out[f * p.ld_hard + v] = h;
       }
@@ -374,7 +388,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
     const int all_integral = __syncthreads_and(integral);
     const int any_odd = __syncthreads_or(odd);
     if (tid == 0) {
-      const uint32_t o = cl_mapa(smem_u32(outslot + 3 * rank), 0);
+      const uint32_t o = cl_addr<C>(smem_u32(outslot + 3 * rank), 0, 4);
       cl_st_u32(o, static_cast<uint32_t>(all_integral));
       cl_st_u32(o + 4, static_cast<uint32_t>(misc[1]));
       cl_st_u32(o + 8, static_cast<uint32_t>(any_odd));

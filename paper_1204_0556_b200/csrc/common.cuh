@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
+#include <cstdio>
 
 namespace admm {
 
@@ -93,6 +94,55 @@ template <typename T> __device__ __forceinline__ T warp_allsum(T v) {
   return v;
 }
 
+// ---------------------------------------------------------------------------
+// Checked build (make checked -> libadmm_b200_checked.so, -DADMM_CHECKED):
+// compute-sanitizer is closed on the GPU pool, so the kernels carry their own
+// instrumentation, compiled in only here:
+//   * every bare shared-memory access (lds*/sts*) and every DSMEM address
+//     (cl_addr) is bounds-checked against the CTA's shared window
+//     (static + dynamic, %dynamic_smem_size), and the cluster rank against
+//     the cluster size; a violation prints the address and traps;
+//   * ADMM_JITTER() sleeps a pseudo-random 0-1 us per warp at the phase
+//     boundaries of the barrier-synchronous kernels, so a missing barrier
+//     turns into wrong or nondeterministic results in the parity tests.
+// ---------------------------------------------------------------------------
+#ifdef ADMM_CHECKED
+extern __shared__ __align__(16) unsigned char admm_dyn_smem[];
+__device__ __forceinline__ uint32_t admm_smem_end() {
+  uint32_t dyn;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+  return static_cast<uint32_t>(__cvta_generic_to_shared(admm_dyn_smem)) + dyn;
+}
+__device__ __forceinline__ void admm_check_smem(uint32_t a, uint32_t bytes) {
+  if (a + bytes > admm_smem_end() || (a & (bytes - 1)) != 0) {
+    printf("ADMM_CHECKED: shared access [%u, +%u) outside [0, %u) or misaligned (block %d thread %d)\n", a, bytes,
+           admm_smem_end(), blockIdx.x, threadIdx.x);
+    __trap();
+  }
+}
+#define ADMM_CHECK_SMEM(a, bytes) admm::admm_check_smem((a), (bytes))
+#define ADMM_ASSERT(cond)                                                                          \
+  do {                                                                                             \
+    if (!(cond)) {                                                                                 \
+      printf("ADMM_CHECKED: %s:%d assertion %s failed (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+             blockIdx.x, threadIdx.x);                                                             \
+      __trap();                                                                                    \
+    }                                                                                              \
+  } while (0)
+__device__ __forceinline__ void admm_jitter() {
+  uint32_t x = static_cast<uint32_t>(clock64()) ^ (blockIdx.x * 0x9E3779B9u) ^ ((threadIdx.x >> 5) * 0x85EBCA6Bu);
+  x ^= x >> 15;
+  x *= 0x2C1B3C6Du;
+  x ^= x >> 12;
+  __nanosleep(x & 1023u);
+}
+#define ADMM_JITTER() admm::admm_jitter()
+#else
+#define ADMM_CHECK_SMEM(a, bytes) ((void)0)
+#define ADMM_ASSERT(cond) ((void)0)
+#define ADMM_JITTER() ((void)0)
+#endif
+
 // 32-bit shared-memory addressing.  Addresses are computed once (per CTA or
 // per frame) and kept in registers, so the hot loops issue bare LDS/STS with
 // no generic-to-shared conversion.  The "memory" clobber keeps the compiler
@@ -101,46 +151,56 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 __device__ __forceinline__ float lds(uint32_t a, float) {
+  ADMM_CHECK_SMEM(a, 4);
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ double lds(uint32_t a, double) {
+  ADMM_CHECK_SMEM(a, 8);
   double v;
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ void sts(uint32_t a, float v) {
+  ADMM_CHECK_SMEM(a, 4);
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
 }
 __device__ __forceinline__ void sts(uint32_t a, double v) {
+  ADMM_CHECK_SMEM(a, 8);
   asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
 // Four adjacent fp32 words (16-byte aligned address).
 __device__ __forceinline__ float4 lds4(uint32_t a) {
+  ADMM_CHECK_SMEM(a, 16);
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ void sts4(uint32_t a, float4 v) {
+  ADMM_CHECK_SMEM(a, 16);
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
 // Two adjacent fp64 words (16-byte aligned address).
 __device__ __forceinline__ double2 lds2d(uint32_t a) {
+  ADMM_CHECK_SMEM(a, 16);
   double2 v;
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ void sts2d(uint32_t a, double2 v) {
+  ADMM_CHECK_SMEM(a, 16);
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
 // Two adjacent fp32 words (8-byte aligned address).
 __device__ __forceinline__ float2 lds2(uint32_t a) {
+  ADMM_CHECK_SMEM(a, 8);
   float2 v;
   asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ void sts2(uint32_t a, float2 v) {
+  ADMM_CHECK_SMEM(a, 8);
   asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
 }
 

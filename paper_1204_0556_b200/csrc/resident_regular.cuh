@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
           sts(xst[q], xv);
         }
       }
+      ADMM_JITTER();
       __syncthreads();
 
       // ---- fused z-update, projection, residuals, lambda-update ----
@@ -367,6 +368,7 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
       // ---- stop rule (admm_decoder.py:169,174-181) ----
       // (p.thr is eps^2 E rounded up to T: a partial >= thr is >= the fp64
       // threshold; the exact sums below are accumulated in fp64)
+      ADMM_JITTER();
       if (__syncthreads_or(primal >= p.thr || moved >= p.thr)) continue;
       const double pa = warp_allsum(static_cast<double>(primal));
       const double pb = warp_allsum(static_cast<double>(moved));

@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(ShardThreads<T>::value, 1) sharded_decode_kern
     misc[0] = static_cast<int>(first);
     *reinterpret_cast<long long*>(misc + 2) = first;
   }
+  ADMM_JITTER();
   grid.sync();
 
   const long long max_passes = ((long long)(p.batch + S - 1) / S + 1) * ((long long)p.t_max + 2) + 4;
@@ -245,6 +246,7 @@ __global__ void __launch_bounds__(ShardThreads<T>::value, 1) sharded_decode_kern
       if (sint[S + s]) atomicOr(p.nonint + s, 1);
     }
     long long tp1 = prof ? clock64() : 0;
+    ADMM_JITTER();
     grid.sync();
     long long tp2 = prof ? clock64() : 0;
 
@@ -352,6 +354,7 @@ __global__ void __launch_bounds__(ShardThreads<T>::value, 1) sharded_decode_kern
       }
     }
     long long tp3 = prof ? clock64() : 0;
+    ADMM_JITTER();
     grid.sync();
     long long tp4 = prof ? clock64() : 0;
 

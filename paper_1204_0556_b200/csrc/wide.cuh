@@ -854,6 +854,7 @@ __global__ void __launch_bounds__(kWideThreads, MINB) wide_decode_kernel(const W
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x)
       p.gfr[q] = static_cast<T>(synth_llr(p.synth, p.synth.trial0 + q / p.n_vars, static_cast<int>(q % p.n_vars)));
   }
+  ADMM_JITTER();
   grid.sync();
 
   const long long max_passes = ((long long)(p.batch + p.S - 1) / p.S + 1) * ((long long)p.t_max + 2) + 4;
@@ -868,6 +869,7 @@ __global__ void __launch_bounds__(kWideThreads, MINB) wide_decode_kernel(const W
       wide_step<T, VS, D, DVMAX, REG, NS>(p, ring, tslot, TS, sa, p.ctr + 2);
     }
     if (prof) tp[1] = clock64();
+    ADMM_JITTER();
     grid.sync();
     if (prof) tp[2] = clock64();
     // slot phase of G1; reset the counters step B will use and list A
@@ -878,6 +880,7 @@ __global__ void __launch_bounds__(kWideThreads, MINB) wide_decode_kernel(const W
     }
     if (pass > 0)
       for (int s = h * W + gwarp; s < p.S; s += n_gwarp) wide_phase_s<T, VS>(p, s, list_b, p.ctr + 7);
+    ADMM_JITTER();
     grid.sync();
     if (prof) tp[3] = clock64();
     // step B: phase C of G0, phase V of G1
@@ -887,6 +890,7 @@ __global__ void __launch_bounds__(kWideThreads, MINB) wide_decode_kernel(const W
       wide_step<T, VS, D, DVMAX, REG, NS>(p, ring, tslot, TS, sb, p.ctr + 3);
     }
     if (prof) tp[4] = clock64();
+    ADMM_JITTER();
     grid.sync();
     if (prof) tp[5] = clock64();
     // slot phase of G0; reset the counters step A will use and list B
@@ -896,6 +900,7 @@ __global__ void __launch_bounds__(kWideThreads, MINB) wide_decode_kernel(const W
       p.ctr[7] = 0;
     }
     for (int s = gwarp; s < h * W; s += n_gwarp) wide_phase_s<T, VS>(p, s, list_a, p.ctr + 5);
+    ADMM_JITTER();
     grid.sync();
     if (prof) {
       tp[6] = clock64();

@@ -1,0 +1,13 @@
+#!/bin/bash
+# The GPU test-suite and the every-kernel driver against the CHECKED build
+# (make checked: shared/DSMEM bounds checks, asserts, barrier jitter) --
+# the stand-in for compute-sanitizer, which is closed on the GPU pool.
+#   gpurun --timeout 3000 -- 'bash tools/checked_run.sh TAG'
+set -u
+TAG=${1:-checked}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+export ADMM_B200_LIB=$PWD/paper_1204_0556_b200/libadmm_b200_checked.so
+timeout 900 python tools/sanitize.py > $OUT/kernels.log 2>&1; echo "kernels exit $? $(grep -c ADMM_CHECKED $OUT/kernels.log) violations"
+timeout 2400 python -m pytest tests -m gpu -q > $OUT/pytest.log 2>&1; echo "pytest exit $? $(tail -1 $OUT/pytest.log)"
+grep -h ADMM_CHECKED $OUT/*.log | head -5
