@@ -213,6 +213,14 @@ int admm_membership_batch(int dtype, int64_t m, int32_t d, const void* values, d
 
 const char* admm_last_error(void);
 int admm_version(void);
+/* Build flags: ADMM_BUILD_CHECKED = the checked build (make checked): shared-memory /
+ * DSMEM bounds checks, asserts and barrier jitter compiled into the kernels. */
+#define ADMM_BUILD_CHECKED 1
+int admm_build_flags(void);
+/* Negative control of the checked build: a one-CTA kernel that reads one word
+ * past its shared memory when bad != 0 (the checked build traps; the normal
+ * build reads garbage) or the last in-bounds word otherwise.  out: 1 device float. */
+int admm_checked_probe(int bad, float* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -26,6 +26,8 @@ KERNELS = {1: "resident", 2: "regular", 3: "sharded", 4: "cluster", 5: "wide"}
 #: Every symbol the public header declares (checked by the CPU test-suite).
 EXPORTED = (
     "admm_version",
+    "admm_build_flags",
+    "admm_checked_probe",
     "admm_last_error",
     "admm_graph_create",
     "admm_graph_create_ex",
@@ -90,6 +92,9 @@ def load() -> ctypes.CDLL:
     lib = ctypes.CDLL(path)
     P, I32, I64, SZ, D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t, ctypes.c_double
     lib.admm_version.restype = ctypes.c_int
+    lib.admm_build_flags.restype = ctypes.c_int
+    lib.admm_checked_probe.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+    lib.admm_checked_probe.restype = ctypes.c_int
     lib.admm_last_error.restype = ctypes.c_char_p
     lib.admm_graph_create.argtypes = [ctypes.c_int, I32, I32, P, P, ctypes.POINTER(P)]
     lib.admm_graph_create.restype = ctypes.c_int

@@ -153,6 +153,21 @@ extern "C" {
 
 int admm_version(void) { return ADMM_B200_VERSION; }
 
+int admm_checked_probe(int bad, float* out, void* stream) {
+  if (!out) return fail(ADMM_E_ARG, "null pointer argument");
+  const cudaError_t e = admm::launch_checked_probe(bad, out, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "checked probe launch");
+  return ADMM_OK;
+}
+
+int admm_build_flags(void) {
+#ifdef ADMM_CHECKED
+  return ADMM_BUILD_CHECKED;
+#else
+  return 0;
+#endif
+}
+
 const char* admm_last_error(void) { return g_last_error.c_str(); }
 
 int admm_graph_create(int device, int32_t n_vars, int32_t n_checks, const int32_t* check_ptr,

@@ -220,4 +220,19 @@ bool launch_membership(int dtype, int D, long long m, int d, const void* in, dou
   return dtype ? membership_t<double>(D, m, d, in, tol, out, st) : membership_t<float>(D, m, d, in, tol, out, st);
 }
 
+// Negative control of the checked build: one CTA reads one word past its
+// dynamic shared memory (bad = 1) or the last word (bad = 0).
+__global__ void checked_probe_kernel(int bad, float* out) {
+  extern __shared__ __align__(16) unsigned char probe_smem[];
+  const uint32_t a = smem_u32(probe_smem) + (bad ? 256u : 252u);
+  sts(smem_u32(probe_smem) + 252u, 1.0f);
+  __syncthreads();
+  if (threadIdx.x == 0) out[0] = lds(a, 0.f);
+}
+
+cudaError_t launch_checked_probe(int bad, float* out, cudaStream_t st) {
+  checked_probe_kernel<<<1, 32, 256, st>>>(bad, out);
+  return cudaGetLastError();
+}
+
 }  // namespace admm

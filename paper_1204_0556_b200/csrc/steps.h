@@ -26,4 +26,6 @@ void launch_lambda_update(int dtype, long long batch, int n_edges, const void* l
 bool launch_membership(int dtype, int D, long long m, int d, const void* in, double tol, uint8_t* out,
                        cudaStream_t st);
 
+cudaError_t launch_checked_probe(int bad, float* out, cudaStream_t st);
+
 }  // namespace admm

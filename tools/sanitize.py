@@ -18,6 +18,7 @@ import torch  # noqa: E402
 
 import paper_1204_0556_b200 as P  # noqa: E402
 
+print("library", P._lib.load()._name, "build flags", P._lib.load().admm_build_flags(), flush=True)
 which = set(sys.argv[1:]) or {"regular", "generic", "f64regular", "sharded", "wide", "cluster", "bp", "steps", "project"}
 cfg = P.AdmmConfig(mu=5.0, t_max=200)
 c1 = P.baseline_code("cfg1_n96")
