@@ -80,15 +80,14 @@ struct admm_graph {
   // cluster engine (cluster.cuh, fp32): one 4-CTA cluster per frame
   bool cluster_ok = false;
   int cl_nt = 0, cl_smem = 0, cl_clusters = 0, cl_regs = 0;
-  int cl_NPL = 0, cl_NIN = 0, cl_NXS = 0, cl_NMS = 0, cl_MC = 0, cl_NO = 0;
-  int cl_n_xs[admm::kClusterMax] = {}, cl_n_ms[admm::kClusterMax] = {}, cl_n_in[admm::kClusterMax] = {};
+  int cl_NPL = 0, cl_NXS = 0, cl_NMS = 0, cl_MC = 0, cl_NO = 0;
+  int cl_n_xs[admm::kClusterMax] = {}, cl_n_ms[admm::kClusterMax] = {};
   long long cl_exchange = 0;
   int* cl_chk_slot = nullptr;
   int* cl_chk_orig = nullptr;
   int* cl_own_var = nullptr;
   uint32_t* cl_xsend = nullptr;
   uint32_t* cl_msend = nullptr;
-  uint16_t* cl_scatter = nullptr;
   int* wctbl = nullptr;  // wide engine index tables (wide.cuh)
   int* wvtbl = nullptr;
   int engine_req = 0;
@@ -411,30 +410,24 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
           const admm::ClusterLayout CL =
               admm::build_cluster_layout(rows, n_vars, 6, 3, C, NT, CPT, VPT, pm, bm, 4242);
           if (dbg)
-            std::fprintf(stderr, "[admm] cluster layout ok=%d %s NPL=%d NIN=%d ghosts=%lld bank %.0f->%.0f\n", (int)CL.ok,
-                         CL.error.c_str(), CL.NPL, CL.NIN, CL.ghost_total, CL.bank_cost_before, CL.bank_cost_after);
+            std::fprintf(stderr, "[admm] cluster layout ok=%d %s NPL=%d ghosts=%lld messages=%lld runs=%d bank %.0f->%.0f\n",
+                         (int)CL.ok, CL.error.c_str(), CL.NPL, CL.ghost_total, CL.msg_total, CL.msg_runs,
+                         CL.bank_cost_before, CL.bank_cost_after);
           if (CL.ok) {
-            const int smem = admm::cluster_smem_bytes(CL.NPL, 3, CL.NIN, CL.NXS, CL.NMS);
+            const int smem = admm::cluster_smem_bytes(CL.NPL, 3, CL.NXS, CL.NMS);
             int clusters = 0, regs = 0;
-            const bool fits = smem <= smem_optin && CL.NO <= 8192 && (3 + 1) * CL.NPL < 65536 && CL.NPL < 65536 &&
-                              CL.NIN < 8192;  // xs_pack / ms_pack fields
+            const bool fits = smem <= smem_optin && CL.NO <= 4096 && CL.NPL <= 8192;  // table fields
             if (fits && admm::cluster_query(C, NT, smem, &clusters, &regs) == cudaSuccess && clusters > 0) {
-              // packed exchange tables: src | dst << 15 | rank << 30
-              std::vector<uint32_t> xs((size_t)C * CL.NXS, 0), ms((size_t)C * CL.NMS, 0);
+              // packed x-send table: own slot | ghost slot << 13 | rank << 29
+              std::vector<uint32_t> xs((size_t)C * CL.NXS, 0);
               for (int p = 0; p < C; ++p) {
                 for (int r = 0; r < C; ++r)
                   for (int i = CL.xs_start[p * (C + 1) + r]; i < CL.xs_start[p * (C + 1) + r + 1]; ++i) {
                     const uint32_t dst = CL.gbase[r * C + p] + (i - CL.xs_start[p * (C + 1) + r]);
                     xs[(size_t)p * CL.NXS + i] = admm::xs_pack(CL.xsend[(size_t)p * CL.NXS + i], dst, (uint32_t)r);
                   }
-                for (int o = 0; o < C; ++o)
-                  for (int i = CL.ms_start[p * (C + 1) + o]; i < CL.ms_start[p * (C + 1) + o + 1]; ++i) {
-                    const uint32_t dst = CL.ibase[o * C + p] + (i - CL.ms_start[p * (C + 1) + o]);
-                    ms[(size_t)p * CL.NMS + i] = admm::ms_pack(CL.msend[(size_t)p * CL.NMS + i], dst, (uint32_t)o);
-                  }
                 g->cl_n_xs[p] = CL.xs_start[p * (C + 1) + C];
-                g->cl_n_ms[p] = CL.ms_start[p * (C + 1) + C];
-                g->cl_n_in[p] = CL.n_in[p];
+                g->cl_n_ms[p] = CL.n_ms[p];
               }
               auto upc = [&](void** dst, const void* src, size_t bytes) -> bool {
                 if (cudaMalloc(dst, bytes) != cudaSuccess) return false;
@@ -445,8 +438,7 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
                   upc((void**)&g->cl_chk_orig, CL.chk_orig.data(), CL.chk_orig.size() * sizeof(int)) &&
                   upc((void**)&g->cl_own_var, CL.own_var.data(), CL.own_var.size() * sizeof(int)) &&
                   upc((void**)&g->cl_xsend, xs.data(), xs.size() * sizeof(uint32_t)) &&
-                  upc((void**)&g->cl_msend, ms.data(), ms.size() * sizeof(uint32_t)) &&
-                  upc((void**)&g->cl_scatter, CL.scatter.data(), CL.scatter.size() * sizeof(uint16_t));
+                  upc((void**)&g->cl_msend, CL.msend.data(), CL.msend.size() * sizeof(uint32_t));
               if (up_ok) {
                 g->cluster_ok = true;
                 g->C = C;
@@ -455,12 +447,11 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
                 g->cl_clusters = clusters;
                 g->cl_regs = regs;
                 g->cl_NPL = CL.NPL;
-                g->cl_NIN = CL.NIN;
                 g->cl_NXS = CL.NXS;
                 g->cl_NMS = CL.NMS;
                 g->cl_MC = CL.MC;
                 g->cl_NO = CL.NO;
-                g->cl_exchange = CL.ghost_total + CL.inbox_total;
+                g->cl_exchange = CL.ghost_total + CL.msg_total;
               }
             }
           }
@@ -666,7 +657,6 @@ int admm_graph_destroy(admm_graph* g) {
   cudaFree(g->cl_own_var);
   cudaFree(g->cl_xsend);
   cudaFree(g->cl_msend);
-  cudaFree(g->cl_scatter);
   cudaFree(g->wvtbl);
   cudaFree(g->var_orig);
   cudaFree(g->edge_ref);
@@ -875,9 +865,7 @@ int decode_impl(const admm_graph* g, int dtype, int64_t batch, const void* gamma
     cp.own_var = g->cl_own_var;
     cp.xsend = g->cl_xsend;
     cp.msend = g->cl_msend;
-    cp.scatter = g->cl_scatter;
     cp.NPL = g->cl_NPL;
-    cp.NIN = g->cl_NIN;
     cp.NXS = g->cl_NXS;
     cp.NMS = g->cl_NMS;
     cp.MC = g->cl_MC;
@@ -885,7 +873,6 @@ int decode_impl(const admm_graph* g, int dtype, int64_t batch, const void* gamma
     for (int r = 0; r < admm::kClusterMax; ++r) {
       cp.n_xs[r] = g->cl_n_xs[r];
       cp.n_ms[r] = g->cl_n_ms[r];
-      cp.n_in[r] = g->cl_n_in[r];
     }
     cp.n_vars = g->n_vars;
     cp.n_checks = g->n_checks;

@@ -38,7 +38,7 @@ bool cluster_supported(int D, int DV, int C, int CPT, int VPT) {
   return D == kD && DV == kDV && (C == 4 || C == 8) && CPT == kCPT && VPT == kVPT;
 }
 
-int cluster_smem_bytes(int NPL, int DV, int NIN, int NXS, int NMS) { return ClusterSmem(NPL, DV, NIN, NXS, NMS).total; }
+int cluster_smem_bytes(int NPL, int DV, int NXS, int NMS) { return ClusterSmem(NPL, DV, NXS, NMS).total; }
 
 // Spread the CTAs of a cluster over distinct SMs (two CTAs of DIFFERENT
 // clusters then share an SM at C = 8, so one hides the other's barriers).

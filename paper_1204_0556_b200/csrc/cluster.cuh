@@ -11,13 +11,12 @@
 // CONSECUTIVE words of the destination (~20-25 B/cycle; scattered 4-byte
 // remote accesses cost ~2.6 cycles each, tools/micro/dsmem.cu):
 //
-//   scatter-in  inbox -> message rows of own variables        (local)
 //   variable    x = clip((sum_j msg_j - gamma/mu) / DV) of own variables
 //   x-send      own x -> ghost slots of the CTAs holding them  (DSMEM)
 //   -- cluster barrier A --
 //   check       gather x (own + ghost slots), project, dual update, message
 //               to msg[color][slot(v)] (own rows, or ghost rows)
-//   msg-send    ghost-row messages -> owners' inboxes            (DSMEM)
+//   msg-send    ghost-row messages -> the owners' message rows  (DSMEM)
 //               stop-rule header {flag, exact sums} -> every CTA
 //   -- cluster barrier B --
 //   decision    every thread reads the C headers: uniform, deterministic
@@ -39,9 +38,9 @@ constexpr int kClusterMax = 8;
 
 // Packed exchange-table entries (cluster_layout.h / abi.cu):
 //   x-send   own slot (13 bits) | ghost slot in the destination (16) << 13 | rank (3) << 29
-//   msg-send message word (16)  | inbox index in the destination (13) << 16 | rank (3) << 29
+//   msg-send color (2) | ghost slot here (13) << 2 | own slot at the owner (12) << 15 | owner (3) << 27
+//            (cluster_layout.h ms_entry)
 __host__ __device__ constexpr uint32_t xs_pack(uint32_t src, uint32_t dst, uint32_t r) { return src | dst << 13 | r << 29; }
-__host__ __device__ constexpr uint32_t ms_pack(uint32_t src, uint32_t dst, uint32_t r) { return src | dst << 16 | r << 29; }
 
 __device__ __forceinline__ uint32_t cl_rank() {
   uint32_t r;
@@ -85,10 +84,9 @@ struct ClusterParams {
   const int* chk_orig;   // [C][MC] original check (-1: idle slot)
   const int* own_var;    // [C][NO]
   const uint32_t* xsend; // [C][NXS] xs_pack(own slot, ghost slot, rank)
-  const uint32_t* msend; // [C][NMS] ms_pack(message word, inbox index, rank)
-  const uint16_t* scatter;  // [C][NIN] message-row word of inbox entry i
-  int NPL, NIN, NXS, NMS, MC, NO;
-  int n_xs[kClusterMax], n_ms[kClusterMax], n_in[kClusterMax];
+  const uint32_t* msend; // [C][NMS] ms_entry(color, ghost slot, owner's own slot, owner)
+  int NPL, NXS, NMS, MC, NO;
+  int n_xs[kClusterMax], n_ms[kClusterMax];
   int n_vars, n_checks;
   // frames
   long long batch;
@@ -108,24 +106,22 @@ struct ClusterParams {
   SynthParams synth;
 };
 
-// Shared memory (bytes): X | MSG[DV] | GM (each NPL fp32) | inbox[NIN] fp32 |
-// xsend[NXS] u32 | msend[NMS] u32 | scatter[NIN] u16 | header | misc.
+// Shared memory (bytes): X | MSG[DV] | GM (each NPL fp32) | xsend[NXS] u32 |
+// msend[NMS] u32 | header | misc.
 struct ClusterSmem {
-  int x, inbox, xs, ms, sc, hdr, misc, total;
-  __host__ __device__ ClusterSmem(int NPL, int DV, int NIN, int NXS, int NMS) {
+  int x, xs, ms, hdr, misc, total;
+  __host__ __device__ ClusterSmem(int NPL, int DV, int NXS, int NMS) {
     x = 0;
-    inbox = 4 * NPL * (DV + 2);
-    xs = inbox + 4 * NIN;
+    xs = 4 * NPL * (DV + 2);
     ms = xs + 4 * NXS;
-    sc = ms + 4 * NMS;
-    hdr = (sc + 2 * NIN + 15) & ~15;   // [kClusterMax] {double primal, double moved}, then int flags
+    hdr = (ms + 4 * NMS + 15) & ~15;   // [kClusterMax] {double primal, double moved}, then int flags
     misc = hdr + kClusterMax * 16 + 16;  // ints: frame, weight, nonint, odd, ... + per-CTA output slots
     total = misc + 4 * (8 + 3 * kClusterMax) + 64 * 8;  // + fp64 block-reduction slots
   }
 };
 
 // Phase profiler (admm_cluster_phase_profile; the PROF instantiation): thread
-// 0 of CTA 0 accumulates clock64() per phase: {scatter-in, variable, x-send,
+// 0 of CTA 0 accumulates clock64() per phase: {-, variable, x-send,
 // barrier A, check, msg-send, barrier B + decision, iterations}.
 __device__ unsigned long long g_cl_cycles[8];
 
@@ -134,7 +130,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
   static_assert(D % DV == 0 && D % 2 == 0 && VPT % 2 == 0, "cluster engine: colored fp32 layout");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int NPL = p.NPL;
-  const ClusterSmem L(NPL, DV, p.NIN, p.NXS, p.NMS);
+  const ClusterSmem L(NPL, DV, p.NXS, p.NMS);
   const uint32_t rank = cl_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarps = NT / 32;
@@ -150,13 +146,10 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
   {
     const uint32_t* gx = p.xsend + static_cast<size_t>(rank) * p.NXS;
     const uint32_t* gms = p.msend + static_cast<size_t>(rank) * p.NMS;
-    const uint16_t* gsc = p.scatter + static_cast<size_t>(rank) * p.NIN;
     uint32_t* sx = reinterpret_cast<uint32_t*>(smem_raw + L.xs);
     uint32_t* sm = reinterpret_cast<uint32_t*>(smem_raw + L.ms);
-    uint16_t* ss = reinterpret_cast<uint16_t*>(smem_raw + L.sc);
     for (int i = tid; i < p.NXS; i += NT) sx[i] = __ldg(gx + i);
     for (int i = tid; i < p.NMS; i += NT) sm[i] = __ldg(gms + i);
-    for (int i = tid; i < p.NIN; i += NT) ss[i] = __ldg(gsc + i);
   }
 
   // ---- per-thread graph registers: checks lc = tid + q NT, own variable
@@ -272,14 +265,6 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
     for (;;) {
       ++t;
       if (prof) g_cl_cycles[7]++;
-      if (t > 1) {
-        // scatter-in: messages of own variables computed by other CTAs
-        const uint16_t* ss = reinterpret_cast<const uint16_t*>(smem_raw + L.sc);
-        const uint32_t inbox_a = smem_u32(smem_raw) + L.inbox;
-        for (int i = tid; i < p.n_in[rank]; i += NT) sts(xs_a + 4u * ss[i], lds(inbox_a + 4u * i, 0.f));
-        ADMM_JITTER();
-        __syncthreads();
-      }
       phase(0);
       // ---- x-update of the own variables ----
 #pragma unroll
@@ -324,14 +309,14 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
         sb = warp_allsum(b);
       }
       phase(4);
-      // ---- msg-send: ghost-row messages -> owners' inboxes; stop-rule header ----
+      // ---- msg-send: ghost-row messages -> the owners' message rows; stop-rule header ----
       {
         const uint32_t* sm = reinterpret_cast<const uint32_t*>(smem_raw + L.ms);
-        const uint32_t inbox_a = smem_u32(smem_raw) + L.inbox;
         for (int i = tid; i < p.n_ms[rank]; i += NT) {
           const uint32_t u = sm[i];
-          const float v = lds(xs_a + 4u * (u & 0xffffu), 0.f);
-          cl_st(cl_addr<C>(inbox_a + 4u * ((u >> 16) & 0x1fffu), u >> 29), v);
+          const uint32_t row = mstride * ((u & 3u) + 1);
+          const float v = lds(xs_a + row + 4u * ((u >> 2) & 0x1fffu), 0.f);
+          cl_st(cl_addr<C>(xs_a + row + 4u * ((u >> 15) & 0xfffu), u >> 27), v);
         }
       }
       if (tid < C) {
@@ -342,7 +327,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
       }
       phase(5);
       ADMM_JITTER();
-      cl_barrier();  // B: inboxes and headers visible
+      cl_barrier();  // B: messages and headers visible
       bool anync = false;
       double A = 0.0, B = 0.0;
 #pragma unroll

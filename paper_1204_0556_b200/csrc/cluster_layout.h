@@ -14,10 +14,14 @@
 // DSMEM prices scattered 4-byte remote accesses at ~2.6 SM cycles each but
 // moves warp-coalesced stores at ~20-25 B/cycle (tools/micro/dsmem.cu), so
 // every exchange is table-driven: a warp gathers 32 local values and stores
-// them to 32 CONSECUTIVE words of the destination (its ghost-x region, or
-// its message inbox, scattered locally into the message rows after the
-// barrier).  Simulated annealing over check swaps between parts (balance is
-// kept exactly), from a BFS-grown initial partition.
+// them to 32 CONSECUTIVE words of the destination.  For the x-send that is
+// the destination's ghost region (ordered like the sender's list); for the
+// messages it is the owner's message rows THEMSELVES: the owner's variables
+// are ordered by their edge signature (the part holding each color's edge),
+// so the messages one part sends for one color land in a few long runs of
+// consecutive own slots -- no inbox and no scatter on the receiving side.
+// Simulated annealing over check swaps between parts (balance is kept
+// exactly), from a BFS-grown initial partition.
 #pragma once
 
 #include <algorithm>
@@ -32,6 +36,12 @@
 #include "layout.h"
 
 namespace admm {
+
+// Packed message-table entry: color j (2 bits) | ghost slot in the sender
+// (13) | own slot in the owner (12) | owner rank (3) -- shared with cluster.cuh.
+inline constexpr uint32_t ms_entry(uint32_t j, uint32_t gslot, uint32_t oslot, uint32_t rank) {
+  return j | gslot << 2 | oslot << 15 | rank << 27;
+}
 
 struct ClusterPartition {
   int C = 0;
@@ -172,30 +182,28 @@ inline ClusterPartition partition_checks(const std::vector<std::vector<int>>& ro
 // The message of edge (c, v) of color j (equitable coloring of layout.h:
 // every variable has one edge per color, slot k of a check has color k % DV)
 // lives at MSG[j][slot(v)]: for own v it is consumed by the variable phase,
-// for a ghost v it is shipped to the owner's inbox (msend table) and the
-// owner scatters it to MSG[j][own slot] (scatter table).
+// for a ghost v it is shipped (msend table) to MSG[j][own slot of v] of the
+// owner.
 struct ClusterLayout {
   int C = 0, NT = 0, CPT = 0, VPT = 0, D = 0, DV = 0;
   int MC = 0;   // local check slots per part (NT * CPT)
   int NO = 0;   // own variable slots per part (NT * VPT)
   int NPL = 0;  // local slots per part (own + ghosts + spare), multiple of 32
-  int NIN = 0, NXS = 0, NMS = 0;  // table capacities (max over parts), multiples of 32
+  int NXS = 0, NMS = 0;  // table capacities (max over parts), multiples of 32
   std::vector<int> chk_slot;        // [C][D][MC] local slot of the variable in slot k of local check lc
   std::vector<int> chk_orig;        // [C][MC] original check (-1: idle)
   std::vector<int> own_var;         // [C][NO] original variable of an own slot (-1: dummy)
   std::vector<int> xs_start;        // [C][C+1] xsend range of part p for destination r: [xs_start[p][r], xs_start[p][r+1])
   std::vector<int> gbase;           // [C][C] gbase[r][o]: first ghost slot in part r of the variables owned by o
-  std::vector<int> ms_start;        // [C][C+1] msend range of part p for destination o
-  std::vector<int> ibase;           // [C][C] ibase[o][p]: first inbox entry of part o filled by part p
-  std::vector<int> n_in;            // [C] inbox entries of part p
+  std::vector<int> n_ms;            // [C] msend entries of part p
   std::vector<int> nb;              // [C] own slots [0, nb) hold the boundary variables; the kernel
                                     // updates the pairs starting below nb first
   std::vector<int> nic;             // [C] local check slots [0, nic) hold the interior checks
   std::vector<uint16_t> xsend;      // [C][NXS] own slots whose x goes to ghosts (grouped by destination)
-  std::vector<uint16_t> msend;      // [C][NMS] word offsets (j+1)*NPL + ghost slot (grouped by destination)
-  std::vector<uint16_t> scatter;    // [C][NIN] word offsets (j+1)*NPL + own slot of the inbox entries
+  std::vector<uint32_t> msend;      // [C][NMS] ms_entry(color, ghost slot here, own slot at the owner, owner)
   ClusterPartition part;
-  long long ghost_total = 0, inbox_total = 0;
+  long long ghost_total = 0, msg_total = 0;
+  int msg_runs = 0;                 // maximal runs of consecutive destination words (all parts)
   double bank_cost_before = 0, bank_cost_after = 0;
   bool ok = false;
   std::string error;
@@ -293,25 +301,41 @@ inline ClusterLayout build_cluster_layout(const std::vector<std::vector<int>>& r
         L.nic[pc[c]] += interior;
       }
     }
-  // Own slots: boundary then interior owned variables, in index order (the
-  // bank annealer permutes them inside each class).
+  // Own slots: owned variables sorted by their edge signature (the part of
+  // the color-0, -1, -2 edge), so that the messages part q sends to part o
+  // for color j land in runs of consecutive own slots of o; ties in index
+  // order (the bank annealer permutes slots inside a signature class).
+  std::vector<int> sig(n_vars, 0);
+  for (int c = 0; c < M; ++c)
+    for (int r = 0; r < D; ++r) {
+      const int j = col.edge_slot[c * D + r] % DV, v = rows[c][r];
+      int w = 1;
+      for (int i = j + 1; i < DV; ++i) w *= C;
+      sig[v] += pc[c] * w;
+    }
   std::vector<std::vector<int>> slot_var(C);  // [p][slot] -> variable (-1 dummy / spare)
   std::vector<std::vector<int>> ghosts_of(C * C);  // [r][o] ghost variables of part r owned by o
+  std::vector<std::vector<int>> slot_class(C);  // [p][own slot] signature class (dummy: -1)
   L.nb.assign(C, 0);
-  for (int p = 0; p < C; ++p) slot_var[p].assign(L.NO, -1);
+  for (int p = 0; p < C; ++p) {
+    slot_var[p].assign(L.NO, -1);
+    slot_class[p].assign(L.NO, -1);
+  }
   {
-    std::vector<int> fill(C, 0);
-    for (int pass = 0; pass < 2; ++pass) {
-      for (int v = 0; v < n_vars; ++v)
-        if (boundary[v] == (pass == 0)) slot_var[owner[v]][fill[owner[v]]++] = v;
-      if (pass == 0)
-        for (int p = 0; p < C; ++p) L.nb[p] = fill[p];
-    }
-    for (int p = 0; p < C; ++p)
-      if (fill[p] > L.NO) {
+    std::vector<std::vector<int>> mine(C);
+    for (int v = 0; v < n_vars; ++v) mine[owner[v]].push_back(v);
+    for (int p = 0; p < C; ++p) {
+      if (static_cast<int>(mine[p].size()) > L.NO) {
         L.error = "cluster engine: own slots overflow";
         return L;
       }
+      std::stable_sort(mine[p].begin(), mine[p].end(), [&](int a, int b) { return sig[a] < sig[b]; });
+      for (size_t i = 0; i < mine[p].size(); ++i) {
+        slot_var[p][i] = mine[p][i];
+        slot_class[p][i] = sig[mine[p][i]];
+        L.nb[p] += boundary[mine[p][i]] ? 1 : 0;
+      }
+    }
     for (int v = 0; v < n_vars; ++v)
       for (int r = 0; r < C; ++r)
         if (r != owner[v] && cnt[static_cast<size_t>(v) * C + r] > 0) ghosts_of[r * C + owner[v]].push_back(v);
@@ -398,7 +422,7 @@ inline ClusterLayout build_cluster_layout(const std::vector<std::vector<int>>& r
         if (kind == 0) {
           s1 = static_cast<int>(rng() % L.NO);
           s2 = static_cast<int>(rng() % L.NO);
-          if ((s1 < L.nb[p]) != (s2 < L.nb[p])) continue;  // keep the boundary / interior classes
+          if (slot_class[p][s1] != slot_class[p][s2]) continue;  // keep the signature classes
         } else {
           const int o = static_cast<int>(rng() % C);
           const int n = static_cast<int>(ghosts_of[p * C + o].size());
@@ -465,11 +489,10 @@ inline ClusterLayout build_cluster_layout(const std::vector<std::vector<int>>& r
     for (int s = 0; s < L.NO; ++s) L.own_var[static_cast<size_t>(p) * L.NO + s] = slot_var[p][s];
   }
   // xsend: part o ships x of its own slot(v) to ghost slot gbase[r][o] + i of part r
-  std::vector<std::vector<uint16_t>> xs(C), ms(C), sc(C);
+  std::vector<std::vector<uint16_t>> xs(C);
+  std::vector<std::vector<uint32_t>> ms(C);
   L.xs_start.assign(C * (C + 1), 0);
-  L.ms_start.assign(C * (C + 1), 0);
-  L.ibase.assign(C * C, 0);
-  L.n_in.assign(C, 0);
+  L.n_ms.assign(C, 0);
   for (int o = 0; o < C; ++o)
     for (int r = 0; r < C; ++r) {
       L.xs_start[o * (C + 1) + r] = static_cast<int>(xs[o].size());
@@ -478,51 +501,48 @@ inline ClusterLayout build_cluster_layout(const std::vector<std::vector<int>>& r
       for (int i = 0; i < n; ++i) xs[o].push_back(static_cast<uint16_t>(slot_of[o][slot_var[r][g0 + i]]));
     }
   for (int o = 0; o < C; ++o) L.xs_start[o * (C + 1) + C] = static_cast<int>(xs[o].size());
-  // messages: for each part o (owner), inbox grouped by source part p; entries
-  // (v, j) with owner(v) = o and the color-j edge of v in a check of part p
-  std::vector<std::vector<std::vector<std::pair<int, int>>>> inbox(C, std::vector<std::vector<std::pair<int, int>>>(C));
+  // messages: part p ships the message of its edge (c, v), v owned by o != p,
+  // color j, from MSG[j][ghost slot of v here] to MSG[j][own slot of v] of o;
+  // sorted by destination word so warps store runs of consecutive words
+  struct Msg {
+    int o, j, os, gs;
+  };
+  std::vector<std::vector<Msg>> out(C);
   for (int c = 0; c < M; ++c)
     for (int r = 0; r < D; ++r) {
       const int v = rows[c][r], o = owner[v], p = pc[c];
       if (o == p) continue;
-      inbox[o][p].push_back({slot_of[o][v], eslot[c * D + r] % DV});
+      out[p].push_back({o, eslot[c * D + r] % DV, slot_of[o][v], slot_of[p][v]});
     }
-  for (int o = 0; o < C; ++o) {
-    for (int p = 0; p < C; ++p) {
-      std::sort(inbox[o][p].begin(), inbox[o][p].end());
-      L.ibase[o * C + p] = static_cast<int>(sc[o].size());
-      for (auto [s, j] : inbox[o][p]) sc[o].push_back(static_cast<uint16_t>((j + 1) * L.NPL + s));
+  for (int p = 0; p < C; ++p) {
+    std::sort(out[p].begin(), out[p].end(), [](const Msg& a, const Msg& b) {
+      return a.o != b.o ? a.o < b.o : a.j != b.j ? a.j < b.j : a.os < b.os;
+    });
+    for (size_t i = 0; i < out[p].size(); ++i) {
+      const Msg& m = out[p][i];
+      ms[p].push_back(ms_entry(m.j, m.gs, m.os, m.o));
+      if (i == 0 || m.o != out[p][i - 1].o || m.j != out[p][i - 1].j || m.os != out[p][i - 1].os + 1) L.msg_runs++;
     }
-    L.n_in[o] = static_cast<int>(sc[o].size());
-    L.inbox_total += sc[o].size();
+    L.n_ms[p] = static_cast<int>(ms[p].size());
+    L.msg_total += ms[p].size();
   }
-  for (int p = 0; p < C; ++p)
-    for (int o = 0; o < C; ++o) {
-      L.ms_start[p * (C + 1) + o] = static_cast<int>(ms[p].size());
-      if (o == p) continue;
-      for (auto [s, j] : inbox[o][p]) {
-        const int v = slot_var[o][s];
-        ms[p].push_back(static_cast<uint16_t>((j + 1) * L.NPL + slot_of[p][v]));
-      }
-    }
-  for (int p = 0; p < C; ++p) L.ms_start[p * (C + 1) + C] = static_cast<int>(ms[p].size());
-  auto cap = [&](const std::vector<std::vector<uint16_t>>& t) {
-    size_t m = 0;
-    for (const auto& x : t) m = std::max(m, x.size());
-    return static_cast<int>((m + 31) / 32 * 32);
-  };
-  L.NXS = cap(xs), L.NMS = cap(ms), L.NIN = cap(sc);
-  if ((DV + 1) * L.NPL > 32767) {  // 15-bit fields of the packed exchange tables
-    L.error = "cluster engine: local slot space exceeds 16-bit table offsets";
+  if (L.NO > 4096 || L.NPL > 8192 || DV > 4) {  // fields of ms_entry / xs_pack
+    L.error = "cluster engine: slot space exceeds the packed table fields";
     return L;
   }
-  auto flat = [&](const std::vector<std::vector<uint16_t>>& t, int capn, std::vector<uint16_t>& out) {
-    out.assign(static_cast<size_t>(C) * capn, 0);
-    for (int p = 0; p < C; ++p) std::copy(t[p].begin(), t[p].end(), out.begin() + static_cast<size_t>(p) * capn);
-  };
-  flat(xs, L.NXS, L.xsend);
-  flat(ms, L.NMS, L.msend);
-  flat(sc, L.NIN, L.scatter);
+  auto cap = [&](size_t m) { return static_cast<int>((m + 31) / 32 * 32); };
+  size_t mx = 0, mm = 0;
+  for (int p = 0; p < C; ++p) {
+    mx = std::max(mx, xs[p].size());
+    mm = std::max(mm, ms[p].size());
+  }
+  L.NXS = cap(mx), L.NMS = cap(mm);
+  L.xsend.assign(static_cast<size_t>(C) * L.NXS, 0);
+  L.msend.assign(static_cast<size_t>(C) * L.NMS, 0);
+  for (int p = 0; p < C; ++p) {
+    std::copy(xs[p].begin(), xs[p].end(), L.xsend.begin() + static_cast<size_t>(p) * L.NXS);
+    std::copy(ms[p].begin(), ms[p].end(), L.msend.begin() + static_cast<size_t>(p) * L.NMS);
+  }
   L.ok = true;
   return L;
 }
