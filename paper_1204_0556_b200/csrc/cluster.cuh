@@ -328,18 +328,23 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
       phase(5);
       ADMM_JITTER();
       cl_barrier();  // B: messages and headers visible
-      bool anync = false;
-      double A = 0.0, B = 0.0;
+      // flags first; the fp64 sums only when every CTA's partials were below
+      // the threshold (rare)
+      int anync = 0;
 #pragma unroll
-      for (int r = 0; r < C; ++r) {
-        anync |= hflag[r] != 0;
-        A += hsum[2 * r];
-        B += hsum[2 * r + 1];
-      }
+      for (int r = 0; r < C; ++r) anync |= hflag[r];
       phase(6);
-      if (!anync && A < p.thr_d && B < p.thr_d) {
-        converged = true;
-        break;
+      if (!anync) {
+        double A = 0.0, B = 0.0;
+#pragma unroll
+        for (int r = 0; r < C; ++r) {
+          A += hsum[2 * r];
+          B += hsum[2 * r + 1];
+        }
+        if (A < p.thr_d && B < p.thr_d) {
+          converged = true;
+          break;
+        }
       }
       if (t >= p.t_max) break;
     }
