@@ -11,7 +11,6 @@ namespace {
 constexpr int kD = 6, kDV = 3, kCPT = 2, kVPT = 4;
 bool g_prof = false;  // launch the profiling instantiation
 const bool g_spread = std::getenv("ADMM_B200_CLUSTER_SPREAD") != nullptr;
-const bool g_zs = std::getenv("ADMM_B200_CLUSTER_ZS") != nullptr;  // A/B: second check's state in smem
 
 // Instantiations: C = 4 CTAs of 1024 threads (one per SM), C = 8 of 512 (two per SM).
 template <int C, bool PROF>
@@ -31,18 +30,6 @@ void set_smem_all(int C, int smem) {
     fns[1] = reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, 4, 1024, true>);
   }
   for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const int zs = smem + 16 * (4096 / C) * (kD / 2);
-  if (C == 8) {
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, 8, 512, false, 1>),
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, zs);
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, 8, 512, true, 1>),
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, zs);
-  } else {
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, 4, 1024, false, 1>),
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, zs);
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, 4, 1024, true, 1>),
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, zs);
-  }
 }
 
 }  // namespace
@@ -106,11 +93,7 @@ cudaError_t launch_t(const ClusterParams& p, int clusters, int smem, cudaStream_
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  if (g_zs) {
-    cfg.dynamicSmemBytes = smem + 16 * NT * (kD / 2);
-    return cudaLaunchKernelEx(&cfg, cluster_decode_kernel<kD, kDV, kCPT, kVPT, C, NT, PROF, 1>, p);
-  }
-  return cudaLaunchKernelEx(&cfg, cluster_decode_kernel<kD, kDV, kCPT, kVPT, C, NT, PROF, 0>, p);
+  return cudaLaunchKernelEx(&cfg, cluster_decode_kernel<kD, kDV, kCPT, kVPT, C, NT, PROF>, p);
 }
 
 cudaError_t cluster_launch(int C, const ClusterParams& p, int clusters, int nt, int smem, cudaStream_t st) {

@@ -125,10 +125,7 @@ struct ClusterSmem {
 // barrier A, check, msg-send, barrier B + decision, iterations}.
 __device__ unsigned long long g_cl_cycles[8];
 
-// ZQ: the edge state (z, lambda/mu) of the last ZQ checks of each thread lives
-// in shared memory as float4 columns {z_2j, z_2j+1, l_2j, l_2j+1} (zs region
-// after the other arrays) instead of registers.
-template <int D, int DV, int CPT, int VPT, int C, int NT, bool PROF = false, int ZQ = 0>
+template <int D, int DV, int CPT, int VPT, int C, int NT, bool PROF = false>
 __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) cluster_decode_kernel(const ClusterParams p) {
   static_assert(D % DV == 0 && D % 2 == 0 && VPT % 2 == 0, "cluster engine: colored fp32 layout");
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -176,10 +173,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
   auto vorig = [&](int q) -> int { return __ldg(own_var + 2 * tid + 2 * NT * (q >> 1) + (q & 1)); };
 
   const float2 rho2 = make_float2(p.rho, p.rho), omr2 = make_float2(p.one_minus_rho, p.one_minus_rho);
-  constexpr int QR = CPT - ZQ;  // checks with register state
-  float2 zp[QR > 0 ? QR : 1][D / 2], lp[QR > 0 ? QR : 1][D / 2];
-  const uint32_t zs_a = smem_u32(smem_raw) + L.total + 16u * tid;  // this thread's float4 column
-  auto zsa = [&](int q, int j) -> uint32_t { return zs_a + 16u * NT * ((q - QR) * (D / 2) + j); };
+  float2 zp[CPT][D / 2], lp[CPT][D / 2];
   const bool prof = PROF && blockIdx.x == 0 && tid == 0;
   long long tp = 0;
   auto phase = [&](int k) {
@@ -206,19 +200,9 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
 #pragma unroll
     for (int j = 0; j < D / 2; ++j) gx2[j] = make_float2(lds(xaddr[q][2 * j], 0.f), lds(xaddr[q][2 * j + 1], 0.f));
     float u[D], zn[D];
-    float2 zo2[D / 2];
 #pragma unroll
     for (int j = 0; j < D / 2; ++j) {
-      float2 l2;
-      if (q >= QR) {
-        const float4 v = lds4(zsa(q, j));
-        zo2[j] = make_float2(v.x, v.y);
-        l2 = make_float2(v.z, v.w);
-      } else {
-        zo2[j] = zp[q][j];
-        l2 = lp[q][j];
-      }
-      u2[j] = __fadd2_rn(__ffma2_rn(rho2, gx2[j], __fmul2_rn(omr2, zo2[j])), l2);
+      u2[j] = __fadd2_rn(__ffma2_rn(rho2, gx2[j], __fmul2_rn(omr2, zp[q][j])), lp[q][j]);
       u[2 * j] = u2[j].x;
       u[2 * j + 1] = u2[j].y;
     }
@@ -228,19 +212,15 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
     for (int j = 0; j < D / 2; ++j) {
       const float2 zn2 = make_float2(zn[2 * j], zn[2 * j + 1]);
       const float2 r1 = fsub2_rn(gx2[j], zn2);
-      const float2 r2 = fsub2_rn(zn2, zo2[j]);
+      const float2 r2 = fsub2_rn(zn2, zp[q][j]);
       if (act) {
         pr2 = __ffma2_rn(r1, r1, pr2);
         mv2 = __ffma2_rn(r2, r2, mv2);
       }
       const float2 ln = fsub2_rn(u2[j], zn2);  // l' = (w + l) - z' = u - z'
       const float2 m2 = fsub2_rn(zn2, ln);
-      if (q >= QR) {
-        sts4(zsa(q, j), make_float4(zn2.x, zn2.y, ln.x, ln.y));
-      } else {
-        lp[q][j] = ln;
-        zp[q][j] = zn2;
-      }
+      lp[q][j] = ln;
+      zp[q][j] = zn2;
       sts(xaddr[q][2 * j] + mstride * (1 + (2 * j) % DV), m2.x);
       sts(xaddr[q][2 * j + 1] + mstride * (1 + (2 * j + 1) % DV), m2.y);
     }
@@ -273,12 +253,8 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
     for (int q = 0; q < CPT; ++q)
 #pragma unroll
       for (int j = 0; j < D / 2; ++j) {
-        if (q >= QR) {
-          sts4(zsa(q, j), make_float4(0.f, 0.f, 0.f, 0.f));
-        } else {
-          zp[q][j] = make_float2(0.f, 0.f);
-          lp[q][j] = make_float2(0.f, 0.f);
-        }
+        zp[q][j] = make_float2(0.f, 0.f);
+        lp[q][j] = make_float2(0.f, 0.f);
       }
     if (tid == 0) misc[1] = 0;
     __syncthreads();
