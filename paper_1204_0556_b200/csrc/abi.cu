@@ -82,6 +82,8 @@ struct admm_graph {
   int cl_nt = 0, cl_smem = 0, cl_clusters = 0, cl_regs = 0;
   int cl_NPL = 0, cl_NXS = 0, cl_NMS = 0, cl_MC = 0, cl_NO = 0;
   int cl_n_xs[admm::kClusterMax] = {}, cl_n_ms[admm::kClusterMax] = {};
+  uint32_t cl_rx_x[admm::kClusterMax] = {}, cl_rx_m[admm::kClusterMax] = {};
+  bool cl_dense = false;  // every part ships x to every other part (mbarrier-variant safety)
   long long cl_exchange = 0;
   int* cl_chk_slot = nullptr;
   int* cl_chk_orig = nullptr;
@@ -429,6 +431,22 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
                 g->cl_n_xs[p] = CL.xs_start[p * (C + 1) + C];
                 g->cl_n_ms[p] = CL.n_ms[p];
               }
+              // bytes each CTA receives per iteration (mbarrier variant): ghost x;
+              // messages + one 20-byte stop-rule header from every CTA
+              bool dense = true;
+              for (int p = 0; p < C; ++p) {
+                uint32_t gx = 0, gm = 0;
+                for (int o = 0; o < C; ++o) {
+                  const int n = CL.xs_start[o * (C + 1) + p + 1] - CL.xs_start[o * (C + 1) + p];
+                  gx += n;
+                  dense = dense && (o == p || n > 0);
+                }
+                for (int q = 0; q < C; ++q)
+                  for (int i = 0; i < CL.n_ms[q]; ++i) gm += (CL.msend[(size_t)q * CL.NMS + i] >> 27) == (uint32_t)p;
+                g->cl_rx_x[p] = 4 * gx;
+                g->cl_rx_m[p] = 4 * gm + 20 * C;
+              }
+              g->cl_dense = dense;
               auto upc = [&](void** dst, const void* src, size_t bytes) -> bool {
                 if (cudaMalloc(dst, bytes) != cudaSuccess) return false;
                 return cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
@@ -873,6 +891,9 @@ int decode_impl(const admm_graph* g, int dtype, int64_t batch, const void* gamma
     for (int r = 0; r < admm::kClusterMax; ++r) {
       cp.n_xs[r] = g->cl_n_xs[r];
       cp.n_ms[r] = g->cl_n_ms[r];
+      cp.rx_x[r] = g->cl_rx_x[r];
+      cp.rx_m[r] = g->cl_rx_m[r];
+      cp.dense = g->cl_dense ? 1 : 0;
     }
     cp.n_vars = g->n_vars;
     cp.n_checks = g->n_checks;

@@ -11,6 +11,7 @@ namespace {
 constexpr int kD = 6, kDV = 3, kCPT = 2, kVPT = 4;
 bool g_prof = false;  // launch the profiling instantiation
 const bool g_spread = std::getenv("ADMM_B200_CLUSTER_SPREAD") != nullptr;
+const bool g_barrier = std::getenv("ADMM_B200_CLUSTER_BARRIER") != nullptr;  // A/B: all-to-all cluster barriers
 
 // Instantiations: C = 4 CTAs of 1024 threads (one per SM), C = 8 of 512 (two per SM).
 template <int C, bool PROF>
@@ -20,15 +21,20 @@ const void* fn_of() {
 
 const void* kernel_fn(int C) { return C == 8 ? fn_of<8, false>() : fn_of<4, false>(); }
 
+template <int C, int NT>
+void fns_of(const void** fns) {
+  fns[0] = reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, C, NT, false, false>);
+  fns[1] = reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, C, NT, true, false>);
+  fns[2] = reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, C, NT, false, true>);
+  fns[3] = reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, C, NT, true, true>);
+}
+
 void set_smem_all(int C, int smem) {
-  const void* fns[2];
-  if (C == 8) {
-    fns[0] = reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, 8, 512, false>);
-    fns[1] = reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, 8, 512, true>);
-  } else {
-    fns[0] = reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, 4, 1024, false>);
-    fns[1] = reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, 4, 1024, true>);
-  }
+  const void* fns[4];
+  if (C == 8)
+    fns_of<8, 512>(fns);
+  else
+    fns_of<4, 1024>(fns);
   for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
@@ -93,7 +99,9 @@ cudaError_t launch_t(const ClusterParams& p, int clusters, int smem, cudaStream_
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  return cudaLaunchKernelEx(&cfg, cluster_decode_kernel<kD, kDV, kCPT, kVPT, C, NT, PROF>, p);
+  if (p.dense && !g_barrier)
+    return cudaLaunchKernelEx(&cfg, cluster_decode_kernel<kD, kDV, kCPT, kVPT, C, NT, PROF, true>, p);
+  return cudaLaunchKernelEx(&cfg, cluster_decode_kernel<kD, kDV, kCPT, kVPT, C, NT, PROF, false>, p);
 }
 
 cudaError_t cluster_launch(int C, const ClusterParams& p, int clusters, int nt, int smem, cudaStream_t st) {

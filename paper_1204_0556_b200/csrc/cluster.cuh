@@ -69,6 +69,48 @@ __device__ __forceinline__ void cl_st_u32(uint32_t a, uint32_t v) {
 __device__ __forceinline__ void cl_st_f64(uint32_t a, double v) {
   asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
+// st.async: non-blocking DSMEM store whose completion releases tx bytes on the
+// destination CTA's mbarrier `mb` (shared::cluster address).
+__device__ __forceinline__ void cl_st_async(uint32_t a, float v, uint32_t mb) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(a),
+               "r"(__float_as_uint(v)), "r"(mb)
+               : "memory");
+}
+__device__ __forceinline__ void cl_st_async_u32(uint32_t a, uint32_t v, uint32_t mb) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(a), "r"(v), "r"(mb)
+               : "memory");
+}
+__device__ __forceinline__ void cl_st_async_f64(uint32_t a, double v, uint32_t mb) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(a),
+               "l"(__double_as_longlong(v)), "r"(mb)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t mb, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mb), "r"(count) : "memory");
+}
+// One arrival that also expects `bytes` of transactions in the current phase.
+__device__ __forceinline__ void mbar_expect(uint32_t mb, uint32_t bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(mb),
+               "r"(bytes)
+               : "memory");
+}
+// Wait for the phase with parity `par` to complete (acquire); a wait that never
+// completes traps after ~2^26 tries instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t par) {
+  for (uint32_t k = 0;; ++k) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(mb), "r"(par)
+        : "memory");
+    if (done) return;
+    if (k > (1u << 26)) {
+      printf("ADMM: cluster mbarrier wait timed out (block %d thread %d)\n", blockIdx.x, threadIdx.x);
+      __trap();
+    }
+  }
+}
 __device__ __forceinline__ void cl_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -87,6 +129,10 @@ struct ClusterParams {
   const uint32_t* msend; // [C][NMS] ms_entry(color, ghost slot, owner's own slot, owner)
   int NPL, NXS, NMS, MC, NO;
   int n_xs[kClusterMax], n_ms[kClusterMax];
+  uint32_t rx_x[kClusterMax], rx_m[kClusterMax];  // MBAR: bytes each CTA receives per iteration
+  // every CTA ships ghost x to every other CTA: the point-to-point (MBAR)
+  // syncs then order every pair of CTAs within one iteration (see the kernel)
+  int dense;
   int n_vars, n_checks;
   // frames
   long long batch;
@@ -108,14 +154,22 @@ struct ClusterParams {
 
 // Shared memory (bytes): X | MSG[DV] | GM (each NPL fp32) | xsend[NXS] u32 |
 // msend[NMS] u32 | header | misc.
+// Stop-rule header one CTA sends to every CTA each iteration: its exact fp64
+// sums (valid when its flag is clear) and its "some partial >= threshold" flag.
+struct ClusterHeader {
+  double primal, moved;
+  uint32_t flag, pad;
+};
+
 struct ClusterSmem {
-  int x, xs, ms, hdr, misc, total;
+  int x, xs, ms, hdr, mbar, misc, total;
   __host__ __device__ ClusterSmem(int NPL, int DV, int NXS, int NMS) {
     x = 0;
     xs = 4 * NPL * (DV + 2);
     ms = xs + 4 * NXS;
-    hdr = (ms + 4 * NMS + 15) & ~15;   // [kClusterMax] {double primal, double moved}, then int flags
-    misc = hdr + kClusterMax * 16 + 16;  // ints: frame, weight, nonint, odd, ... + per-CTA output slots
+    hdr = (ms + 4 * NMS + 15) & ~15;   // [2 parities][kClusterMax] ClusterHeader
+    mbar = hdr + 2 * kClusterMax * 24;   // two mbarriers (x, messages)
+    misc = mbar + 16;                    // ints: frame, weight + per-CTA output slots
     total = misc + 4 * (8 + 3 * kClusterMax) + 64 * 8;  // + fp64 block-reduction slots
   }
 };
@@ -125,7 +179,22 @@ struct ClusterSmem {
 // barrier A, check, msg-send, barrier B + decision, iterations}.
 __device__ unsigned long long g_cl_cycles[8];
 
-template <int D, int DV, int CPT, int VPT, int C, int NT, bool PROF = false>
+// MBAR (default when p.dense): the two per-iteration syncs are point-to-point:
+// every remote store is an st.async that completes tx bytes on the
+// destination's mbarrier, and a CTA waits only for the bytes it receives
+// (ghost x; messages + every CTA's header) instead of an all-to-all cluster
+// barrier (333 -> 354 G edge-updates/s on config 5).  Why no store can land
+// in a buffer or an mbarrier phase still in use:
+//   * o's x-send of iteration t+1 into q follows o's message wait of t, which
+//     needs q's header of t, which q sends after its check phase of t (the
+//     last reader of its ghost x of t, and after q's x-wait of t completed);
+//   * q's msg-send of t+1 into o follows q's x-wait of t+1, which needs o's
+//     x-send of t+1 (dense: every CTA ships x to every other), which follows
+//     o's variable phase of t+1 (the last reader of its message rows of t)
+//     and o's message wait of t;
+//   * headers alternate between two buffers by iteration parity, and the
+//     same chains keep every pair of CTAs within one iteration.
+template <int D, int DV, int CPT, int VPT, int C, int NT, bool PROF = false, bool MBAR = false>
 __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) cluster_decode_kernel(const ClusterParams p) {
   static_assert(D % DV == 0 && D % 2 == 0 && VPT % 2 == 0, "cluster engine: colored fp32 layout");
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -136,8 +205,8 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
   constexpr int nwarps = NT / 32;
   const uint32_t xs_a = smem_u32(smem_raw) + L.x;  // X[NPL]; MSG[j] at +4 NPL (j + 1); GM at +4 NPL (DV + 1)
   const uint32_t mstride = 4u * NPL;
-  double* hsum = reinterpret_cast<double*>(smem_raw + L.hdr);                // [C][2]
-  int* hflag = reinterpret_cast<int*>(smem_raw + L.hdr + kClusterMax * 16);  // [C]
+  ClusterHeader* hdr = reinterpret_cast<ClusterHeader*>(smem_raw + L.hdr);  // [2][kClusterMax]
+  const uint32_t mb_x = smem_u32(smem_raw + L.mbar), mb_m = mb_x + 8;        // mbarriers (MBAR)
   int* misc = reinterpret_cast<int*>(smem_raw + L.misc);                     // [0] frame [1] weight
   int* outslot = misc + 8;                                                   // [C][3] integral, weight, odd
   double* red = reinterpret_cast<double*>(smem_raw + L.misc + 4 * (8 + 3 * kClusterMax));
@@ -228,6 +297,12 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
 
   // zero the whole local slot space once (ghost / spare slots hold finite values)
   for (int i = tid; i < NPL * (DV + 2); i += NT) sts(xs_a + 4u * i, 0.f);
+  if (MBAR && tid == 0) {
+    mbar_init(mb_x, 1);
+    mbar_init(mb_m, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  uint32_t gi = 0;  // iterations run by this CTA (all frames): mbarrier phase parity
   __syncthreads();
   cl_barrier();  // every CTA of the cluster is running before any DSMEM access
 
@@ -279,14 +354,22 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
         for (int i = tid; i < p.n_xs[rank]; i += NT) {
           const uint32_t u = sx[i];
           const float v = lds(xs_a + 4u * (u & 0x1fffu), 0.f);
-          cl_st(cl_addr<C>(xs_a + 4u * ((u >> 13) & 0xffffu), u >> 29), v);
+          if constexpr (MBAR)
+            cl_st_async(cl_addr<C>(xs_a + 4u * ((u >> 13) & 0xffffu), u >> 29), v, cl_mapa(mb_x, u >> 29));
+          else
+            cl_st(cl_addr<C>(xs_a + 4u * ((u >> 13) & 0xffffu), u >> 29), v);
         }
       }
       pr2 = make_float2(0.f, 0.f);
       mv2 = make_float2(0.f, 0.f);
       phase(2);
       ADMM_JITTER();
-      cl_barrier();  // A: ghost x visible; every CTA done with its message rows
+      if constexpr (MBAR) {
+        if (tid == 0) mbar_expect(mb_x, p.rx_x[rank]);
+        mbar_wait(mb_x, gi & 1);  // A: every ghost x of this iteration landed
+      } else {
+        cl_barrier();  // A: ghost x visible; every CTA done with its message rows
+      }
       phase(3);
 #pragma unroll
       for (int q = 0; q < CPT; ++q) check(q);
@@ -316,30 +399,48 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
           const uint32_t u = sm[i];
           const uint32_t row = mstride * ((u & 3u) + 1);
           const float v = lds(xs_a + row + 4u * ((u >> 2) & 0x1fffu), 0.f);
-          cl_st(cl_addr<C>(xs_a + row + 4u * ((u >> 15) & 0xfffu), u >> 27), v);
+          if constexpr (MBAR)
+            cl_st_async(cl_addr<C>(xs_a + row + 4u * ((u >> 15) & 0xfffu), u >> 27), v, cl_mapa(mb_m, u >> 27));
+          else
+            cl_st(cl_addr<C>(xs_a + row + 4u * ((u >> 15) & 0xfffu), u >> 27), v);
         }
       }
       if (tid < C) {
         const uint32_t r = tid;
-        cl_st_f64(cl_addr<C>(smem_u32(hsum + 2 * rank), r, 8), sa);
-        cl_st_f64(cl_addr<C>(smem_u32(hsum + 2 * rank + 1), r, 8), sb);
-        cl_st_u32(cl_addr<C>(smem_u32(hflag + rank), r), static_cast<uint32_t>(nc));
+        ClusterHeader* h = hdr + (MBAR ? (gi & 1) * kClusterMax : 0) + rank;
+        if constexpr (MBAR) {
+          const uint32_t mb = cl_addr<C>(mb_m, r, 8);
+          cl_st_async_f64(cl_addr<C>(smem_u32(&h->primal), r, 8), sa, mb);
+          cl_st_async_f64(cl_addr<C>(smem_u32(&h->moved), r, 8), sb, mb);
+          cl_st_async_u32(cl_addr<C>(smem_u32(&h->flag), r), static_cast<uint32_t>(nc), mb);
+        } else {
+          cl_st_f64(cl_addr<C>(smem_u32(&h->primal), r, 8), sa);
+          cl_st_f64(cl_addr<C>(smem_u32(&h->moved), r, 8), sb);
+          cl_st_u32(cl_addr<C>(smem_u32(&h->flag), r), static_cast<uint32_t>(nc));
+        }
       }
       phase(5);
       ADMM_JITTER();
-      cl_barrier();  // B: messages and headers visible
+      if constexpr (MBAR) {
+        if (tid == 0) mbar_expect(mb_m, p.rx_m[rank]);
+        mbar_wait(mb_m, gi & 1);  // B: our messages and every CTA's header landed
+      } else {
+        cl_barrier();  // B: messages and headers visible
+      }
+      const ClusterHeader* hd = hdr + (MBAR ? (gi & 1) * kClusterMax : 0);
+      ++gi;
       // flags first; the fp64 sums only when every CTA's partials were below
       // the threshold (rare)
-      int anync = 0;
+      uint32_t anync = 0;
 #pragma unroll
-      for (int r = 0; r < C; ++r) anync |= hflag[r];
+      for (int r = 0; r < C; ++r) anync |= hd[r].flag;
       phase(6);
       if (!anync) {
         double A = 0.0, B = 0.0;
 #pragma unroll
         for (int r = 0; r < C; ++r) {
-          A += hsum[2 * r];
-          B += hsum[2 * r + 1];
+          A += hd[r].primal;
+          B += hd[r].moved;
         }
         if (A < p.thr_d && B < p.thr_d) {
           converged = true;
