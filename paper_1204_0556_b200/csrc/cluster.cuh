@@ -276,16 +276,15 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
       u[2 * j + 1] = u2[j].y;
     }
     project_pp_fixed<float, D>(u, zn);
-    const bool act = (cmask >> q) & 1u;
+    // idle checks run on the part's spare slot, whose x, z, l and messages stay
+    // exactly 0 (u = 0 projects to 0): their residuals are 0, no predicate
 #pragma unroll
     for (int j = 0; j < D / 2; ++j) {
       const float2 zn2 = make_float2(zn[2 * j], zn[2 * j + 1]);
       const float2 r1 = fsub2_rn(gx2[j], zn2);
       const float2 r2 = fsub2_rn(zn2, zp[q][j]);
-      if (act) {
-        pr2 = __ffma2_rn(r1, r1, pr2);
-        mv2 = __ffma2_rn(r2, r2, mv2);
-      }
+      pr2 = __ffma2_rn(r1, r1, pr2);
+      mv2 = __ffma2_rn(r2, r2, mv2);
       const float2 ln = fsub2_rn(u2[j], zn2);  // l' = (w + l) - z' = u - z'
       const float2 m2 = fsub2_rn(zn2, ln);
       lp[q][j] = ln;

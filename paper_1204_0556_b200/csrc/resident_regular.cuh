@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
   const float2 rho2 = make_float2(float(p.rho), float(p.rho));
   const float2 omr2 = make_float2(float(p.one_minus_rho), float(p.one_minus_rho));
 
+  if (COL && tid == 0) sts(xs_a + ES * N, T(0));  // spare slot (no thread owns it when N == VPT * NT)
   for (;;) {
     __syncthreads();
     if (tid == 0) {
@@ -214,7 +215,8 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
           z[q][k] = z0;
           lam[q][k] = s0;
         }
-        if (cact[q]) sts(xaddr[q][k] + moff(q, k), sub_rn(z0, s0));
+        // (COL: idle checks zero the spare slot's messages, so its x stays 0)
+        if (COL || cact[q]) sts(xaddr[q][k] + moff(q, k), sub_rn(z0, s0));
       }
     }
     __syncthreads();
@@ -281,8 +283,8 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
         float2 pr2 = make_float2(0.f, 0.f), mv2 = make_float2(0.f, 0.f);
 #pragma unroll
         for (int q = 0; q < CPT; ++q) {
-          // COL: idle checks run on the spare slot; their residuals are dropped
-          const float2 pr_in = pr2, mv_in = mv2;
+          // COL: idle checks run on the spare slot N, whose x, z, l and messages
+          // stay exactly 0 (u = 0 projects to 0), so their residuals are 0
           if (COL || cact[q]) {
             float2 gx2[D / 2], u2[D / 2], z2[D / 2], l2[D / 2];
 #pragma unroll
@@ -325,10 +327,6 @@ __global__ void __launch_bounds__(MAXT, MINB) resident_regular_kernel(const Resi
               sts(xaddr[q][2 * j] + moff(q, 2 * j), m2.x);
               sts(xaddr[q][2 * j + 1] + moff(q, 2 * j + 1), m2.y);
             }
-          }
-          if (COL && !cact[q]) {
-            pr2 = pr_in;
-            mv2 = mv_in;
           }
         }
         primal = pr2.x + pr2.y;
