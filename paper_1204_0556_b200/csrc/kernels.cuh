@@ -77,6 +77,17 @@ inline T thr_round_up(double thr) {
   }
 }
 
+// Fixed-point scale of the fp32 stop-rule sums (ResidentParams::fx_scale):
+// the power of two that puts the fp32 threshold in [2^20, 2^21).
+inline float fx_scale_of(double thr) {
+  int e;
+  std::frexp(static_cast<double>(thr_round_up<float>(thr)), &e);  // thr_f = m 2^e, m in [0.5, 1)
+  return std::ldexp(1.0f, 21 - e);
+}
+inline unsigned long long fx_thr_of(double thr) {
+  return static_cast<unsigned long long>(std::ceil(thr * static_cast<double>(fx_scale_of(thr)) * 2097152.0));
+}
+
 template <typename T>
 ResidentParams<T> make_params(const ResidentGraphArgs& g, const ResidentFrameArgs& a) {
   ResidentParams<T> p;
@@ -99,6 +110,8 @@ ResidentParams<T> make_params(const ResidentGraphArgs& g, const ResidentFrameArg
   p.one_minus_rho = T(1.0 - a.rho);
   p.thr = thr_round_up<T>(a.thr);
   p.thr_d = a.thr;
+  p.fx_scale = fx_scale_of(a.thr);
+  p.fx_thr = fx_thr_of(a.thr);
   p.t_max = a.t_max;
   p.z_in = static_cast<const T*>(a.z_in);
   p.lam_in = static_cast<const T*>(a.lam_in);

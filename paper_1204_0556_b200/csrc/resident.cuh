@@ -52,6 +52,11 @@ struct ResidentParams {
   // rounded UP, so a per-thread partial >= thr implies partial >= thr_d.
   T mu, inv_mu, rho, one_minus_rho, thr;
   double thr_d;
+  // fp32 regular kernel: the exact stop-rule sums as 42-bit fixed point
+  // (fx_sum below): fx_scale = 2^k with thr * fx_scale in [2^20, 2^21),
+  // fx_thr = ceil(thr_d * fx_scale * 2^21).
+  float fx_scale;
+  unsigned long long fx_thr;
   int t_max;
   // optional initial state (reference edge order), null = zeros
   const T* z_in;
