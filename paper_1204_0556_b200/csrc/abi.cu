@@ -888,6 +888,14 @@ int decode_impl(const admm_graph* g, int dtype, int64_t batch, const void* gamma
     cp.NMS = g->cl_NMS;
     cp.MC = g->cl_MC;
     cp.NO = g->cl_NO;
+    {
+      const admm::ClusterSmem L(cp.NPL, 3, cp.NXS, cp.NMS);
+      cp.sm_xs = L.xs;
+      cp.sm_ms = L.ms;
+      cp.sm_hdr = L.hdr;
+      cp.sm_mbar = L.mbar;
+      cp.sm_misc = L.misc;
+    }
     for (int r = 0; r < admm::kClusterMax; ++r) {
       cp.n_xs[r] = g->cl_n_xs[r];
       cp.n_ms[r] = g->cl_n_ms[r];

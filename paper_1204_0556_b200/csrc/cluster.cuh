@@ -114,6 +114,18 @@ __device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t par) {
 __device__ __forceinline__ void cl_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// CTA-rank bits of a shared::cluster address (checked at kernel start)
+constexpr uint32_t kCtaBits = 0xff000000u;
+__device__ __forceinline__ uint2 lds2u(uint32_t a) {
+  ADMM_CHECK_SMEM(a, 8);
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts2u(uint32_t a, uint32_t x, uint32_t y) {
+  ADMM_CHECK_SMEM(a, 8);
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
+}
 __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
@@ -128,6 +140,7 @@ struct ClusterParams {
   const uint32_t* xsend; // [C][NXS] xs_pack(own slot, ghost slot, rank)
   const uint32_t* msend; // [C][NMS] ms_entry(color, ghost slot, owner's own slot, owner)
   int NPL, NXS, NMS, MC, NO;
+  int sm_xs, sm_ms, sm_hdr, sm_mbar, sm_misc;  // ClusterSmem offsets (host-computed: constant-bank operands)
   int n_xs[kClusterMax], n_ms[kClusterMax];
   uint32_t rx_x[kClusterMax], rx_m[kClusterMax];  // MBAR: bytes each CTA receives per iteration
   // every CTA ships ghost x to every other CTA: the point-to-point (MBAR)
@@ -152,8 +165,8 @@ struct ClusterParams {
   SynthParams synth;
 };
 
-// Shared memory (bytes): X | MSG[DV] | GM (each NPL fp32) | xsend[NXS] u32 |
-// msend[NMS] u32 | header | misc.
+// Shared memory (bytes): X | MSG[DV] | GM (each NPL fp32) | xsend[NXS] |
+// msend[NMS] (8-byte pre-mapped entries, below) | header | mbarriers | misc.
 // Stop-rule header one CTA sends to every CTA each iteration: its exact fp64
 // sums (valid when its flag is clear) and its "some partial >= threshold" flag.
 struct ClusterHeader {
@@ -166,8 +179,8 @@ struct ClusterSmem {
   __host__ __device__ ClusterSmem(int NPL, int DV, int NXS, int NMS) {
     x = 0;
     xs = 4 * NPL * (DV + 2);
-    ms = xs + 4 * NXS;
-    hdr = (ms + 4 * NMS + 15) & ~15;   // [2 parities][kClusterMax] ClusterHeader
+    ms = xs + 8 * NXS;
+    hdr = (ms + 8 * NMS + 15) & ~15;   // [2 parities][kClusterMax] ClusterHeader
     mbar = hdr + 2 * kClusterMax * 24;   // two mbarriers (x, messages)
     misc = mbar + 16;                    // ints: frame, weight + per-CTA output slots
     total = misc + 4 * (8 + 3 * kClusterMax) + 64 * 8;  // + fp64 block-reduction slots
@@ -199,26 +212,45 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
   static_assert(D % DV == 0 && D % 2 == 0 && VPT % 2 == 0, "cluster engine: colored fp32 layout");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int NPL = p.NPL;
-  const ClusterSmem L(NPL, DV, p.NXS, p.NMS);
   const uint32_t rank = cl_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarps = NT / 32;
-  const uint32_t xs_a = smem_u32(smem_raw) + L.x;  // X[NPL]; MSG[j] at +4 NPL (j + 1); GM at +4 NPL (DV + 1)
+  const uint32_t xs_a = smem_u32(smem_raw);  // X[NPL]; MSG[j] at +4 NPL (j + 1); GM at +4 NPL (DV + 1)
   const uint32_t mstride = 4u * NPL;
-  ClusterHeader* hdr = reinterpret_cast<ClusterHeader*>(smem_raw + L.hdr);  // [2][kClusterMax]
-  const uint32_t mb_x = smem_u32(smem_raw + L.mbar), mb_m = mb_x + 8;        // mbarriers (MBAR)
-  int* misc = reinterpret_cast<int*>(smem_raw + L.misc);                     // [0] frame [1] weight
+  ClusterHeader* hdr = reinterpret_cast<ClusterHeader*>(smem_raw + p.sm_hdr);  // [2][kClusterMax]
+  const uint32_t mb_x = smem_u32(smem_raw + p.sm_mbar), mb_m = mb_x + 8;        // mbarriers (MBAR)
+  int* misc = reinterpret_cast<int*>(smem_raw + p.sm_misc);                     // [0] frame [1] weight
   int* outslot = misc + 8;                                                   // [C][3] integral, weight, odd
-  double* red = reinterpret_cast<double*>(smem_raw + L.misc + 4 * (8 + 3 * kClusterMax));
+  double* red = reinterpret_cast<double*>(smem_raw + p.sm_misc + 4 * (8 + 3 * kClusterMax));
 
-  // ---- per-part tables into shared memory (once per CTA) ----
+  // ---- per-part exchange tables into shared memory (once per CTA), pre-mapped:
+  // 8-byte entries {local source address, DSMEM destination address}, so an
+  // exchange costs per entry one LDS.64, the source LDS, one LOP3 (the
+  // destination's mbarrier: same CTA bits, fixed offset) and the st.async ----
+  const uint32_t tx_a = smem_u32(smem_raw) + p.sm_xs + 8u * tid, tm_a = smem_u32(smem_raw) + p.sm_ms + 8u * tid;
   {
     const uint32_t* gx = p.xsend + static_cast<size_t>(rank) * p.NXS;
     const uint32_t* gms = p.msend + static_cast<size_t>(rank) * p.NMS;
-    uint32_t* sx = reinterpret_cast<uint32_t*>(smem_raw + L.xs);
-    uint32_t* sm = reinterpret_cast<uint32_t*>(smem_raw + L.ms);
-    for (int i = tid; i < p.NXS; i += NT) sx[i] = __ldg(gx + i);
-    for (int i = tid; i < p.NMS; i += NT) sm[i] = __ldg(gms + i);
+    for (int i = tid; i < p.n_xs[rank]; i += NT) {
+      const uint32_t u = __ldg(gx + i);
+      sts2u(tx_a + 8u * (i - tid), xs_a + 4u * (u & 0x1fffu), cl_addr<C>(xs_a + 4u * ((u >> 13) & 0xffffu), u >> 29));
+    }
+    for (int i = tid; i < p.n_ms[rank]; i += NT) {
+      const uint32_t u = __ldg(gms + i);
+      const uint32_t row = 4u * NPL * ((u & 3u) + 1);
+      sts2u(tm_a + 8u * (i - tid), xs_a + row + 4u * ((u >> 2) & 0x1fffu),
+            cl_addr<C>(xs_a + row + 4u * ((u >> 15) & 0xfffu), u >> 27));
+    }
+    // shared::cluster addresses keep the CTA in the bits above the offset (a
+    // CTA's own shared addresses carry its own): a destination's mbarrier is
+    // (dst & kCtaBits) | (own mbarrier & ~kCtaBits)
+    if (tid < C) {
+      const uint32_t m = cl_mapa(mb_x, tid), a = cl_mapa(xs_a, tid);
+      if (((m ^ mb_x) & ~kCtaBits) != 0 || ((a ^ xs_a) & ~kCtaBits) != 0 || (m & kCtaBits) != (a & kCtaBits)) {
+        printf("ADMM: unexpected shared::cluster address layout (%x -> %x, %x -> %x)\n", mb_x, m, xs_a, a);
+        __trap();
+      }
+    }
   }
 
   // ---- per-thread graph registers: checks lc = tid + q NT, own variable
@@ -253,6 +285,17 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
     }
   };
 
+  // one table-driven exchange: entry i of this CTA's table is handled by thread i mod NT
+  auto exchange = [&](uint32_t ta, int n, uint32_t mb) {
+    for (int k = n - tid; k > 0; k -= NT, ta += 8u * NT) {
+      const uint2 e = lds2u(ta);
+      const float v = lds(e.x, 0.f);
+      if constexpr (MBAR)
+        cl_st_async(e.y, v, (e.y & kCtaBits) | (mb & ~kCtaBits));
+      else
+        cl_st(e.y, v);
+    }
+  };
   // x-update of own pair h (admm_decoder.py:108-124; colors summed in order)
   auto var_pair = [&](int h) {
     const uint32_t a = xst(2 * h);
@@ -348,17 +391,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
       __syncthreads();
       phase(1);
       // ---- x-send: own x -> ghost slots of the other CTAs (coalesced per warp) ----
-      {
-        const uint32_t* sx = reinterpret_cast<const uint32_t*>(smem_raw + L.xs);
-        for (int i = tid; i < p.n_xs[rank]; i += NT) {
-          const uint32_t u = sx[i];
-          const float v = lds(xs_a + 4u * (u & 0x1fffu), 0.f);
-          if constexpr (MBAR)
-            cl_st_async(cl_addr<C>(xs_a + 4u * ((u >> 13) & 0xffffu), u >> 29), v, cl_mapa(mb_x, u >> 29));
-          else
-            cl_st(cl_addr<C>(xs_a + 4u * ((u >> 13) & 0xffffu), u >> 29), v);
-        }
-      }
+      exchange(tx_a, p.n_xs[rank], mb_x);
       pr2 = make_float2(0.f, 0.f);
       mv2 = make_float2(0.f, 0.f);
       phase(2);
@@ -392,18 +425,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
       }
       phase(4);
       // ---- msg-send: ghost-row messages -> the owners' message rows; stop-rule header ----
-      {
-        const uint32_t* sm = reinterpret_cast<const uint32_t*>(smem_raw + L.ms);
-        for (int i = tid; i < p.n_ms[rank]; i += NT) {
-          const uint32_t u = sm[i];
-          const uint32_t row = mstride * ((u & 3u) + 1);
-          const float v = lds(xs_a + row + 4u * ((u >> 2) & 0x1fffu), 0.f);
-          if constexpr (MBAR)
-            cl_st_async(cl_addr<C>(xs_a + row + 4u * ((u >> 15) & 0xfffu), u >> 27), v, cl_mapa(mb_m, u >> 27));
-          else
-            cl_st(cl_addr<C>(xs_a + row + 4u * ((u >> 15) & 0xfffu), u >> 27), v);
-        }
-      }
+      exchange(tm_a, p.n_ms[rank], mb_m);
       if (tid < C) {
         const uint32_t r = tid;
         ClusterHeader* h = hdr + (MBAR ? (gi & 1) * kClusterMax : 0) + rank;
