@@ -419,10 +419,9 @@ def decode_batch(
                lam_out=lo, workspace=ws, stream=st)
     res = BatchResult(iterations=iters, flags=flags, weight=weight, x=x, hard=hard, z=zo, lam=lo,
                       info=dg.call_info(code_dt, B))
-    # the temporaries were allocated on `st`, so the allocator reuses their
-    # memory only for work ordered after the kernel; the reference keeps the
-    # host-side objects alive for the caller's convenience
-    res._keepalive = (g, zi, li, ws)  # type: ignore[attr-defined]
+    # the temporaries (converted inputs, workspace: up to 12 GiB on the wide
+    # kernel) were allocated on `st`, so the allocator reuses their memory only
+    # for work ordered after the kernel: nothing has to be kept alive
     return res
 
 
@@ -531,5 +530,5 @@ def decode_synth(code, channel, config: AdmmConfig = AdmmConfig(), *, seed: int,
             _ptr(x), N, _ptr(hard), N, iters.data_ptr(), flags.data_ptr(), weight.data_ptr(),
             ws.data_ptr(), ws_bytes, st.cuda_stream))
     res = BatchResult(iterations=iters, flags=flags, weight=weight, x=x, hard=hard, info=dg.call_info(code_dt, batch))
-    res._keepalive = (ws,)  # type: ignore[attr-defined]
+    # (ws was allocated on `st`: its memory is only reused by work ordered after the kernel)
     return res

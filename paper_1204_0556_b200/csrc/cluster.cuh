@@ -344,6 +344,11 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
     mbar_init(mb_m, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (PROF && tid == 0) {  // placement: which CTAs share an SM (tools/cluster_phases.py --placement)
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    printf("cta %d cluster %d rank %u smid %u\n", blockIdx.x, blockIdx.x / C, rank, smid);
+  }
   uint32_t gi = 0;  // iterations run by this CTA (all frames): mbarrier phase parity
   __syncthreads();
   cl_barrier();  // every CTA of the cluster is running before any DSMEM access

@@ -300,6 +300,28 @@ def test_cluster_engine_matches_wide_and_synthesis(cuda_ok):
         assert torch.equal(c1.iterations, a.iterations[:17])
 
 
+def test_cluster_sizes_agree(cuda_ok, monkeypatch):
+    """The default 8-CTA clusters (two CTAs per SM) and the 4-CTA fallback
+    decode every frame identically: the partition changes which CTA owns a
+    check, not the arithmetic of any edge or the (exact) stop rule."""
+    import copy
+
+    from paper_1204_0556_b200 import AdmmConfig, Awgn, baseline_code, decode_synth
+
+    code = baseline_code("cfg5_n16384")
+    cfg = AdmmConfig(mu=5.0)
+    ch = Awgn(2.0, code.design_rate)
+    a = decode_synth(code, ch, cfg, seed=11, point=0, trial0=7, batch=96, want_hard=True, engine="cluster")
+    assert a.info["cluster_size"] == 8 and a.info["cluster_threads"] == 512
+    monkeypatch.setenv("ADMM_B200_CLUSTER", "4")
+    code4 = copy.copy(code)
+    code4._device_graphs = {}
+    b = decode_synth(code4, ch, cfg, seed=11, point=0, trial0=7, batch=96, want_hard=True, engine="cluster")
+    assert b.info["cluster_size"] == 4 and b.info["cluster_threads"] == 1024
+    assert torch.equal(a.iterations, b.iterations) and torch.equal(a.flags, b.flags)
+    assert torch.equal(a.hard, b.hard) and torch.equal(a.weight, b.weight)
+
+
 def test_cluster_engine_rejects_fp64_and_state_io(cuda_ok):
     from paper_1204_0556_b200 import AdmmConfig, baseline_code, decode_batch
 

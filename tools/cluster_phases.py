@@ -13,6 +13,9 @@ from paper_1204_0556_b200 import AdmmConfig, Awgn, baseline_code, decode_synth, 
 ap = argparse.ArgumentParser()
 ap.add_argument("--frames", type=int, default=4096)
 a = ap.parse_args()
+# The profiling instantiation also prints one "cta B cluster K rank R smid S"
+# line per CTA: pipe the output through `grep ^cta` to see which CTAs share an
+# SM (8-CTA clusters: two CTAs per SM, never of the same cluster).
 code = baseline_code("cfg5_n16384")
 cfg = AdmmConfig(mu=5.0)
 ch = Awgn(2.5, 0.5)
