@@ -89,6 +89,8 @@ def parse():
     ap.add_argument("--e2e-block", type=int, default=65536, help="frames per host block of the e2e pipeline")
     ap.add_argument("--e2e-pool", type=int, default=131072,
                     help="distinct host LLR frames per point of the e2e leg of synthesised workloads")
+    ap.add_argument("--e2e-seconds", type=float, default=60.0,
+                    help="time budget of the e2e leg: it times min(--steps, what fits) steps, at least 2")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--cpu-frames", type=int, default=0, help="oracle frames per point (0 = auto)")
     ap.add_argument("--stub", action="store_true",
@@ -398,7 +400,10 @@ def run_ours(args, wl: Workload):
     # results (iterations, flags, weights) out
     e2e = None
     if not args.no_e2e:
-        blk = min(args.e2e_block, frames_local // len(wl.points))
+        # (multi-GPU: smaller blocks and pool per rank -- the ranks of one node
+        # share the host's pinned memory; every step still copies the LLRs of all
+        # of the rank's frames)
+        blk = min(args.e2e_block, max(frames_local // len(wl.points) // (4 if world > 1 else 1), 1))
         # outputs as in the device-timed leg: per-frame iterations, flags and
         # Hamming weight (the harness's TrialStats inputs; hard decisions on request)
         pipe = HostPipeline(code, cfg, dtype=tdt, device=dev, max_batch=blk, want_hard=False, reuse_outputs=True)
@@ -410,7 +415,7 @@ def run_ours(args, wl: Workload):
             # rank's shard), staged once in pinned host memory; the blocks of a
             # step cycle through it so that every step copies the LLRs of all of
             # the rank's frames
-            P = max(blk, min(args.e2e_pool, len(mine)) // blk * blk)
+            P = max(blk, min(args.e2e_pool // world, len(mine)) // blk * blk)
             host = []
             for k, ch in enumerate(chans):
                 pool = torch.empty((P, code.n_vars), dtype=tdt, pin_memory=True)
@@ -429,10 +434,14 @@ def run_ours(args, wl: Workload):
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
+        # the e2e leg times min(K, what fits --e2e-seconds) steps (same on every
+        # rank: `elapsed` is the max over ranks), so a large --steps does not
+        # double the run; the count is reported beside the value
+        e_steps = max(2, min(args.steps, int(args.e2e_seconds / max(elapsed / args.steps, 1e-9))))
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(e_steps):
             pipe.run(host)
         e1.record(stream)
         torch.cuda.synchronize(dev)
@@ -440,7 +449,7 @@ def run_ours(args, wl: Workload):
         nb = torch.tensor([pipe.h2d_bytes_per_run(host), pipe.d2h_bytes_per_run(host)], dtype=torch.int64, device=dev)
         if world > 1:
             dist.all_reduce(nb)
-        e2e = {"value": frames_all * args.steps / e_el, "unit": "frames/s",
+        e2e = {"value": frames_all * e_steps / e_el, "unit": "frames/s", "steps": e_steps,
                "h2d_bytes_per_step": int(nb[0]), "d2h_bytes_per_step": int(nb[1]),
                "api": "paper_1204_0556_b200.pipeline.HostPipeline.run (decode_batch on three streams)",
                "inputs": pool_note, "block_frames": blk}
