@@ -173,6 +173,11 @@ def cpu_sample(wl: Workload, code, frames_per_point: int, workers: int, seed_bas
     t0 = time.perf_counter()
     iters, _conv, _hard = O.decode_parallel(gam, g, O.Params(mu=MU, epsilon=EPS, t_max=TMAX, rho=RHO), workers)
     dt = time.perf_counter() - t0
+    # the sample's own statistics, for a cross-check of the GPU line's (same
+    # channel points, all-zero codeword: a word error is any non-zero decision)
+    cpu_sample.last_stats = {"mean_iterations": float(np.mean(iters)),
+                             "word_errors": int(np.count_nonzero(np.asarray(_hard).reshape(len(gam), -1).any(axis=1))),
+                             "frames": len(gam)}
     return dt, len(gam), int(iters.sum()) * code.n_edges
 
 
@@ -461,6 +466,7 @@ def run_ours(args, wl: Workload):
         fpp = args.cpu_frames or auto_cpu_frames(wl, code, workers)
         dt, nf, eu = cpu_sample(wl, code, fpp, workers)
         cpu = {"value": nf / dt, "unit": "frames/s", "cores": workers, "kind": "port", "edge_updates_per_s": eu / dt,
+               "sample_stats": getattr(cpu_sample, "last_stats", None),
                "sample": f"{fpp} frames per channel point x {len(wl.points)} points (the same workload's channel "
                          f"points, numpy-seeded trials), oracle/admm_oracle.py over {workers} processes, {cpu_model()}"}
 
