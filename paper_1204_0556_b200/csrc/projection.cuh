@@ -1,32 +1,23 @@
 // Exact Euclidean projection onto the parity polytope PP_d, in registers.
 //
-// Contract: the reference's project_batch (parity_polytope.py:352-421).
-//   v  = u sorted descending (stable)                      :366-367
-//   c  = clip(v, 0, 1); r = 2 floor(sum c / 2), r <= d       :368-372
-//   f  = +1 on the top r+1 coordinates, -1 elsewhere          :374
-//   fz = 2 * sum_{k<=r} c_k - sum c                           :375-376
-//   beta_max = (v_r - v_{r+1}) / 2, or v_r when r = d-1       :378-380
-//   inside (return c) when r >= d, fz <= r + TOL, beta_max<=0 :382
-//   otherwise z = clip(v - beta f, 0, 1) with beta the root of
-//   g(beta) = f . clip(v - beta f, 0, 1) = r on [0, beta_max], capped at
-//   beta_max when g stays above r                             :385-414
-//
-// B200 formulation (no grid, no permutation).  Writing s_k for the shift at
-// which coordinate k enters the open band (0,1) -- s_k = u_k - 1 on the +1
-// block and s_k = -u_k on the -1 block -- every coordinate is active on
-// exactly (s_k, s_k + 1), so g(beta) = (r + 1) - sum_k clip(beta - s_k, 0, 1)
-// and g(beta) = r  <=>  sum_k max(beta - s_k, 0) = 1 below the root.  That is
-// water-filling: with s sorted ascending and P_j = 1 + s_(1) + ... + s_(j),
-// every partial line (P_j)/j over-estimates the root and the active prefix
-// attains it, so
-//          beta* = min(beta_max, min_j P_j / j).
-// Two value-only sorting networks (no index payload: f is recovered as
-// u_k >= v_r, exact whenever the row is projected because v_r > v_{r+1}
-// then) and one prefix scan replace the reference's O(d^2) grid evaluation.
-// The result agrees with project_batch to rounding (tests/test_projection*).
+// Contract: the reference's project_batch (parity_polytope.py:352-421), which
+//   sorts v = u descending, takes r = 2 floor(sum clip(v) / 2)        :366-372
+//   tests the facet f = +1 on the top r+1 coordinates, -1 elsewhere   :374-382
+//   and otherwise returns z = clip(v - beta f, 0, 1) with beta the root of
+//   g(beta) = f . clip(v - beta f, 0, 1) = r on [0, beta_max]         :385-414
+// Writing s_k for the shift at which coordinate k enters the open band (0,1)
+// -- s_k = u_k - 1 on the +1 block, -u_k on the -1 block -- every coordinate is
+// active on exactly (s_k, s_k + 1), so g(beta) = (r + 1) - sum_k clip(beta -
+// s_k, 0, 1) and the root solves sum_k max(beta - s_k, 0) = 1: water-filling.
+// With s sorted ascending and P_j = 1 + s_(1) + ... + s_(j) every P_j / j
+// over-estimates the root and the active prefix attains it.  The cut-search
+// formulation below gets the block f, the sorted shifts and the facet test
+// from ONE sorting network.  Results agree with project_batch to rounding
+// (tests/test_gpu_projection.py against the reference's goldens,
+// tests/test_projection_cut.py for the formulation itself).
 //
 // Degree handling: arrays are sized D (a compile-time bucket); the active
-// degree d <= D is a runtime value and padded slots must hold -inf in u.
+// degree d <= D is implied by the padding: slots k >= d must hold -inf in u.
 #pragma once
 
 #include "common.cuh"
@@ -37,8 +28,9 @@ namespace admm {
 // Sum of c[0..d) in numpy's pairwise_sum order for short rows: sequential
 // below 8 elements, eight interleaved partial sums combined as a tree and a
 // sequential tail otherwise.  Zeros in padded slots leave the sequential sum
-// unchanged.  Only matters at rounding level (it fixes r = even floor of the
-// l1 norm bit-exactly in fp64 where the norm sits on an even integer).
+// unchanged.  Used by the membership kernel (steps.cu), whose r = even floor
+// of the l1 norm must match the reference bit for bit where the norm sits on
+// an even integer.
 template <typename T, int D>
 __device__ __forceinline__ T numpy_rowsum(const T (&c)[D], int d) {
   T seq = c[0];
@@ -182,167 +174,17 @@ __device__ __forceinline__ void project_pp_cut(const T (&u)[D], T (&z)[D]) {
   }
 }
 
-// Project u (degree d <= D; u[k] = -inf for k >= d) onto PP_d.  z[k] for
-// k >= d is left as 0.  Returns true when the facet test sent the row through
-// the water-filling search (diagnostics only).
+// Project u (degree d <= D; u[k] = -inf for k >= d) onto PP_d; z[k] = 0 for
+// k >= d.  Generic-degree kernels (resident.cuh, steps.cu, project.cu).
 template <typename T, int D>
-__device__ __forceinline__ bool project_pp(const T (&u)[D], T (&z)[D], int d) {
-#ifndef ADMM_PROJ_TWO_SORT
+__device__ __forceinline__ void project_pp(const T (&u)[D], T (&z)[D], int /*d*/) {
   project_pp_cut<T, D>(u, z);
-  return true;
-#endif
-  T v[D];
-#pragma unroll
-  for (int k = 0; k < D; ++k) v[k] = u[k];
-  SortNet<D>::desc(v);
-
-  T c[D];
-#pragma unroll
-  for (int k = 0; k < D; ++k) c[k] = clip01(v[k]);
-  const T total = numpy_rowsum<T, D>(c, d);
-  int r = 2 * static_cast<int>(floor(total * T(0.5)));
-  r = r < d ? r : d;
-  const int top = r < d - 1 ? r : d - 1;
-  const int nxt = (r + 1) < (d - 1) ? (r + 1) : (d - 1);
-
-  // Order statistics v_top, v_nxt and the head sum sum_{k<=top} c_k, read
-  // out of the sorted registers with compile-time indices.
-  T v_top = v[0], v_nxt = v[0], head = c[0], run = c[0];
-#pragma unroll
-  for (int k = 1; k < D; ++k) {
-    run = add_rn(run, c[k]);
-    if (k == top) { v_top = v[k]; head = run; }
-    if (k == nxt) v_nxt = v[k];
-  }
-  const T fz = sub_rn(mul_rn(T(2), head), total);
-  const T beta_max = (r <= d - 2) ? mul_rn(T(0.5), sub_rn(v_top, v_nxt)) : v_top;
-  const bool inside = (r >= d) || (fz <= T(r) + Num<T>::kTol) || (beta_max <= T(0));
-
-  if (inside) {
-#pragma unroll
-    for (int k = 0; k < D; ++k) z[k] = (k < d) ? clip01(u[k]) : T(0);
-    return false;
-  }
-
-  // Water-filling for the shift beta (see header comment).
-  T s[D];
-#pragma unroll
-  for (int k = 0; k < D; ++k) s[k] = (u[k] >= v_top) ? sub_rn(u[k], T(1)) : -u[k];  // pads: +inf
-  SortNet<D>::asc(s);
-  T beta = beta_max;
-  T p = T(1);
-#pragma unroll
-  for (int j = 0; j < D; ++j) {
-    p = add_rn(p, s[j]);
-    beta = vmin(beta, mul_rn(p, T(1) / T(j + 1)));
-  }
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    const T t = (u[k] >= v_top) ? sub_rn(u[k], beta) : add_rn(u[k], beta);
-    z[k] = (k < d) ? clip01(t) : T(0);
-  }
-  return true;
 }
 
-// Bitonic merger (ascending) for a V-shaped sequence of length D, padded
-// conceptually to the next power of two with +inf: compare-exchanges that
-// touch a padded slot are no-ops and are pruned at compile time (7 for
-// D = 6, 22 for D = 13, versus 12 / 48 for a full sorting network).
-constexpr int next_pow2(int d) { return d <= 1 ? 1 : 2 * next_pow2((d + 1) / 2); }
-
-template <typename T, int D>
-__device__ __forceinline__ void bitonic_merge_asc(T (&s)[D]) {
-  constexpr int P = next_pow2(D);
-#pragma unroll
-  for (int h = P / 2; h >= 1; h /= 2) {
-#pragma unroll
-    for (int i = 0; i < P; ++i)
-      if ((i & h) == 0 && i + h < D) ce_asc(s[i], s[i + h]);
-  }
-}
-
-#ifndef ADMM_PROJ_FMA_MASK
-#define ADMM_PROJ_FMA_MASK 0
-#endif
-
-// Fixed-degree variant used by the regular-code kernels: d == D at compile
-// time, no padding, and branch-free -- a row that passes the facet test gets
-// beta = 0, and clip(u - 0 * f) is exactly the cube clip the reference
-// returns for it (:418).  Same contract as project_pp.
+// Fixed-degree entry of the regular-code kernels (d == D at compile time).
 template <typename T, int D>
 __device__ __forceinline__ void project_pp_fixed(const T (&u)[D], T (&z)[D]) {
-#ifndef ADMM_PROJ_TWO_SORT
   project_pp_cut<T, D>(u, z);
-  return;
-#endif
-  T v[D];
-#pragma unroll
-  for (int k = 0; k < D; ++k) v[k] = u[k];
-  SortNet<D>::desc(v);
-  T c[D];
-#pragma unroll
-  for (int k = 0; k < D; ++k) c[k] = clip01(v[k]);
-  const T total = numpy_rowsum<T, D>(c, D);
-  const int r = 2 * static_cast<int>(floor(total * T(0.5)));
-  // Projected rows have r even and r <= D - 1, so r indexes an even slot.
-  T v_top = v[0], v_nxt = v[D > 1 ? 1 : 0], head = c[0], run = c[0];
-#pragma unroll
-  for (int k = 1; k < D; ++k) {
-    run = add_rn(run, c[k]);
-    if ((k & 1) == 0 && k == r) {
-      v_top = v[k];
-      v_nxt = v[k + 1 < D ? k + 1 : k];
-      head = run;
-    }
-  }
-  const T fz = sub_rn(mul_rn(T(2), head), total);
-  const T beta_max = (r <= D - 2) ? mul_rn(T(0.5), sub_rn(v_top, v_nxt)) : v_top;
-  const bool inside = (r >= D) || (fz <= T(r) + Num<T>::kTol) || (beta_max <= T(0));
-
-  // Activation shifts in SORTED order: s = v_k - 1 on the +1 block (k <= r,
-  // descending) then -v_k (ascending) -- a V-shaped sequence whatever r is,
-  // so a bitonic merger sorts it.
-  T s[D];
-  if constexpr (sizeof(T) == 4 && ADMM_PROJ_FMA_MASK) {
-    // fp32 (throughput mode): the block mask as a float on the FMA pipe,
-    // m_k = [k <= r] = sat(r + 1 - k), and s_k = m_k (2 v_k - 1) - v_k, in
-    // place of integer compares and selects on the ALU pipe (the kernel is
-    // ALU-issue bound).  Same values up to the rounding of 2 v_k - 1.
-    const float rp1 = static_cast<float>(r + 1);
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      const float m = __saturatef(rp1 - static_cast<float>(k));
-      s[k] = __fmaf_rn(m, __fmaf_rn(2.f, v[k], -1.f), -v[k]);
-    }
-  } else {
-    const int r2 = r >> 1;
-#pragma unroll
-    for (int k = 0; k < D; ++k) s[k] = (((k + 1) >> 1) <= r2) ? sub_rn(v[k], T(1)) : -v[k];
-  }
-  bitonic_merge_asc<T, D>(s);
-  T beta = beta_max, p = T(1);
-#pragma unroll
-  for (int j = 0; j < D; ++j) {
-    p = add_rn(p, s[j]);
-    beta = vmin(beta, mul_rn(p, T(1) / T(j + 1)));
-  }
-  beta = inside ? T(0) : beta;
-  if constexpr (sizeof(T) == 4) {
-    // z_k = clip(u_k -/+ beta): the sign of u_k - v_top (+0 on a tie: the
-    // +1 block) moved onto beta >= 0 with one bit operation.
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      const float d = u[k] - v_top;
-      const float sb = __int_as_float(__float_as_int(beta) | (__float_as_int(d) & 0x80000000));
-      z[k] = __saturatef(u[k] - sb);
-    }
-  } else {
-    bool up[D];
-#pragma unroll
-    for (int k = 0; k < D; ++k) up[k] = u[k] >= v_top;
-#pragma unroll
-    for (int k = 0; k < D; ++k) z[k] = clip01(up[k] ? sub_rn(u[k], beta) : add_rn(u[k], beta));
-  }
 }
 
 }  // namespace admm
