@@ -77,12 +77,13 @@ struct admm_graph {
   bool shard_ok[2] = {false, false};
   admm::WideLaunch wlaunch[2];
   bool wide_ok[2] = {false, false};
-  // cluster engine (cluster.cuh, fp32): one 4-CTA cluster per frame
-  bool cluster_ok = false;
+  // cluster engine (cluster.cuh): one cluster per frame; fp64 on 8-CTA clusters only
+  bool cluster_ok = false, cluster64_ok = false;
   int cl_nt = 0, cl_smem = 0, cl_clusters = 0, cl_regs = 0;
+  int cl64_smem = 0, cl64_clusters = 0, cl64_regs = 0;
   int cl_NPL = 0, cl_NXS = 0, cl_NMS = 0, cl_MC = 0, cl_NO = 0;
   int cl_n_xs[admm::kClusterMax] = {}, cl_n_ms[admm::kClusterMax] = {};
-  uint32_t cl_rx_x[admm::kClusterMax] = {}, cl_rx_m[admm::kClusterMax] = {};
+  uint32_t cl_rx_x[admm::kClusterMax] = {}, cl_rx_m[admm::kClusterMax] = {};  // ELEMENTS received per iteration
   bool cl_dense = false;  // every part ships x to every other part (mbarrier-variant safety)
   long long cl_exchange = 0;
   int* cl_chk_slot = nullptr;
@@ -415,7 +416,7 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
         const int CPT = 2, VPT = 4;
         const int NT = 4096 / std::max(C, 1);  // compiled CTA size (cluster.cu)
         const int nt_need = ((n_checks + C - 1) / C + CPT - 1) / CPT;
-        if (admm::cluster_supported(6, 3, C, CPT, VPT) && nt_need <= NT && n_vars <= C * NT * VPT) {
+        if (admm::cluster_supported(0, 6, 3, C, CPT, VPT) && nt_need <= NT && n_vars <= C * NT * VPT) {
           long long pm = 20000000, bm = 20000000;
           if (const char* e = std::getenv("ADMM_B200_CLUSTER_MOVES")) pm = bm = std::atoll(e);
           const admm::ClusterLayout CL =
@@ -425,10 +426,10 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
                          (int)CL.ok, CL.error.c_str(), CL.NPL, CL.ghost_total, CL.msg_total, CL.msg_runs,
                          CL.bank_cost_before, CL.bank_cost_after);
           if (CL.ok) {
-            const int smem = admm::cluster_smem_bytes(CL.NPL, 3, CL.NXS, CL.NMS);
+            const int smem = admm::cluster_smem_bytes(0, CL.NPL, 3, CL.NXS, CL.NMS);
             int clusters = 0, regs = 0;
             const bool fits = smem <= smem_optin && CL.NO <= 4096 && CL.NPL <= 8192;  // table fields
-            if (fits && admm::cluster_query(C, NT, smem, &clusters, &regs) == cudaSuccess && clusters > 0) {
+            if (fits && admm::cluster_query(0, C, NT, smem, &clusters, &regs) == cudaSuccess && clusters > 0) {
               // packed x-send table: own slot | ghost slot << 13 | rank << 29
               std::vector<uint32_t> xs((size_t)C * CL.NXS, 0);
               for (int p = 0; p < C; ++p) {
@@ -440,8 +441,8 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
                 g->cl_n_xs[p] = CL.xs_start[p * (C + 1) + C];
                 g->cl_n_ms[p] = CL.n_ms[p];
               }
-              // bytes each CTA receives per iteration (mbarrier variant): ghost x;
-              // messages + one 20-byte stop-rule header from every CTA
+              // elements each CTA receives per iteration (mbarrier variant): ghost x;
+              // messages (+ one 20-byte stop-rule header from every CTA, added at launch)
               bool dense = true;
               for (int p = 0; p < C; ++p) {
                 uint32_t gx = 0, gm = 0;
@@ -452,8 +453,8 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
                 }
                 for (int q = 0; q < C; ++q)
                   for (int i = 0; i < CL.n_ms[q]; ++i) gm += (CL.msend[(size_t)q * CL.NMS + i] >> 27) == (uint32_t)p;
-                g->cl_rx_x[p] = 4 * gx;
-                g->cl_rx_m[p] = 4 * gm + 20 * C;
+                g->cl_rx_x[p] = gx;
+                g->cl_rx_m[p] = gm;
               }
               g->cl_dense = dense;
               auto upc = [&](void** dst, const void* src, size_t bytes) -> bool {
@@ -479,6 +480,21 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
                 g->cl_MC = CL.MC;
                 g->cl_NO = CL.NO;
                 g->cl_exchange = CL.ghost_total + CL.msg_total;
+                // fp64 (parity mode) on the same layout: twice the shared memory,
+                // 128 registers, one 512-thread CTA per SM -- 8-CTA clusters only
+                const int smem64 = admm::cluster_smem_bytes(1, CL.NPL, 3, CL.NXS, CL.NMS);
+                int clusters64 = 0, regs64 = 0;
+                if (admm::cluster_supported(1, 6, 3, C, CPT, VPT) && smem64 <= smem_optin &&
+                    std::getenv("ADMM_B200_NO_CLUSTER64") == nullptr &&
+                    admm::cluster_query(1, C, NT, smem64, &clusters64, &regs64) == cudaSuccess && clusters64 > 0) {
+                  g->cluster64_ok = true;
+                  g->cl64_smem = smem64;
+                  g->cl64_clusters = clusters64;
+                  g->cl64_regs = regs64;
+                }
+                if (dbg)
+                  std::fprintf(stderr, "[admm] cluster fp32: C=%d smem=%d clusters=%d regs=%d; fp64: ok=%d smem=%d clusters=%d regs=%d\n",
+                               C, smem, clusters, regs, (int)g->cluster64_ok, smem64, clusters64, regs64);
               }
             }
           }
@@ -762,7 +778,7 @@ bool use_wide(const admm_graph* g, int dtype, int64_t batch) {
 // Cluster engine for this call?  fp32 on graphs that placed it, unless the
 // caller forced the streaming kernels.
 bool use_cluster(const admm_graph* g, int dtype, int64_t /*batch*/) {
-  if (g->kind != 3 || !g->cluster_ok || dtype != ADMM_F32) return false;
+  if (g->kind != 3 || !(dtype == ADMM_F32 ? g->cluster_ok : g->cluster64_ok)) return false;
   return g->engine_req == ADMM_ENGINE_AUTO || g->engine_req == ADMM_ENGINE_CLUSTER;
 }
 
@@ -881,60 +897,66 @@ int decode_impl(const admm_graph* g, int dtype, int64_t batch, const void* gamma
   DeviceGuard guard(g->device);
   ADMM_CUDA(guard.error());
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (g->kind == 3 && g->engine_req == ADMM_ENGINE_CLUSTER && dtype != ADMM_F32)
-    return fail(ADMM_E_UNSUPPORTED, "the cluster engine is fp32 only (fp64 runs on the streaming engine)");
+  if (g->kind == 3 && g->engine_req == ADMM_ENGINE_CLUSTER && dtype == ADMM_F64 && !g->cluster64_ok)
+    return fail(ADMM_E_UNSUPPORTED, "the fp64 cluster engine needs 8-CTA clusters with room for the fp64 state "
+                                    "(fp64 runs on the streaming engine for this graph)");
   if (g->kind == 3 && use_cluster(g, dtype, batch)) {
     if (z_in || z_out) return fail(ADMM_E_UNSUPPORTED, "state input/output is not supported by the cluster engine");
     ADMM_CUDA(cudaMemsetAsync(workspace, 0, sizeof(int), st));
-    admm::ClusterParams cp{};
-    cp.chk_slot = g->cl_chk_slot;
-    cp.chk_orig = g->cl_chk_orig;
-    cp.own_var = g->cl_own_var;
-    cp.xsend = g->cl_xsend;
-    cp.msend = g->cl_msend;
-    cp.NPL = g->cl_NPL;
-    cp.NXS = g->cl_NXS;
-    cp.NMS = g->cl_NMS;
-    cp.MC = g->cl_MC;
-    cp.NO = g->cl_NO;
-    {
-      const admm::ClusterSmem L(cp.NPL, 3, cp.NXS, cp.NMS);
+    const double thr = epsilon * epsilon * (double)g->n_edges;  // admm_decoder.py:169
+    auto launch = [&](auto tag) -> cudaError_t {
+      using T = decltype(tag);
+      constexpr int ES = sizeof(T);
+      admm::ClusterParamsT<T> cp{};
+      cp.chk_slot = g->cl_chk_slot;
+      cp.chk_orig = g->cl_chk_orig;
+      cp.own_var = g->cl_own_var;
+      cp.xsend = g->cl_xsend;
+      cp.msend = g->cl_msend;
+      cp.NPL = g->cl_NPL;
+      cp.NXS = g->cl_NXS;
+      cp.NMS = g->cl_NMS;
+      cp.MC = g->cl_MC;
+      cp.NO = g->cl_NO;
+      const admm::ClusterSmem L(ES, cp.NPL, 3, cp.NXS, cp.NMS);
       cp.sm_xs = L.xs;
       cp.sm_ms = L.ms;
       cp.sm_hdr = L.hdr;
       cp.sm_mbar = L.mbar;
       cp.sm_misc = L.misc;
-    }
-    for (int r = 0; r < admm::kClusterMax; ++r) {
-      cp.n_xs[r] = g->cl_n_xs[r];
-      cp.n_ms[r] = g->cl_n_ms[r];
-      cp.rx_x[r] = g->cl_rx_x[r];
-      cp.rx_m[r] = g->cl_rx_m[r];
+      for (int r = 0; r < admm::kClusterMax; ++r) {
+        cp.n_xs[r] = g->cl_n_xs[r];
+        cp.n_ms[r] = g->cl_n_ms[r];
+        // bytes received per iteration: ghost x; messages + one 20-byte header from every CTA
+        cp.rx_x[r] = ES * g->cl_rx_x[r];
+        cp.rx_m[r] = ES * g->cl_rx_m[r] + 20 * g->C;
+      }
       cp.dense = g->cl_dense ? 1 : 0;
-    }
-    cp.n_vars = g->n_vars;
-    cp.n_checks = g->n_checks;
-    cp.batch = batch;
-    cp.gamma = static_cast<const float*>(gamma);
-    cp.ld_gamma = ld_gamma;
-    cp.mu = static_cast<float>(mu);
-    cp.rho = static_cast<float>(rho);
-    cp.one_minus_rho = static_cast<float>(1.0 - rho);
-    const double thr = epsilon * epsilon * (double)g->n_edges;  // admm_decoder.py:169
-    cp.thr = admm::thr_round_up<float>(thr);
-    cp.thr_d = thr;
-    cp.t_max = t_max;
-    cp.x_out = static_cast<float*>(x_out);
-    cp.ld_x = ld_x;
-    cp.hard_out = hard_out;
-    cp.ld_hard = ld_hard;
-    cp.iters_out = iters_out;
-    cp.flags_out = flags_out;
-    cp.weight_out = weight_out;
-    cp.queue = reinterpret_cast<int*>(workspace);
-    cp.synth = synth;
-    const int clusters = (int)std::min<long long>(batch, g->cl_clusters);
-    const cudaError_t le = admm::cluster_launch(g->C, cp, clusters, g->cl_nt, g->cl_smem, st);
+      cp.n_vars = g->n_vars;
+      cp.n_checks = g->n_checks;
+      cp.batch = batch;
+      cp.gamma = static_cast<const T*>(gamma);
+      cp.ld_gamma = ld_gamma;
+      cp.mu = static_cast<T>(mu);
+      cp.rho = static_cast<T>(rho);
+      cp.one_minus_rho = static_cast<T>(1.0 - rho);
+      cp.thr = admm::thr_round_up<T>(thr);
+      cp.thr_d = thr;
+      cp.t_max = t_max;
+      cp.x_out = static_cast<T*>(x_out);
+      cp.ld_x = ld_x;
+      cp.hard_out = hard_out;
+      cp.ld_hard = ld_hard;
+      cp.iters_out = iters_out;
+      cp.flags_out = flags_out;
+      cp.weight_out = weight_out;
+      cp.queue = reinterpret_cast<int*>(workspace);
+      cp.synth = synth;
+      const bool f64 = ES == 8;
+      const int clusters = (int)std::min<long long>(batch, f64 ? g->cl64_clusters : g->cl_clusters);
+      return admm::cluster_launch(g->C, cp, clusters, g->cl_nt, f64 ? g->cl64_smem : g->cl_smem, st);
+    };
+    const cudaError_t le = dtype == ADMM_F64 ? launch(double()) : launch(float());
     if (le != cudaSuccess) return cuda_fail(le, "cluster kernel launch");
     return ADMM_OK;
   }

@@ -13,54 +13,54 @@ bool g_prof = false;  // launch the profiling instantiation
 const bool g_spread = std::getenv("ADMM_B200_CLUSTER_SPREAD") != nullptr;
 const bool g_barrier = std::getenv("ADMM_B200_CLUSTER_BARRIER") != nullptr;  // A/B: all-to-all cluster barriers
 
-// Instantiations: C = 4 CTAs of 1024 threads (one per SM), C = 8 of 512 (two per SM).
-template <int C, bool PROF>
-const void* fn_of() {
-  return reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, C, 4096 / C, PROF>);
-}
-
-const void* kernel_fn(int C) { return C == 8 ? fn_of<8, false>() : fn_of<4, false>(); }
-
-template <int C, int NT>
+// Instantiations: fp32 C = 4 CTAs of 1024 threads (one per SM) and C = 8 of 512
+// (two per SM); fp64 C = 8 of 512 (one per SM, 128 registers).
+// fns: {plain, PROF} x {cluster barriers, mbarrier syncs}
+template <typename T, int C, int NT>
 void fns_of(const void** fns) {
-  fns[0] = reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, C, NT, false, false>);
-  fns[1] = reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, C, NT, true, false>);
-  fns[2] = reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, C, NT, false, true>);
-  fns[3] = reinterpret_cast<const void*>(&cluster_decode_kernel<kD, kDV, kCPT, kVPT, C, NT, true, true>);
+  fns[0] = reinterpret_cast<const void*>(&cluster_decode_kernel<T, kD, kDV, kCPT, kVPT, C, NT, false, false>);
+  fns[1] = reinterpret_cast<const void*>(&cluster_decode_kernel<T, kD, kDV, kCPT, kVPT, C, NT, true, false>);
+  fns[2] = reinterpret_cast<const void*>(&cluster_decode_kernel<T, kD, kDV, kCPT, kVPT, C, NT, false, true>);
+  fns[3] = reinterpret_cast<const void*>(&cluster_decode_kernel<T, kD, kDV, kCPT, kVPT, C, NT, true, true>);
 }
 
-void set_smem_all(int C, int smem) {
-  const void* fns[4];
-  if (C == 8)
-    fns_of<8, 512>(fns);
-  else
-    fns_of<4, 1024>(fns);
-  for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+bool fns_for(int dtype, int C, const void** fns) {
+  if (dtype == 0 && C == 4) fns_of<float, 4, 1024>(fns);
+  else if (dtype == 0 && C == 8) fns_of<float, 8, 512>(fns);
+  else if (dtype == 1 && C == 8) fns_of<double, 8, 512>(fns);
+  else return false;
+  return true;
 }
 
 }  // namespace
 
-bool cluster_supported(int D, int DV, int C, int CPT, int VPT) {
-  return D == kD && DV == kDV && (C == 4 || C == 8) && CPT == kCPT && VPT == kVPT;
+bool cluster_supported(int dtype, int D, int DV, int C, int CPT, int VPT) {
+  const void* fns[4];
+  return D == kD && DV == kDV && CPT == kCPT && VPT == kVPT && fns_for(dtype, C, fns);
 }
 
-int cluster_smem_bytes(int NPL, int DV, int NXS, int NMS) { return ClusterSmem(NPL, DV, NXS, NMS).total; }
+int cluster_smem_bytes(int dtype, int NPL, int DV, int NXS, int NMS) {
+  return ClusterSmem(dtype ? 8 : 4, NPL, DV, NXS, NMS).total;
+}
 
-// Spread the CTAs of a cluster over distinct SMs (two CTAs of DIFFERENT
-// clusters then share an SM at C = 8, so one hides the other's barriers).
+// Spread the CTAs of a cluster over distinct SMs (the hardware already does:
+// tools/cluster_phases.py prints the placement).
 cudaLaunchAttributeValue spread_value() {
   cudaLaunchAttributeValue v{};
   v.clusterSchedulingPolicyPreference = cudaClusterSchedulingPolicySpread;
   return v;
 }
 
-cudaError_t cluster_query(int C, int nt, int smem, int* clusters, int* regs) {
-  const void* fn = kernel_fn(C);
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  set_smem_all(C, smem);
+cudaError_t cluster_query(int dtype, int C, int nt, int smem, int* clusters, int* regs) {
+  const void* fns[4];
+  if (!fns_for(dtype, C, fns)) return cudaErrorInvalidConfiguration;
+  for (const void* f : fns) {
+    const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+  }
+  const void* fn = fns[2];
   cudaFuncAttributes fa{};
-  e = cudaFuncGetAttributes(&fa, fn);
+  cudaError_t e = cudaFuncGetAttributes(&fa, fn);
   if (e != cudaSuccess) return e;
   *regs = fa.numRegs;
   if (fa.numRegs * nt > 65536) {
@@ -83,8 +83,10 @@ cudaError_t cluster_query(int C, int nt, int smem, int* clusters, int* regs) {
   return cudaOccupancyMaxActiveClusters(clusters, fn, &cfg);
 }
 
-template <int C, int NT, bool PROF>
-cudaError_t launch_t(const ClusterParams& p, int clusters, int smem, cudaStream_t st) {
+namespace {
+
+template <typename T, int C, int NT, bool PROF>
+cudaError_t launch_t(const ClusterParamsT<T>& p, int clusters, int smem, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(clusters * C);
   cfg.blockDim = dim3(NT);
@@ -100,15 +102,24 @@ cudaError_t launch_t(const ClusterParams& p, int clusters, int smem, cudaStream_
   cfg.attrs = attr;
   cfg.numAttrs = na;
   if (p.dense && !g_barrier)
-    return cudaLaunchKernelEx(&cfg, cluster_decode_kernel<kD, kDV, kCPT, kVPT, C, NT, PROF, true>, p);
-  return cudaLaunchKernelEx(&cfg, cluster_decode_kernel<kD, kDV, kCPT, kVPT, C, NT, PROF, false>, p);
+    return cudaLaunchKernelEx(&cfg, cluster_decode_kernel<T, kD, kDV, kCPT, kVPT, C, NT, PROF, true>, p);
+  return cudaLaunchKernelEx(&cfg, cluster_decode_kernel<T, kD, kDV, kCPT, kVPT, C, NT, PROF, false>, p);
 }
 
-cudaError_t cluster_launch(int C, const ClusterParams& p, int clusters, int nt, int smem, cudaStream_t st) {
+}  // namespace
+
+cudaError_t cluster_launch(int C, const ClusterParamsT<float>& p, int clusters, int nt, int smem, cudaStream_t st) {
   if (nt != 4096 / C) return cudaErrorInvalidConfiguration;  // compiled CTA sizes
   cudaGetLastError();
-  if (C == 8) return g_prof ? launch_t<8, 512, true>(p, clusters, smem, st) : launch_t<8, 512, false>(p, clusters, smem, st);
-  return g_prof ? launch_t<4, 1024, true>(p, clusters, smem, st) : launch_t<4, 1024, false>(p, clusters, smem, st);
+  if (C == 8)
+    return g_prof ? launch_t<float, 8, 512, true>(p, clusters, smem, st) : launch_t<float, 8, 512, false>(p, clusters, smem, st);
+  return g_prof ? launch_t<float, 4, 1024, true>(p, clusters, smem, st) : launch_t<float, 4, 1024, false>(p, clusters, smem, st);
+}
+
+cudaError_t cluster_launch(int C, const ClusterParamsT<double>& p, int clusters, int nt, int smem, cudaStream_t st) {
+  if (C != 8 || nt != 512) return cudaErrorInvalidConfiguration;
+  cudaGetLastError();
+  return g_prof ? launch_t<double, 8, 512, true>(p, clusters, smem, st) : launch_t<double, 8, 512, false>(p, clusters, smem, st);
 }
 
 bool cluster_phase_profile(int enable, unsigned long long* out8) {

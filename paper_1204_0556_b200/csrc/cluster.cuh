@@ -1,7 +1,10 @@
 // Cluster engine: one thread-block CLUSTER of C CTAs decodes one frame of a
 // code too large for one SM (BASELINE config 5, n = 16384: C = 4 CTAs of
 // 1024 threads, one per SM), with every byte of the frame's decoder state on
-// chip.  fp32 (throughput mode) only; fp64 stays on the streaming engines.
+// chip.  fp32 (throughput mode): C = 8 CTAs of 512 threads, two per SM (or
+// C = 4 of 1024); fp64 (parity mode): C = 8 CTAs of 512 threads at 128
+// registers, one per SM -- the reference's expression tree per edge
+// (resident_regular.cuh's fp64 path), state twice the size.
 //
 // Layout (cluster_layout.h): CTA p owns M/C checks and N/C variables; the
 // variables its checks touch but other CTAs own are GHOSTS with local slots.
@@ -76,6 +79,14 @@ __device__ __forceinline__ void cl_st_async(uint32_t a, float v, uint32_t mb) {
                "r"(__float_as_uint(v)), "r"(mb)
                : "memory");
 }
+__device__ __forceinline__ void cl_st_async(uint32_t a, double v, uint32_t mb) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(a),
+               "l"(__double_as_longlong(v)), "r"(mb)
+               : "memory");
+}
+__device__ __forceinline__ void cl_st(uint32_t a, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
 __device__ __forceinline__ void cl_st_async_u32(uint32_t a, uint32_t v, uint32_t mb) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(a), "r"(v), "r"(mb)
                : "memory");
@@ -132,7 +143,8 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
   return v;
 }
 
-struct ClusterParams {
+template <typename T>
+struct ClusterParamsT {
   // graph (cluster_layout.h), per-part arrays flattened [C][...]
   const int* chk_slot;   // [C][D][MC]
   const int* chk_orig;   // [C][MC] original check (-1: idle slot)
@@ -149,12 +161,12 @@ struct ClusterParams {
   int n_vars, n_checks;
   // frames
   long long batch;
-  const float* gamma;
+  const T* gamma;
   long long ld_gamma;
-  float mu, rho, one_minus_rho, thr;  // thr: eps^2 E rounded up to fp32 (early-out)
-  double thr_d;                       // eps^2 E
+  T mu, rho, one_minus_rho, thr;  // thr: eps^2 E rounded up to T (early-out)
+  double thr_d;                   // eps^2 E
   int t_max;
-  float* x_out;
+  T* x_out;
   long long ld_x;
   uint8_t* hard_out;
   long long ld_hard;
@@ -164,8 +176,9 @@ struct ClusterParams {
   int* queue;
   SynthParams synth;
 };
+using ClusterParams = ClusterParamsT<float>;
 
-// Shared memory (bytes): X | MSG[DV] | GM (each NPL fp32) | xsend[NXS] |
+// Shared memory (bytes): X | MSG[DV] | GM (each NPL elements) | xsend[NXS] |
 // msend[NMS] (8-byte pre-mapped entries, below) | header | mbarriers | misc.
 // Stop-rule header one CTA sends to every CTA each iteration: its exact fp64
 // sums (valid when its flag is clear) and its "some partial >= threshold" flag.
@@ -176,9 +189,9 @@ struct ClusterHeader {
 
 struct ClusterSmem {
   int x, xs, ms, hdr, mbar, misc, total;
-  __host__ __device__ ClusterSmem(int NPL, int DV, int NXS, int NMS) {
+  __host__ __device__ ClusterSmem(int elem, int NPL, int DV, int NXS, int NMS) {
     x = 0;
-    xs = 4 * NPL * (DV + 2);
+    xs = elem * NPL * (DV + 2);
     ms = xs + 8 * NXS;
     hdr = (ms + 8 * NMS + 15) & ~15;   // [2 parities][kClusterMax] ClusterHeader
     mbar = hdr + 2 * kClusterMax * 24;   // two mbarriers (x, messages)
@@ -207,16 +220,19 @@ __device__ unsigned long long g_cl_cycles[8];
 //     and o's message wait of t;
 //   * headers alternate between two buffers by iteration parity, and the
 //     same chains keep every pair of CTAs within one iteration.
-template <int D, int DV, int CPT, int VPT, int C, int NT, bool PROF = false, bool MBAR = false>
-__global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) cluster_decode_kernel(const ClusterParams p) {
-  static_assert(D % DV == 0 && D % 2 == 0 && VPT % 2 == 0, "cluster engine: colored fp32 layout");
+template <typename T, int D, int DV, int CPT, int VPT, int C, int NT, bool PROF = false, bool MBAR = false>
+__global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, (sizeof(T) == 4 ? 1024 : 512) / NT)
+    cluster_decode_kernel(const ClusterParamsT<T> p) {
+  static_assert(D % DV == 0 && D % 2 == 0 && VPT % 2 == 0, "cluster engine: colored layout");
+  constexpr uint32_t ES = sizeof(T);
+  constexpr bool kF64 = ES == 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int NPL = p.NPL;
   const uint32_t rank = cl_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarps = NT / 32;
-  const uint32_t xs_a = smem_u32(smem_raw);  // X[NPL]; MSG[j] at +4 NPL (j + 1); GM at +4 NPL (DV + 1)
-  const uint32_t mstride = 4u * NPL;
+  const uint32_t xs_a = smem_u32(smem_raw);  // X[NPL]; MSG[j] at +ES NPL (j + 1); GM at +ES NPL (DV + 1)
+  const uint32_t mstride = ES * NPL;
   ClusterHeader* hdr = reinterpret_cast<ClusterHeader*>(smem_raw + p.sm_hdr);  // [2][kClusterMax]
   const uint32_t mb_x = smem_u32(smem_raw + p.sm_mbar), mb_m = mb_x + 8;        // mbarriers (MBAR)
   int* misc = reinterpret_cast<int*>(smem_raw + p.sm_misc);                     // [0] frame [1] weight
@@ -233,13 +249,14 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
     const uint32_t* gms = p.msend + static_cast<size_t>(rank) * p.NMS;
     for (int i = tid; i < p.n_xs[rank]; i += NT) {
       const uint32_t u = __ldg(gx + i);
-      sts2u(tx_a + 8u * (i - tid), xs_a + 4u * (u & 0x1fffu), cl_addr<C>(xs_a + 4u * ((u >> 13) & 0xffffu), u >> 29));
+      sts2u(tx_a + 8u * (i - tid), xs_a + ES * (u & 0x1fffu),
+            cl_addr<C>(xs_a + ES * ((u >> 13) & 0xffffu), u >> 29, ES));
     }
     for (int i = tid; i < p.n_ms[rank]; i += NT) {
       const uint32_t u = __ldg(gms + i);
-      const uint32_t row = 4u * NPL * ((u & 3u) + 1);
-      sts2u(tm_a + 8u * (i - tid), xs_a + row + 4u * ((u >> 2) & 0x1fffu),
-            cl_addr<C>(xs_a + row + 4u * ((u >> 15) & 0xfffu), u >> 27));
+      const uint32_t row = mstride * ((u & 3u) + 1);
+      sts2u(tm_a + 8u * (i - tid), xs_a + row + ES * ((u >> 2) & 0x1fffu),
+            cl_addr<C>(xs_a + row + ES * ((u >> 15) & 0xfffu), u >> 27, ES));
     }
     // shared::cluster addresses keep the CTA in the bits above the offset (a
     // CTA's own shared addresses carry its own): a destination's mbarrier is
@@ -264,17 +281,20 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       const int s = __ldg(p.chk_slot + (static_cast<size_t>(rank) * D + k) * p.MC + lc);
-      xaddr[q][k] = xs_a + 4u * s;
+      xaddr[q][k] = xs_a + ES * s;
     }
   }
-  // own slots: xst(q) = xs0 + 4 (2 NT (q >> 1) + (q & 1)) (compile-time offsets)
-  const uint32_t xs0 = xs_a + 8u * tid;
+  // own slots: xst(q) = xs0 + ES (2 NT (q >> 1) + (q & 1)) (compile-time offsets)
+  const uint32_t xs0 = xs_a + 2u * ES * tid;
   const int* own_var = p.own_var + static_cast<size_t>(rank) * p.NO;
-  auto xst = [&](int q) -> uint32_t { return xs0 + 4u * (2 * NT * (q >> 1) + (q & 1)); };
+  auto xst = [&](int q) -> uint32_t { return xs0 + ES * (2 * NT * (q >> 1) + (q & 1)); };
   auto vorig = [&](int q) -> int { return __ldg(own_var + 2 * tid + 2 * NT * (q >> 1) + (q & 1)); };
 
-  const float2 rho2 = make_float2(p.rho, p.rho), omr2 = make_float2(p.one_minus_rho, p.one_minus_rho);
-  float2 zp[CPT][D / 2], lp[CPT][D / 2];
+  // edge state in registers: packed fp32 pairs, or the fp64 replicas and scaled duals
+  const float2 rho2 = make_float2(float(p.rho), float(p.rho));
+  const float2 omr2 = make_float2(float(p.one_minus_rho), float(p.one_minus_rho));
+  float2 zp[kF64 ? 1 : CPT][kF64 ? 1 : D / 2], lp[kF64 ? 1 : CPT][kF64 ? 1 : D / 2];
+  double zd[kF64 ? CPT : 1][kF64 ? D : 1], ld[kF64 ? CPT : 1][kF64 ? D : 1];
   const bool prof = PROF && blockIdx.x == 0 && tid == 0;
   long long tp = 0;
   auto phase = [&](int k) {
@@ -289,7 +309,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
   auto exchange = [&](uint32_t ta, int n, uint32_t mb) {
     for (int k = n - tid; k > 0; k -= NT, ta += 8u * NT) {
       const uint2 e = lds2u(ta);
-      const float v = lds(e.x, 0.f);
+      const T v = lds(e.x, T());
       if constexpr (MBAR)
         cl_st_async(e.y, v, (e.y & kCtaBits) | (mb & ~kCtaBits));
       else
@@ -299,22 +319,61 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
   // x-update of own pair h (admm_decoder.py:108-124; colors summed in order)
   auto var_pair = [&](int h) {
     const uint32_t a = xst(2 * h);
-    float2 acc = lds2(a + mstride);
+    if constexpr (kF64) {
+      // fp64: the resident fp64 kernel's variable update (16-byte pairs, colors
+      // summed in order, times the reciprocal degree)
+      double2 acc = lds2d(a + mstride);
 #pragma unroll
-    for (int j = 1; j < DV; ++j) acc = __fadd2_rn(acc, lds2(a + mstride * (j + 1)));
-    const float2 num = fsub2_rn(acc, lds2(a + mstride * (DV + 1)));
-    sts2(a, make_float2(clip01(num.x * (1.f / DV)), clip01(num.y * (1.f / DV))));
+      for (int j = 1; j < DV; ++j) {
+        const double2 m = lds2d(a + mstride * (j + 1));
+        acc.x = add_rn(acc.x, m.x);
+        acc.y = add_rn(acc.y, m.y);
+      }
+      const double2 gm = lds2d(a + mstride * (DV + 1));
+      const double inv = 1.0 / DV;
+      sts2d(a, make_double2(clip01(mul_rn(sub_rn(acc.x, gm.x), inv)), clip01(mul_rn(sub_rn(acc.y, gm.y), inv))));
+    } else {
+      float2 acc = lds2(a + mstride);
+#pragma unroll
+      for (int j = 1; j < DV; ++j) acc = __fadd2_rn(acc, lds2(a + mstride * (j + 1)));
+      const float2 num = fsub2_rn(acc, lds2(a + mstride * (DV + 1)));
+      sts2(a, make_float2(clip01(num.x * (1.f / DV)), clip01(num.y * (1.f / DV))));
+    }
   };
-  // fused z-update, projection, residuals, dual update of check q (packed fp32)
+  // fused z-update, projection, residuals, dual update of check q: packed fp32
+  // pairs, or (fp64) the reference's expression tree edge by edge
+  // (admm_decoder.py:127-149 in the scaled-dual form of resident_regular.cuh)
   float2 pr2, mv2;
+  double prd = 0.0, mvd = 0.0;
   auto check = [&](int q) {
+    if constexpr (kF64) {
+      double gx[D], w[D], u[D], zn[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) gx[k] = lds(xaddr[q][k], double());
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        w[k] = add_rn(mul_rn(p.rho, gx[k]), mul_rn(p.one_minus_rho, zd[q][k]));
+        u[k] = add_rn(w[k], ld[q][k]);
+      }
+      project_pp_fixed<double, D>(u, zn);
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const double r1 = sub_rn(gx[k], zn[k]);
+        const double r2 = sub_rn(zn[k], zd[q][k]);
+        prd = add_rn(prd, mul_rn(r1, r1));
+        mvd = add_rn(mvd, mul_rn(r2, r2));
+        ld[q][k] = add_rn(ld[q][k], sub_rn(w[k], zn[k]));
+        zd[q][k] = zn[k];
+        sts(xaddr[q][k] + mstride * (1 + k % DV), sub_rn(zn[k], ld[q][k]));
+      }
+    } else {
     float2 gx2[D / 2], u2[D / 2];
 #pragma unroll
     for (int j = 0; j < D / 2; ++j) gx2[j] = make_float2(lds(xaddr[q][2 * j], 0.f), lds(xaddr[q][2 * j + 1], 0.f));
     float u[D], zn[D];
 #pragma unroll
     for (int j = 0; j < D / 2; ++j) {
-      u2[j] = __fadd2_rn(__ffma2_rn(rho2, gx2[j], __fmul2_rn(omr2, zp[q][j])), lp[q][j]);
+      u2[j] = __fadd2_rn(__ffma2_rn(rho2, gx2[j], __fmul2_rn(omr2, zp[kF64 ? 0 : q][kF64 ? 0 : j])), lp[kF64 ? 0 : q][kF64 ? 0 : j]);
       u[2 * j] = u2[j].x;
       u[2 * j + 1] = u2[j].y;
     }
@@ -325,20 +384,21 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
     for (int j = 0; j < D / 2; ++j) {
       const float2 zn2 = make_float2(zn[2 * j], zn[2 * j + 1]);
       const float2 r1 = fsub2_rn(gx2[j], zn2);
-      const float2 r2 = fsub2_rn(zn2, zp[q][j]);
+      const float2 r2 = fsub2_rn(zn2, zp[kF64 ? 0 : q][kF64 ? 0 : j]);
       pr2 = __ffma2_rn(r1, r1, pr2);
       mv2 = __ffma2_rn(r2, r2, mv2);
       const float2 ln = fsub2_rn(u2[j], zn2);  // l' = (w + l) - z' = u - z'
       const float2 m2 = fsub2_rn(zn2, ln);
-      lp[q][j] = ln;
-      zp[q][j] = zn2;
+      lp[kF64 ? 0 : q][kF64 ? 0 : j] = ln;
+      zp[kF64 ? 0 : q][kF64 ? 0 : j] = zn2;
       sts(xaddr[q][2 * j] + mstride * (1 + (2 * j) % DV), m2.x);
       sts(xaddr[q][2 * j + 1] + mstride * (1 + (2 * j + 1) % DV), m2.y);
+    }
     }
   };
 
   // zero the whole local slot space once (ghost / spare slots hold finite values)
-  for (int i = tid; i < NPL * (DV + 2); i += NT) sts(xs_a + 4u * i, 0.f);
+  for (int i = tid; i < NPL * (DV + 2); i += NT) sts(xs_a + ES * i, T(0));
   if (MBAR && tid == 0) {
     mbar_init(mb_x, 1);
     mbar_init(mb_m, 1);
@@ -366,18 +426,27 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
 #pragma unroll
     for (int q = 0; q < VPT; ++q) {
       const int v = vorig(q);
-      const float g = v >= 0 ? __fdividef(frame_llr<float>(p, f, v), p.mu) : 0.f;
+      const T g = v >= 0 ? div_rn(frame_llr<T>(p, f, v), p.mu) : T(0);  // fp32: __fdividef
       sts(xst(q) + mstride * (DV + 1), g);
 #pragma unroll
-      for (int j = 0; j < DV; ++j) sts(xst(q) + mstride * (j + 1), 0.f);
+      for (int j = 0; j < DV; ++j) sts(xst(q) + mstride * (j + 1), T(0));
     }
 #pragma unroll
-    for (int q = 0; q < CPT; ++q)
+    for (int q = 0; q < CPT; ++q) {
+      if constexpr (kF64) {
 #pragma unroll
-      for (int j = 0; j < D / 2; ++j) {
-        zp[q][j] = make_float2(0.f, 0.f);
-        lp[q][j] = make_float2(0.f, 0.f);
+        for (int k = 0; k < D; ++k) {
+          zd[q][k] = 0.0;
+          ld[q][k] = 0.0;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < D / 2; ++j) {
+          zp[kF64 ? 0 : q][kF64 ? 0 : j] = make_float2(0.f, 0.f);
+          lp[kF64 ? 0 : q][kF64 ? 0 : j] = make_float2(0.f, 0.f);
+        }
       }
+    }
     if (tid == 0) misc[1] = 0;
     __syncthreads();
 
@@ -399,6 +468,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
       exchange(tx_a, p.n_xs[rank], mb_x);
       pr2 = make_float2(0.f, 0.f);
       mv2 = make_float2(0.f, 0.f);
+      prd = mvd = 0.0;
       phase(2);
       ADMM_JITTER();
       if constexpr (MBAR) {
@@ -411,7 +481,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
 #pragma unroll
       for (int q = 0; q < CPT; ++q) check(q);
 
-      const float primal = pr2.x + pr2.y, moved = mv2.x + mv2.y;
+      const T primal = kF64 ? T(prd) : T(pr2.x + pr2.y), moved = kF64 ? T(mvd) : T(mv2.x + mv2.y);
       ADMM_JITTER();
       const int nc = __syncthreads_or(primal >= p.thr || moved >= p.thr);
       double sa = 0.0, sb = 0.0;
@@ -483,10 +553,10 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
     for (int q = 0; q < VPT; ++q) {
       const int v = vorig(q);
       if (v >= 0) {
-        const float xv = lds(xst(q), 0.f);
-        const bool h = xv > 0.5f;
+        const T xv = lds(xst(q), T());
+        const bool h = xv > T(0.5);
         ones += h;
-        integral &= fminf(fabsf(xv), fabsf(1.f - xv)) <= 1e-5f;
+        integral &= vmin(fabs(xv), fabs(T(1) - xv)) <= T(1e-5);
         ADMM_ASSERT(v < p.n_vars && f < p.batch);
         if (p.x_out) p.x_out[f * p.ld_x + v] = xv;
         if (p.hard_out) p.hard_out[f * p.ld_hard + v] = h;
@@ -497,7 +567,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, 1024 / NT) clust
     for (int q = 0; q < CPT; ++q) {
       int par = 0;
 #pragma unroll
-      for (int k = 0; k < D; ++k) par ^= (lds(xaddr[q][k], 0.f) > 0.5f);
+      for (int k = 0; k < D; ++k) par ^= (lds(xaddr[q][k], T()) > T(0.5));
       odd |= ((cmask >> q) & 1u) && par;
     }
     ones = __reduce_add_sync(0xffffffffu, ones);

@@ -178,15 +178,23 @@ def test_wide_kernel_large_batch_matches_sharded(cuda_ok):
     cfg = AdmmConfig(mu=5.0)
     ch = Awgn(2.5, code.design_rate)
     B = 2304  # > the 1024-frame switch, not a multiple of the 4096 slots
-    w64 = decode_synth(code, ch, cfg, seed=1, point=1, trial0=0, batch=B, dtype=torch.float64, want_hard=True)
+    w64 = decode_synth(code, ch, cfg, seed=1, point=1, trial0=0, batch=B, dtype=torch.float64, want_hard=True,
+                       engine="streaming")
     assert w64.info["kernel"] == 5
     # the sharded kernel on a sub-batch (below the switch) of the same trials
-    sub = decode_synth(code, ch, cfg, seed=1, point=1, trial0=1000, batch=200, dtype=torch.float64, want_hard=True)
+    sub = decode_synth(code, ch, cfg, seed=1, point=1, trial0=1000, batch=200, dtype=torch.float64, want_hard=True,
+                       engine="streaming")
     assert sub.info["kernel"] == 3
+    # ... and the fp64 cluster engine (the automatic choice on this code)
+    c64 = decode_synth(code, ch, cfg, seed=1, point=1, trial0=1000, batch=200, dtype=torch.float64, want_hard=True)
+    assert c64.info["kernel_name"] == "cluster"
+    assert torch.equal(c64.iterations, sub.iterations) and torch.equal(c64.hard, sub.hard)
+    assert torch.equal(c64.flags, sub.flags)
     assert torch.equal(sub.iterations, w64.iterations[1000:1200])
     assert torch.equal(sub.hard, w64.hard[1000:1200])
     assert torch.equal(sub.flags, w64.flags[1000:1200])
-    w32 = decode_synth(code, ch, cfg, seed=1, point=1, trial0=0, batch=B, dtype=torch.float32, want_hard=True)
+    w32 = decode_synth(code, ch, cfg, seed=1, point=1, trial0=0, batch=B, dtype=torch.float32, want_hard=True,
+                       engine="streaming")
     same = w32.hard.eq(w64.hard).all(dim=1).float().mean().item()
     assert same >= 0.999
     assert abs(int(w32.iterations.sum()) - int(w64.iterations.sum())) <= 0.02 * int(w64.iterations.sum())
@@ -322,14 +330,23 @@ def test_cluster_sizes_agree(cuda_ok, monkeypatch):
     assert torch.equal(a.hard, b.hard) and torch.equal(a.weight, b.weight)
 
 
-def test_cluster_engine_rejects_fp64_and_state_io(cuda_ok):
+def test_cluster_engine_fp64_and_state_io(cuda_ok, monkeypatch):
+    import copy
+
     from paper_1204_0556_b200 import AdmmConfig, baseline_code, decode_batch
 
     code = baseline_code("cfg5_n16384")
     g = np.full((2, code.n_vars), 3.0)
+    r = decode_batch(g, code, AdmmConfig(), dtype=torch.float64, engine="cluster")
+    assert r.info["kernel_name"] == "cluster" and bool(r.converged.all())
+    for dt in (torch.float32, torch.float64):  # state I/O goes through the step API at this size
+        with pytest.raises(RuntimeError):
+            decode_batch(g, code, AdmmConfig(), dtype=dt, want_state=True, engine="cluster")
+    # 4-CTA clusters have no room for the fp64 state: explicit requests are refused, auto streams
+    monkeypatch.setenv("ADMM_B200_CLUSTER", "4")
+    code4 = copy.copy(code)
+    code4._device_graphs = {}
     with pytest.raises(RuntimeError):
-        decode_batch(g, code, AdmmConfig(), dtype=torch.float64, engine="cluster")
-    with pytest.raises(RuntimeError):
-        decode_batch(g, code, AdmmConfig(), dtype=torch.float32, want_state=True, engine="cluster")
-    r = decode_batch(g, code, AdmmConfig(), dtype=torch.float64)  # auto: fp64 on the streaming engine
+        decode_batch(g, code4, AdmmConfig(), dtype=torch.float64, engine="cluster")
+    r = decode_batch(g, code4, AdmmConfig(), dtype=torch.float64)
     assert r.info["kernel_name"] in ("sharded", "wide") and bool(r.converged.all())

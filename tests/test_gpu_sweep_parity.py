@@ -54,7 +54,7 @@ ENGINES = ["auto", "streaming", "wide", "cluster"]
 def _engines(name, dtype):
     if "cfg5" not in name:
         return ["auto"]
-    return ENGINES if dtype == torch.float32 else ["auto", "streaming", "wide"]  # the cluster engine is fp32 only
+    return ENGINES  # config 5: every engine in both dtypes (fp64 cluster: 8-CTA clusters at 128 registers)
 
 
 def _decode(name, dtype, engine):
@@ -77,6 +77,9 @@ def test_f64_sweep_endpoint_matches_reference(cuda_ok, name, engine):
         pytest.skip("one engine for codes that fit one SM")
     f, code, gam, cfg, want = _case(name)
     res = _decode(name, torch.float64, engine)
+    if "cfg5" in name:
+        assert res.info["kernel_name"] == {"auto": "cluster", "cluster": "cluster", "wide": "wide",
+                                           "streaming": "sharded"}[engine]
     it = res.iterations.cpu().numpy()
     fl = res.flags.cpu().numpy()
     hard = res.hard.cpu().numpy()
