@@ -48,10 +48,10 @@ enum admm_status {
 
 /* Engine selection for admm_graph_create_ex. */
 enum admm_engine {
-  ADMM_ENGINE_AUTO = 0,      /* resident if the code fits one SM, else streaming placement (cluster engine for fp32) */
+  ADMM_ENGINE_AUTO = 0,      /* resident if the code fits one SM, else streaming placement (cluster engine where placed) */
   ADMM_ENGINE_RESIDENT = 1,  /* one CTA per frame, state on chip (fails if it does not fit) */
   ADMM_ENGINE_STREAMING = 3, /* codes beyond one SM: sharded kernel (small batches), wide HBM kernel (>= 1024 frames) */
-  ADMM_ENGINE_CLUSTER = 4,   /* streaming placement + the cluster engine required (fp32 calls run on it) */
+  ADMM_ENGINE_CLUSTER = 4,   /* streaming placement + the cluster engine required (fp32; fp64 on 8-CTA clusters) */
   ADMM_ENGINE_WIDE = 5       /* streaming placement, wide HBM-streaming kernel for every batch size */
 };
 
@@ -60,7 +60,7 @@ enum admm_kernel {
   ADMM_KERNEL_RESIDENT = 1,  /* generic resident (one CTA per frame)              */
   ADMM_KERNEL_REGULAR = 2,   /* regular-code resident                              */
   ADMM_KERNEL_SHARDED = 3,   /* sharded / L2 streaming (codes beyond one SM)       */
-  ADMM_KERNEL_CLUSTER = 4,   /* cluster engine: one 4-CTA cluster per frame, fp32  */
+  ADMM_KERNEL_CLUSTER = 4,   /* cluster engine: one 8- (or 4-) CTA cluster per frame */
   ADMM_KERNEL_WIDE = 5       /* wide HBM streaming (large batches beyond one SM)   */
 };
 
