@@ -67,6 +67,11 @@ if "cluster" in which:
     s = P.decode_synth(c2, P.Bsc(0.04), cfg, seed=2, point=0, trial0=0, batch=6, engine="cluster")
     torch.cuda.synchronize()
     print("cluster synth iterations", s.iterations.tolist(), flush=True)
+    c = P.decode_batch(g2, c2, cfg, dtype=torch.float64, want_hard=True, engine="cluster")
+    torch.cuda.synchronize()
+    print(f"cluster fp64: kernel {c.info['kernel_name']}, iterations equal to the resident fp64 kernel: "
+          f"{torch.equal(c.iterations, b.iterations)}", flush=True)
+    assert c.info["kernel_name"] == "cluster" and torch.equal(c.iterations, b.iterations) and torch.equal(c.hard, b.hard)
 if "bp" in which:
     r = P.decode_bp_batch(g1, c1, P.BpConfig(t_max=30), dtype=torch.float64)
     torch.cuda.synchronize()
