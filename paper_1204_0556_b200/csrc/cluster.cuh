@@ -133,6 +133,12 @@ __device__ __forceinline__ uint2 lds2u(uint32_t a) {
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
   return v;
 }
+__device__ __forceinline__ uint4 lds4u(uint32_t a) {
+  ADMM_CHECK_SMEM(a, 16);
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
 __device__ __forceinline__ void sts2u(uint32_t a, uint32_t x, uint32_t y) {
   ADMM_CHECK_SMEM(a, 8);
   asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
@@ -182,9 +188,11 @@ using ClusterParams = ClusterParamsT<float>;
 // msend[NMS] (8-byte pre-mapped entries, below) | header | mbarriers | misc.
 // Stop-rule header one CTA sends to every CTA each iteration: its exact fp64
 // sums (valid when its flag is clear) and its "some partial >= threshold" flag.
+// Structure of arrays, so the C flags every thread reads each iteration are
+// two 16-byte loads.
 struct ClusterHeader {
-  double primal, moved;
-  uint32_t flag, pad;
+  double primal[kClusterMax], moved[kClusterMax];
+  uint32_t flag[kClusterMax];
 };
 
 struct ClusterSmem {
@@ -193,8 +201,8 @@ struct ClusterSmem {
     x = 0;
     xs = elem * NPL * (DV + 2);
     ms = xs + 8 * NXS;
-    hdr = (ms + 8 * NMS + 15) & ~15;   // [2 parities][kClusterMax] ClusterHeader
-    mbar = hdr + 2 * kClusterMax * 24;   // two mbarriers (x, messages)
+    hdr = (ms + 8 * NMS + 15) & ~15;   // [2 parities] ClusterHeader
+    mbar = hdr + 2 * static_cast<int>(sizeof(ClusterHeader));  // two mbarriers (x, messages)
     misc = mbar + 16;                    // ints: frame, weight + per-CTA output slots
     total = misc + 4 * (8 + 3 * kClusterMax) + 64 * 8;  // + fp64 block-reduction slots
   }
@@ -233,7 +241,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, (sizeof(T) == 4 
   constexpr int nwarps = NT / 32;
   const uint32_t xs_a = smem_u32(smem_raw);  // X[NPL]; MSG[j] at +ES NPL (j + 1); GM at +ES NPL (DV + 1)
   const uint32_t mstride = ES * NPL;
-  ClusterHeader* hdr = reinterpret_cast<ClusterHeader*>(smem_raw + p.sm_hdr);  // [2][kClusterMax]
+  ClusterHeader* hdr = reinterpret_cast<ClusterHeader*>(smem_raw + p.sm_hdr);  // [2 parities]
   const uint32_t mb_x = smem_u32(smem_raw + p.sm_mbar), mb_m = mb_x + 8;        // mbarriers (MBAR)
   int* misc = reinterpret_cast<int*>(smem_raw + p.sm_misc);                     // [0] frame [1] weight
   int* outslot = misc + 8;                                                   // [C][3] integral, weight, odd
@@ -503,16 +511,16 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, (sizeof(T) == 4 
       exchange(tm_a, p.n_ms[rank], mb_m);
       if (tid < C) {
         const uint32_t r = tid;
-        ClusterHeader* h = hdr + (MBAR ? (gi & 1) * kClusterMax : 0) + rank;
+        ClusterHeader* h = hdr + (MBAR ? (gi & 1) : 0);
         if constexpr (MBAR) {
           const uint32_t mb = cl_addr<C>(mb_m, r, 8);
-          cl_st_async_f64(cl_addr<C>(smem_u32(&h->primal), r, 8), sa, mb);
-          cl_st_async_f64(cl_addr<C>(smem_u32(&h->moved), r, 8), sb, mb);
-          cl_st_async_u32(cl_addr<C>(smem_u32(&h->flag), r), static_cast<uint32_t>(nc), mb);
+          cl_st_async_f64(cl_addr<C>(smem_u32(&h->primal[rank]), r, 8), sa, mb);
+          cl_st_async_f64(cl_addr<C>(smem_u32(&h->moved[rank]), r, 8), sb, mb);
+          cl_st_async_u32(cl_addr<C>(smem_u32(&h->flag[rank]), r), static_cast<uint32_t>(nc), mb);
         } else {
-          cl_st_f64(cl_addr<C>(smem_u32(&h->primal), r, 8), sa);
-          cl_st_f64(cl_addr<C>(smem_u32(&h->moved), r, 8), sb);
-          cl_st_u32(cl_addr<C>(smem_u32(&h->flag), r), static_cast<uint32_t>(nc));
+          cl_st_f64(cl_addr<C>(smem_u32(&h->primal[rank]), r, 8), sa);
+          cl_st_f64(cl_addr<C>(smem_u32(&h->moved[rank]), r, 8), sb);
+          cl_st_u32(cl_addr<C>(smem_u32(&h->flag[rank]), r), static_cast<uint32_t>(nc));
         }
       }
       phase(5);
@@ -523,20 +531,23 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, (sizeof(T) == 4 
       } else {
         cl_barrier();  // B: messages and headers visible
       }
-      const ClusterHeader* hd = hdr + (MBAR ? (gi & 1) * kClusterMax : 0);
+      const ClusterHeader* hd = hdr + (MBAR ? (gi & 1) : 0);
       ++gi;
       // flags first; the fp64 sums only when every CTA's partials were below
       // the threshold (rare)
       uint32_t anync = 0;
 #pragma unroll
-      for (int r = 0; r < C; ++r) anync |= hd[r].flag;
+      for (int r = 0; r < C; r += 4) {
+        const uint4 fl = lds4u(smem_u32(&hd->flag[r]));  // C is 4 or 8
+        anync |= fl.x | fl.y | fl.z | fl.w;
+      }
       phase(6);
       if (!anync) {
         double A = 0.0, B = 0.0;
 #pragma unroll
         for (int r = 0; r < C; ++r) {
-          A += hd[r].primal;
-          B += hd[r].moved;
+          A += hd->primal[r];
+          B += hd->moved[r];
         }
         if (A < p.thr_d && B < p.thr_d) {
           converged = true;
