@@ -126,7 +126,7 @@ __device__ __forceinline__ void cl_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 // CTA-rank bits of a shared::cluster address (checked at kernel start)
-constexpr uint32_t kCtaBits = 0xff000000u;
+constexpr uint32_t kCtaBits = 0xff000000u;  // (the top byte: exchange() splices it with PRMT)
 __device__ __forceinline__ uint2 lds2u(uint32_t a) {
   ADMM_CHECK_SMEM(a, 8);
   uint2 v;
@@ -248,23 +248,25 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, (sizeof(T) == 4 
   double* red = reinterpret_cast<double*>(smem_raw + p.sm_misc + 4 * (8 + 3 * kClusterMax));
 
   // ---- per-part exchange tables into shared memory (once per CTA), pre-mapped:
-  // 8-byte entries {local source address, DSMEM destination address}, so an
+  // 8-byte entries {DSMEM destination address, local source address} (the
+  // order st.async wants its {address, mbarrier} register pair in), so an
   // exchange costs per entry one LDS.64, the source LDS, one LOP3 (the
   // destination's mbarrier: same CTA bits, fixed offset) and the st.async ----
-  const uint32_t tx_a = smem_u32(smem_raw) + p.sm_xs + 8u * tid, tm_a = smem_u32(smem_raw) + p.sm_ms + 8u * tid;
+  const uint32_t tx_b = smem_u32(smem_raw) + p.sm_xs, tm_b = smem_u32(smem_raw) + p.sm_ms;
+  const uint32_t tx_a = tx_b + 8u * tid, tm_a = tm_b + 8u * tid;
   {
     const uint32_t* gx = p.xsend + static_cast<size_t>(rank) * p.NXS;
     const uint32_t* gms = p.msend + static_cast<size_t>(rank) * p.NMS;
     for (int i = tid; i < p.n_xs[rank]; i += NT) {
       const uint32_t u = __ldg(gx + i);
-      sts2u(tx_a + 8u * (i - tid), xs_a + ES * (u & 0x1fffu),
-            cl_addr<C>(xs_a + ES * ((u >> 13) & 0xffffu), u >> 29, ES));
+      sts2u(tx_a + 8u * (i - tid), cl_addr<C>(xs_a + ES * ((u >> 13) & 0xffffu), u >> 29, ES),
+            xs_a + ES * (u & 0x1fffu));
     }
     for (int i = tid; i < p.n_ms[rank]; i += NT) {
       const uint32_t u = __ldg(gms + i);
       const uint32_t row = mstride * ((u & 3u) + 1);
-      sts2u(tm_a + 8u * (i - tid), xs_a + row + ES * ((u >> 2) & 0x1fffu),
-            cl_addr<C>(xs_a + row + ES * ((u >> 15) & 0xfffu), u >> 27, ES));
+      sts2u(tm_a + 8u * (i - tid), cl_addr<C>(xs_a + row + ES * ((u >> 15) & 0xfffu), u >> 27, ES),
+            xs_a + row + ES * ((u >> 2) & 0x1fffu));
     }
     // shared::cluster addresses keep the CTA in the bits above the offset (a
     // CTA's own shared addresses carry its own): a destination's mbarrier is
@@ -313,15 +315,17 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, (sizeof(T) == 4 
     }
   };
 
-  // one table-driven exchange: entry i of this CTA's table is handled by thread i mod NT
-  auto exchange = [&](uint32_t ta, int n, uint32_t mb) {
-    for (int k = n - tid; k > 0; k -= NT, ta += 8u * NT) {
-      const uint2 e = lds2u(ta);
-      const T v = lds(e.x, T());
-      if constexpr (MBAR)
-        cl_st_async(e.y, v, (e.y & kCtaBits) | (mb & ~kCtaBits));
+  // one table-driven exchange: entry i of this CTA's table (at tb + 8 i) is
+  // handled by thread i mod NT
+  auto exchange = [&](uint32_t tb, int n, uint32_t mb) {
+    const uint32_t end = tb + 8u * n;
+    for (uint32_t a = tb + 8u * tid; a < end; a += 8u * NT) {
+      const uint2 e = lds2u(a);  // {destination, source}
+      const T v = lds(e.y, T());
+      if constexpr (MBAR)  // the destination's mbarrier: its CTA byte over our mbarrier's offset (one PRMT)
+        cl_st_async(e.x, v, __byte_perm(mb, e.x, 0x7210));
       else
-        cl_st(e.y, v);
+        cl_st(e.x, v);
     }
   };
   // x-update of own pair h (admm_decoder.py:108-124; colors summed in order)
@@ -473,7 +477,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, (sizeof(T) == 4 
       __syncthreads();
       phase(1);
       // ---- x-send: own x -> ghost slots of the other CTAs (coalesced per warp) ----
-      exchange(tx_a, p.n_xs[rank], mb_x);
+      exchange(tx_b, p.n_xs[rank], mb_x);
       pr2 = make_float2(0.f, 0.f);
       mv2 = make_float2(0.f, 0.f);
       prd = mvd = 0.0;
@@ -508,7 +512,7 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, (sizeof(T) == 4 
       }
       phase(4);
       // ---- msg-send: ghost-row messages -> the owners' message rows; stop-rule header ----
-      exchange(tm_a, p.n_ms[rank], mb_m);
+      exchange(tm_b, p.n_ms[rank], mb_m);
       if (tid < C) {
         const uint32_t r = tid;
         ClusterHeader* h = hdr + (MBAR ? (gi & 1) : 0);
