@@ -25,11 +25,10 @@ __device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t par) {
   }
 }
 
-constexpr int TOTAL = 12288;  // bytes sent per CTA per iteration (4096 B to each peer)
 constexpr int SRC = 0, DST = 16384, SMEM = 32768 + 64;
 
 // MODE 0: st.async 4 B per lane, coalesced; MODE 1: cp.async.bulk runs of RUN bytes
-template <int MODE, int RUN>
+template <int MODE, int RUN, int TOTAL = 12288>  // TOTAL: bytes sent per CTA per iteration (a third to each peer)
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(1024, 1) bench(int iters, unsigned long long* out, float* sink) {
   extern __shared__ __align__(128) unsigned char sm[];
   uint32_t rank;
@@ -84,23 +83,23 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(1024, 1) bench(int i
   if (reinterpret_cast<float*>(sm)[threadIdx.x] == 12345.f) sink[threadIdx.x] = 1.f;
 }
 
-template <int MODE, int RUN>
+template <int MODE, int RUN, int TOTAL = 12288>
 void run(const char* name) {
   const int iters = 2000, nblocks = 33 * 4;
   unsigned long long* d;
   float* sink;
   cudaMalloc(&d, nblocks * sizeof(unsigned long long));
   cudaMalloc(&sink, 4096);
-  cudaFuncSetAttribute(bench<MODE, RUN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-  bench<MODE, RUN><<<nblocks, 1024, SMEM>>>(10, d, sink);
-  bench<MODE, RUN><<<nblocks, 1024, SMEM>>>(iters, d, sink);
+  cudaFuncSetAttribute(bench<MODE, RUN, TOTAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  bench<MODE, RUN, TOTAL><<<nblocks, 1024, SMEM>>>(10, d, sink);
+  bench<MODE, RUN, TOTAL><<<nblocks, 1024, SMEM>>>(iters, d, sink);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h[33 * 4];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   double mean = 0;
   for (int i = 0; i < nblocks; ++i) mean += h[i];
   mean /= nblocks;
-  printf("%-40s %s %8.1f cycles/iter  %6.2f B/cycle sent per SM\n", name, e == cudaSuccess ? "ok " : cudaGetErrorString(e),
+  printf("%-40s %6d B  %s %8.1f cycles/iter  %6.2f B/cycle sent per SM\n", name, TOTAL, e == cudaSuccess ? "ok " : cudaGetErrorString(e),
          mean / iters, TOTAL / (mean / iters));
   fflush(stdout);
   cudaFree(d);
@@ -108,6 +107,9 @@ void run(const char* name) {
 }
 
 int main() {
+  run<0, 4, 384>("st.async 4 B/lane coalesced");
+  run<0, 4, 1536>("st.async 4 B/lane coalesced");
+  run<0, 4, 6144>("st.async 4 B/lane coalesced");
   run<0, 4>("st.async 4 B/lane coalesced");
   run<1, 64>("cp.async.bulk runs of 64 B");
   run<1, 128>("cp.async.bulk runs of 128 B");
