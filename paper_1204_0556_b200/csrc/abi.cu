@@ -458,6 +458,8 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
               }
               g->cl_dense = dense;
               auto upc = [&](void** dst, const void* src, size_t bytes) -> bool {
+                if (*dst) cudaFree(*dst);  // a failed attempt at another cluster size
+                *dst = nullptr;
                 if (cudaMalloc(dst, bytes) != cudaSuccess) return false;
                 return cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
               };
