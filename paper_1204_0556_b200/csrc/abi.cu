@@ -944,6 +944,8 @@ int decode_impl(const admm_graph* g, int dtype, int64_t batch, const void* gamma
       cp.one_minus_rho = static_cast<T>(1.0 - rho);
       cp.thr = admm::thr_round_up<T>(thr);
       cp.thr_d = thr;
+      cp.fx_scale = admm::fx_scale_of(thr);
+      cp.fx_thr = admm::fx_thr_of(thr);
       cp.t_max = t_max;
       cp.x_out = static_cast<T*>(x_out);
       cp.ld_x = ld_x;

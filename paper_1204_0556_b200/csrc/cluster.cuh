@@ -139,6 +139,10 @@ __device__ __forceinline__ uint4 lds4u(uint32_t a) {
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
   return v;
 }
+__device__ __forceinline__ void sts4u(uint32_t a, uint32_t v) {  // four words of v
+  ADMM_CHECK_SMEM(a, 16);
+  asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(a), "r"(v) : "memory");
+}
 __device__ __forceinline__ void sts2u(uint32_t a, uint32_t x, uint32_t y) {
   ADMM_CHECK_SMEM(a, 8);
   asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
@@ -171,6 +175,8 @@ struct ClusterParamsT {
   long long ld_gamma;
   T mu, rho, one_minus_rho, thr;  // thr: eps^2 E rounded up to T (early-out)
   double thr_d;                   // eps^2 E
+  float fx_scale;                 // fp32: 42-bit fixed-point stop-rule sums (ResidentParams::fx_scale)
+  unsigned long long fx_thr;
   int t_max;
   T* x_out;
   long long ld_x;
@@ -459,7 +465,13 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, (sizeof(T) == 4 
         }
       }
     }
-    if (tid == 0) misc[1] = 0;
+    if (tid == 0) {
+      misc[1] = 0;
+      if (!kF64) {  // fixed-point stop-rule accumulators, both parities
+        sts4u(smem_u32(red), 0u);
+        sts4u(smem_u32(red) + 16, 0u);
+      }
+    }
     __syncthreads();
 
     int t = 0;
@@ -475,6 +487,9 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, (sizeof(T) == 4 
         var_pair(h);
       ADMM_JITTER();
       __syncthreads();
+      // (fp32 stop-rule accumulators: the buffer of iteration gi + 1 was last
+      // read in iteration gi - 1, which every thread left before this barrier)
+      if (!kF64 && tid == 0) sts4u(smem_u32(red) + 16u * ((gi + 1) & 1), 0u);
       phase(1);
       // ---- x-send: own x -> ghost slots of the other CTAs (coalesced per warp) ----
       exchange(tx_b, p.n_xs[rank], mb_x);
@@ -497,7 +512,32 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, (sizeof(T) == 4 
       ADMM_JITTER();
       const int nc = __syncthreads_or(primal >= p.thr || moved >= p.thr);
       double sa = 0.0, sb = 0.0;
-      if (!nc) {  // exact CTA sums in fp64 (rare: only near convergence)
+      if constexpr (!kF64) {
+        // fp32: exact, order-free CTA sums in 42-bit fixed point (every partial
+        // is below thr; resident_regular.cuh has the derivation): ~35
+        // instructions where the fp64 butterfly costs ~125 -- on low-SNR points
+        // the stuck frames take this path in most iterations.  The header
+        // carries the 64-bit integers in its double slots.
+        if (!nc) {
+          uint32_t* fx = reinterpret_cast<uint32_t*>(red) + 4 * (gi & 1);
+          const float ps = primal * p.fx_scale, ms = moved * p.fx_scale;
+          const uint32_t ph = __float2uint_rz(ps), mh = __float2uint_rz(ms);
+          const uint32_t pl = __float2uint_rz((ps - __uint2float_rn(ph)) * 2097152.f);
+          const uint32_t ml = __float2uint_rz((ms - __uint2float_rn(mh)) * 2097152.f);
+          const uint32_t s0 = __reduce_add_sync(0xffffffffu, ph), s1 = __reduce_add_sync(0xffffffffu, pl);
+          const uint32_t s2 = __reduce_add_sync(0xffffffffu, mh), s3 = __reduce_add_sync(0xffffffffu, ml);
+          if (lane == 0) {
+            atomicAdd(fx, s0);
+            atomicAdd(fx + 1, s1);
+            atomicAdd(fx + 2, s2);
+            atomicAdd(fx + 3, s3);
+          }
+          __syncthreads();
+          const uint4 v = lds4u(smem_u32(fx));
+          sa = __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(v.x) << 21) + v.y));
+          sb = __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(v.z) << 21) + v.w));
+        }
+      } else if (!nc) {  // fp64: exact CTA sums in fp64 (fixed order)
         const double wa = warp_allsum(static_cast<double>(primal));
         const double wb = warp_allsum(static_cast<double>(moved));
         if (lane == 0) {
@@ -547,13 +587,25 @@ __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, (sizeof(T) == 4 
       }
       phase(6);
       if (!anync) {
-        double A = 0.0, B = 0.0;
+        bool conv;
+        if constexpr (kF64) {
+          double A = 0.0, B = 0.0;
 #pragma unroll
-        for (int r = 0; r < C; ++r) {
-          A += hd->primal[r];
-          B += hd->moved[r];
+          for (int r = 0; r < C; ++r) {
+            A += hd->primal[r];
+            B += hd->moved[r];
+          }
+          conv = A < p.thr_d && B < p.thr_d;
+        } else {
+          unsigned long long A = 0, B = 0;
+#pragma unroll
+          for (int r = 0; r < C; ++r) {
+            A += static_cast<unsigned long long>(__double_as_longlong(hd->primal[r]));
+            B += static_cast<unsigned long long>(__double_as_longlong(hd->moved[r]));
+          }
+          conv = A < p.fx_thr && B < p.fx_thr;
         }
-        if (A < p.thr_d && B < p.thr_d) {
+        if (conv) {
           converged = true;
           break;
         }
