@@ -79,8 +79,9 @@ def test_streaming_irregular_and_zero_degree(cuda_ok, engine):
 
 @pytest.mark.parametrize("engine", ["auto", "streaming", "wide"])
 def test_config5_large_block_matches_oracle(cuda_ok, engine):
-    """n = 16384 does not fit one SM: the automatic engine is the streaming
-    placement (sharded kernel below 1024 frames); the wide kernel is forced too."""
+    """n = 16384 does not fit one SM: the automatic engine is the cluster
+    engine (fp64: 8-CTA clusters); the sharded and the wide kernels are
+    forced too."""
     from paper_1204_0556_b200 import AdmmConfig, baseline_code, decode_batch
 
     code = baseline_code("cfg5_n16384")
@@ -97,6 +98,13 @@ def test_config5_large_block_matches_oracle(cuda_ok, engine):
         assert np.array_equal(res.hard[t].cpu().numpy(), r.hard_decision)
     r32 = decode_batch(gam, code, cfg, dtype=torch.float32, want_hard=True, engine=engine)
     assert torch.equal(r32.hard, res.hard)
+    # fixed iteration count (north star: fp64 x within 1e-9 after T iterations)
+    fixed = AdmmConfig(mu=5.0, epsilon=1e-300, t_max=12)
+    rt = decode_batch(gam[:2], code, fixed, dtype=torch.float64, engine=engine)
+    for t in range(2):
+        r = O.decode(gam[t], g, O.Params(mu=5.0, epsilon=1e-300, t_max=12))
+        assert int(rt.iterations[t]) == 12 == r.iterations
+        assert np.abs(rt.x[t].cpu().numpy() - r.x).max() <= 1e-9
 
 
 @pytest.mark.parametrize("engine", ["streaming", "wide"])
