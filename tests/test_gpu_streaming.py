@@ -358,3 +358,32 @@ def test_cluster_engine_fp64_and_state_io(cuda_ok, monkeypatch):
         decode_batch(g, code4, AdmmConfig(), dtype=torch.float64, engine="cluster")
     r = decode_batch(g, code4, AdmmConfig(), dtype=torch.float64)
     assert r.info["kernel_name"] in ("sharded", "wide") and bool(r.converged.all())
+
+
+def test_config5_large_batch_properties(cuda_ok):
+    """At bench scale the oracle cannot follow, so size-independent properties
+    stand in: 131,072 config-5 frames per point decoded in one launch equal
+    the same trials decoded in uneven pieces (a frame's result depends only
+    on its trial index), every frame converges to the transmitted all-zero
+    codeword with its ML certificate at these channel points, and fp32 and
+    fp64 agree on every hard decision of a 4,096-frame sub-block."""
+    from paper_1204_0556_b200 import AdmmConfig, Awgn, Bsc, baseline_code, decode_synth
+
+    code = baseline_code("cfg5_n16384")
+    cfg = AdmmConfig(mu=5.0)
+    B = 131072
+    for k, ch in enumerate((Bsc(0.04), Awgn(2.5, code.design_rate))):
+        a = decode_synth(code, ch, cfg, seed=1, point=k, trial0=0, batch=B)
+        assert a.info["kernel_name"] == "cluster"
+        cuts = [0, 7, 4096 + 13, 70001, B]
+        parts = [decode_synth(code, ch, cfg, seed=1, point=k, trial0=lo, batch=hi - lo) for lo, hi in zip(cuts, cuts[1:])]
+        assert torch.equal(a.iterations, torch.cat([q.iterations for q in parts]))
+        assert torch.equal(a.flags, torch.cat([q.flags for q in parts]))
+        assert torch.equal(a.weight, torch.cat([q.weight for q in parts]))
+        assert bool(a.converged.all()) and bool(a.codeword.all()) and int(a.weight.sum()) == 0
+        assert int(a.iterations.max()) < cfg.t_max
+        h32 = decode_synth(code, ch, cfg, seed=1, point=k, trial0=50000, batch=4096, want_hard=True)
+        h64 = decode_synth(code, ch, cfg, seed=1, point=k, trial0=50000, batch=4096, want_hard=True, dtype=torch.float64)
+        assert torch.equal(h32.hard, h64.hard)
+        assert torch.equal(h32.iterations, a.iterations[50000:54096])
+        assert (h32.iterations - h64.iterations).abs().float().mean().item() <= 0.05
