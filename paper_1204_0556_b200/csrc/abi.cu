@@ -426,10 +426,22 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
                          (int)CL.ok, CL.error.c_str(), CL.NPL, CL.ghost_total, CL.msg_total, CL.msg_runs,
                          CL.bank_cost_before, CL.bank_cost_after);
           if (CL.ok) {
-            const int smem = admm::cluster_smem_bytes(0, CL.NPL, 3, CL.NXS, CL.NMS);
+            int npl = CL.NPL, smem = admm::cluster_smem_bytes(0, npl, 3, CL.NXS, CL.NMS);
             int clusters = 0, regs = 0;
             const bool fits = smem <= smem_optin && CL.NO <= 4096 && CL.NPL <= 8192;  // table fields
-            if (fits && admm::cluster_query(0, C, NT, smem, &clusters, &regs) == cudaSuccess && clusters > 0) {
+            const bool cl_placed = fits && admm::cluster_query(0, C, NT, smem, &clusters, &regs) == cudaSuccess && clusters > 0;
+            // pad the slot space to a count with a compile-time kernel variant
+            // (message rows at immediate offsets: +3 %) when that keeps the occupancy
+            if (const int fixed = cl_placed ? admm::cluster_fixed_npl(C, npl) : 0) {
+              const int smem_f = admm::cluster_smem_bytes(0, fixed, 3, CL.NXS, CL.NMS);
+              int cl_f = 0, regs_f = 0;
+              if (smem_f <= smem_optin && std::getenv("ADMM_B200_NO_FIXED_NPL") == nullptr &&
+                  admm::cluster_query(0, C, NT, smem_f, &cl_f, &regs_f) == cudaSuccess && cl_f >= clusters) {
+                npl = fixed;
+                smem = smem_f;
+              }
+            }
+            if (cl_placed) {
               // packed x-send table: own slot | ghost slot << 13 | rank << 29
               std::vector<uint32_t> xs((size_t)C * CL.NXS, 0);
               for (int p = 0; p < C; ++p) {
@@ -476,7 +488,7 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
                 g->cl_smem = smem;
                 g->cl_clusters = clusters;
                 g->cl_regs = regs;
-                g->cl_NPL = CL.NPL;
+                g->cl_NPL = npl;
                 g->cl_NXS = CL.NXS;
                 g->cl_NMS = CL.NMS;
                 g->cl_MC = CL.MC;
@@ -484,7 +496,7 @@ int admm_graph_create_ex(int device, int32_t n_vars, int32_t n_checks, const int
                 g->cl_exchange = CL.ghost_total + CL.msg_total;
                 // fp64 (parity mode) on the same layout: twice the shared memory,
                 // 128 registers, one 512-thread CTA per SM -- 8-CTA clusters only
-                const int smem64 = admm::cluster_smem_bytes(1, CL.NPL, 3, CL.NXS, CL.NMS);
+                const int smem64 = admm::cluster_smem_bytes(1, npl, 3, CL.NXS, CL.NMS);
                 int clusters64 = 0, regs64 = 0;
                 if (admm::cluster_supported(1, 6, 3, C, CPT, VPT) && smem64 <= smem_optin &&
                     std::getenv("ADMM_B200_NO_CLUSTER64") == nullptr &&

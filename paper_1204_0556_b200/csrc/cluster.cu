@@ -9,6 +9,9 @@ namespace admm {
 namespace {
 
 constexpr int kD = 6, kDV = 3, kCPT = 2, kVPT = 4;
+// Slot counts per part with a compiled variant (8-CTA clusters): the
+// BASELINE config-5 layout has 3904 slots and is padded to the first of them.
+constexpr int kNplA = 3968, kNplB = 4032;
 bool g_prof = false;  // launch the profiling instantiation
 const bool g_spread = std::getenv("ADMM_B200_CLUSTER_SPREAD") != nullptr;
 const bool g_barrier = std::getenv("ADMM_B200_CLUSTER_BARRIER") != nullptr;  // A/B: all-to-all cluster barriers
@@ -24,6 +27,12 @@ void fns_of(const void** fns) {
   fns[3] = reinterpret_cast<const void*>(&cluster_decode_kernel<T, kD, kDV, kCPT, kVPT, C, NT, true, true>);
 }
 
+template <typename T>
+void fixed_fns(const void** f2) {
+  f2[0] = reinterpret_cast<const void*>(&cluster_decode_kernel<T, kD, kDV, kCPT, kVPT, 8, 512, false, true, kNplA>);
+  f2[1] = reinterpret_cast<const void*>(&cluster_decode_kernel<T, kD, kDV, kCPT, kVPT, 8, 512, false, true, kNplB>);
+}
+
 bool fns_for(int dtype, int C, const void** fns) {
   if (dtype == 0 && C == 4) fns_of<float, 4, 1024>(fns);
   else if (dtype == 0 && C == 8) fns_of<float, 8, 512>(fns);
@@ -37,6 +46,11 @@ bool fns_for(int dtype, int C, const void** fns) {
 bool cluster_supported(int dtype, int D, int DV, int C, int CPT, int VPT) {
   const void* fns[4];
   return D == kD && DV == kDV && CPT == kCPT && VPT == kVPT && fns_for(dtype, C, fns);
+}
+
+int cluster_fixed_npl(int C, int npl) {
+  if (C != 8) return 0;
+  return npl <= kNplA ? kNplA : npl <= kNplB ? kNplB : 0;
 }
 
 int cluster_smem_bytes(int dtype, int NPL, int DV, int NXS, int NMS) {
@@ -57,6 +71,14 @@ cudaError_t cluster_query(int dtype, int C, int nt, int smem, int* clusters, int
   for (const void* f : fns) {
     const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
+  }
+  if (C == 8) {  // the compile-time-NPL variants share the launch shape
+    const void* f2[2];
+    if (dtype == 0) fixed_fns<float>(f2); else fixed_fns<double>(f2);
+    for (const void* f : f2) {
+      const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+    }
   }
   const void* fn = fns[2];
   cudaFuncAttributes fa{};
@@ -101,6 +123,14 @@ cudaError_t launch_t(const ClusterParamsT<T>& p, int clusters, int smem, cudaStr
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
+  // compile-time slot counts (8-CTA clusters, mbarrier syncs): the message rows
+  // sit at immediate offsets from the x slots (cluster_fixed_npl)
+  if constexpr (C == 8 && !PROF) {
+    if (p.dense && !g_barrier) {
+      if (p.NPL == kNplA) return cudaLaunchKernelEx(&cfg, cluster_decode_kernel<T, kD, kDV, kCPT, kVPT, C, NT, false, true, kNplA>, p);
+      if (p.NPL == kNplB) return cudaLaunchKernelEx(&cfg, cluster_decode_kernel<T, kD, kDV, kCPT, kVPT, C, NT, false, true, kNplB>, p);
+    }
+  }
   if (p.dense && !g_barrier)
     return cudaLaunchKernelEx(&cfg, cluster_decode_kernel<T, kD, kDV, kCPT, kVPT, C, NT, PROF, true>, p);
   return cudaLaunchKernelEx(&cfg, cluster_decode_kernel<T, kD, kDV, kCPT, kVPT, C, NT, PROF, false>, p);

@@ -234,14 +234,14 @@ __device__ unsigned long long g_cl_cycles[8];
 //     and o's message wait of t;
 //   * headers alternate between two buffers by iteration parity, and the
 //     same chains keep every pair of CTAs within one iteration.
-template <typename T, int D, int DV, int CPT, int VPT, int C, int NT, bool PROF = false, bool MBAR = false>
+template <typename T, int D, int DV, int CPT, int VPT, int C, int NT, bool PROF = false, bool MBAR = false, int NPLC = 0>
 __global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(NT, (sizeof(T) == 4 ? 1024 : 512) / NT)
     cluster_decode_kernel(const ClusterParamsT<T> p) {
   static_assert(D % DV == 0 && D % 2 == 0 && VPT % 2 == 0, "cluster engine: colored layout");
   constexpr uint32_t ES = sizeof(T);
   constexpr bool kF64 = ES == 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int NPL = p.NPL;
+  const int NPL = NPLC ? NPLC : p.NPL;  // NPLC: compile-time slot count (message rows at immediate offsets)
   const uint32_t rank = cl_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarps = NT / 32;
